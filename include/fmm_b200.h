@@ -1,0 +1,205 @@
+/*
+ * fmm_b200.h -- C ABI of libfmm_b200.so, the B200 (sm_100a) Laplace FMM
+ * hot path: Morton-key tree build, vertical passes, dual-tree traversal to
+ * CSR lists, M2L and P2P.
+ *
+ * Conventions (mirroring the reference's numba-core seam):
+ *  - every pointer is a DEVICE pointer (cudaMalloc / torch.Tensor.data_ptr())
+ *    unless named host_*; outputs are preallocated by the caller and filled
+ *    or accumulated in place;
+ *  - the library allocates nothing persistent; scratch space is a
+ *    caller-owned workspace whose size is obtained from a *_workspace_bytes
+ *    query;
+ *  - the last argument is the cudaStream_t (as void*); calls are
+ *    asynchronous on that stream unless they return counts through host_*
+ *    pointers (those synchronise the stream);
+ *  - return value: FMM_OK, or an error code.  FMM_ERR_CAPACITY means an
+ *    output array was too small; the exact required size is returned through
+ *    the documented out-parameter and the call may be repeated with bigger
+ *    buffers (the reference's grow-and-retry contract, src/tree.py:400-418,
+ *    src/traversal.py:806-828).  FMM_ERR_MAX_DEPTH mirrors the reference's
+ *    "max depth exceeded" ValueError (src/tree.py:419-423).
+ *
+ * Index widths: bodies and cells are int32 (N < 2^31), keys uint64.
+ * Reference paths: src/ = fmmkit/ (/root/reference/pkg/src/fmmkit/).
+ */
+#ifndef FMM_B200_H
+#define FMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FMM_API __attribute__((visibility("default")))
+#else
+#define FMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMM_OK 0
+#define FMM_ERR_CAPACITY 1
+#define FMM_ERR_MAX_DEPTH 2
+#define FMM_ERR_INVALID 3
+#define FMM_ERR_CUDA 4
+
+#define FMM_DTYPE_F64 0
+#define FMM_DTYPE_F32 1
+
+#define FMM_PREC_FP64 0
+#define FMM_PREC_FP32 1
+/* FP32 near field on offsets from a per-row anchor, with sources split
+ * into float32 hi + lo parts: for float64 inputs that float32 cannot
+ * represent (tight clusters), keeps dx accurate to the leaf scale. */
+#define FMM_PREC_FP32_ANCHORED 2
+
+FMM_API int fmm_abi_version(void);
+/* Message of the last error on the calling thread ("" when none). */
+FMM_API const char *fmm_last_error(void);
+/* Number of SMs of the current device (grid sizing). */
+FMM_API int fmm_device_sm_count(void);
+
+/* ---- tree build (replaces src/tree.py:370-454 and src/geometry.py:134-206) */
+
+/* Scratch bytes needed by every call below for n bodies (or cells/pairs). */
+FMM_API int fmm_workspace_bytes(int64_t n, size_t *host_bytes);
+
+/* Upcast x,y,z,q (FMM_DTYPE_*) into float64 SoA and compute the root cube
+ * (compute_bounds + cubic root, src/geometry.py:200-206, src/tree.py:387-392).
+ * root[8] = {lo0, lo1, lo2, size, inv_h, hi0, hi1, hi2} on the device. */
+FMM_API int fmm_ingest_bounds(const void *x, const void *y, const void *z, const void *q, int dtype,
+                      int64_t n, double *x64, double *y64, double *z64, double *q64, double *root,
+                      void *ws, size_t ws_bytes, void *stream);
+
+/* Depth-21 Morton keys (src/geometry.py:134-161) and iota values. */
+FMM_API int fmm_morton_keys(const double *x, const double *y, const double *z, int64_t n, const double *root,
+                    uint64_t *keys, int32_t *iota, void *stream);
+
+/* Stable radix sort of (key, value) pairs over key bits [0, end_bit)
+ * (np.argsort(kind="stable"), src/tree.py:395). */
+FMM_API int fmm_sort_pairs_u64(const uint64_t *keys_in, const int32_t *vals_in, uint64_t *keys_out,
+                       int32_t *vals_out, int64_t n, int end_bit, void *ws, size_t ws_bytes,
+                       void *stream);
+
+/* Gather bodies into Morton order: float64 SoA plus a float4 (x,y,z,q)
+ * copy for the FP32 P2P path (src/tree.py:396-398) and its float4
+ * residual (x - fp32(x), ...); dev_inexact[0] is set when any residual
+ * is non-zero (inputs not representable in float32). */
+FMM_API int fmm_permute_bodies(const int32_t *perm, const double *x, const double *y, const double *z,
+                       const double *q, int64_t n, double *xs, double *ys, double *zs, double *qs,
+                       void *b32, void *b32lo, int *dev_inexact, void *stream);
+
+/* One level of the level-synchronous carve (src/tree.py:43-77 _build_rec).
+ * node[i] = id of the still-splitting level-`level` cell holding body i, or
+ * -1.  Emits the level+1 children as cells [base, base+count) (BFS ids) and
+ * updates node[].  host_count receives the number of new cells;
+ * FMM_ERR_CAPACITY when base+count > cap (host_count still exact);
+ * FMM_ERR_MAX_DEPTH when a depth-21 cell holds > ncrit bodies and
+ * !allow_big.  cell arrays are indexed by BFS id. */
+FMM_API int fmm_build_level(const uint64_t *keys, int32_t *node, int64_t n, int level, int32_t ncrit,
+                    int allow_big, int32_t base, int32_t cap, int32_t *c_start, int32_t *c_end,
+                    int32_t *c_parent, int8_t *c_level, uint64_t *c_key, uint8_t *c_split,
+                    int32_t *host_count, void *ws, size_t ws_bytes, void *stream);
+
+/* Renumber BFS cells into the reference's pre-order and derive children
+ * (indexed by octant, -1 when empty), parent, sub_end, leaf, and the
+ * per-body leaf index.  pre_of_bfs[b] = pre-order id of BFS cell b. */
+FMM_API int fmm_finalize_cells(int32_t ncells, int64_t n, const int32_t *b_start, const int32_t *b_end,
+                       const int32_t *b_parent, const int8_t *b_level, const uint64_t *b_key,
+                       const uint8_t *b_split, int32_t *pre_of_bfs, int32_t *children,
+                       int32_t *parent, int8_t *level, uint64_t *key, int32_t *start, int32_t *end,
+                       int32_t *sub_end, uint8_t *leaf, int32_t *body_leaf, void *ws,
+                       size_t ws_bytes, void *stream);
+
+/* Cubic/geometric cell geometry, bit-exact (src/tree.py:80-160). */
+FMM_API int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, const int32_t *start,
+                      const int32_t *end, const double *xs, const double *ys, const double *zs,
+                      const double *root, double *lo, double *hi, double *ctr, double *bmax,
+                      double *rmax, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- vertical passes (src/tree.py:163-189, src/_taylor.py:102-269) ------ */
+
+/* P2M at every leaf (M zeroed first), then M2M bottom-up level by level.
+ * cells_by_level lists pre-order cell ids grouped by level;
+ * host_level_off[L]..host_level_off[L+1] is level L (host array, nlev+1). */
+FMM_API int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *start, const int32_t *end,
+               const uint8_t *leaf, const double *ctr, const double *xs, const double *ys,
+               const double *zs, const double *qs, const int32_t *cells_by_level,
+               const int32_t *host_level_off, int nlev, double *M, void *stream);
+
+/* L2L top-down then L2P; phi/f are ACCUMULATED (f -= grad). */
+FMM_API int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *leaf, const double *ctr,
+                 const int32_t *cells_by_level, const int32_t *host_level_off, int nlev,
+                 int64_t n, const int32_t *body_leaf, const double *xs, const double *ys,
+                 const double *zs, double *L, double *phi, double *fx, double *fy, double *fz,
+                 void *stream);
+
+/* ---- dual traversal (src/traversal.py:144-262, directed, MAC "fmm") ---- */
+
+/* One breadth-first step over frontier pairs (fa[k], fb[k]).  Appends P2P
+ * pairs, M2L pairs and the next frontier; counters live in dev_counts[3]
+ * = {n_p2p, n_m2l, n_next} and keep counting past capacity.
+ * kind: MAC kind code (0 bh, 1 bmax, 2 fmm; src/mac.py:21-22); th2 = theta*theta
+ * computed by the caller exactly as the reference. */
+FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, const int32_t *children,
+                      const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                      int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                      int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
+                      unsigned long long *dev_counts, void *stream);
+
+/* Sort (t, s) pairs by target then source and build row offsets over all
+ * cells: rows[c]..rows[c+1] are the sources of target c (ascending). */
+FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs, int32_t ncells,
+                     int32_t *src_sorted, int64_t *rows, void *ws, size_t ws_bytes, void *stream);
+
+/* P2P work decomposition: merge Morton-adjacent source leaves of every
+ * target-leaf row into contiguous body runs and split off the self leaf.
+ * Outputs the leaf rows (leaf_rows[r] = target leaf), run_off[r..r+1],
+ * runs as int4 {bstart, bend, self_flag, 0}; host_nruns = total runs.
+ * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
+ * into dev_stats[2] (src/_taylor.py:366-407 accounting). */
+FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
+                 const int64_t *rows, const int32_t *src_sorted, const double *xs, const double *ys,
+                 const double *zs, int32_t *leaf_rows, int64_t *run_off, void *runs, int64_t cap_runs,
+                 int64_t *host_nruns, int32_t *host_nleaf_rows, unsigned long long *dev_stats,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* ---- executors (src/traversal.py:500-548) ------------------------------ */
+
+/* L[t] += sum over row sources of M2L(M[s], ctr[t]-ctr[s]) (src/_taylor.py:169-188). */
+FMM_API int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const double *ctr,
+                const double *M, double *L, void *stream);
+
+/* Near field over the P2P plan.  precision FMM_PREC_FP32 reads the float4
+ * body copy b32; FMM_PREC_FP64 reads the float64 SoA.  Results are STORED
+ * (not accumulated) into phi/fx/fy/fz for every body of a planned leaf row.
+ * use_rsqrt (FP64 only) mirrors src/_taylor.py:318-323.
+ * dev_flag[0] is set when a non-finite sum was produced (FP32 collision of
+ * distinct bodies); the caller reruns with safe=1. */
+FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *leaf_rows,
+            const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
+            const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
+            const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);
+
+/* Final combine: out = p2p + far (phi, f) for all n bodies. */
+FMM_API int fmm_combine(int64_t n, const double *a_phi, const double *a_fx, const double *a_fy,
+                const double *a_fz, double *phi, double *fx, double *fy, double *fz, void *stream);
+
+/* ---- oracle-free utilities --------------------------------------------- */
+
+/* Direct O(S*N) sums onto target indices tidx (src/_taylor.py:496-528). */
+FMM_API int fmm_direct(int64_t n, const double *x, const double *y, const double *z, const double *q,
+               int64_t nt, const int64_t *tidx, double *phi, double *fx, double *fy, double *fz,
+               void *stream);
+
+/* FP32 FMA throughput probe: `iters` dependent-free FFMA (packed=0) or
+ * FFMA2 (packed=1) per thread over `blocks` x 256 threads; the caller
+ * times it with events.  Returns flops per launch via host_flops. */
+FMM_API int fmm_ffma_probe(int packed, int blocks, int iters, float *sink, double *host_flops, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

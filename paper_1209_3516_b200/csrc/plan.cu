@@ -1,0 +1,156 @@
+// plan.cu -- P2P work decomposition and the reference's pair counters.
+//
+// The P2P list from the traversal (leaf pairs, src/traversal.py:185-195) is
+// CSR over target leaves with ascending source-leaf ids.  Leaves in
+// pre-order own consecutive body ranges, so Morton-adjacent source leaves
+// of a row merge into one contiguous body run (664 source
+// leaves per row collapse to ~28 runs of ~770 bodies at C2).  The target
+// leaf's own bodies always form a separate "self" run, the only place the
+// kernel needs the i != j / r2 > 0 guards.
+//
+// Counters follow src/_taylor.py:366-407: pairs = sum |t||s| - sum_self |t|
+// - skipped, skipped = ordered i != j pairs of one leaf with r2 == 0.0 in
+// float64 (coincident bodies always share a leaf: equal positions give
+// equal depth-21 keys).  Compiled with --fmad=false so r2 matches.
+#include <cub/cub.cuh>
+
+#include "fmm_common.cuh"
+
+namespace fmm {
+
+__device__ inline bool run_start(const int32_t *src, int64_t k, int64_t k0, int32_t t,
+                                 const int32_t *start, const int32_t *end) {
+    if (k == k0) return true;
+    int32_t s = src[k], sp = src[k - 1];
+    return s == t || sp == t || start[s] != end[sp];
+}
+
+__global__ void plan_count(int32_t nrows, const int32_t *__restrict__ leaf_rows,
+                           const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
+                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                           int64_t *nr) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
+         r += (gridDim.x * blockDim.x) >> 5) {
+        const int32_t t = leaf_rows[r];
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        int64_t cnt = 0;
+        for (int64_t kb = k0; kb < k1; kb += 32) {
+            int64_t k = kb + lane;
+            bool f = k < k1 && run_start(src, k, k0, t, start, end);
+            cnt += __popc(__ballot_sync(0xffffffffu, f));
+        }
+        if (lane == 0) nr[r] = cnt;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) nr[nrows] = 0;
+}
+
+__global__ void plan_write(int32_t nrows, const int32_t *__restrict__ leaf_rows,
+                           const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
+                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                           const int64_t *__restrict__ run_off, int4 *runs) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
+         r += (gridDim.x * blockDim.x) >> 5) {
+        const int32_t t = leaf_rows[r];
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        int64_t base = run_off[r] - 1;  // index of the run holding the previous entry
+        for (int64_t kb = k0; kb < k1; kb += 32) {
+            int64_t k = kb + lane;
+            bool valid = k < k1;
+            bool f = valid && run_start(src, k, k0, t, start, end);
+            bool last = valid && (k + 1 == k1 || run_start(src, k + 1, k0, t, start, end));
+            unsigned m = __ballot_sync(0xffffffffu, f);
+            int64_t idx = base + __popc(m & ((2u << lane) - 1u));
+            if (f) {
+                int32_t s = src[k];
+                runs[idx].x = start[s];
+                runs[idx].z = (s == t) ? 1 : 0;
+                runs[idx].w = 0;
+            }
+            if (last) runs[idx].y = end[src[k]];
+            base += __popc(m);
+        }
+    }
+}
+
+// per target row: sum |t| |s| - self |t|, and coincident ordered pairs
+__global__ void plan_stats(int32_t nrows, const int32_t *__restrict__ leaf_rows,
+                           const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
+                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                           const double *__restrict__ xs, const double *__restrict__ ys,
+                           const double *__restrict__ zs, unsigned long long *stats) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
+         r += (gridDim.x * blockDim.x) >> 5) {
+        const int32_t t = leaf_rows[r];
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        const int64_t nt = end[t] - start[t];
+        unsigned long long blocks = 0, skipped = 0;
+        for (int64_t k = k0 + lane; k < k1; k += 32) {
+            int32_t s = src[k];
+            blocks += (unsigned long long)(nt * (end[s] - start[s]));
+            if (s == t) blocks -= (unsigned long long)nt;
+        }
+        // coincident pairs inside the target leaf (only if the self pair is listed)
+        for (int64_t i = start[t] + lane; i < end[t]; i += 32) {
+            for (int64_t j = start[t]; j < end[t]; j++) {
+                if (j == i) continue;
+                double dx = xs[i] - xs[j], dy = ys[i] - ys[j], dz = zs[i] - zs[j];
+                double r2 = dx * dx + dy * dy + dz * dz;
+                if (r2 == 0.0) skipped++;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            blocks += __shfl_xor_sync(0xffffffffu, blocks, o);
+            skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&stats[0], blocks - skipped);
+            atomicAdd(&stats[1], skipped);
+        }
+    }
+}
+
+}  // namespace fmm
+
+using namespace fmm;
+
+extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
+                            const int64_t *rows, const int32_t *src_sorted, const double *xs,
+                            const double *ys, const double *zs, int32_t *leaf_rows, int64_t *run_off,
+                            void *runs, int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows,
+                            unsigned long long *dev_stats, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    Arena ar(ws, ws_bytes);
+    int32_t *nsel = ar.take<int32_t>(1);
+    int64_t *nr = ar.take<int64_t>((size_t)ncells + 1);
+    if (!nsel || !nr) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    size_t need = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    cub::DeviceSelect::Flagged(nullptr, need, it, leaf, leaf_rows, nsel, ncells, s);
+    if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceSelect::Flagged(ar.rest(), need, it, leaf, leaf_rows, nsel, ncells, s);
+    int32_t nrows = 0;
+    cudaMemcpyAsync(&nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
+    *host_nleaf_rows = nrows;
+    const int g = grid_for((int64_t)nrows * 32, 256, 148 * 16);
+    plan_count<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, nr);
+    need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, nrows + 1, s);
+    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, nr, run_off, nrows + 1, s);
+    int64_t total = 0;
+    cudaMemcpyAsync(&total, run_off + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
+    *host_nruns = total;
+    if (total > cap_runs) { set_error("run capacity %lld < %lld", (long long)cap_runs, (long long)total); return FMM_ERR_CAPACITY; }
+    plan_write<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs);
+    if (dev_stats) {
+        cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
+        plan_stats<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, dev_stats);
+    }
+    FMM_CUDA_CHECK("fmm_p2p_plan");
+    return FMM_OK;
+}

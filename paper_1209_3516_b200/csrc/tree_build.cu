@@ -1,0 +1,569 @@
+// tree_build.cu -- Morton-key tree construction on the GPU, bit-exact with
+// the reference (src/geometry.py:134-206, src/tree.py:43-160, :370-454).
+//
+// Compiled with --fmad=false: the reference (numba, no fastmath) never fuses
+// a*b+c, and keys, centers, bmax and rmax must match it bit for bit.
+//
+// Layout: bodies are float64 SoA in Morton order (plus a float4 copy for
+// the FP32 P2P path); cells are SoA int32/uint64/double arrays indexed by
+// the reference's pre-order cell id.  The carve is level-synchronous: the
+// children of all splitting level-L cells are the runs of equal level-(L+1)
+// key prefix among their bodies, found with one flag pass, one scan and one
+// binary search per child (the reference's searchsorted, tree.py:67).
+// Pre-order numbering is then a sort by (start, level): a cell precedes its
+// descendants (same start, lower level) and every later sibling subtree
+// (larger start).
+#include <cub/cub.cuh>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "fmm_common.cuh"
+
+namespace fmm {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", where, cudaGetErrorString(e));
+        return FMM_ERR_CUDA;
+    }
+    return FMM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ingest + bounds
+// ---------------------------------------------------------------------------
+constexpr int kBoundsBlocks = 592;  // 4 x 148 SMs
+
+template <class T>
+__global__ void ingest_bounds_partial(const T *__restrict__ x, const T *__restrict__ y,
+                                      const T *__restrict__ z, const T *__restrict__ q, int64_t n,
+                                      double *x64, double *y64, double *z64, double *q64,
+                                      bool copy, double *partial) {
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double a = (double)x[i], b = (double)y[i], c = (double)z[i];
+        if (copy) {
+            x64[i] = a;
+            y64[i] = b;
+            z64[i] = c;
+            q64[i] = (double)q[i];
+        }
+        mn[0] = fmin(mn[0], a); mx[0] = fmax(mx[0], a);
+        mn[1] = fmin(mn[1], b); mx[1] = fmax(mx[1], b);
+        mn[2] = fmin(mn[2], c); mx[2] = fmax(mx[2], c);
+    }
+    __shared__ double s[6][32];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int d = 0; d < 3; d++) {
+        double a = mn[d], b = mx[d];
+        for (int o = 16; o > 0; o >>= 1) {
+            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (lane == 0) { s[d][w] = a; s[3 + d][w] = b; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        int nw = blockDim.x >> 5;
+        double v = s[threadIdx.x][0];
+        for (int k = 1; k < nw; k++)
+            v = threadIdx.x < 3 ? fmin(v, s[threadIdx.x][k]) : fmax(v, s[threadIdx.x][k]);
+        partial[blockIdx.x * 6 + threadIdx.x] = v;
+    }
+}
+
+__global__ void bounds_final(const double *partial, int nb, double *root) {
+    if (threadIdx.x != 0) return;
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; d++) {
+        lo[d] = partial[d];
+        hi[d] = partial[3 + d];
+        for (int b = 1; b < nb; b++) {
+            lo[d] = fmin(lo[d], partial[b * 6 + d]);
+            hi[d] = fmax(hi[d], partial[b * 6 + 3 + d]);
+        }
+    }
+    // size = max extent; 0 -> 1.0 (src/tree.py:388-392); extents in x, y, z order
+    double size = hi[0] - lo[0];
+    double e1 = hi[1] - lo[1], e2 = hi[2] - lo[2];
+    if (e1 > size) size = e1;
+    if (e2 > size) size = e2;
+    if (size == 0.0) size = 1.0;
+    root[0] = lo[0];
+    root[1] = lo[1];
+    root[2] = lo[2];
+    root[3] = size;
+    root[4] = (double)(1 << MAX_LEVEL) / size;
+    root[5] = hi[0];
+    root[6] = hi[1];
+    root[7] = hi[2];
+}
+
+// ---------------------------------------------------------------------------
+// Morton keys (src/geometry.py:134-161)
+// ---------------------------------------------------------------------------
+__global__ void morton_kernel(const double *__restrict__ x, const double *__restrict__ y,
+                              const double *__restrict__ z, int64_t n, const double *__restrict__ root,
+                              uint64_t *keys, int32_t *iota) {
+    const double lo0 = root[0], lo1 = root[1], lo2 = root[2], inv_h = root[4];
+    const int64_t top = (1ll << MAX_LEVEL) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ix = (int64_t)((x[i] - lo0) * inv_h);
+        int64_t iy = (int64_t)((y[i] - lo1) * inv_h);
+        int64_t iz = (int64_t)((z[i] - lo2) * inv_h);
+        ix = ix < 0 ? 0 : (ix > top ? top : ix);
+        iy = iy < 0 ? 0 : (iy > top ? top : iy);
+        iz = iz < 0 ? 0 : (iz > top ? top : iz);
+        keys[i] = spread21((uint64_t)ix) | spread21((uint64_t)iy) << 1 | spread21((uint64_t)iz) << 2;
+        if (iota) iota[i] = (int32_t)i;
+    }
+}
+
+__global__ void permute_kernel(const int32_t *__restrict__ perm, const double *__restrict__ x,
+                               const double *__restrict__ y, const double *__restrict__ z,
+                               const double *__restrict__ q, int64_t n, double *xs, double *ys,
+                               double *zs, double *qs, float4 *b32, float4 *b32lo, int *inexact) {
+    bool any = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t o = perm[i];
+        double a = x[o], b = y[o], c = z[o], d = q[o];
+        xs[i] = a;
+        ys[i] = b;
+        zs[i] = c;
+        qs[i] = d;
+        if (b32) {
+            float4 h = make_float4((float)a, (float)b, (float)c, (float)d);
+            b32[i] = h;
+            float4 l = make_float4((float)(a - (double)h.x), (float)(b - (double)h.y),
+                                   (float)(c - (double)h.z), 0.0f);
+            if (b32lo) b32lo[i] = l;
+            any |= (l.x != 0.0f) | (l.y != 0.0f) | (l.z != 0.0f);
+        }
+    }
+    if (inexact && __syncthreads_or(any) && threadIdx.x == 0) atomicOr(inexact, 1);
+}
+
+// ---------------------------------------------------------------------------
+// level-synchronous carve (src/tree.py:43-77)
+// ---------------------------------------------------------------------------
+__global__ void level_flags(const uint64_t *__restrict__ keys, const int32_t *__restrict__ node,
+                            int64_t n, int shift, int32_t *flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int f = 0;
+        if (node[i] >= 0) f = (i == 0) || ((keys[i] >> shift) != (keys[i - 1] >> shift));
+        flags[i] = f;
+    }
+}
+
+__device__ inline int64_t lower_bound_u64(const uint64_t *a, int64_t lo, int64_t hi, uint64_t v) {
+    while (lo < hi) {
+        int64_t mid = lo + ((hi - lo) >> 1);
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void level_emit(const uint64_t *__restrict__ keys, const int32_t *__restrict__ node,
+                           const int32_t *__restrict__ flags, const int32_t *__restrict__ incl, int64_t n,
+                           int level, int shift, int32_t ncrit, int allow_big, int32_t base,
+                           int32_t *c_start, int32_t *c_end, int32_t *c_parent, int8_t *c_level,
+                           uint64_t *c_key, uint8_t *c_split, int *err) {
+    const int clev = level + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (!flags[i]) continue;
+        int32_t c = base + incl[i] - 1;
+        uint64_t pre = shift >= 64 ? 0 : (keys[i] >> shift);
+        int64_t e = (clev == 0) ? n : lower_bound_u64(keys, i, n, (pre + 1) << shift);
+        int64_t cnt = e - i;
+        c_start[c] = (int32_t)i;
+        c_end[c] = (int32_t)e;
+        c_parent[c] = (clev == 0) ? -1 : node[i];
+        c_level[c] = (int8_t)clev;
+        c_key[c] = pre;
+        bool split = cnt > ncrit && clev < MAX_LEVEL;
+        c_split[c] = split ? 1 : 0;
+        if (cnt > ncrit && clev == MAX_LEVEL && !allow_big) atomicExch(err, 1);
+    }
+}
+
+__global__ void level_update(int32_t *node, const int32_t *__restrict__ incl, int64_t n, int32_t base,
+                             const uint8_t *__restrict__ c_split) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (node[i] < 0) continue;
+        int32_t c = base + incl[i] - 1;
+        node[i] = c_split[c] ? c : -1;
+    }
+}
+
+__global__ void fill_i32(int32_t *a, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// pre-order renumbering
+// ---------------------------------------------------------------------------
+__global__ void preorder_keys(int32_t ncells, const int32_t *b_start, const int8_t *b_level,
+                              uint64_t *sk, int32_t *iota) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncells; i += gridDim.x * blockDim.x) {
+        sk[i] = ((uint64_t)(uint32_t)b_start[i] << 5) | (uint64_t)(uint8_t)b_level[i];
+        iota[i] = i;
+    }
+}
+
+__global__ void preorder_gather(int32_t ncells, const int32_t *order, const int32_t *b_start,
+                                const int32_t *b_end, const int8_t *b_level, const uint64_t *b_key,
+                                const uint8_t *b_split, int32_t *pre_of_bfs, int8_t *level,
+                                uint64_t *key, int32_t *start, int32_t *end, uint8_t *leaf,
+                                int32_t *children) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncells; j += gridDim.x * blockDim.x) {
+        int32_t b = order[j];
+        pre_of_bfs[b] = j;
+        level[j] = b_level[b];
+        key[j] = b_key[b];
+        start[j] = b_start[b];
+        end[j] = b_end[b];
+        leaf[j] = b_split[b] ? 0 : 1;
+        for (int o = 0; o < 8; o++) children[j * 8 + o] = -1;
+    }
+}
+
+__global__ void preorder_links(int32_t ncells, const int32_t *order, const int32_t *b_parent,
+                               const int32_t *pre_of_bfs, const uint64_t *key, const int32_t *start,
+                               const int32_t *end, int32_t *parent, int32_t *children,
+                               int32_t *sub_end) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncells; j += gridDim.x * blockDim.x) {
+        int32_t pb = b_parent[order[j]];
+        int32_t pj = pb >= 0 ? pre_of_bfs[pb] : -1;
+        parent[j] = pj;
+        if (pj >= 0) children[pj * 8 + (int)(key[j] & 7ull)] = j;
+        // first later cell whose body range starts at or after our end
+        int32_t e = end[j];
+        int lo = j + 1, hi = ncells;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (start[mid] < e) lo = mid + 1;
+            else hi = mid;
+        }
+        sub_end[j] = lo;
+    }
+}
+
+__global__ void body_leaf_kernel(int32_t ncells, const uint8_t *leaf, const int32_t *start,
+                                 const int32_t *end, int32_t *body_leaf) {
+    // one warp per cell; leaves write their body range
+    int lane = threadIdx.x & 31;
+    for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < ncells;
+         c += (gridDim.x * blockDim.x) >> 5) {
+        if (!leaf[c]) continue;
+        for (int32_t i = start[c] + lane; i < end[c]; i += 32) body_leaf[i] = c;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cell geometry (src/tree.py:80-160, cubic + geometric)
+// ---------------------------------------------------------------------------
+constexpr int kChunk = 1024;  // bodies per bmax work item
+
+__global__ void geometry_cells(int32_t ncells, const int8_t *__restrict__ level,
+                               const uint64_t *__restrict__ key, const int32_t *__restrict__ start,
+                               const int32_t *__restrict__ end, const double *__restrict__ root,
+                               double *lo, double *hi, double *ctr, double *rmax,
+                               unsigned long long *b2, int32_t *nchunk) {
+    const double r[3] = {root[0], root[1], root[2]};
+    const double root_size = root[3];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+        int lvl = level[c];
+        double size = root_size / (double)(1ll << lvl);
+        uint64_t full = key[c] << (3 * (MAX_LEVEL - lvl));
+        double idx[3] = {(double)(compact21(full) >> (MAX_LEVEL - lvl)),
+                         (double)(compact21(full >> 1) >> (MAX_LEVEL - lvl)),
+                         (double)(compact21(full >> 2) >> (MAX_LEVEL - lvl))};
+        double a[3];
+        for (int d = 0; d < 3; d++) {
+            double l = r[d] + idx[d] * size;
+            double h = l + size;
+            double m = 0.5 * (l + h);
+            lo[c * 3 + d] = l;
+            hi[c * 3 + d] = h;
+            ctr[c * 3 + d] = m;
+            double u = fabs(l - m), v = fabs(h - m);
+            a[d] = (v > u) ? v : u;
+        }
+        rmax[c] = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+        b2[c] = 0ull;
+        nchunk[c] = (end[c] - start[c] + kChunk - 1) / kChunk;
+    }
+}
+
+__device__ inline int upper_bound_i32(const int32_t *a, int n, int32_t v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void geometry_bmax(int32_t ncells, const int32_t *__restrict__ choff,
+                              const int32_t *__restrict__ nchunk, const int32_t *__restrict__ start,
+                              const int32_t *__restrict__ end, const double *__restrict__ ctr,
+                              const double *__restrict__ xs, const double *__restrict__ ys,
+                              const double *__restrict__ zs, unsigned long long *b2) {
+    const int lane = threadIdx.x & 31;
+    const int total = choff[ncells - 1] + nchunk[ncells - 1];
+    for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total;
+         it += (gridDim.x * blockDim.x) >> 5) {
+        int c = upper_bound_i32(choff, ncells, it) - 1;
+        int k = it - choff[c];
+        int32_t s = start[c] + k * kChunk;
+        int32_t e = min(end[c], s + kChunk);
+        const double cx = ctr[c * 3], cy = ctr[c * 3 + 1], cz = ctr[c * 3 + 2];
+        double best = 0.0;
+        for (int32_t j = s + lane; j < e; j += 32) {
+            double dx = xs[j] - cx, dy = ys[j] - cy, dz = zs[j] - cz;
+            double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 > best) best = d2;
+        }
+        for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0 && best > 0.0) atomicMax(&b2[c], (unsigned long long)__double_as_longlong(best));
+    }
+}
+
+__global__ void geometry_finish(int32_t ncells, const unsigned long long *b2, double *bmax) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x)
+        bmax[c] = sqrt(__longlong_as_double((long long)b2[c]));
+}
+
+static size_t sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, n, 0, 64);
+    return bytes;
+}
+
+static size_t sortkeys_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr, n, 0,
+                                   64);
+    return bytes;
+}
+
+static size_t scan_temp_bytes(int64_t n) {
+    size_t a = 0, b = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, a, (const int32_t *)nullptr, (int32_t *)nullptr, n);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const int64_t *)nullptr, (int64_t *)nullptr, n);
+    return a > b ? a : b;
+}
+
+size_t workspace_bytes(int64_t n) {
+    int64_t m = n < 1024 ? 1024 : n;
+    size_t s = sort_temp_bytes(m);
+    size_t k = sortkeys_temp_bytes(m);
+    size_t c = scan_temp_bytes(m);
+    size_t t = s > k ? s : k;
+    t = t > c ? t : c;
+    // + two int32 arrays of m, one uint64 array of m, one int64 array of m, slack
+    return t + (size_t)m * (4 + 4 + 8 + 8 + 8) + (1 << 20);
+}
+
+}  // namespace fmm
+
+using namespace fmm;
+
+extern "C" {
+
+int fmm_abi_version(void) { return 1; }
+
+const char *fmm_last_error(void) { return fmm::g_err; }
+
+int fmm_device_sm_count(void) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return sms;
+}
+
+int fmm_workspace_bytes(int64_t n, size_t *host_bytes) {
+    *host_bytes = fmm::workspace_bytes(n);
+    return FMM_OK;
+}
+
+int fmm_ingest_bounds(const void *x, const void *y, const void *z, const void *q, int dtype, int64_t n,
+                      double *x64, double *y64, double *z64, double *q64, double *root, void *ws,
+                      size_t ws_bytes, void *stream) {
+    if (n <= 0) { set_error("empty particle set"); return FMM_ERR_INVALID; }
+    Arena ar(ws, ws_bytes);
+    double *partial = ar.take<double>(kBoundsBlocks * 6);
+    if (!partial) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    cudaStream_t s = as_stream(stream);
+    int nb = grid_for(n, 256, kBoundsBlocks);
+    if (dtype == FMM_DTYPE_F64) {
+        bool copy = (x != (const void *)x64);
+        ingest_bounds_partial<double><<<nb, 256, 0, s>>>((const double *)x, (const double *)y,
+                                                         (const double *)z, (const double *)q, n, x64,
+                                                         y64, z64, q64, copy, partial);
+    } else if (dtype == FMM_DTYPE_F32) {
+        ingest_bounds_partial<float><<<nb, 256, 0, s>>>((const float *)x, (const float *)y,
+                                                        (const float *)z, (const float *)q, n, x64, y64,
+                                                        z64, q64, true, partial);
+    } else {
+        set_error("bad dtype %d", dtype);
+        return FMM_ERR_INVALID;
+    }
+    bounds_final<<<1, 32, 0, s>>>(partial, nb, root);
+    FMM_CUDA_CHECK("fmm_ingest_bounds");
+    return FMM_OK;
+}
+
+int fmm_morton_keys(const double *x, const double *y, const double *z, int64_t n, const double *root,
+                    uint64_t *keys, int32_t *iota, void *stream) {
+    morton_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, y, z, n, root, keys, iota);
+    FMM_CUDA_CHECK("fmm_morton_keys");
+    return FMM_OK;
+}
+
+int fmm_sort_pairs_u64(const uint64_t *keys_in, const int32_t *vals_in, uint64_t *keys_out,
+                       int32_t *vals_out, int64_t n, int end_bit, void *ws, size_t ws_bytes,
+                       void *stream) {
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in, keys_out, vals_in, vals_out, n, 0, end_bit,
+                                    as_stream(stream));
+    if (need > ws_bytes) { set_error("sort workspace %zu > %zu", need, ws_bytes); return FMM_ERR_INVALID; }
+    cub::DeviceRadixSort::SortPairs(ws, need, keys_in, keys_out, vals_in, vals_out, n, 0, end_bit,
+                                    as_stream(stream));
+    FMM_CUDA_CHECK("fmm_sort_pairs_u64");
+    return FMM_OK;
+}
+
+int fmm_permute_bodies(const int32_t *perm, const double *x, const double *y, const double *z,
+                       const double *q, int64_t n, double *xs, double *ys, double *zs, double *qs,
+                       void *b32, void *b32lo, int *dev_inexact, void *stream) {
+    permute_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(perm, x, y, z, q, n, xs, ys, zs, qs,
+                                                                    (float4 *)b32, (float4 *)b32lo,
+                                                                    dev_inexact);
+    FMM_CUDA_CHECK("fmm_permute_bodies");
+    return FMM_OK;
+}
+
+int fmm_build_level(const uint64_t *keys, int32_t *node, int64_t n, int level, int32_t ncrit,
+                    int allow_big, int32_t base, int32_t cap, int32_t *c_start, int32_t *c_end,
+                    int32_t *c_parent, int8_t *c_level, uint64_t *c_key, uint8_t *c_split,
+                    int32_t *host_count, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    Arena ar(ws, ws_bytes);
+    int32_t *flags = ar.take<int32_t>(n);
+    int32_t *incl = ar.take<int32_t>(n);
+    int *err = ar.take<int>(4);
+    if (!flags || !incl || !err) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    void *tmp = ar.rest();
+    size_t tmp_bytes = ar.left();
+    int g = grid_for(n, 256);
+    if (level < 0) fill_i32<<<g, 256, 0, s>>>(node, n, 0);
+    const int clev = level + 1;
+    const int shift = 3 * (MAX_LEVEL - clev);
+    level_flags<<<g, 256, 0, s>>>(keys, node, n, shift >= 64 ? 63 : shift, flags);
+    size_t need = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, need, flags, incl, n, s);
+    if (need > tmp_bytes) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::InclusiveSum(tmp, need, flags, incl, n, s);
+    int32_t count = 0;
+    cudaMemcpyAsync(&count, incl + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemsetAsync(err, 0, sizeof(int), s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_build_level sync");
+    *host_count = count;
+    if (count == 0) return FMM_OK;
+    if ((int64_t)base + count > cap) {
+        set_error("cell capacity %d < %lld", cap, (long long)base + count);
+        return FMM_ERR_CAPACITY;
+    }
+    level_emit<<<g, 256, 0, s>>>(keys, node, flags, incl, n, level, shift, ncrit, allow_big, base,
+                                 c_start, c_end, c_parent, c_level, c_key, c_split, err);
+    level_update<<<g, 256, 0, s>>>(node, incl, n, base, c_split);
+    FMM_CUDA_CHECK("fmm_build_level");
+    if (clev == MAX_LEVEL) {
+        int h = 0;
+        cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_build_level sync");
+        if (h) {
+            set_error("max depth exceeded: more than ncrit=%d bodies share one depth-%d grid cell "
+                      "(pass allow_oversized_leaves=True to keep them in one leaf)",
+                      ncrit, MAX_LEVEL);
+            return FMM_ERR_MAX_DEPTH;
+        }
+    }
+    return FMM_OK;
+}
+
+int fmm_finalize_cells(int32_t ncells, int64_t n, const int32_t *b_start, const int32_t *b_end,
+                       const int32_t *b_parent, const int8_t *b_level, const uint64_t *b_key,
+                       const uint8_t *b_split, int32_t *pre_of_bfs, int32_t *children, int32_t *parent,
+                       int8_t *level, uint64_t *key, int32_t *start, int32_t *end, int32_t *sub_end,
+                       uint8_t *leaf, int32_t *body_leaf, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    Arena ar(ws, ws_bytes);
+    uint64_t *sk = ar.take<uint64_t>(ncells);
+    uint64_t *sk2 = ar.take<uint64_t>(ncells);
+    int32_t *iota = ar.take<int32_t>(ncells);
+    int32_t *order = ar.take<int32_t>(ncells);
+    if (!sk || !sk2 || !iota || !order) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    int g = grid_for(ncells, 256);
+    preorder_keys<<<g, 256, 0, s>>>(ncells, b_start, b_level, sk, iota);
+    int end_bit = 5;
+    while (end_bit < 64 && ((uint64_t)n << 5) >> end_bit) end_bit++;
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, sk, sk2, iota, order, ncells, 0, end_bit, s);
+    if (need > ar.left()) { set_error("sort workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceRadixSort::SortPairs(ar.rest(), need, sk, sk2, iota, order, ncells, 0, end_bit, s);
+    preorder_gather<<<g, 256, 0, s>>>(ncells, order, b_start, b_end, b_level, b_key, b_split, pre_of_bfs,
+                                      level, key, start, end, leaf, children);
+    preorder_links<<<g, 256, 0, s>>>(ncells, order, b_parent, pre_of_bfs, key, start, end, parent,
+                                     children, sub_end);
+    body_leaf_kernel<<<grid_for((int64_t)ncells * 32, 256), 256, 0, s>>>(ncells, leaf, start, end,
+                                                                        body_leaf);
+    FMM_CUDA_CHECK("fmm_finalize_cells");
+    return FMM_OK;
+}
+
+int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, const int32_t *start,
+                      const int32_t *end, const double *xs, const double *ys, const double *zs,
+                      const double *root, double *lo, double *hi, double *ctr, double *bmax,
+                      double *rmax, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    Arena ar(ws, ws_bytes);
+    unsigned long long *b2 = ar.take<unsigned long long>(ncells);
+    int32_t *nchunk = ar.take<int32_t>(ncells);
+    int32_t *choff = ar.take<int32_t>(ncells);
+    if (!b2 || !nchunk || !choff) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    int g = grid_for(ncells, 256);
+    geometry_cells<<<g, 256, 0, s>>>(ncells, level, key, start, end, root, lo, hi, ctr, rmax, b2, nchunk);
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, nchunk, choff, ncells, s);
+    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, nchunk, choff, ncells, s);
+    geometry_bmax<<<148 * 8, 256, 0, s>>>(ncells, choff, nchunk, start, end, ctr, xs, ys, zs, b2);
+    geometry_finish<<<g, 256, 0, s>>>(ncells, b2, bmax);
+    FMM_CUDA_CHECK("fmm_cell_geometry");
+    return FMM_OK;
+}
+
+}  // extern "C"

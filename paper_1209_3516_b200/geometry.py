@@ -1,0 +1,145 @@
+"""Particles and boxes (the reference's src/geometry.py:168-270 surface).
+
+``ParticleSet`` keeps the reference's structure-of-arrays contract:
+positions and charges in, ``phi`` and ``fx/fy/fz`` accumulators out, one
+length for all arrays.  Two storage forms are accepted:
+
+* NumPy arrays (the reference's form): upcast to float64 exactly as the
+  reference does (``geometry.py:231-241``); ``build_tree`` copies them to
+  the device.
+* torch CUDA tensors (float32 or float64): kept on the device as given, so
+  a device-resident cloud is solved without host traffic.  The kernels
+  upcast to float64 for keys and geometry (bit-exact with the reference).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+MAX_LEVEL = 21  # src/geometry.py:17
+
+__all__ = ["MAX_LEVEL", "Aabb", "ParticleSet", "compute_bounds"]
+
+
+def _is_torch(a) -> bool:
+    return isinstance(a, torch.Tensor)
+
+
+@dataclass(frozen=True)
+class Aabb:
+    """Axis-aligned box given by its two corners (src/geometry.py:168-197)."""
+
+    lo: np.ndarray
+    hi: np.ndarray
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "lo", np.asarray(self.lo, dtype=np.float64).reshape(3).copy())
+        object.__setattr__(self, "hi", np.asarray(self.hi, dtype=np.float64).reshape(3).copy())
+        if not np.all(self.hi >= self.lo):
+            raise ValueError("Aabb hi must be >= lo on every axis")
+
+    @property
+    def center(self) -> np.ndarray:
+        return 0.5 * (self.lo + self.hi)
+
+    @property
+    def extent(self) -> np.ndarray:
+        return self.hi - self.lo
+
+    def contains(self, pts: np.ndarray) -> np.ndarray:
+        pts = np.atleast_2d(pts)
+        return np.all((pts >= self.lo) & (pts <= self.hi), axis=1)
+
+
+class ParticleSet:
+    """Structure-of-arrays bodies (src/geometry.py:213-270)."""
+
+    def __init__(self, x, y, z, q, phi=None, fx=None, fy=None, fz=None):
+        if _is_torch(x):
+            arrs = [x, y, z, q]
+            if not all(_is_torch(a) for a in arrs):
+                raise TypeError("mix of torch tensors and other arrays")
+            dev = x.device
+            arrs = [a.contiguous() for a in arrs]
+            if any(a.device != dev for a in arrs):
+                raise ValueError("particle tensors live on different devices")
+            if any(a.dtype not in (torch.float32, torch.float64) for a in arrs):
+                raise TypeError("particle tensors must be float32 or float64")
+            if len({a.dtype for a in arrs}) != 1:
+                arrs = [a.to(torch.float64) for a in arrs]
+            self.x, self.y, self.z, self.q = arrs
+            n = self.x.shape[0]
+            acc = []
+            for a in (phi, fx, fy, fz):
+                acc.append(torch.zeros(n, dtype=torch.float64, device=dev) if a is None
+                           else torch.as_tensor(a, dtype=torch.float64, device=dev).contiguous())
+            self.phi, self.fx, self.fy, self.fz = acc
+        else:
+            self.x = np.ascontiguousarray(x, dtype=np.float64)
+            self.y = np.ascontiguousarray(y, dtype=np.float64)
+            self.z = np.ascontiguousarray(z, dtype=np.float64)
+            self.q = np.ascontiguousarray(q, dtype=np.float64)
+            n = self.x.shape[0]
+            acc = []
+            for a in (phi, fx, fy, fz):
+                acc.append(np.zeros(n) if a is None else np.ascontiguousarray(a, dtype=np.float64))
+            self.phi, self.fx, self.fy, self.fz = acc
+        lengths = {int(a.shape[0]) for a in (self.x, self.y, self.z, self.q, self.phi, self.fx, self.fy,
+                                             self.fz)}
+        if lengths != {int(n)}:
+            raise ValueError(f"particle arrays disagree on length: {sorted(lengths)}")
+
+    @property
+    def n(self) -> int:
+        return int(self.x.shape[0])
+
+    @property
+    def on_device(self) -> bool:
+        return _is_torch(self.x)
+
+    def positions(self) -> np.ndarray:
+        return np.column_stack([_np(self.x), _np(self.y), _np(self.z)])
+
+    def reset_accumulators(self) -> None:
+        for a in (self.phi, self.fx, self.fy, self.fz):
+            a[:] = 0.0
+
+    def view(self, start: int, stop: int) -> "ParticleSet":
+        """Shared-memory slice; writes to accumulators land in the parent."""
+        return ParticleSet(*(a[start:stop] for a in (self.x, self.y, self.z, self.q, self.phi, self.fx,
+                                                     self.fy, self.fz)))
+
+    def copy(self) -> "ParticleSet":
+        return ParticleSet(*(a.clone() if _is_torch(a) else a.copy()
+                             for a in (self.x, self.y, self.z, self.q, self.phi, self.fx, self.fy, self.fz)))
+
+    def permuted(self, perm) -> "ParticleSet":
+        return ParticleSet(*(a[perm].clone() if _is_torch(a) else a[perm].copy()
+                             for a in (self.x, self.y, self.z, self.q, self.phi, self.fx, self.fy, self.fz)))
+
+    def numpy(self) -> "ParticleSet":
+        """Host float64 copy (the reference's storage form)."""
+        return ParticleSet(*(_np(a) for a in (self.x, self.y, self.z, self.q, self.phi, self.fx, self.fy,
+                                              self.fz)))
+
+
+def _np(a) -> np.ndarray:
+    if _is_torch(a):
+        return a.detach().to("cpu", torch.float64).numpy()
+    return np.asarray(a, dtype=np.float64)
+
+
+def compute_bounds(ps: ParticleSet) -> Aabb:
+    """Tight bounding box of all bodies (src/geometry.py:200-206)."""
+    if ps.n == 0:
+        raise ValueError("empty particle set")
+    if ps.on_device:
+        lo = [float(a.min()) for a in (ps.x, ps.y, ps.z)]
+        hi = [float(a.max()) for a in (ps.x, ps.y, ps.z)]
+        return Aabb(np.array(lo), np.array(hi))
+    lo = np.array([ps.x.min(), ps.y.min(), ps.z.min()])
+    hi = np.array([ps.x.max(), ps.y.max(), ps.z.max()])
+    return Aabb(lo, hi)

@@ -1,0 +1,310 @@
+"""Dual-tree evaluation on the B200 (src/traversal.py:54-137, :864-932, :1202-1206).
+
+``evaluate_dual_tree`` runs, all on the device:
+
+1. ``upward_pass`` if the tree has no multipoles of order p;
+2. the breadth-first dual traversal (csrc/traverse.cu) -> M2L and P2P pair
+   lists, bit-exact sets with the reference's ``_collect_units``;
+3. CSR by target (radix sort), the P2P run plan (csrc/plan.cu) and the
+   reference's pair counters;
+4. M2L over the target CSR (csrc/m2l.cu) and P2P over the plan
+   (csrc/p2p.cu, FP32 or FP64);
+5. ``downward_pass`` (L2L, L2P).
+
+Phase times follow the reference's ``EvalReport`` (build, upward, traversal,
+downward; ``total_time`` sums them) and are measured with CUDA events on the
+evaluation stream; ``stats.times`` holds the per-kernel-class split
+("list", "m2l", "p2p").
+
+Scope: ``strategy="dualtree"``, directed (``mutual=False``), one shared
+tree.  ``treecode``/``listfmm``, ``mutual=True`` and ``source_tree`` are
+outside the B200 hot path and raise NotImplementedError.
+``precision`` is a new knob: "fp64" (default, the reference's arithmetic)
+or "fp32" (FP32 near field; far field stays float64).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from .kernels import TMAX, KernelStats, ncoef
+from .mac import MacConfig
+from .tree import Tree, downward_pass, upward_pass
+
+STRATEGIES = ("treecode", "listfmm", "dualtree")
+PRECISIONS = ("fp64", "fp32")
+REPORT_SCHEMA = "fmmkit-report-v1"
+
+__all__ = ["STRATEGIES", "PRECISIONS", "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_on_tree",
+           "interaction_lists"]
+
+
+@dataclass
+class EvalConfig:
+    """Knobs of one evaluation run (src/traversal.py:61-80) + ``precision``."""
+
+    strategy: str = "dualtree"
+    mac: MacConfig = field(default_factory=lambda: MacConfig("fmm", 0.6))
+    p: int = 4
+    mutual: bool = False
+    task_grain: int = 5000
+    use_rsqrt: bool = False
+    precision: str = "fp64"
+
+    def __post_init__(self) -> None:
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {self.strategy!r}: expected one of {STRATEGIES}")
+        if not isinstance(self.mac, MacConfig):
+            raise TypeError("mac must be a MacConfig")
+        if not 1 <= self.p <= TMAX:
+            raise ValueError(f"expansion order {self.p} outside supported range 1..{TMAX}")
+        if self.task_grain < 1:
+            raise ValueError(f"task_grain must be >= 1, got {self.task_grain}")
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r}: expected one of {PRECISIONS}")
+
+
+@dataclass
+class EvalReport:
+    """Outcome of one evaluation (src/traversal.py:83-137)."""
+
+    strategy: str
+    n: int
+    n_sources: int
+    p: int
+    mac_kind: str
+    theta: float
+    mutual: bool
+    threads: int
+    task_grain: int
+    stats: KernelStats
+    build_time: float
+    upward_time: float
+    traversal_time: float
+    downward_time: float
+    achieved_error: float | None = None
+    trace: list | None = None
+
+    @property
+    def total_time(self) -> float:
+        return self.build_time + self.upward_time + self.traversal_time + self.downward_time
+
+    def to_dict(self) -> dict:
+        counts = {k: v for k, v in self.stats.as_dict().items() if k != "times"}
+        return {
+            "schema": REPORT_SCHEMA,
+            "params": {"strategy": self.strategy, "n": self.n, "n_sources": self.n_sources, "p": self.p,
+                       "mac": self.mac_kind, "theta": self.theta, "mutual": self.mutual,
+                       "threads": self.threads, "task_grain": self.task_grain},
+            "counts": counts,
+            "times_ms": {"build": int(round(self.build_time * 1e3)),
+                         "upward": int(round(self.upward_time * 1e3)),
+                         "traversal": int(round(self.traversal_time * 1e3)),
+                         "downward": int(round(self.downward_time * 1e3)),
+                         "total": int(round(self.total_time * 1e3))},
+            "kernel_times_ms": {k: int(round(v * 1e3)) for k, v in sorted(self.stats.times.items())},
+            "achieved_error": self.achieved_error,
+        }
+
+    def to_json(self, indent: int = 2) -> str:
+        return json.dumps(self.to_dict(), indent=indent)
+
+
+# ---------------------------------------------------------------------------
+# traversal -> CSR lists
+# ---------------------------------------------------------------------------
+class Lists:
+    """Device interaction lists of one traversal (CSR by target cell)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    def host_pairs(self, which: str):
+        """(targets, sources) int64 numpy arrays sorted by (target, source)."""
+        rows = getattr(self, which + "_rows").cpu()
+        src = getattr(self, which + "_src").cpu().long()
+        t = torch.repeat_interleave(torch.arange(rows.numel() - 1), rows[1:] - rows[:-1])
+        return t.numpy(), src.numpy()
+
+
+_hint = {}
+
+
+def _grow(buf, used, need, dtype, dev):
+    nb = torch.empty(int(need), dtype=dtype, device=dev)
+    if used:
+        nb[:used].copy_(buf[:used])
+    return nb
+
+
+def interaction_lists(tree: Tree, mac: MacConfig) -> Lists:
+    """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
+    (the sets of src/traversal.py:159-262)."""
+    dev = tree.device
+    P = _lib.ptr
+    st = _lib.stream_handle()
+    i32 = torch.int32
+    th2 = mac.theta * mac.theta
+    key = (tree.ncells, tree.nleaves, mac.kind, th2)
+    cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
+                                                 max(4096, tree.ncells * 8)))
+    p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
+    p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
+    m2l_t = torch.empty(cap_m2l, dtype=i32, device=dev)
+    m2l_s = torch.empty(cap_m2l, dtype=i32, device=dev)
+    fa = torch.zeros(max(cap_next, 1), dtype=i32, device=dev)
+    fb = torch.zeros(max(cap_next, 1), dtype=i32, device=dev)
+    na = torch.empty(cap_next, dtype=i32, device=dev)
+    nb = torch.empty(cap_next, dtype=i32, device=dev)
+    counts = torch.zeros(3, dtype=torch.int64, device=dev)
+    done_p2p = done_m2l = 0
+    nfront = 1
+    peak = 1
+    while nfront > 0:
+        _lib.call("fmm_traverse_step", P(fa), P(fb), nfront, P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr),
+                  P(tree.d_bmax), P(tree.d_rmax), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
+                  cap_m2l, P(na), P(nb), cap_next, P(counts), st)
+        c_p2p, c_m2l, c_next = counts.tolist()
+        if c_p2p > cap_p2p or c_m2l > cap_m2l or c_next > cap_next:
+            if c_p2p > cap_p2p:
+                cap_p2p = int(c_p2p * 1.5) + 4096
+                p2p_t = _grow(p2p_t, done_p2p, cap_p2p, i32, dev)
+                p2p_s = _grow(p2p_s, done_p2p, cap_p2p, i32, dev)
+            if c_m2l > cap_m2l:
+                cap_m2l = int(c_m2l * 1.5) + 4096
+                m2l_t = _grow(m2l_t, done_m2l, cap_m2l, i32, dev)
+                m2l_s = _grow(m2l_s, done_m2l, cap_m2l, i32, dev)
+            if c_next > cap_next:
+                cap_next = int(c_next * 1.5) + 4096
+                na = torch.empty(cap_next, dtype=i32, device=dev)
+                nb = torch.empty(cap_next, dtype=i32, device=dev)
+            counts.copy_(torch.tensor([done_p2p, done_m2l, 0], dtype=torch.int64))
+            continue
+        done_p2p, done_m2l = c_p2p, c_m2l
+        fa, na = na, fa
+        fb, nb = nb, fb
+        nfront = c_next
+        peak = max(peak, nfront)
+        if na.numel() < cap_next:
+            na = torch.empty(cap_next, dtype=i32, device=dev)
+            nb = torch.empty(cap_next, dtype=i32, device=dev)
+        cap_next_now = na.numel()
+        cap_next = cap_next_now
+        counts[2] = 0
+    _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
+    ncells = tree.ncells
+    m2l_src = torch.empty(max(done_m2l, 1), dtype=i32, device=dev)
+    m2l_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev)
+    _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), wsp, wsb, st)
+    p2p_src = torch.empty(max(done_p2p, 1), dtype=i32, device=dev)
+    p2p_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
+    _lib.call("fmm_pairs_to_csr", P(p2p_t), P(p2p_s), done_p2p, ncells, P(p2p_src), P(p2p_rows), wsp, wsb, st)
+    del p2p_t, p2p_s, m2l_t, m2l_s, fa, fb, na, nb
+    # P2P run plan + the reference's pair counters
+    leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
+    run_off = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
+    dev_stats = torch.zeros(2, dtype=torch.int64, device=dev)
+    cap_runs = min(max(done_p2p, 1), tree.nleaves * 96 + 1024)
+    nruns = C.c_int64(0)
+    nrows = C.c_int32(0)
+    while True:
+        runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
+        try:
+            _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), P(p2p_rows),
+                      P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(leaf_rows), P(run_off), P(runs),
+                      cap_runs, C.byref(nruns), C.byref(nrows), P(dev_stats), wsp, wsb, st)
+            break
+        except _lib.CapacityError:
+            cap_runs = int(nruns.value)
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+                 p2p_rows=p2p_rows, leaf_rows=leaf_rows, nrows=int(nrows.value), run_off=run_off, runs=runs,
+                 nruns=int(nruns.value), dev_stats=dev_stats, peak_frontier=peak)
+
+
+def run_m2l(tree: Tree, lists: Lists, p: int) -> None:
+    P = _lib.ptr
+    _lib.call("fmm_m2l_csr", p, tree.ncells, P(lists.m2l_rows), P(lists.m2l_src), P(tree.d_ctr), P(tree._M),
+              P(tree._L), _lib.stream_handle())
+
+
+def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, safe: bool = False,
+            flag=None) -> None:
+    P = _lib.ptr
+    prec = _lib.PREC_FP32 if precision == "fp32" else _lib.PREC_FP64
+    _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), lists.nrows, P(lists.leaf_rows), P(tree.d_start),
+              P(tree.d_end), P(lists.run_off), P(lists.runs), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_q),
+              P(tree.d_b32), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag),
+              _lib.stream_handle())
+
+
+def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
+                       trace: bool = False) -> EvalReport:
+    """Simultaneous traversal of the tree against itself, on the GPU."""
+    if source_tree is not None and source_tree is not tree:
+        raise NotImplementedError("separate source trees are outside the B200 hot path")
+    if cfg.mutual:
+        raise NotImplementedError("mutual traversal is outside the B200 hot path")
+    if threads < 1:
+        raise ValueError(f"threads must be >= 1, got {threads}")
+    stats = KernelStats()
+    dev = tree.device
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        ev[0].record(stream)
+        if tree._M is None or tree.p != cfg.p:
+            upward_pass(tree, cfg.p, stats)
+        tree._L = torch.zeros((tree.ncells, ncoef(cfg.p)), dtype=torch.float64, device=dev)
+        tree.p = cfg.p
+        ev[1].record(stream)
+        lists = interaction_lists(tree, cfg.mac)
+        tree.list_cache = lists
+        ev[2].record(stream)
+        run_m2l(tree, lists, cfg.p)
+        ev[3].record(stream)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+        ev[4].record(stream)
+        if cfg.precision == "fp32" and int(flag.item()) != 0:
+            # two distinct bodies collided in FP32 outside a self run: redo guarded
+            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+            ev[4].record(stream)
+        ev[5].record(stream)
+        downward_pass(tree, stats, sync=False)
+        ev[6].record(stream)
+        ev[6].synchronize()
+        pairs, skipped = lists.dev_stats.tolist()
+    stats.p2p_pairs += int(pairs)
+    stats.p2p_skipped += int(skipped)
+    stats.p2p_flops += 20 * int(pairs)
+    stats.m2l_calls += lists.n_m2l
+    stats.add_time("list", ev[1].elapsed_time(ev[2]) * 1e-3)
+    stats.add_time("m2l", ev[2].elapsed_time(ev[3]) * 1e-3)
+    stats.add_time("p2p", ev[3].elapsed_time(ev[4]) * 1e-3)
+    tree._results_changed()
+    events = None
+    if trace:
+        events = []
+        mt, ms = lists.host_pairs("m2l")
+        events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
+        pt, ps = lists.host_pairs("p2p")
+        events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
+    return EvalReport(strategy="dualtree", n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
+                      theta=cfg.mac.theta, mutual=False, threads=threads, task_grain=cfg.task_grain, stats=stats,
+                      build_time=tree.build_time, upward_time=ev[0].elapsed_time(ev[1]) * 1e-3,
+                      traversal_time=ev[1].elapsed_time(ev[5]) * 1e-3,
+                      downward_time=ev[5].elapsed_time(ev[6]) * 1e-3, trace=events)
+
+
+def evaluate_on_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
+                     trace: bool = False) -> EvalReport:
+    """Run ``cfg.strategy`` on the tree; results land in ``tree.bodies``."""
+    if cfg.strategy != "dualtree":
+        raise NotImplementedError(f"strategy {cfg.strategy!r} is outside the B200 hot path (dualtree only)")
+    return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)

@@ -1,0 +1,140 @@
+"""CPU-only checks: the C ABI library loads and exports what include/*.h
+declares (no compute calls), and the host-side API mirrors the reference's
+validation and error behaviour."""
+
+import ctypes
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1209_3516_b200 as fb
+from paper_1209_3516_b200 import _lib, workloads
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_decls():
+    decls = {}
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for m in re.finditer(r"FMM_API\s+[\w\s\*]+?\b(fmm_\w+)\s*\(([^;]*?)\)\s*;", txt, flags=re.S):
+            args = m.group(2).strip()
+            nargs = 0 if args in ("", "void") else len(args.split(","))
+            decls[m.group(1)] = nargs
+    return decls
+
+
+def test_library_exports_every_declared_symbol():
+    decls = header_decls()
+    assert len(decls) >= 20
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name, nargs in decls.items():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, name
+        assert len(_lib.SIGNATURES[name]) == nargs, (name, nargs, len(_lib.SIGNATURES[name]))
+    assert set(_lib.SIGNATURES) == set(decls)
+
+
+def test_library_loads_without_gpu():
+    lib = _lib.load()
+    assert lib.fmm_abi_version() == 1
+    assert lib.fmm_last_error() == b""
+
+
+def test_workspace_query_is_host_only():
+    n = ctypes.c_size_t(0)
+    _lib.call("fmm_workspace_bytes", 1 << 20, ctypes.byref(n))
+    assert n.value > (1 << 20) * 16
+
+
+def test_sm100a_cubin_in_library():
+    data = open(_lib.LIB_PATH, "rb").read()
+    assert b"sm_100a" in data
+
+
+def test_build_validation_matches_reference():
+    pos, q = workloads.uniform_unit(10, 0)
+    ps = fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], q)
+    with pytest.raises(ValueError):
+        fb.build_tree(ps, ncrit=0)
+    with pytest.raises(ValueError, match="shape"):
+        fb.build_tree(ps, shape="spherical")
+    with pytest.raises(ValueError, match="center"):
+        fb.build_tree(ps, center_mode="origin")
+    with pytest.raises(ValueError):
+        fb.build_tree(fb.ParticleSet(np.empty(0), np.empty(0), np.empty(0), np.empty(0)))
+
+
+def test_config_validation():
+    with pytest.raises(ValueError, match="MAC kind"):
+        fb.MacConfig("nope", 0.5)
+    with pytest.raises(ValueError, match="theta"):
+        fb.MacConfig("fmm", 0.0)
+    with pytest.raises(ValueError, match="theta"):
+        fb.MacConfig("fmm", 2.5)
+    with pytest.raises(ValueError, match="expansion order"):
+        fb.EvalConfig(p=13)
+    with pytest.raises(ValueError, match="strategy"):
+        fb.EvalConfig(strategy="fast")
+    with pytest.raises(ValueError, match="precision"):
+        fb.EvalConfig(precision="fp16")
+    with pytest.raises(TypeError):
+        fb.EvalConfig(mac=0.5)
+    assert fb.EvalConfig().precision == "fp64"
+
+
+def test_particle_set_contract():
+    ps = fb.ParticleSet([0, 1], [0, 0], [0, 0], [1, 1])
+    assert ps.x.dtype == np.float64 and ps.phi.shape == (2,)
+    with pytest.raises(ValueError, match="disagree"):
+        fb.ParticleSet([0, 1], [0], [0, 0], [1, 1])
+    v = ps.view(0, 1)
+    v.phi[:] = 3.0
+    assert ps.phi[0] == 3.0
+
+
+def test_mac_accept_matches_reference_formula():
+    class Cell:
+        def __init__(self, c, b, r):
+            self.center, self.bmax, self.rmax = np.array(c, float), b, r
+    a, b = Cell([0, 0, 0], 0.1, 0.2), Cell([1, 0, 0], 0.1, 0.2)
+    assert fb.accept(fb.MacConfig("fmm", 0.3), a, b)        # 0.2 < 0.3
+    assert not fb.accept(fb.MacConfig("fmm", 0.2), a, b)    # strict <
+    assert not fb.accept(fb.MacConfig("fmm", 2.0), a, a)    # r == 0 rejects
+    assert fb.accept(fb.MacConfig("bh", 0.5), a, b) and not fb.accept(fb.MacConfig("bh", 0.4), a, b)
+
+
+def test_ncoef():
+    assert [fb.ncoef(p) for p in (1, 4, 5, 10, 12)] == [1, 20, 35, 220, 364]
+
+
+def test_report_schema():
+    st = fb.KernelStats(p2p_pairs=10, p2p_flops=200)
+    st.add_time("p2p", 0.5)
+    rep = fb.EvalReport("dualtree", 4, 4, 4, "fmm", 0.4, False, 1, 5000, st, 0.1, 0.2, 0.3, 0.4)
+    d = rep.to_dict()
+    assert d["schema"] == "fmmkit-report-v1"
+    assert d["times_ms"]["total"] == 1000 and d["kernel_times_ms"]["p2p"] == 500
+    assert d["counts"]["p2p_flops"] == 200
+
+
+def test_workload_generators_are_seeded():
+    a, qa = workloads.plummer(4096, 0)
+    b, qb = workloads.plummer(4096, 0)
+    assert np.array_equal(a, b) and a.dtype == np.float32
+    r = np.linalg.norm(a.astype(np.float64), axis=1)
+    assert r.max() <= 10.0 + 1e-4 and np.all(qa == np.float32(1.0 / 4096))
+    p2, q2 = workloads.config2(1000, 0)
+    assert p2.dtype == np.float32 and q2.min() >= 0.0 and q2.max() < 1.0
+    p1, q1 = workloads.config1(1000, 0)
+    assert abs(q1.mean()) < 1e-15
+
+
+def test_out_of_scope_paths_raise():
+    cfg = fb.EvalConfig(strategy="treecode")
+    with pytest.raises(NotImplementedError):
+        fb.evaluate_on_tree(object(), cfg)
