@@ -208,7 +208,8 @@ def fp32_peak(torch, lib_call, stream):
     from paper_1209_3516_b200 import _lib
     sink = torch.zeros(148 * 64, dtype=torch.float32, device="cuda")
     best = {}
-    for packed in (0, 1):
+    names = {0: "ffma_imm", 1: "ffma2_imm", 2: "ffma_reg", 3: "ffma2_reg", 4: "fmul_fadd_reg"}
+    for packed in (0, 1, 2, 3, 4):
         flops = C.c_double(0)
         for _ in range(2):
             lib_call("fmm_ffma_probe", packed, 148 * 16, 4096, _lib.ptr(sink), C.byref(flops), stream)
@@ -218,8 +219,8 @@ def fp32_peak(torch, lib_call, stream):
             lib_call("fmm_ffma_probe", packed, 148 * 16, 4096, _lib.ptr(sink), C.byref(flops), stream)
         e1.record()
         e1.synchronize()
-        best["ffma2" if packed else "ffma"] = 5 * flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
-    return max(best.values()), best
+        best[names[packed]] = 5 * flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    return max(best["ffma_imm"], best["ffma2_imm"]), best
 
 
 def run_ours(args):
@@ -260,7 +261,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = fdist_clocks = Clocks(local)
+    clocks = Clocks(local)
     clocks.start()
     times, p2p_times, reps = [], [], []
     torch.cuda.synchronize()

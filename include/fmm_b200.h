@@ -121,18 +121,22 @@ FMM_API int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_
 
 /* ---- vertical passes (src/tree.py:163-189, src/_taylor.py:102-269) ------ */
 
-/* P2M at every leaf (M zeroed first), then M2M bottom-up level by level.
+/* P2M at every listed leaf, then M2M bottom-up level by level over the
+ * listed internal cells (their M rows must be zero on entry).
  * cells_by_level lists pre-order cell ids grouped by level;
- * host_level_off[L]..host_level_off[L+1] is level L (host array, nlev+1). */
+ * host_level_off[L]..host_level_off[L+1] is level L (host array, nlev+1).
+ * Passing every cell gives the reference's upward pass; a multi-GPU rank
+ * passes the cells it owns, then the shared top cells. */
 FMM_API int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *start, const int32_t *end,
                const uint8_t *leaf, const double *ctr, const double *xs, const double *ys,
                const double *zs, const double *qs, const int32_t *cells_by_level,
                const int32_t *host_level_off, int nlev, double *M, void *stream);
 
-/* L2L top-down then L2P; phi/f are ACCUMULATED (f -= grad). */
+/* L2L top-down over the listed cells, then L2P for bodies [body_lo,
+ * body_hi); phi/f are ACCUMULATED (f -= grad). */
 FMM_API int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *leaf, const double *ctr,
                  const int32_t *cells_by_level, const int32_t *host_level_off, int nlev,
-                 int64_t n, const int32_t *body_leaf, const double *xs, const double *ys,
+                 int64_t body_lo, int64_t body_hi, const int32_t *body_leaf, const double *xs, const double *ys,
                  const double *zs, double *L, double *phi, double *fx, double *fy, double *fz,
                  void *stream);
 
@@ -142,9 +146,12 @@ FMM_API int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uin
  * pairs, M2L pairs and the next frontier; counters live in dev_counts[3]
  * = {n_p2p, n_m2l, n_next} and keep counting past capacity.
  * kind: MAC kind code (0 bh, 1 bmax, 2 fmm; src/mac.py:21-22); th2 = theta*theta
- * computed by the caller exactly as the reference. */
+ * computed by the caller exactly as the reference.  Pairs whose target
+ * cell's body range misses [body_lo, body_hi) are dropped (a multi-GPU rank
+ * keeps only its own targets; [0, n) keeps everything). */
 FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                      const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
                       int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
                       unsigned long long *dev_counts, void *stream);
@@ -156,11 +163,13 @@ FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs,
 
 /* P2P work decomposition: merge Morton-adjacent source leaves of every
  * target-leaf row into contiguous body runs and split off the self leaf.
+ * Rows are the leaves whose bodies lie in [body_lo, body_hi).
  * Outputs the leaf rows (leaf_rows[r] = target leaf), run_off[r..r+1],
  * runs as int4 {bstart, bend, self_flag, 0}; host_nruns = total runs.
  * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
  * into dev_stats[2] (src/_taylor.py:366-407 accounting). */
 FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
+                 int32_t body_lo, int32_t body_hi,
                  const int64_t *rows, const int32_t *src_sorted, const double *xs, const double *ys,
                  const double *zs, int32_t *leaf_rows, int64_t *run_off, void *runs, int64_t cap_runs,
                  int64_t *host_nruns, int32_t *host_nleaf_rows, unsigned long long *dev_stats,
@@ -194,10 +203,14 @@ FMM_API int fmm_direct(int64_t n, const double *x, const double *y, const double
                int64_t nt, const int64_t *tidx, double *phi, double *fx, double *fy, double *fz,
                void *stream);
 
-/* FP32 FMA throughput probe: `iters` dependent-free FFMA (packed=0) or
- * FFMA2 (packed=1) per thread over `blocks` x 256 threads; the caller
- * times it with events.  Returns flops per launch via host_flops. */
-FMM_API int fmm_ffma_probe(int packed, int blocks, int iters, float *sink, double *host_flops, void *stream);
+/* FP32 pipe throughput probe over `blocks` x 256 threads, 16 independent
+ * chains per thread, `iters` iterations: mode 0 FFMA (immediate operands),
+ * 1 FFMA2 (packed f32x2), 2 FFMA (register operands), 3 FFMA2 (register
+ * operands), 4 FMUL/FADD (register operands), 5 the P2P pair math on
+ * register sources (20 flops/pair), 6 the same without MUFU.  sink needs blocks*2+2
+ * floats (zeroed).  The caller times it with events; host_flops = flops
+ * per launch (2 per FMA lane-op, 1 per FMUL/FADD). */
+FMM_API int fmm_ffma_probe(int mode, int blocks, int iters, float *sink, double *host_flops, void *stream);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,8 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfmm_b200.so")
+# FMM_B200_LIB selects an alternative in-tree build (kernel A/B experiments)
+LIB_PATH = os.environ.get("FMM_B200_LIB") or os.path.join(HERE, "libfmm_b200.so")
 
 FMM_OK, FMM_ERR_CAPACITY, FMM_ERR_MAX_DEPTH, FMM_ERR_INVALID, FMM_ERR_CUDA = range(5)
 DTYPE_F64, DTYPE_F32 = 0, 1
@@ -40,10 +41,10 @@ SIGNATURES = {
     "fmm_finalize_cells": [I32, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
-    "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, P, P, P, P, P, P, P, P, P, P],
-    "fmm_traverse_step": [P, P, I64, P, P, P, P, P, INT, DBL, P, P, I64, P, P, I64, P, P, I64, P, P],
+    "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],
+    "fmm_traverse_step": [P, P, I64, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64, P, P, I64, P, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
-    "fmm_p2p_plan": [I32, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, SZ, P],
+    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, I64, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_combine": [I64, P, P, P, P, P, P, P, P, P],

@@ -52,6 +52,10 @@ constexpr Tables make_tables() {
 
 constexpr Tables kTab = make_tables();
 
+// Runtime-indexed copy in global memory, one per translation unit (device
+// symbols do not link across units without -rdc).
+static __device__ Tables d_tab = kTab;
+
 // Spread / compact the low 21 bits to every third bit (src/geometry.py:112-131).
 __host__ __device__ inline uint64_t spread21(uint64_t v) {
     v &= 0x1FFFFFull;

@@ -20,8 +20,6 @@
 
 namespace fmm {
 
-extern __device__ Tables d_tab;
-
 // ---- register kernel, compile-time multi-indices ------------------------
 // static_for hands each iteration its index as a type, so every table
 // lookup below is a constant expression and D / M / L stay in registers.

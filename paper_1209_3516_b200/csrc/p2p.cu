@@ -35,143 +35,457 @@ struct Anchor {
     float hx, hy, hz, lx, ly, lz;
 };
 
+// Non-coherent 128-bit load issued where it is written (volatile: the
+// compiler may not sink it next to its use, which defeats the prefetch).
+__device__ __forceinline__ float4 ldg_pinned(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <bool ANCHOR>
+__device__ __forceinline__ float4 load_body(const float4 *__restrict__ b, const float4 *__restrict__ blo,
+                                            const Anchor &an, int32_t j) {
+    float4 s = ldg_pinned(&b[j]);
+    if (ANCHOR) {
+        const float4 l = __ldg(&blo[j]);
+        s.x = (s.x - an.hx) + (l.x - an.lx);
+        s.y = (s.y - an.hy) + (l.y - an.ly);
+        s.z = (s.z - an.hz) + (l.z - an.lz);
+    }
+    return s;
+}
+
+// K target-source interactions for one source s (13 FP32 ops + 1 MUFU each).
+template <int K, bool GUARD>
+__device__ __forceinline__ void p2p_f32_pairs(const float4 &s, int32_t rel, const float (&tx)[K],
+                                              const float (&ty)[K], const float (&tz)[K], float (&ap)[K],
+                                              float (&ax)[K], float (&ay)[K], float (&az)[K]) {
+#pragma unroll
+    for (int u = 0; u < K; u++) {
+        const float dx = tx[u] - s.x;
+        const float dy = ty[u] - s.y;
+        const float dz = tz[u] - s.z;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        float rinv = rsqrt_approx(r2);
+        if (GUARD) rinv = (r2 > 0.0f && rel != u) ? rinv : 0.0f;
+        const float qr = s.w * rinv;
+        const float qr3 = qr * rinv * rinv;
+        ap[u] += qr;
+        ax[u] = fmaf(qr3, dx, ax[u]);
+        ay[u] = fmaf(qr3, dy, ay[u]);
+        az[u] = fmaf(qr3, dz, az[u]);
+    }
+}
+
+// Packed variant: targets (u, u+1) share one f32x2 register pair, the
+// source is a scalar broadcast operand (SASS `Rn.F32`), so one FADD2 /
+// FMUL2 / FFMA2 does two pairs' work: 13 packed ops + 2 MUFU per 2 pairs.
+// The FP32 lanes (128/clk/SM) become the bound instead of issue slots.
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_sub_s(f2_t a, float s) {  // a - {s, s}
+    f2_t r, b = f2_pack(s, s);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_mul_s(f2_t a, float s) {
+    return f2_mul(a, f2_pack(s, s));
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+    f2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+template <int K, bool GUARD>
+__device__ __forceinline__ void p2p_f32x2_pairs(const float4 &s, int32_t rel, const f2_t (&tx)[K / 2],
+                                                const f2_t (&ty)[K / 2], const f2_t (&tz)[K / 2], f2_t (&ap)[K / 2],
+                                                f2_t (&ax)[K / 2], f2_t (&ay)[K / 2], f2_t (&az)[K / 2]) {
+    // stage-major order: every step runs for all K/2 target pairs before the
+    // next, so K/2 independent chains sit between dependent instructions
+    constexpr int V = K / 2;
+    f2_t dx[V], dy[V], dz[V], r2[V], rinv[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) dx[v] = f2_sub_s(tx[v], s.x);
+#pragma unroll
+    for (int v = 0; v < V; v++) dy[v] = f2_sub_s(ty[v], s.y);
+#pragma unroll
+    for (int v = 0; v < V; v++) dz[v] = f2_sub_s(tz[v], s.z);
+#pragma unroll
+    for (int v = 0; v < V; v++) r2[v] = f2_mul(dx[v], dx[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) r2[v] = f2_fma(dy[v], dy[v], r2[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) r2[v] = f2_fma(dz[v], dz[v], r2[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        float r2l, r2h;
+        f2_unpack(r2[v], r2l, r2h);
+        float rl = rsqrt_approx(r2l), rh = rsqrt_approx(r2h);
+        if (GUARD) {
+            rl = (r2l > 0.0f && rel != 2 * v) ? rl : 0.0f;
+            rh = (r2h > 0.0f && rel != 2 * v + 1) ? rh : 0.0f;
+        }
+        rinv[v] = f2_pack(rl, rh);
+    }
+    f2_t qr[V], rr[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) qr[v] = f2_mul_s(rinv[v], s.w);
+#pragma unroll
+    for (int v = 0; v < V; v++) rr[v] = f2_mul(rinv[v], rinv[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) ap[v] = f2_add(ap[v], qr[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) rr[v] = f2_mul(qr[v], rr[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) ax[v] = f2_fma(rr[v], dx[v], ax[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) ay[v] = f2_fma(rr[v], dy[v], ay[v]);
+#pragma unroll
+    for (int v = 0; v < V; v++) az[v] = f2_fma(rr[v], dz[v], az[v]);
+}
+
+// cp.async (LDGSTS) helpers: each lane streams ITS OWN sources through a
+// private ring of kStages 16-byte slots in shared memory, so no cross-lane
+// synchronisation is needed; wait_group(kStages - 2) leaves the next
+// kStages - 2 fetches in flight while the current source is consumed.
+constexpr int kStages = 4;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// One lane-strided sweep over sources [j0, j1) for K register targets.
+// Non-anchored: sources stream through the lane's cp.async ring `ring`.
+// Anchored: register loads (the extra residual makes the ring twice as big).
+// GUARD (self run only): skip j == own index (rel == u) and r2 == 0.
 template <int K, bool GUARD, bool ANCHOR>
 __device__ __forceinline__ void p2p_f32_span(int32_t j0, int32_t j1, int step, const float4 *__restrict__ b,
-                                             const float4 *__restrict__ blo, const Anchor &an,
-                                             const float (&tx)[K], const float (&ty)[K],
-                                             const float (&tz)[K], const int32_t (&ti)[K], float (&ap)[K],
-                                             float (&ax)[K], float (&ay)[K], float (&az)[K]) {
-    for (int32_t j = j0; j < j1; j += step) {
-        float4 s = __ldg(&b[j]);
-        if (ANCHOR) {
-            const float4 l = __ldg(&blo[j]);
-            s.x = (s.x - an.hx) + (l.x - an.lx);
-            s.y = (s.y - an.hy) + (l.y - an.ly);
-            s.z = (s.z - an.hz) + (l.z - an.lz);
-        }
+                                             const float4 *__restrict__ blo, const Anchor &an, int32_t i0,
+                                             float4 *ring, const f2_t (&tx)[K / 2], const f2_t (&ty)[K / 2],
+                                             const f2_t (&tz)[K / 2], f2_t (&ap)[K / 2], f2_t (&ax)[K / 2],
+                                             f2_t (&ay)[K / 2], f2_t (&az)[K / 2]) {
+    if (j0 >= j1) return;
+    if (ANCHOR) {
+        for (int32_t j = j0; j < j1; j += step)
+            p2p_f32x2_pairs<K, GUARD>(load_body<ANCHOR>(b, blo, an, j), j - i0, tx, ty, tz, ap, ax, ay, az);
+        return;
+    }
+    const int32_t nit = (j1 - j0 + step - 1) / step;
+    const float4 *gp = b + j0;
 #pragma unroll
-        for (int u = 0; u < K; u++) {
-            const float dx = tx[u] - s.x;
-            const float dy = ty[u] - s.y;
-            const float dz = tz[u] - s.z;
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            float rinv = rsqrt_approx(r2);
-            if (GUARD) rinv = (r2 > 0.0f && j != ti[u]) ? rinv : 0.0f;
-            const float qr = s.w * rinv;
-            const float qr3 = qr * rinv * rinv;
-            ap[u] += qr;
-            ax[u] = fmaf(qr3, dx, ax[u]);
-            ay[u] = fmaf(qr3, dy, ay[u]);
-            az[u] = fmaf(qr3, dz, az[u]);
+    for (int k = 0; k < kStages - 1; k++) {
+        if (k < nit) cp_async16(&ring[k * 32], gp + k * step);
+        cp_async_commit();
+    }
+    const float4 *gnext = gp + (kStages - 1) * step;
+    int32_t it = 0;
+    // steady state, unrolled by the ring depth: slots are compile-time and
+    // every fetch is in range (no predicate, no modulo)
+    if (it + 2 * kStages - 1 <= nit) {
+        // the LDS of the next slot is issued before the current slot's math
+        cp_async_wait<kStages - 2>();
+        float4 cur = ring[0];
+        for (; it + 2 * kStages - 1 <= nit; it += kStages) {
+#pragma unroll
+            for (int q = 0; q < kStages; q++) {
+                cp_async16(&ring[((q + kStages - 1) % kStages) * 32], gnext);
+                gnext += step;
+                cp_async_commit();
+                cp_async_wait<kStages - 2>();
+                const float4 nxt = ring[((q + 1) % kStages) * 32];
+                p2p_f32x2_pairs<K, GUARD>(cur, j0 + (it + q) * step - i0, tx, ty, tz, ap, ax, ay, az);
+                cur = nxt;
+            }
+        }
+    }
+    for (; it < nit; it++) {
+        const int32_t nx = it + kStages - 1;
+        if (nx < nit) cp_async16(&ring[(nx % kStages) * 32], gnext);
+        gnext += step;
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();
+        const float4 s = ring[(it % kStages) * 32];
+        p2p_f32x2_pairs<K, GUARD>(s, j0 + it * step - i0, tx, ty, tz, ap, ax, ay, az);
+    }
+}
+
+// Block of KB consecutive targets starting at i0 (padded with the last
+// valid target), all runs of the row, folded over the warp.  Lane u < KB
+// ends holding target u's sums in (rp, rx, ry, rz).
+template <int KB, bool SAFE, bool ANCHOR>
+__device__ __forceinline__ void p2p_f32_block(int32_t i0, int32_t ilast, int64_t r0, int64_t r1, int part,
+                                              int nparts, int lane, const int4 *__restrict__ runs,
+                                              const float4 *__restrict__ b, const float4 *__restrict__ blo,
+                                              const Anchor &an, float4 *ring, float &rp, float &rx, float &ry,
+                                              float &rz) {
+    f2_t tx[KB / 2], ty[KB / 2], tz[KB / 2], ap[KB / 2], ax[KB / 2], ay[KB / 2], az[KB / 2];
+#pragma unroll
+    for (int v = 0; v < KB / 2; v++) {
+        const float4 e = load_body<ANCHOR>(b, blo, an, min(i0 + 2 * v, ilast));
+        const float4 o = load_body<ANCHOR>(b, blo, an, min(i0 + 2 * v + 1, ilast));
+        tx[v] = f2_pack(e.x, o.x);
+        ty[v] = f2_pack(e.y, o.y);
+        tz[v] = f2_pack(e.z, o.z);
+        ap[v] = ax[v] = ay[v] = az[v] = 0ull;
+    }
+    const int step = 32 * nparts;
+    for (int64_t r = r0; r < r1; r++) {
+        const int4 run = __ldg(&runs[r]);
+        const int32_t j0 = run.x + part * 32 + lane;
+        if (SAFE || run.z)
+            p2p_f32_span<KB, true, ANCHOR>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
+        else
+            p2p_f32_span<KB, false, ANCHOR>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
+    }
+    float fp[KB], fx_[KB], fy_[KB], fz_[KB];
+#pragma unroll
+    for (int v = 0; v < KB / 2; v++) {
+        f2_unpack(ap[v], fp[2 * v], fp[2 * v + 1]);
+        f2_unpack(ax[v], fx_[2 * v], fx_[2 * v + 1]);
+        f2_unpack(ay[v], fy_[2 * v], fy_[2 * v + 1]);
+        f2_unpack(az[v], fz_[2 * v], fz_[2 * v + 1]);
+    }
+#pragma unroll
+    for (int u = 0; u < KB; u++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            fp[u] += __shfl_xor_sync(0xffffffffu, fp[u], o);
+            fx_[u] += __shfl_xor_sync(0xffffffffu, fx_[u], o);
+            fy_[u] += __shfl_xor_sync(0xffffffffu, fy_[u], o);
+            fz_[u] += __shfl_xor_sync(0xffffffffu, fz_[u], o);
+        }
+        if (lane == u) { rp = fp[u]; rx = fx_[u]; ry = fy_[u]; rz = fz_[u]; }
+    }
+}
+
+// Streamed block (the fast path): all non-self runs of the row form ONE
+// lane-strided source sequence (the run table sits in shared memory), so the
+// cp.async ring runs continuously across runs -- no per-run prologue or
+// epilogue and no idle lanes at run ends.  The target leaf's own bodies are
+// swept first in a short guarded pass (the only place i == j or r2 == 0 can
+// occur for float32-exact inputs), and the stream then runs unguarded.
+constexpr int kMaxRuns = 512;
+
+__device__ __forceinline__ void stream_seek(int &rf, int32_t &jf, int32_t &rend, int nr, const int2 *srun) {
+    while (rf < nr && jf >= rend) {
+        const int32_t over = jf - rend;
+        if (++rf < nr) {
+            const int2 rr = srun[rf];
+            jf = rr.x + over;
+            rend = rr.y;
         }
     }
 }
 
-template <int K, bool SAFE, bool ANCHOR>
-__global__ void __launch_bounds__(kP2PWarps * 32) p2p_f32_kernel(
+template <int KB>
+__device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, int32_t ts, int32_t te,
+                                                     const int2 *srun, int nr, int32_t total, int part, int nparts,
+                                                     int lane, const float4 *__restrict__ b, float4 *ring, float &rp,
+                                                     float &rx, float &ry, float &rz) {
+    f2_t tx[KB / 2], ty[KB / 2], tz[KB / 2], ap[KB / 2], ax[KB / 2], ay[KB / 2], az[KB / 2];
+#pragma unroll
+    for (int v = 0; v < KB / 2; v++) {
+        const float4 e = __ldg(&b[min(i0 + 2 * v, ilast)]);
+        const float4 o = __ldg(&b[min(i0 + 2 * v + 1, ilast)]);
+        tx[v] = f2_pack(e.x, o.x);
+        ty[v] = f2_pack(e.y, o.y);
+        tz[v] = f2_pack(e.z, o.z);
+        ap[v] = ax[v] = ay[v] = az[v] = 0ull;
+    }
+    const int step = 32 * nparts;
+    // 1) self leaf, guarded
+    for (int32_t j = ts + part * 32 + lane; j < te; j += step)
+        p2p_f32x2_pairs<KB, true>(__ldg(&b[j]), j - i0, tx, ty, tz, ap, ax, ay, az);
+    // 2) the stream
+    const int32_t pos0 = part * 32 + lane;
+    const int32_t nit = pos0 < total ? (total - pos0 + step - 1) / step : 0;
+    const int32_t posmax = part * 32 + 31;
+    const int32_t nitc = posmax < total ? (total - posmax + step - 1) / step : 0;  // warp-uniform
+    int rf = 0;
+    int32_t jf = 0, rend = 0;
+    if (nr > 0) {
+        const int2 r0v = srun[0];
+        jf = r0v.x + pos0;
+        rend = r0v.y;
+        stream_seek(rf, jf, rend, nr, srun);
+    }
+#pragma unroll
+    for (int k = 0; k < kStages - 1; k++) {
+        if (k < nit) {
+            cp_async16(&ring[k * 32], &b[jf]);
+            jf += step;
+            stream_seek(rf, jf, rend, nr, srun);
+        }
+        cp_async_commit();
+    }
+    int32_t it = 0;
+    for (; it + kStages <= nitc; it += kStages) {
+#pragma unroll
+        for (int q = 0; q < kStages; q++) {
+            if (it + q + kStages - 1 < nit) {
+                cp_async16(&ring[((q + kStages - 1) % kStages) * 32], &b[jf]);
+                jf += step;
+                stream_seek(rf, jf, rend, nr, srun);
+            }
+            cp_async_commit();
+            cp_async_wait<kStages - 1>();
+            p2p_f32x2_pairs<KB, false>(ring[q * 32], 0, tx, ty, tz, ap, ax, ay, az);
+        }
+    }
+    for (; it < nit; it++) {  // <= kStages iterations; the last may be lane-divergent
+        if (it + kStages - 1 < nit) {
+            cp_async16(&ring[((it + kStages - 1) % kStages) * 32], &b[jf]);
+            jf += step;
+            stream_seek(rf, jf, rend, nr, srun);
+        }
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();
+        p2p_f32x2_pairs<KB, false>(ring[(it % kStages) * 32], 0, tx, ty, tz, ap, ax, ay, az);
+    }
+    cp_async_wait<0>();
+    float fp[KB], fx_[KB], fy_[KB], fz_[KB];
+#pragma unroll
+    for (int v = 0; v < KB / 2; v++) {
+        f2_unpack(ap[v], fp[2 * v], fp[2 * v + 1]);
+        f2_unpack(ax[v], fx_[2 * v], fx_[2 * v + 1]);
+        f2_unpack(ay[v], fy_[2 * v], fy_[2 * v + 1]);
+        f2_unpack(az[v], fz_[2 * v], fz_[2 * v + 1]);
+    }
+#pragma unroll
+    for (int u = 0; u < KB; u++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            fp[u] += __shfl_xor_sync(0xffffffffu, fp[u], o);
+            fx_[u] += __shfl_xor_sync(0xffffffffu, fx_[u], o);
+            fy_[u] += __shfl_xor_sync(0xffffffffu, fy_[u], o);
+            fz_[u] += __shfl_xor_sync(0xffffffffu, fz_[u], o);
+        }
+        if (lane == u) { rp = fp[u]; rx = fx_[u]; ry = fy_[u]; rz = fz_[u]; }
+    }
+}
+
+// Target blocks of a leaf: cnt / 8 blocks of 8, then the remainder as one
+// block of 4 (r <= 4) or 8 -- at most 3 padded slots per leaf.
+template <bool SAFE, bool ANCHOR>
+__global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
     int32_t nrows, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const float4 *__restrict__ b, const float4 *__restrict__ blo, double *phi, double *fx, double *fy,
     double *fz, int *flag) {
-    __shared__ float red[kP2PWarps][4 * K];
+    __shared__ float red[kP2PWarps][4][32];
+    __shared__ float4 rings[kP2PWarps][kStages * 32];
+    __shared__ int2 srun[kMaxRuns];
+    __shared__ int32_t stotal;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float4 *ring = &rings[w][lane];
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
         const int32_t t = leaf_rows[row];
         const int32_t ts = start[t], cnt = end[t] - ts;
-        const int nblk = (cnt + K - 1) / K;
+        const int rem = cnt & 7;
+        const int nblk = (cnt >> 3) + (rem ? 1 : 0);
+        const bool small_last = rem != 0 && rem <= 4;
         const int nparts = nblk >= kP2PWarps ? 1 : kP2PWarps / nblk;
         const int64_t r0 = run_off[row], r1 = run_off[row + 1];
-        const int rounds = (nblk + kP2PWarps - 1) / kP2PWarps;  // nparts == 1 case
-        for (int rd = 0; rd < (nparts > 1 ? 1 : rounds); rd++) {
-            int tb, part;
-            if (nparts > 1) { tb = w % nblk; part = w / nblk; }
-            else { tb = rd * kP2PWarps + w; part = 0; }
-            const bool active = (nparts > 1) ? (part < nparts) : (tb < nblk);
-            float tx[K], ty[K], tz[K], ap[K], ax[K], ay[K], az[K];
-            int32_t ti[K];
-            if (active) {
-                Anchor an{};
-                if (ANCHOR) {
-                    const float4 h = __ldg(&b[ts]), l = __ldg(&blo[ts]);
-                    an = Anchor{h.x, h.y, h.z, l.x, l.y, l.z};
-                }
-#pragma unroll
-                for (int u = 0; u < K; u++) {
-                    int32_t i = ts + min(tb * K + u, cnt - 1);
-                    float4 v = __ldg(&b[i]);
-                    if (ANCHOR) {
-                        const float4 l = __ldg(&blo[i]);
-                        v.x = (v.x - an.hx) + (l.x - an.lx);
-                        v.y = (v.y - an.hy) + (l.y - an.ly);
-                        v.z = (v.z - an.hz) + (l.z - an.lz);
-                    }
-                    tx[u] = v.x; ty[u] = v.y; tz[u] = v.z;
-                    ti[u] = i;
-                    ap[u] = ax[u] = ay[u] = az[u] = 0.0f;
-                }
-                const int step = 32 * nparts;
-                for (int64_t r = r0; r < r1; r++) {
-                    const int4 run = __ldg(&runs[r]);
-                    const int32_t j0 = run.x + part * 32 + lane;
-                    if (SAFE || run.z)
-                        p2p_f32_span<K, true, ANCHOR>(j0, run.y, step, b, blo, an, tx, ty, tz, ti, ap, ax, ay, az);
-                    else
-                        p2p_f32_span<K, false, ANCHOR>(j0, run.y, step, b, blo, an, tx, ty, tz, ti, ap, ax, ay, az);
-                }
-#pragma unroll
-                for (int u = 0; u < K; u++) {
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        ap[u] += __shfl_xor_sync(0xffffffffu, ap[u], o);
-                        ax[u] += __shfl_xor_sync(0xffffffffu, ax[u], o);
-                        ay[u] += __shfl_xor_sync(0xffffffffu, ay[u], o);
-                        az[u] += __shfl_xor_sync(0xffffffffu, az[u], o);
-                    }
-                }
+        Anchor an{};
+        if (ANCHOR) {
+            const float4 h = __ldg(&b[ts]), l = __ldg(&blo[ts]);
+            an = Anchor{h.x, h.y, h.z, l.x, l.y, l.z};
+        }
+        const int nr = (int)(r1 - r0);
+        const bool streamed = !ANCHOR && !SAFE && nr <= kMaxRuns;
+        if (streamed) {
+            if (threadIdx.x == 0) stotal = 0;
+            __syncthreads();
+            int32_t len = 0;
+            for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+                const int4 rr = __ldg(&runs[r0 + k]);
+                const int2 v = rr.z ? make_int2(rr.x, rr.x) : make_int2(rr.x, rr.y);  // self run: empty
+                srun[k] = v;
+                len += v.y - v.x;
+            }
+            for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
+            if (lane == 0) atomicAdd(&stotal, len);
+            __syncthreads();
+        }
+        const int32_t total = streamed ? stotal : 0;
+        const int rounds = nparts > 1 ? 1 : (nblk + kP2PWarps - 1) / kP2PWarps;
+        for (int rd = 0; rd < rounds; rd++) {
+            const int tb = nparts > 1 ? w % nblk : rd * kP2PWarps + w;
+            const int part = nparts > 1 ? w / nblk : 0;
+            const bool active = nparts > 1 ? part < nparts : tb < nblk;
+            float rp = 0.f, rx = 0.f, ry = 0.f, rz = 0.f;
+            const int32_t i0 = ts + tb * 8;
+            if (active && streamed) {
+                if (tb == nblk - 1 && small_last)
+                    p2p_f32_stream_block<4>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, nparts, lane, b,
+                                            ring, rp, rx, ry, rz);
+                else
+                    p2p_f32_stream_block<8>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, nparts, lane, b,
+                                            ring, rp, rx, ry, rz);
+            } else if (active) {
+                if (tb == nblk - 1 && small_last)
+                    p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, nparts, lane, runs, b, blo, an,
+                                                   ring, rp, rx, ry, rz);
+                else
+                    p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, nparts, lane, runs, b, blo, an,
+                                                   ring, rp, rx, ry, rz);
             }
             if (nparts > 1) {
-                if (active && lane == 0) {
-#pragma unroll
-                    for (int u = 0; u < K; u++) {
-                        red[w][u] = ap[u];
-                        red[w][K + u] = ax[u];
-                        red[w][2 * K + u] = ay[u];
-                        red[w][3 * K + u] = az[u];
-                    }
+                if (active && lane < 8) {
+                    red[w][0][lane] = rp;
+                    red[w][1][lane] = rx;
+                    red[w][2][lane] = ry;
+                    red[w][3][lane] = rz;
                 }
                 __syncthreads();
-                if (active && part == 0) {
-                    // fold parts in fixed order; lane u finalises target u
-#pragma unroll
-                    for (int u = 0; u < K; u++) {
-                        float p_ = 0.f, x_ = 0.f, y_ = 0.f, z_ = 0.f;
-                        for (int q = 0; q < nparts; q++) {
-                            const int ww = q * nblk + tb;
-                            p_ += red[ww][u];
-                            x_ += red[ww][K + u];
-                            y_ += red[ww][2 * K + u];
-                            z_ += red[ww][3 * K + u];
-                        }
-                        ap[u] = p_; ax[u] = x_; ay[u] = y_; az[u] = z_;
+                if (active && part == 0 && lane < 8) {
+                    rp = rx = ry = rz = 0.f;
+                    for (int q = 0; q < nparts; q++) {  // fixed order: deterministic
+                        const int ww = q * nblk + tb;
+                        rp += red[ww][0][lane];
+                        rx += red[ww][1][lane];
+                        ry += red[ww][2][lane];
+                        rz += red[ww][3][lane];
                     }
                 }
                 __syncthreads();
             }
-            if (active && part == 0) {
-#pragma unroll
-                for (int u = 0; u < K; u++) {
-                    if (lane == u && tb * K + u < cnt) {
-                        const int32_t i = ts + tb * K + u;
-                        phi[i] = (double)ap[u];
-                        fx[i] = (double)ax[u];
-                        fy[i] = (double)ay[u];
-                        fz[i] = (double)az[u];
-                        if (!(isfinite(ap[u]) && isfinite(ax[u]) && isfinite(ay[u]) && isfinite(az[u])))
-                            atomicOr(flag, 1);
-                    }
-                }
+            if (active && part == 0 && lane < 8 && tb * 8 + lane < cnt) {
+                const int32_t i = i0 + lane;
+                phi[i] = (double)rp;
+                fx[i] = (double)rx;
+                fy[i] = (double)ry;
+                fz[i] = (double)rz;
+                if (!(isfinite(rp) && isfinite(rx) && isfinite(ry) && isfinite(rz))) atomicOr(flag, 1);
             }
         }
+        if (streamed) __syncthreads();  // srun is rewritten by the next row
     }
 }
 
@@ -296,8 +610,8 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, co
         if (!b32) { set_error("fp32 P2P needs the float4 body copy"); return FMM_ERR_INVALID; }
         const bool anch = precision == FMM_PREC_FP32_ANCHORED;
         if (anch && !b32lo) { set_error("anchored fp32 P2P needs the float4 residual copy"); return FMM_ERR_INVALID; }
-        auto kern = anch ? (safe ? p2p_f32_kernel<8, true, true> : p2p_f32_kernel<8, false, true>)
-                         : (safe ? p2p_f32_kernel<8, true, false> : p2p_f32_kernel<8, false, false>);
+        auto kern = anch ? (safe ? p2p_f32_kernel<true, true> : p2p_f32_kernel<false, true>)
+                         : (safe ? p2p_f32_kernel<true, false> : p2p_f32_kernel<false, false>);
         kern<<<grid, kP2PWarps * 32, 0, s>>>(nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
                                              (const float4 *)b32, (const float4 *)b32lo, phi, fx, fy, fz,
                                              dev_flag);

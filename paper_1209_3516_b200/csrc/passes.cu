@@ -10,8 +10,6 @@
 
 namespace fmm {
 
-__device__ Tables d_tab = kTab;
-
 // x^a / a! for a = 0..deg (recurrence of src/_taylor.py:102-115 per axis)
 __device__ inline void pow_fact_axis(double d, int deg, double *out) {
     out[0] = 1.0;
@@ -26,7 +24,8 @@ __device__ inline void pow_axis(double d, int deg, double *out) {
 // ---- P2M: block per leaf, thread per coefficient; bodies staged in smem --
 constexpr int kP2MTile = 64;
 
-__global__ void p2m_kernel(int p, int32_t ncells, const uint8_t *__restrict__ leaf,
+__global__ void p2m_kernel(int p, const int32_t *__restrict__ cells, int32_t ncells,
+                           const uint8_t *__restrict__ leaf,
                            const int32_t *__restrict__ start, const int32_t *__restrict__ end,
                            const double *__restrict__ ctr, const double *__restrict__ xs,
                            const double *__restrict__ ys, const double *__restrict__ zs,
@@ -34,7 +33,8 @@ __global__ void p2m_kernel(int p, int32_t ncells, const uint8_t *__restrict__ le
     __shared__ double sp[kP2MTile][3][TMAX];
     __shared__ double sq[kP2MTile];
     const int nc = ncoef(p);
-    for (int c = blockIdx.x; c < ncells; c += gridDim.x) {
+    for (int ci = blockIdx.x; ci < ncells; ci += gridDim.x) {
+        const int32_t c = cells[ci];
         if (!leaf[c]) continue;
         const double cx = ctr[c * 3], cy = ctr[c * 3 + 1], cz = ctr[c * 3 + 2];
         const int32_t s = start[c], e = end[c];
@@ -126,13 +126,13 @@ __global__ void l2l_level(int p, const int32_t *__restrict__ cells, int32_t coun
 }
 
 // ---- L2P: thread per body (src/_taylor.py:243-269); f = -grad phi -------
-__global__ void l2p_kernel(int p, int64_t n, const int32_t *__restrict__ body_leaf,
+__global__ void l2p_kernel(int p, int64_t b0, int64_t n, const int32_t *__restrict__ body_leaf,
                            const double *__restrict__ ctr, const double *__restrict__ xs,
                            const double *__restrict__ ys, const double *__restrict__ zs,
                            const double *__restrict__ L, double *phi, double *fx, double *fy,
                            double *fz) {
     const int nc = ncoef(p);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+    for (int64_t i = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t c = body_leaf[i];
         double ux[TMAX], uy[TMAX], uz[TMAX];
@@ -170,8 +170,10 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
     cudaStream_t s = as_stream(stream);
     const int nc = ncoef(p);
     int blk = nc <= 32 ? 32 : (nc <= 64 ? 64 : (nc <= 128 ? 128 : (nc <= 256 ? 256 : 384)));
-    p2m_kernel<<<grid_for(ncells, 1, 148 * 32), blk, 0, s>>>(p, ncells, leaf, start, end, ctr, xs, ys, zs,
-                                                            qs, M);
+    const int32_t total = host_level_off[nlev];
+    if (total > 0)
+        p2m_kernel<<<grid_for(total, 1, 148 * 32), blk, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr,
+                                                               xs, ys, zs, qs, M);
     for (int L = nlev - 2; L >= 0; L--) {
         int32_t off = host_level_off[L], cnt = host_level_off[L + 1] - off;
         if (cnt <= 0) continue;
@@ -183,8 +185,8 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
 }
 
 int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *leaf, const double *ctr,
-                 const int32_t *cells_by_level, const int32_t *host_level_off, int nlev, int64_t n,
-                 const int32_t *body_leaf, const double *xs, const double *ys, const double *zs,
+                 const int32_t *cells_by_level, const int32_t *host_level_off, int nlev, int64_t body_lo,
+                 int64_t body_hi, const int32_t *body_leaf, const double *xs, const double *ys, const double *zs,
                  double *L, double *phi, double *fx, double *fy, double *fz, void *stream) {
     if (p < 1 || p > TMAX) { set_error("expansion order %d outside supported range 1..%d", p, TMAX); return FMM_ERR_INVALID; }
     cudaStream_t s = as_stream(stream);
@@ -195,7 +197,9 @@ int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *le
         l2l_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, parent,
                                                                   ctr, L);
     }
-    l2p_kernel<<<grid_for(n, 128), 128, 0, s>>>(p, n, body_leaf, ctr, xs, ys, zs, L, phi, fx, fy, fz);
+    if (body_hi > body_lo)
+        l2p_kernel<<<grid_for(body_hi - body_lo, 128), 128, 0, s>>>(p, body_lo, body_hi, body_leaf, ctr, xs, ys,
+                                                                    zs, L, phi, fx, fy, fz);
     FMM_CUDA_CHECK("fmm_downward");
     return FMM_OK;
 }

@@ -112,11 +112,19 @@ __global__ void plan_stats(int32_t nrows, const int32_t *__restrict__ leaf_rows,
     }
 }
 
+__global__ void leaf_in_range(int32_t ncells, const uint8_t *leaf, const int32_t *start, int32_t lo, int32_t hi,
+                              uint8_t *flag) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x)
+        flag[c] = leaf[c] && start[c] >= lo && start[c] < hi;
+}
+
 }  // namespace fmm
 
 using namespace fmm;
 
+
 extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
+                            int32_t body_lo, int32_t body_hi,
                             const int64_t *rows, const int32_t *src_sorted, const double *xs,
                             const double *ys, const double *zs, int32_t *leaf_rows, int64_t *run_off,
                             void *runs, int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows,
@@ -125,12 +133,14 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     Arena ar(ws, ws_bytes);
     int32_t *nsel = ar.take<int32_t>(1);
     int64_t *nr = ar.take<int64_t>((size_t)ncells + 1);
-    if (!nsel || !nr) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    uint8_t *flag = ar.take<uint8_t>((size_t)ncells);
+    if (!nsel || !nr || !flag) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag);
     size_t need = 0;
     cub::CountingInputIterator<int32_t> it(0);
-    cub::DeviceSelect::Flagged(nullptr, need, it, leaf, leaf_rows, nsel, ncells, s);
+    cub::DeviceSelect::Flagged(nullptr, need, it, flag, leaf_rows, nsel, ncells, s);
     if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
-    cub::DeviceSelect::Flagged(ar.rest(), need, it, leaf, leaf_rows, nsel, ncells, s);
+    cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, leaf_rows, nsel, ncells, s);
     int32_t nrows = 0;
     cudaMemcpyAsync(&nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");

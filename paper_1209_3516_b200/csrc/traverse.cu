@@ -41,7 +41,9 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                                      int64_t nfront, const int32_t *__restrict__ children,
                                      const uint8_t *__restrict__ leaf, const double *__restrict__ ctr,
                                      const double *__restrict__ bmax, const double *__restrict__ rmax,
-                                     int kind_mac, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
+                                     const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
+                                     int32_t blo, int32_t bhi, int kind_mac, double th2, int32_t *p2p_t,
+                                     int32_t *p2p_s, int64_t cap_p2p,
                                      int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l, int32_t *na,
                                      int32_t *nb, int64_t cap_next, unsigned long long *counts) {
     const int lane = threadIdx.x & 31;
@@ -59,6 +61,10 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
         if (valid) {
             a = fa[k];
             b = fb[k];
+            // multi-GPU: only targets whose body range meets [blo, bhi)
+            if (cend[a] <= blo || cstart[a] >= bhi) valid = false;
+        }
+        if (valid) {
             bool la = leaf[a], lb = leaf[b];
             if (la && lb) {
                 kind = 1;
@@ -146,12 +152,13 @@ extern "C" {
 
 int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                      const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
                       int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
                       unsigned long long *dev_counts, void *stream) {
     if (nfront <= 0) return FMM_OK;
     traverse_step_kernel<<<grid_for(nfront, 256, 148 * 16), 256, 0, as_stream(stream)>>>(
-        fa, fb, nfront, children, leaf, ctr, bmax, rmax, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
+        fa, fb, nfront, children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
         na, nb, cap_next, dev_counts);
     FMM_CUDA_CHECK("fmm_traverse_step");
     return FMM_OK;

@@ -142,15 +142,19 @@ def _grow(buf, used, need, dtype, dev):
     return nb
 
 
-def interaction_lists(tree: Tree, mac: MacConfig) -> Lists:
+def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
-    (the sets of src/traversal.py:159-262)."""
+    (the sets of src/traversal.py:159-262).
+
+    ``body_range=(lo, hi)`` keeps only pairs whose target cell holds bodies
+    in [lo, hi) (a multi-GPU rank's share); the default keeps all."""
+    blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev = tree.device
     P = _lib.ptr
     st = _lib.stream_handle()
     i32 = torch.int32
     th2 = mac.theta * mac.theta
-    key = (tree.ncells, tree.nleaves, mac.kind, th2)
+    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi)
     cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
                                                  max(4096, tree.ncells * 8)))
     p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
@@ -167,7 +171,7 @@ def interaction_lists(tree: Tree, mac: MacConfig) -> Lists:
     peak = 1
     while nfront > 0:
         _lib.call("fmm_traverse_step", P(fa), P(fb), nfront, P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr),
-                  P(tree.d_bmax), P(tree.d_rmax), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
+                  P(tree.d_bmax), P(tree.d_rmax), P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
                   cap_m2l, P(na), P(nb), cap_next, P(counts), st)
         c_p2p, c_m2l, c_next = counts.tolist()
         if c_p2p > cap_p2p or c_m2l > cap_m2l or c_next > cap_next:
@@ -216,7 +220,7 @@ def interaction_lists(tree: Tree, mac: MacConfig) -> Lists:
     while True:
         runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
         try:
-            _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), P(p2p_rows),
+            _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
                       P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(leaf_rows), P(run_off), P(runs),
                       cap_runs, C.byref(nruns), C.byref(nrows), P(dev_stats), wsp, wsb, st)
             break
@@ -236,10 +240,14 @@ def run_m2l(tree: Tree, lists: Lists, p: int) -> None:
 def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, safe: bool = False,
             flag=None) -> None:
     P = _lib.ptr
-    prec = _lib.PREC_FP32 if precision == "fp32" else _lib.PREC_FP64
+    if precision == "fp32":
+        # float32 cannot hold these float64 inputs: anchor offsets per row
+        prec = _lib.PREC_FP32 if tree.fp32_exact else _lib.PREC_FP32_ANCHORED
+    else:
+        prec = _lib.PREC_FP64
     _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), lists.nrows, P(lists.leaf_rows), P(tree.d_start),
               P(tree.d_end), P(lists.run_off), P(lists.runs), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_q),
-              P(tree.d_b32), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag),
+              P(tree.d_b32), P(tree.d_b32lo), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag),
               _lib.stream_handle())
 
 

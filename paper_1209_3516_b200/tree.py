@@ -284,8 +284,10 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         _lib.call("fmm_sort_pairs_u64", P(keys), P(iota), P(skeys), P(perm), n, 63, wsp, wsb, st)
         xs, ys, zs, qs = (torch.empty_like(x64) for _ in range(4))
         b32 = torch.empty((n, 4), dtype=torch.float32, device=dev)
+        b32lo = torch.empty((n, 4), dtype=torch.float32, device=dev)
+        inexact = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.call("fmm_permute_bodies", P(perm), P(x64), P(y64), P(z64), P(q64), n, P(xs), P(ys), P(zs),
-                  P(qs), P(b32), st)
+                  P(qs), P(b32), P(b32lo), P(inexact), st)
         del x64, y64, z64, q64, keys, iota
 
         # level-synchronous carve (BFS ids), grow-and-retry on capacity
@@ -343,12 +345,12 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         _lib.call("fmm_cell_geometry", ncells, P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
                   P(xs), P(ys), P(zs), P(root), P(lo), P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
         zeros = [torch.zeros(n, dtype=f64, device=dev) for _ in range(4)]
-        torch.cuda.current_stream(dev).synchronize()
+        fp32_exact = int(inexact.item()) == 0  # synchronises the stream
     tree = Tree(
         device=dev, n=n, ncrit=ncrit, shape=shape, center_mode=center_mode,
         allow_oversized_leaves=bool(allow_oversized_leaves), _ncells=ncells, _nleaves=nleaves,
         level_off=level_off, d_root=root, d_keys=skeys, d_perm=perm,
-        d_x=xs, d_y=ys, d_z=zs, d_q=qs, d_b32=b32,
+        d_x=xs, d_y=ys, d_z=zs, d_q=qs, d_b32=b32, d_b32lo=b32lo, fp32_exact=fp32_exact,
         d_phi=zeros[0], d_fx=zeros[1], d_fy=zeros[2], d_fz=zeros[3],
         d_children=cc["children"], d_parent=cc["parent"], d_level=cc["level"], d_key=cc["key"],
         d_start=cc["start"], d_end=cc["end"], d_sub_end=cc["sub_end"], d_leaf=cc["leaf"],
@@ -383,17 +385,20 @@ def upward_pass(tree: Tree, p: int, stats: KernelStats | None = None) -> None:
         stats.m2m_calls += tree.ncells - 1
 
 
-def downward_pass(tree: Tree, stats: KernelStats | None = None, *, sync: bool = True) -> None:
+def downward_pass(tree: Tree, stats: KernelStats | None = None, *, sync: bool = True,
+                  body_range: tuple[int, int] | None = None) -> None:
     """L2L down the tree, L2P into the leaf bodies (src/tree.py:475-488).
 
-    Requires local expansions populated by a traversal (``tree.local``)."""
+    Requires local expansions populated by a traversal (``tree.local``).
+    ``body_range=(lo, hi)`` restricts L2P to those bodies (multi-GPU)."""
+    blo, bhi = body_range if body_range is not None else (0, tree.n)
     if tree._L is None or tree.p is None:
         raise ValueError("local expansions not populated; run a traversal first")
     dev = tree.device
     with torch.cuda.device(dev):
         P = _lib.ptr
         _lib.call("fmm_downward", tree.p, tree.ncells, P(tree.d_parent), P(tree.d_leaf), P(tree.d_ctr),
-                  P(tree.d_cells_by_level), tree.level_off_c(), len(tree.level_off) - 1, tree.n,
+                  P(tree.d_cells_by_level), tree.level_off_c(), len(tree.level_off) - 1, blo, bhi,
                   P(tree.d_body_leaf), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree._L), P(tree.d_phi),
                   P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), _lib.stream_handle())
         if sync:

@@ -138,3 +138,56 @@ def test_out_of_scope_paths_raise():
     cfg = fb.EvalConfig(strategy="treecode")
     with pytest.raises(NotImplementedError):
         fb.evaluate_on_tree(object(), cfg)
+
+
+def _static_len(node, env):
+    """Length of a starred argument when it is statically knowable."""
+    import ast
+    if isinstance(node, (ast.Tuple, ast.List)):
+        return len(node.elts)
+    if isinstance(node, ast.GeneratorExp) and len(node.generators) == 1:
+        it = node.generators[0].iter
+        if isinstance(it, (ast.Tuple, ast.List)):
+            return len(it.elts)
+        if isinstance(it, ast.Name) and it.id in env:
+            return env[it.id]
+    return None
+
+
+def test_call_sites_match_abi_arity():
+    """Every _lib.call("fmm_*", ...) in the package passes exactly the
+    arguments the C ABI declares (catches host/ABI drift without a GPU)."""
+    import ast
+    pkg = os.path.join(ROOT, "paper_1209_3516_b200")
+    checked = 0
+    for fn in glob.glob(os.path.join(pkg, "*.py")) + [os.path.join(ROOT, "bench.py")]:
+        tree = ast.parse(open(fn).read())
+        env = {}
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Assign) and len(node.targets) == 1 and isinstance(node.targets[0], ast.Name):
+                if isinstance(node.value, (ast.Tuple, ast.List)):
+                    env[node.targets[0].id] = len(node.value.elts)
+                elif isinstance(node.value, ast.ListComp) and isinstance(node.value.generators[0].iter, ast.Call):
+                    c = node.value.generators[0].iter
+                    if getattr(c.func, "id", "") == "range" and c.args and isinstance(c.args[0], ast.Constant):
+                        env[node.targets[0].id] = c.args[0].value
+        for node in ast.walk(tree):
+            if not (isinstance(node, ast.Call) and node.args and isinstance(node.args[0], ast.Constant)
+                    and isinstance(node.args[0].value, str) and node.args[0].value.startswith("fmm_")):
+                continue
+            name = node.args[0].value
+            n = 0
+            for a in node.args[1:]:
+                if isinstance(a, ast.Starred):
+                    k = _static_len(a.value, env)
+                    if k is None:
+                        n = None
+                        break
+                    n += k
+                else:
+                    n += 1
+            if n is None:
+                continue
+            assert n == len(_lib.SIGNATURES[name]), (fn, node.lineno, name, n, len(_lib.SIGNATURES[name]))
+            checked += 1
+    assert checked >= 15
