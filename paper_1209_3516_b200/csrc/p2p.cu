@@ -94,6 +94,14 @@ __device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
 __device__ __forceinline__ void f2_unpack(f2_t v, float &lo, float &hi) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
+// Re-materialise a packed value through a real FADD2 (+0): the result is
+// born in an aligned register pair, so ptxas stops re-pairing its halves
+// with two MOVs before every packed use.
+__device__ __forceinline__ f2_t f2_fresh(f2_t a) {
+    f2_t r, z = 0ull;
+    asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(z));
+    return r;
+}
 __device__ __forceinline__ f2_t f2_sub_s(f2_t a, float s) {  // a - {s, s}
     f2_t r, b = f2_pack(s, s);
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -249,9 +257,9 @@ __device__ __forceinline__ void p2p_f32_block(int32_t i0, int32_t ilast, int64_t
     for (int v = 0; v < KB / 2; v++) {
         const float4 e = load_body<ANCHOR>(b, blo, an, min(i0 + 2 * v, ilast));
         const float4 o = load_body<ANCHOR>(b, blo, an, min(i0 + 2 * v + 1, ilast));
-        tx[v] = f2_pack(e.x, o.x);
-        ty[v] = f2_pack(e.y, o.y);
-        tz[v] = f2_pack(e.z, o.z);
+        tx[v] = f2_fresh(f2_pack(e.x, o.x));
+        ty[v] = f2_fresh(f2_pack(e.y, o.y));
+        tz[v] = f2_fresh(f2_pack(e.z, o.z));
         ap[v] = ax[v] = ay[v] = az[v] = 0ull;
     }
     const int step = 32 * nparts;
@@ -313,9 +321,9 @@ __device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, 
     for (int v = 0; v < KB / 2; v++) {
         const float4 e = __ldg(&b[min(i0 + 2 * v, ilast)]);
         const float4 o = __ldg(&b[min(i0 + 2 * v + 1, ilast)]);
-        tx[v] = f2_pack(e.x, o.x);
-        ty[v] = f2_pack(e.y, o.y);
-        tz[v] = f2_pack(e.z, o.z);
+        tx[v] = f2_fresh(f2_pack(e.x, o.x));
+        ty[v] = f2_fresh(f2_pack(e.y, o.y));
+        tz[v] = f2_fresh(f2_pack(e.z, o.z));
         ap[v] = ax[v] = ay[v] = az[v] = 0ull;
     }
     const int step = 32 * nparts;
@@ -392,13 +400,30 @@ __device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, 
 
 // Target blocks of a leaf: cnt / 8 blocks of 8, then the remainder as one
 // block of 4 (r <= 4) or 8 -- at most 3 padded slots per leaf.
+__device__ __forceinline__ int gcd_small(int a, int b) {
+    while (b) {
+        const int t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// Work units of a row: every target block's source stream is split into P
+// interleaved parts with P = W / gcd(nblk, W), so the nblk * P units divide
+// evenly over the W warps of the CTA (no warp idles at the row barrier).
+// Partial sums of the parts are folded through shared memory in a fixed
+// order (deterministic).  Leaves too large for the fold buffer (oversized
+// leaves) fall back to P = 1 with direct stores.
+constexpr int kMaxUnits = 32;
+
 template <bool SAFE, bool ANCHOR>
 __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
     int32_t nrows, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const float4 *__restrict__ b, const float4 *__restrict__ blo, double *phi, double *fx, double *fy,
     double *fz, int *flag) {
-    __shared__ float red[kP2PWarps][4][32];
+    __shared__ float red[kMaxUnits][4][8];
     __shared__ float4 rings[kP2PWarps][kStages * 32];
     __shared__ int2 srun[kMaxRuns];
     __shared__ int32_t stotal;
@@ -410,7 +435,10 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
         const int rem = cnt & 7;
         const int nblk = (cnt >> 3) + (rem ? 1 : 0);
         const bool small_last = rem != 0 && rem <= 4;
-        const int nparts = nblk >= kP2PWarps ? 1 : kP2PWarps / nblk;
+        int P = kP2PWarps / gcd_small(nblk, kP2PWarps);
+        const bool fold = nblk * P <= kMaxUnits;
+        if (!fold) P = 1;
+        const int nunits = nblk * P;
         const int64_t r0 = run_off[row], r1 = run_off[row + 1];
         Anchor an{};
         if (ANCHOR) {
@@ -434,49 +462,34 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
             __syncthreads();
         }
         const int32_t total = streamed ? stotal : 0;
-        const int rounds = nparts > 1 ? 1 : (nblk + kP2PWarps - 1) / kP2PWarps;
-        for (int rd = 0; rd < rounds; rd++) {
-            const int tb = nparts > 1 ? w % nblk : rd * kP2PWarps + w;
-            const int part = nparts > 1 ? w / nblk : 0;
-            const bool active = nparts > 1 ? part < nparts : tb < nblk;
-            float rp = 0.f, rx = 0.f, ry = 0.f, rz = 0.f;
+        for (int u = w; u < nunits; u += kP2PWarps) {
+            const int tb = u / P, part = u % P;
             const int32_t i0 = ts + tb * 8;
-            if (active && streamed) {
-                if (tb == nblk - 1 && small_last)
-                    p2p_f32_stream_block<4>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, nparts, lane, b,
-                                            ring, rp, rx, ry, rz);
+            float rp = 0.f, rx = 0.f, ry = 0.f, rz = 0.f;
+            const bool k4 = tb == nblk - 1 && small_last;
+            if (streamed) {
+                if (k4)
+                    p2p_f32_stream_block<4>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, P, lane, b, ring,
+                                            rp, rx, ry, rz);
                 else
-                    p2p_f32_stream_block<8>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, nparts, lane, b,
-                                            ring, rp, rx, ry, rz);
-            } else if (active) {
-                if (tb == nblk - 1 && small_last)
-                    p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, nparts, lane, runs, b, blo, an,
-                                                   ring, rp, rx, ry, rz);
+                    p2p_f32_stream_block<8>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, P, lane, b, ring,
+                                            rp, rx, ry, rz);
+            } else {
+                if (k4)
+                    p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring,
+                                                   rp, rx, ry, rz);
                 else
-                    p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, nparts, lane, runs, b, blo, an,
-                                                   ring, rp, rx, ry, rz);
+                    p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring,
+                                                   rp, rx, ry, rz);
             }
-            if (nparts > 1) {
-                if (active && lane < 8) {
-                    red[w][0][lane] = rp;
-                    red[w][1][lane] = rx;
-                    red[w][2][lane] = ry;
-                    red[w][3][lane] = rz;
+            if (fold) {
+                if (lane < 8) {
+                    red[u][0][lane] = rp;
+                    red[u][1][lane] = rx;
+                    red[u][2][lane] = ry;
+                    red[u][3][lane] = rz;
                 }
-                __syncthreads();
-                if (active && part == 0 && lane < 8) {
-                    rp = rx = ry = rz = 0.f;
-                    for (int q = 0; q < nparts; q++) {  // fixed order: deterministic
-                        const int ww = q * nblk + tb;
-                        rp += red[ww][0][lane];
-                        rx += red[ww][1][lane];
-                        ry += red[ww][2][lane];
-                        rz += red[ww][3][lane];
-                    }
-                }
-                __syncthreads();
-            }
-            if (active && part == 0 && lane < 8 && tb * 8 + lane < cnt) {
+            } else if (lane < 8 && tb * 8 + lane < cnt) {
                 const int32_t i = i0 + lane;
                 phi[i] = (double)rp;
                 fx[i] = (double)rx;
@@ -485,7 +498,27 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
                 if (!(isfinite(rp) && isfinite(rx) && isfinite(ry) && isfinite(rz))) atomicOr(flag, 1);
             }
         }
-        if (streamed) __syncthreads();  // srun is rewritten by the next row
+        __syncthreads();  // partial sums complete; srun may be rewritten after this
+        if (fold) {
+            for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+                const int tb = k >> 3, l = k & 7;
+                float p_ = 0.f, x_ = 0.f, y_ = 0.f, z_ = 0.f;
+                for (int q = 0; q < P; q++) {  // fixed order: deterministic
+                    const int uu = tb * P + q;
+                    p_ += red[uu][0][l];
+                    x_ += red[uu][1][l];
+                    y_ += red[uu][2][l];
+                    z_ += red[uu][3][l];
+                }
+                const int32_t i = ts + k;
+                phi[i] = (double)p_;
+                fx[i] = (double)x_;
+                fy[i] = (double)y_;
+                fz[i] = (double)z_;
+                if (!(isfinite(p_) && isfinite(x_) && isfinite(y_) && isfinite(z_))) atomicOr(flag, 1);
+            }
+            __syncthreads();  // red is rewritten by the next row
+        }
     }
 }
 
