@@ -53,7 +53,7 @@ TRAFFIC_PATH = os.path.join(ROOT, "profiles", "p2p_traffic.json")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(workloads.CONFIGS))
@@ -98,7 +98,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -256,14 +256,15 @@ def run_ours(args):
             rep = fb.evaluate_on_tree(tree, cfg)
         return tree, rep
 
+    clocks = Clocks(local)
+    clocks.start()  # sampled through warm-up and the timed region (both under load)
     for _ in range(max(3, args.warmup)):
         tree, rep = step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = Clocks(local)
-    clocks.start()
     times, p2p_times, reps = [], [], []
+    launches0 = _lib.launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -278,6 +279,7 @@ def run_ours(args):
         p2p_times.append(rep.stats.times.get("p2p", float("nan")))
         reps.append(rep)
     torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -293,8 +295,11 @@ def run_ours(args):
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e and world == 1:
+        # host arrays in the configuration's precision (float32 for C2-C5):
+        # ParticleSet keeps them as given and the device upcasts them
         hx, hy, hz = (np.ascontiguousarray(pos[:, k]) for k in range(3))
         hq = np.ascontiguousarray(q)
+        h2d = sum(a.nbytes for a in (hx, hy, hz, hq))
 
         def e2e_step():
             ps = fb.ParticleSet(hx, hy, hz, hq)
@@ -313,9 +318,9 @@ def run_ours(args):
             res = e2e_step()
             et.append(time.perf_counter() - t0)
         e2e = {"value": n / float(np.median(et)), "unit": "particles/s",
-               "h2d_bytes_per_step": 4 * 8 * n, "d2h_bytes_per_step": 8 * 8 * n,
-               "note": "ParticleSet(numpy f64 upcast) -> build_tree -> evaluate_on_tree -> "
-                       "results_in_input_order(); wall clock per step, median"}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * 8 * n,
+               "note": "ParticleSet(host numpy) -> build_tree -> evaluate_on_tree -> results_in_input_order() "
+                       "(phi, f back in input order as float64); wall clock per step, median"}
         del res
 
     peak, peaks = fp32_peak(torch, _lib.call, sh)
@@ -353,7 +358,8 @@ def run_ours(args):
                                     "no FP32 figure" % ", ".join(f"{k} {v:.1f}" for k, v in peaks.items()),
                      "kernel": "p2p_f32_kernel", "flop_model": "20 flops/pair (src/_taylor.py:314)"},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
-        "gpu_launches": None,
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
     }
     if rank == 0:
         print(json.dumps(line))

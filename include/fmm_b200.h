@@ -58,6 +58,9 @@ extern "C" {
 FMM_API int fmm_abi_version(void);
 /* Message of the last error on the calling thread ("" when none). */
 FMM_API const char *fmm_last_error(void);
+/* Kernels launched by this library so far (its own kernels; CUB's internal
+ * sort/scan kernels are not counted). */
+FMM_API long long fmm_launch_count(void);
 /* Number of SMs of the current device (grid sizing). */
 FMM_API int fmm_device_sm_count(void);
 
@@ -142,14 +145,18 @@ FMM_API int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uin
 
 /* ---- dual traversal (src/traversal.py:144-262, directed, MAC "fmm") ---- */
 
-/* One breadth-first step over frontier pairs (fa[k], fb[k]).  Appends P2P
- * pairs, M2L pairs and the next frontier; counters live in dev_counts[3]
- * = {n_p2p, n_m2l, n_next} and keep counting past capacity.
+/* One breadth-first step over frontier pairs (fa[k], fb[k]), each a pair
+ * known to split (classify_self = 1 classifies the frontier pairs
+ * themselves instead -- used for the root pair).  The children pairs are
+ * classified on the spot: P2P and M2L pairs are appended to their lists,
+ * pairs that split again to the next frontier; counters live in
+ * dev_counts[3] = {n_p2p, n_m2l, n_next} and keep counting past capacity.
  * kind: MAC kind code (0 bh, 1 bmax, 2 fmm; src/mac.py:21-22); th2 = theta*theta
  * computed by the caller exactly as the reference.  Pairs whose target
  * cell's body range misses [body_lo, body_hi) are dropped (a multi-GPU rank
  * keeps only its own targets; [0, n) keeps everything). */
-FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, const int32_t *children,
+FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int classify_self,
+                      const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
                       const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
                       int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
@@ -191,6 +198,11 @@ FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const
             const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
             const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
             const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);
+
+/* Scatter four Morton-ordered arrays back to input order:
+ * b_k[perm[i]] = a_k[i] (Tree.results_in_input_order, src/tree.py:344-348). */
+FMM_API int fmm_unpermute(const int32_t *perm, int64_t n, const double *a0, const double *a1, const double *a2,
+                  const double *a3, double *b0, double *b1, double *b2, double *b3, void *stream);
 
 /* Final combine: out = p2p + far (phi, f) for all n bodies. */
 FMM_API int fmm_combine(int64_t n, const double *a_phi, const double *a_fx, const double *a_fy,

@@ -31,6 +31,7 @@ SZ = C.c_size_t
 SIGNATURES = {
     "fmm_abi_version": [],
     "fmm_last_error": [],
+    "fmm_launch_count": [],
     "fmm_device_sm_count": [],
     "fmm_workspace_bytes": [I64, P],
     "fmm_ingest_bounds": [P, P, P, P, INT, I64, P, P, P, P, P, P, SZ, P],
@@ -42,11 +43,12 @@ SIGNATURES = {
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
     "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],
-    "fmm_traverse_step": [P, P, I64, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64, P, P, I64, P, P],
+    "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64, P, P, I64, P, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
     "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, I64, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "fmm_unpermute": [P, I64, P, P, P, P, P, P, P, P, P],
     "fmm_combine": [I64, P, P, P, P, P, P, P, P, P],
     "fmm_direct": [I64, P, P, P, P, I64, P, P, P, P, P, P],
     "fmm_ffma_probe": [INT, INT, INT, P, P, P],
@@ -79,11 +81,16 @@ def load():
             for name, argt in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.argtypes = argt
-                fn.restype = C.c_char_p if name == "fmm_last_error" else C.c_int
+                fn.restype = {"fmm_last_error": C.c_char_p, "fmm_launch_count": C.c_longlong}.get(name, C.c_int)
             if lib.fmm_abi_version() != 1:
                 raise RuntimeError("libfmm_b200.so ABI mismatch")
             _lib = lib
     return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libfmm_b200.so so far (its own, not CUB's)."""
+    return int(load().fmm_launch_count())
 
 
 def exported_symbols():
@@ -129,7 +136,7 @@ def workspace(items: int, device) -> tuple[int, int]:
     """(pointer, bytes) of a scratch buffer valid for ``items`` elements."""
     need = C.c_size_t(0)
     call("fmm_workspace_bytes", int(max(items, 1)), C.byref(need))
-    key = torch.device(device).index or 0
+    key = (torch.device(device).index or 0, threading.get_ident())  # per thread: calls may overlap
     buf = _ws.get(key)
     if buf is None or buf.numel() < need.value:
         _ws[key] = None

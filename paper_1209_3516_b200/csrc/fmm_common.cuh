@@ -77,6 +77,10 @@ __host__ __device__ inline uint64_t compact21(uint64_t v) {
     return v;
 }
 
+// Launch accounting: every kernel launch site of the library calls this
+// (CUB's internal kernels are not counted); read by fmm_launch_count().
+void note_launch();
+
 // Error plumbing ----------------------------------------------------------
 void set_error(const char *fmt, ...);
 int cuda_status(const char *where);

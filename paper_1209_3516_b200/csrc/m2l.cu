@@ -217,14 +217,14 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
     cudaStream_t s = as_stream(stream);
     const int grid = grid_for((int64_t)ncells * 32, 128, 148 * 16);
     switch (p) {
-        case 1: m2l_reg<1><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); break;
-        case 2: m2l_reg<2><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); break;
-        case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); break;
-        case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); break;
-        case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); break;
+        case 1: m2l_reg<1><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
+        case 2: m2l_reg<2><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
+        case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
+        case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
+        case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
         default:
             m2l_warp<<<grid_for((int64_t)ncells * 32, kM2LWarps * 32, 148 * 16), kM2LWarps * 32, 0, s>>>(
-                p, ncells, rows, src, ctr, M, L);
+                p, ncells, rows, src, ctr, M, L); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_m2l_csr");
     return FMM_OK;

@@ -647,11 +647,11 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, co
                          : (safe ? p2p_f32_kernel<true, false> : p2p_f32_kernel<false, false>);
         kern<<<grid, kP2PWarps * 32, 0, s>>>(nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
                                              (const float4 *)b32, (const float4 *)b32lo, phi, fx, fy, fz,
-                                             dev_flag);
+                                             dev_flag); fmm::note_launch();
     } else if (precision == FMM_PREC_FP64) {
         p2p_f64_kernel<4><<<grid, kP2PWarps * 32, 0, s>>>(nrows, leaf_rows, start, end, run_off,
                                                           (const int4 *)runs, xs, ys, zs, qs, use_rsqrt, phi,
-                                                          fx, fy, fz);
+                                                          fx, fy, fz); fmm::note_launch();
     } else {
         set_error("bad precision %d", precision);
         return FMM_ERR_INVALID;

@@ -173,12 +173,12 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
     const int32_t total = host_level_off[nlev];
     if (total > 0)
         p2m_kernel<<<grid_for(total, 1, 148 * 32), blk, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr,
-                                                               xs, ys, zs, qs, M);
+                                                               xs, ys, zs, qs, M); fmm::note_launch();
     for (int L = nlev - 2; L >= 0; L--) {
         int32_t off = host_level_off[L], cnt = host_level_off[L + 1] - off;
         if (cnt <= 0) continue;
         m2m_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, leaf,
-                                                                  children, ctr, M);
+                                                                  children, ctr, M); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_upward");
     return FMM_OK;
@@ -195,11 +195,11 @@ int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *le
         int32_t off = host_level_off[Lv], cnt = host_level_off[Lv + 1] - off;
         if (cnt <= 0) continue;
         l2l_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, parent,
-                                                                  ctr, L);
+                                                                  ctr, L); fmm::note_launch();
     }
     if (body_hi > body_lo)
         l2p_kernel<<<grid_for(body_hi - body_lo, 128), 128, 0, s>>>(p, body_lo, body_hi, body_leaf, ctr, xs, ys,
-                                                                    zs, L, phi, fx, fy, fz);
+                                                                    zs, L, phi, fx, fy, fz); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_downward");
     return FMM_OK;
 }

@@ -135,7 +135,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     int64_t *nr = ar.take<int64_t>((size_t)ncells + 1);
     uint8_t *flag = ar.take<uint8_t>((size_t)ncells);
     if (!nsel || !nr || !flag) { set_error("workspace too small"); return FMM_ERR_INVALID; }
-    leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag);
+    leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag); fmm::note_launch();
     size_t need = 0;
     cub::CountingInputIterator<int32_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, need, it, flag, leaf_rows, nsel, ncells, s);
@@ -146,7 +146,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
     *host_nleaf_rows = nrows;
     const int g = grid_for((int64_t)nrows * 32, 256, 148 * 16);
-    plan_count<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, nr);
+    plan_count<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, nr); fmm::note_launch();
     need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, nrows + 1, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
@@ -156,10 +156,10 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
     *host_nruns = total;
     if (total > cap_runs) { set_error("run capacity %lld < %lld", (long long)cap_runs, (long long)total); return FMM_ERR_CAPACITY; }
-    plan_write<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs);
+    plan_write<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs); fmm::note_launch();
     if (dev_stats) {
         cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
-        plan_stats<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, dev_stats);
+        plan_stats<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, dev_stats); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_p2p_plan");
     return FMM_OK;

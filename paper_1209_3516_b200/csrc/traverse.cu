@@ -37,8 +37,31 @@ __device__ inline unsigned long long warp_reserve(unsigned long long *counter, i
     return base;
 }
 
+// Fate of a pair (src/traversal.py:185-211): 1 = P2P (both leaves, tested
+// before the MAC), 2 = M2L (MAC accepted), 3 = split.
+__device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const uint8_t *__restrict__ leaf,
+                                         const double *__restrict__ ctr, const double *__restrict__ bmax,
+                                         const double *__restrict__ rmax, int kind_mac, double th2) {
+    if (leaf[a] && leaf[b]) return 1;
+    const double dx = ctr[a * 3] - ctr[b * 3];
+    const double dy = ctr[a * 3 + 1] - ctr[b * 3 + 1];
+    const double dz = ctr[a * 3 + 2] - ctr[b * 3 + 2];
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    if (r2 != 0.0) {
+        // src/traversal.py:144-156: 0 = bh, 1 = bmax, 2 = fmm
+        const double s = kind_mac == 2 ? bmax[a] + bmax[b] : (kind_mac == 1 ? bmax[b] : 2.0 * rmax[b]);
+        if (s * s < th2 * r2) return 2;
+    }
+    return 3;
+}
+
+// One breadth-first step.  Every frontier pair is a pair already known to
+// split; its children pairs are classified right here, so P2P and M2L
+// pairs are emitted directly and only pairs that split again reach the
+// next frontier (the root pair (0, 0) is classified by the first step,
+// which the host launches with `classify_self = 1`).
 __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
-                                     int64_t nfront, const int32_t *__restrict__ children,
+                                     int64_t nfront, int classify_self, const int32_t *__restrict__ children,
                                      const uint8_t *__restrict__ leaf, const double *__restrict__ ctr,
                                      const double *__restrict__ bmax, const double *__restrict__ rmax,
                                      const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
@@ -51,65 +74,60 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
     // iterate in warp-uniform trip counts so the shuffles see full warps
     const int64_t nround = (nfront + stride - 1) / stride;
     for (int64_t r = 0; r < nround; r++) {
-        int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-        bool valid = k < nfront;
-        int32_t a = 0, b = 0;
-        int kind = 0;  // 0 none, 1 p2p, 2 m2l, 3 expand
-        int nkids = 0;
-        int32_t kids[8];
-        bool open_a = false;
-        if (valid) {
-            a = fa[k];
-            b = fb[k];
-            // multi-GPU: only targets whose body range meets [blo, bhi)
-            if (cend[a] <= blo || cstart[a] >= bhi) valid = false;
-        }
-        if (valid) {
-            bool la = leaf[a], lb = leaf[b];
-            if (la && lb) {
-                kind = 1;
+        const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        int32_t ca[8], cb[8];
+        int fate[8];
+        int n = 0;
+        if (k < nfront) {
+            const int32_t a = fa[k], b = fb[k];
+            if (classify_self) {
+                ca[0] = a;
+                cb[0] = b;
+                n = 1;
             } else {
-                double dx = ctr[a * 3] - ctr[b * 3];
-                double dy = ctr[a * 3 + 1] - ctr[b * 3 + 1];
-                double dz = ctr[a * 3 + 2] - ctr[b * 3 + 2];
-                double r2 = dx * dx + dy * dy + dz * dz;
-                bool ok = false;
-                if (r2 != 0.0) {
-                    // src/traversal.py:144-156: 0 = bh, 1 = bmax, 2 = fmm
-                    double s = kind_mac == 2 ? bmax[a] + bmax[b] : (kind_mac == 1 ? bmax[b] : 2.0 * rmax[b]);
-                    ok = s * s < th2 * r2;
-                }
-                if (ok) {
-                    kind = 2;
-                } else {
-                    kind = 3;
-                    open_a = la ? false : (lb ? true : (rmax[a] >= rmax[b]));
-                    int32_t who = open_a ? a : b;
+                const bool la = leaf[a], lb = leaf[b];
+                const bool open_a = la ? false : (lb ? true : (rmax[a] >= rmax[b]));
+                const int32_t who = open_a ? a : b;
 #pragma unroll
-                    for (int o = 0; o < 8; o++) {
-                        int32_t ch = children[who * 8 + o];
-                        if (ch >= 0) kids[nkids++] = ch;
+                for (int o = 0; o < 8; o++) {
+                    const int32_t ch = children[who * 8 + o];
+                    if (ch >= 0) {
+                        ca[n] = open_a ? ch : a;
+                        cb[n] = open_a ? b : ch;
+                        n++;
                     }
                 }
             }
         }
-        int off;
-        unsigned long long base = warp_reserve(&counts[0], kind == 1 ? 1 : 0, lane, &off);
-        if (kind == 1) {
-            unsigned long long at = base + off;
-            if (at < (unsigned long long)cap_p2p) { p2p_t[at] = a; p2p_s[at] = b; }
+        int np = 0, nm = 0, nn = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            fate[q] = 0;
+            if (q < n) {
+                // multi-GPU: only targets whose body range meets [blo, bhi)
+                if (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi) continue;
+                fate[q] = pair_fate(ca[q], cb[q], leaf, ctr, bmax, rmax, kind_mac, th2);
+                np += fate[q] == 1;
+                nm += fate[q] == 2;
+                nn += fate[q] == 3;
+            }
         }
-        base = warp_reserve(&counts[1], kind == 2 ? 1 : 0, lane, &off);
-        if (kind == 2) {
-            unsigned long long at = base + off;
-            if (at < (unsigned long long)cap_m2l) { m2l_t[at] = a; m2l_s[at] = b; }
-        }
-        base = warp_reserve(&counts[2], nkids, lane, &off);
-        for (int q = 0; q < nkids; q++) {
-            unsigned long long at = base + off + q;
-            if (at < (unsigned long long)cap_next) {
-                na[at] = open_a ? kids[q] : a;
-                nb[at] = open_a ? b : kids[q];
+        int op, om, on;
+        const unsigned long long bp = warp_reserve(&counts[0], np, lane, &op);
+        const unsigned long long bm = warp_reserve(&counts[1], nm, lane, &om);
+        const unsigned long long bn = warp_reserve(&counts[2], nn, lane, &on);
+        unsigned long long ip = bp + op, im = bm + om, in = bn + on;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (fate[q] == 1) {
+                if (ip < (unsigned long long)cap_p2p) { p2p_t[ip] = ca[q]; p2p_s[ip] = cb[q]; }
+                ip++;
+            } else if (fate[q] == 2) {
+                if (im < (unsigned long long)cap_m2l) { m2l_t[im] = ca[q]; m2l_s[im] = cb[q]; }
+                im++;
+            } else if (fate[q] == 3) {
+                if (in < (unsigned long long)cap_next) { na[in] = ca[q]; nb[in] = cb[q]; }
+                in++;
             }
         }
     }
@@ -138,6 +156,28 @@ __global__ void unpack_rows(const uint64_t *keys, int64_t n, int sbits, int32_t 
     }
 }
 
+// 32-bit variant when (target, source) fit in 32 bits: half the sort traffic
+__global__ void pack_pairs32(const int32_t *t, const int32_t *s, int64_t n, int sbits, uint32_t *keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = ((uint32_t)t[i] << sbits) | (uint32_t)s[i];
+}
+
+__global__ void unpack_rows32(const uint32_t *keys, int64_t n, int sbits, int32_t ncells, int32_t *src,
+                              int64_t *rows) {
+    const uint32_t mask = (1u << sbits) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        src[i] = (int32_t)(k & mask);
+        const int32_t t = (int32_t)(k >> sbits);
+        const int32_t tprev = i > 0 ? (int32_t)(keys[i - 1] >> sbits) : -1;
+        for (int32_t c = tprev + 1; c <= t; c++) rows[c] = i;
+        if (i == n - 1)
+            for (int32_t c = t + 1; c <= ncells; c++) rows[c] = n;
+    }
+}
+
 __global__ void fill_i64(int64_t *a, int64_t n, int64_t v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -150,7 +190,8 @@ using namespace fmm;
 
 extern "C" {
 
-int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, const int32_t *children,
+int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int classify_self,
+                      const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
                       const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
                       int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
@@ -158,8 +199,8 @@ int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, cons
                       unsigned long long *dev_counts, void *stream) {
     if (nfront <= 0) return FMM_OK;
     traverse_step_kernel<<<grid_for(nfront, 256, 148 * 16), 256, 0, as_stream(stream)>>>(
-        fa, fb, nfront, children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
-        na, nb, cap_next, dev_counts);
+        fa, fb, nfront, classify_self, children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
+        na, nb, cap_next, dev_counts); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_traverse_step");
     return FMM_OK;
 }
@@ -168,22 +209,35 @@ int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs, int32_t
                      int32_t *src_sorted, int64_t *rows, void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t st = as_stream(stream);
     if (npairs == 0) {
-        fill_i64<<<grid_for(ncells + 1, 256), 256, 0, st>>>(rows, ncells + 1, 0);
+        fill_i64<<<grid_for(ncells + 1, 256), 256, 0, st>>>(rows, ncells + 1, 0); fmm::note_launch();
         FMM_CUDA_CHECK("fmm_pairs_to_csr");
         return FMM_OK;
     }
     int sbits = 1;
     while ((1ll << sbits) < (int64_t)ncells) sbits++;
     Arena ar(ws, ws_bytes);
+    if (2 * sbits <= 32) {
+        uint32_t *k0 = ar.take<uint32_t>(npairs);
+        uint32_t *k1 = ar.take<uint32_t>(npairs);
+        if (!k0 || !k1) { set_error("workspace too small for %lld pairs", (long long)npairs); return FMM_ERR_INVALID; }
+        pack_pairs32<<<grid_for(npairs, 256), 256, 0, st>>>(t, s, npairs, sbits, k0); fmm::note_launch();
+        size_t need = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, need, k0, k1, npairs, 0, 2 * sbits, st);
+        if (need > ar.left()) { set_error("sort workspace"); return FMM_ERR_INVALID; }
+        cub::DeviceRadixSort::SortKeys(ar.rest(), need, k0, k1, npairs, 0, 2 * sbits, st);
+        unpack_rows32<<<grid_for(npairs, 256), 256, 0, st>>>(k1, npairs, sbits, ncells, src_sorted, rows); fmm::note_launch();
+        FMM_CUDA_CHECK("fmm_pairs_to_csr");
+        return FMM_OK;
+    }
     uint64_t *k0 = ar.take<uint64_t>(npairs);
     uint64_t *k1 = ar.take<uint64_t>(npairs);
     if (!k0 || !k1) { set_error("workspace too small for %lld pairs", (long long)npairs); return FMM_ERR_INVALID; }
-    pack_pairs<<<grid_for(npairs, 256), 256, 0, st>>>(t, s, npairs, sbits, k0);
+    pack_pairs<<<grid_for(npairs, 256), 256, 0, st>>>(t, s, npairs, sbits, k0); fmm::note_launch();
     size_t need = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, need, k0, k1, npairs, 0, 2 * sbits, st);
     if (need > ar.left()) { set_error("sort workspace"); return FMM_ERR_INVALID; }
     cub::DeviceRadixSort::SortKeys(ar.rest(), need, k0, k1, npairs, 0, 2 * sbits, st);
-    unpack_rows<<<grid_for(npairs, 256), 256, 0, st>>>(k1, npairs, sbits, ncells, src_sorted, rows);
+    unpack_rows<<<grid_for(npairs, 256), 256, 0, st>>>(k1, npairs, sbits, ncells, src_sorted, rows); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_pairs_to_csr");
     return FMM_OK;
 }

@@ -14,6 +14,7 @@
 // descendants (same start, lower level) and every later sibling subtree
 // (larger start).
 #include <cub/cub.cuh>
+#include <atomic>
 #include <stdarg.h>
 #include <stdio.h>
 
@@ -22,6 +23,9 @@
 namespace fmm {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
     va_list ap;
@@ -84,16 +88,20 @@ __global__ void ingest_bounds_partial(const T *__restrict__ x, const T *__restri
 }
 
 __global__ void bounds_final(const double *partial, int nb, double *root) {
-    if (threadIdx.x != 0) return;
-    double lo[3], hi[3];
-    for (int d = 0; d < 3; d++) {
-        lo[d] = partial[d];
-        hi[d] = partial[3 + d];
-        for (int b = 1; b < nb; b++) {
+    // one warp: lane-strided over the block partials, then shuffles
+    const int lane = threadIdx.x & 31;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int b = lane; b < nb; b += 32)
+        for (int d = 0; d < 3; d++) {
             lo[d] = fmin(lo[d], partial[b * 6 + d]);
             hi[d] = fmax(hi[d], partial[b * 6 + 3 + d]);
         }
-    }
+    for (int d = 0; d < 3; d++)
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+        }
+    if (lane != 0) return;
     // size = max extent; 0 -> 1.0 (src/tree.py:388-392); extents in x, y, z order
     double size = hi[0] - lo[0];
     double e1 = hi[1] - lo[1], e2 = hi[2] - lo[2];
@@ -396,6 +404,8 @@ int fmm_abi_version(void) { return 1; }
 
 const char *fmm_last_error(void) { return fmm::g_err; }
 
+long long fmm_launch_count(void) { return fmm::g_launches.load(std::memory_order_relaxed); }
+
 int fmm_device_sm_count(void) {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return -1;
@@ -421,23 +431,23 @@ int fmm_ingest_bounds(const void *x, const void *y, const void *z, const void *q
         bool copy = (x != (const void *)x64);
         ingest_bounds_partial<double><<<nb, 256, 0, s>>>((const double *)x, (const double *)y,
                                                          (const double *)z, (const double *)q, n, x64,
-                                                         y64, z64, q64, copy, partial);
+                                                         y64, z64, q64, copy, partial); fmm::note_launch();
     } else if (dtype == FMM_DTYPE_F32) {
         ingest_bounds_partial<float><<<nb, 256, 0, s>>>((const float *)x, (const float *)y,
                                                         (const float *)z, (const float *)q, n, x64, y64,
-                                                        z64, q64, true, partial);
+                                                        z64, q64, true, partial); fmm::note_launch();
     } else {
         set_error("bad dtype %d", dtype);
         return FMM_ERR_INVALID;
     }
-    bounds_final<<<1, 32, 0, s>>>(partial, nb, root);
+    bounds_final<<<1, 32, 0, s>>>(partial, nb, root); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_ingest_bounds");
     return FMM_OK;
 }
 
 int fmm_morton_keys(const double *x, const double *y, const double *z, int64_t n, const double *root,
                     uint64_t *keys, int32_t *iota, void *stream) {
-    morton_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, y, z, n, root, keys, iota);
+    morton_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, y, z, n, root, keys, iota); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_morton_keys");
     return FMM_OK;
 }
@@ -460,7 +470,7 @@ int fmm_permute_bodies(const int32_t *perm, const double *x, const double *y, co
                        void *b32, void *b32lo, int *dev_inexact, void *stream) {
     permute_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(perm, x, y, z, q, n, xs, ys, zs, qs,
                                                                     (float4 *)b32, (float4 *)b32lo,
-                                                                    dev_inexact);
+                                                                    dev_inexact); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_permute_bodies");
     return FMM_OK;
 }
@@ -478,10 +488,10 @@ int fmm_build_level(const uint64_t *keys, int32_t *node, int64_t n, int level, i
     void *tmp = ar.rest();
     size_t tmp_bytes = ar.left();
     int g = grid_for(n, 256);
-    if (level < 0) fill_i32<<<g, 256, 0, s>>>(node, n, 0);
+    if (level < 0) fill_i32<<<g, 256, 0, s>>>(node, n, 0); fmm::note_launch();
     const int clev = level + 1;
     const int shift = 3 * (MAX_LEVEL - clev);
-    level_flags<<<g, 256, 0, s>>>(keys, node, n, shift >= 64 ? 63 : shift, flags);
+    level_flags<<<g, 256, 0, s>>>(keys, node, n, shift >= 64 ? 63 : shift, flags); fmm::note_launch();
     size_t need = 0;
     cub::DeviceScan::InclusiveSum(nullptr, need, flags, incl, n, s);
     if (need > tmp_bytes) { set_error("scan workspace"); return FMM_ERR_INVALID; }
@@ -497,8 +507,8 @@ int fmm_build_level(const uint64_t *keys, int32_t *node, int64_t n, int level, i
         return FMM_ERR_CAPACITY;
     }
     level_emit<<<g, 256, 0, s>>>(keys, node, flags, incl, n, level, shift, ncrit, allow_big, base,
-                                 c_start, c_end, c_parent, c_level, c_key, c_split, err);
-    level_update<<<g, 256, 0, s>>>(node, incl, n, base, c_split);
+                                 c_start, c_end, c_parent, c_level, c_key, c_split, err); fmm::note_launch();
+    level_update<<<g, 256, 0, s>>>(node, incl, n, base, c_split); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_build_level");
     if (clev == MAX_LEVEL) {
         int h = 0;
@@ -527,7 +537,7 @@ int fmm_finalize_cells(int32_t ncells, int64_t n, const int32_t *b_start, const 
     int32_t *order = ar.take<int32_t>(ncells);
     if (!sk || !sk2 || !iota || !order) { set_error("workspace too small"); return FMM_ERR_INVALID; }
     int g = grid_for(ncells, 256);
-    preorder_keys<<<g, 256, 0, s>>>(ncells, b_start, b_level, sk, iota);
+    preorder_keys<<<g, 256, 0, s>>>(ncells, b_start, b_level, sk, iota); fmm::note_launch();
     int end_bit = 5;
     while (end_bit < 64 && ((uint64_t)n << 5) >> end_bit) end_bit++;
     size_t need = 0;
@@ -535,11 +545,11 @@ int fmm_finalize_cells(int32_t ncells, int64_t n, const int32_t *b_start, const 
     if (need > ar.left()) { set_error("sort workspace"); return FMM_ERR_INVALID; }
     cub::DeviceRadixSort::SortPairs(ar.rest(), need, sk, sk2, iota, order, ncells, 0, end_bit, s);
     preorder_gather<<<g, 256, 0, s>>>(ncells, order, b_start, b_end, b_level, b_key, b_split, pre_of_bfs,
-                                      level, key, start, end, leaf, children);
+                                      level, key, start, end, leaf, children); fmm::note_launch();
     preorder_links<<<g, 256, 0, s>>>(ncells, order, b_parent, pre_of_bfs, key, start, end, parent,
-                                     children, sub_end);
+                                     children, sub_end); fmm::note_launch();
     body_leaf_kernel<<<grid_for((int64_t)ncells * 32, 256), 256, 0, s>>>(ncells, leaf, start, end,
-                                                                        body_leaf);
+                                                                        body_leaf); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_finalize_cells");
     return FMM_OK;
 }
@@ -555,13 +565,13 @@ int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, 
     int32_t *choff = ar.take<int32_t>(ncells);
     if (!b2 || !nchunk || !choff) { set_error("workspace too small"); return FMM_ERR_INVALID; }
     int g = grid_for(ncells, 256);
-    geometry_cells<<<g, 256, 0, s>>>(ncells, level, key, start, end, root, lo, hi, ctr, rmax, b2, nchunk);
+    geometry_cells<<<g, 256, 0, s>>>(ncells, level, key, start, end, root, lo, hi, ctr, rmax, b2, nchunk); fmm::note_launch();
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, nchunk, choff, ncells, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
     cub::DeviceScan::ExclusiveSum(ar.rest(), need, nchunk, choff, ncells, s);
-    geometry_bmax<<<148 * 8, 256, 0, s>>>(ncells, choff, nchunk, start, end, ctr, xs, ys, zs, b2);
-    geometry_finish<<<g, 256, 0, s>>>(ncells, b2, bmax);
+    geometry_bmax<<<148 * 8, 256, 0, s>>>(ncells, choff, nchunk, start, end, ctr, xs, ys, zs, b2); fmm::note_launch();
+    geometry_finish<<<g, 256, 0, s>>>(ncells, b2, bmax); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_cell_geometry");
     return FMM_OK;
 }

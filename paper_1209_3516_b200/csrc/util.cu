@@ -48,6 +48,19 @@ __global__ void direct_kernel(int64_t n, const double *__restrict__ x, const dou
     }
 }
 
+__global__ void unpermute_kernel(const int32_t *__restrict__ perm, int64_t n, const double *a0, const double *a1,
+                                 const double *a2, const double *a3, double *b0, double *b1, double *b2,
+                                 double *b3) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t o = perm[i];
+        b0[o] = a0[i];
+        b1[o] = a1[i];
+        b2[o] = a2[i];
+        b3[o] = a3[i];
+    }
+}
+
 __global__ void combine_kernel(int64_t n, const double *a0, const double *a1, const double *a2,
                                const double *a3, double *b0, double *b1, double *b2, double *b3) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -212,15 +225,22 @@ int fmm_direct(int64_t n, const double *x, const double *y, const double *z, con
                const int64_t *tidx, double *phi, double *fx, double *fy, double *fz, void *stream) {
     if (nt <= 0) return FMM_OK;
     direct_kernel<<<grid_for(nt, 1, 148 * 8), 256, 0, as_stream(stream)>>>(n, x, y, z, q, nt, tidx, phi, fx,
-                                                                          fy, fz);
+                                                                          fy, fz); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_direct");
+    return FMM_OK;
+}
+
+int fmm_unpermute(const int32_t *perm, int64_t n, const double *a0, const double *a1, const double *a2,
+                  const double *a3, double *b0, double *b1, double *b2, double *b3, void *stream) {
+    unpermute_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(perm, n, a0, a1, a2, a3, b0, b1, b2, b3); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_unpermute");
     return FMM_OK;
 }
 
 int fmm_combine(int64_t n, const double *a_phi, const double *a_fx, const double *a_fy, const double *a_fz,
                 double *phi, double *fx, double *fy, double *fz, void *stream) {
     combine_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, a_phi, a_fx, a_fy, a_fz, phi, fx, fy,
-                                                                   fz);
+                                                                   fz); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_combine");
     return FMM_OK;
 }
@@ -228,14 +248,14 @@ int fmm_combine(int64_t n, const double *a_phi, const double *a_fx, const double
 int fmm_ffma_probe(int mode, int blocks, int iters, float *sink, double *host_flops, void *stream) {
     cudaStream_t s = as_stream(stream);
     switch (mode) {
-        case 0: fp32_probe_kernel<0><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 1: fp32_probe_kernel<1><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 2: fp32_probe_kernel<2><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 3: fp32_probe_kernel<3><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 4: fp32_probe_kernel<4><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 5: p2p_probe_kernel<5><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 6: p2p_probe_kernel<6><<<blocks, 256, 0, s>>>(iters, sink); break;
-        case 7: p2p_probe_packed_kernel<<<blocks, 256, 0, s>>>(iters, sink); break;
+        case 0: fp32_probe_kernel<0><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 1: fp32_probe_kernel<1><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 2: fp32_probe_kernel<2><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 3: fp32_probe_kernel<3><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 4: fp32_probe_kernel<4><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 5: p2p_probe_kernel<5><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 6: p2p_probe_kernel<6><<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
+        case 7: p2p_probe_packed_kernel<<<blocks, 256, 0, s>>>(iters, sink); fmm::note_launch(); break;
         default: set_error("bad probe mode %d", mode); return FMM_ERR_INVALID;
     }
     // flops: FFMA = 2 per lane-op, FMUL/FADD = 1 (mode 4 counts 1 per op);

@@ -4,9 +4,10 @@
 positions and charges in, ``phi`` and ``fx/fy/fz`` accumulators out, one
 length for all arrays.  Two storage forms are accepted:
 
-* NumPy arrays (the reference's form): upcast to float64 exactly as the
-  reference does (``geometry.py:231-241``); ``build_tree`` copies them to
-  the device.
+* NumPy arrays (the reference's form): ``x, y, z, q`` read as float64
+  exactly as in the reference (``geometry.py:231-241``).  A float32 cloud
+  is kept as given and upcast lazily on access, so ``build_tree`` ships
+  half the bytes to the device and upcasts there (exact either way).
 * torch CUDA tensors (float32 or float64): kept on the device as given, so
   a device-resident cloud is solved without host traffic.  The kernels
   upcast to float64 for keys and geometry (bit-exact with the reference).
@@ -57,6 +58,9 @@ class Aabb:
 class ParticleSet:
     """Structure-of-arrays bodies (src/geometry.py:213-270)."""
 
+    _raw = None
+    _f64 = None
+
     def __init__(self, x, y, z, q, phi=None, fx=None, fy=None, fz=None):
         if _is_torch(x):
             arrs = [x, y, z, q]
@@ -78,11 +82,16 @@ class ParticleSet:
                            else torch.as_tensor(a, dtype=torch.float64, device=dev).contiguous())
             self.phi, self.fx, self.fy, self.fz = acc
         else:
-            self.x = np.ascontiguousarray(x, dtype=np.float64)
-            self.y = np.ascontiguousarray(y, dtype=np.float64)
-            self.z = np.ascontiguousarray(z, dtype=np.float64)
-            self.q = np.ascontiguousarray(q, dtype=np.float64)
-            n = self.x.shape[0]
+            raw = [np.asarray(a) for a in (x, y, z, q)]
+            if all(a.dtype == np.float32 for a in raw):
+                # float32 host cloud: kept as given (the device upcasts it
+                # exactly); the float64 views are materialised on access
+                self._raw = [np.ascontiguousarray(a) for a in raw]
+                self._f64 = [None] * 4
+            else:
+                self._raw = None
+                self._f64 = [np.ascontiguousarray(a, dtype=np.float64) for a in raw]
+            n = (self._raw or self._f64)[0].shape[0]
             acc = []
             for a in (phi, fx, fy, fz):
                 acc.append(np.zeros(n) if a is None else np.ascontiguousarray(a, dtype=np.float64))
@@ -91,6 +100,36 @@ class ParticleSet:
                                              self.fz)}
         if lengths != {int(n)}:
             raise ValueError(f"particle arrays disagree on length: {sorted(lengths)}")
+
+    # float64 views of host inputs (the reference's storage form)
+    def _get(self, k):
+        if self._f64[k] is None:
+            self._f64[k] = self._raw[k].astype(np.float64)
+        return self._f64[k]
+
+    def _set(self, k, v):
+        if self._raw is not None:
+            for j in range(4):
+                self._get(j)
+            self._raw = None
+        self._f64[k] = np.ascontiguousarray(v, dtype=np.float64)
+
+    def __getattr__(self, name):  # x, y, z, q of the host form
+        idx = {"x": 0, "y": 1, "z": 2, "q": 3}.get(name)
+        if idx is None or self.__dict__.get("_f64") is None:
+            raise AttributeError(name)
+        return self._get(idx)
+
+    def __setattr__(self, name, value):
+        idx = {"x": 0, "y": 1, "z": 2, "q": 3}.get(name)
+        if idx is not None and not isinstance(value, torch.Tensor) and self.__dict__.get("_f64") is not None:
+            self._set(idx, value)
+        else:
+            object.__setattr__(self, name, value)
+
+    def host_inputs(self):
+        """(x, y, z, q) host arrays in their stored precision (no copy)."""
+        return tuple(self._raw) if self._raw is not None else tuple(self._f64)
 
     @property
     def n(self) -> int:

@@ -169,8 +169,9 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     done_p2p = done_m2l = 0
     nfront = 1
     peak = 1
+    first = 1  # the root pair is classified, later frontier pairs are expanded
     while nfront > 0:
-        _lib.call("fmm_traverse_step", P(fa), P(fb), nfront, P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr),
+        _lib.call("fmm_traverse_step", P(fa), P(fb), nfront, first, P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr),
                   P(tree.d_bmax), P(tree.d_rmax), P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
                   cap_m2l, P(na), P(nb), cap_next, P(counts), st)
         c_p2p, c_m2l, c_next = counts.tolist()
@@ -190,6 +191,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
             counts.copy_(torch.tensor([done_p2p, done_m2l, 0], dtype=torch.int64))
             continue
         done_p2p, done_m2l = c_p2p, c_m2l
+        first = 0
         fa, na = na, fa
         fb, nb = nb, fb
         nfront = c_next

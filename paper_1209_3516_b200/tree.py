@@ -168,19 +168,44 @@ class Tree:
         self._L = None
 
     def results_in_input_order(self) -> ParticleSet:
-        """Copy of the bodies (with accumulators) in the caller's ordering."""
-        b = self.bodies
-        inv = np.empty(self.n, dtype=np.int64)
-        inv[self.permutation] = np.arange(self.n)
-        return b.permuted(inv)
+        """Copy of the bodies (with accumulators) in the caller's ordering
+        (src/tree.py:344-348).  The permutation is undone on the device and
+        only the accumulators travel back (through pinned buffers); positions
+        and charges come from the caller's own arrays when they were given
+        on the host."""
+        if self._bodies_host is not None:  # host-side edits win (reference semantics)
+            b = self._bodies_host
+            inv = np.empty(self.n, dtype=np.int64)
+            inv[self.permutation] = np.arange(self.n)
+            return b.permuted(inv)
+        acc = self.device_results_in_input_order()
+        host = []
+        for a in acc:
+            h = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
+            h.copy_(a, non_blocking=True)
+            host.append(h)
+        if self._host_input is not None:
+            src = [np.array(a, dtype=np.float64) for a in
+                   (self._host_input.x, self._host_input.y, self._host_input.z, self._host_input.q)]
+        else:
+            src = None
+        torch.cuda.current_stream(self.device).synchronize()
+        if src is None:
+            perm = self.d_perm.long()
+            src = []
+            for a in (self.d_x, self.d_y, self.d_z, self.d_q):
+                o = torch.empty_like(a)
+                o[perm] = a
+                src.append(o.cpu().numpy())
+        return ParticleSet(*src, *(h.numpy() for h in host))
 
     def device_results_in_input_order(self):
         """(phi, fx, fy, fz) on the device, in the caller's ordering."""
-        out = []
-        for a in (self.d_phi, self.d_fx, self.d_fy, self.d_fz):
-            o = torch.empty_like(a)
-            o[self.d_perm.long()] = a
-            out.append(o)
+        out = [torch.empty_like(self.d_phi) for _ in range(4)]
+        with torch.cuda.device(self.device):
+            P = _lib.ptr
+            _lib.call("fmm_unpermute", P(self.d_perm), self.n, P(self.d_phi), P(self.d_fx), P(self.d_fy),
+                      P(self.d_fz), *(P(o) for o in out), _lib.stream_handle())
         return tuple(out)
 
     # ---- expansions --------------------------------------------------------
@@ -224,15 +249,13 @@ class Tree:
         return arr
 
 
-def _to_device(a, dev, dtype):
-    if isinstance(a, torch.Tensor):
-        return a.to(dev, dtype).contiguous()
-    h = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-    if dtype == torch.float64:
-        pinned = torch.empty(h.shape, dtype=torch.float64, pin_memory=True)
-        pinned.copy_(h)
-        return pinned.to(dev, non_blocking=True)
-    return h.to(dev, dtype)
+def _to_device(a: np.ndarray, dev):
+    """Host array -> device through a pinned staging buffer (torch's caching
+    host allocator reuses it across calls)."""
+    h = torch.from_numpy(np.ascontiguousarray(a))
+    pinned = torch.empty(h.shape, dtype=h.dtype, pin_memory=True)
+    pinned.copy_(h)
+    return pinned.to(dev, non_blocking=True)
 
 
 def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mode: str = "geometric",
@@ -263,12 +286,11 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
     with torch.cuda.device(dev):
         st = _lib.stream_handle()
         f64, i32 = torch.float64, torch.int32
-        if ps.on_device and ps.x.device == dev:
-            src = (ps.x, ps.y, ps.z, ps.q)
-            dcode = _lib.DTYPE_F64 if ps.x.dtype == torch.float64 else _lib.DTYPE_F32
+        if ps.on_device:
+            src = tuple(a.to(dev) for a in (ps.x, ps.y, ps.z, ps.q))
         else:
-            src = tuple(_to_device(a, dev, f64) for a in (ps.x, ps.y, ps.z, ps.q))
-            dcode = _lib.DTYPE_F64
+            src = tuple(_to_device(a, dev) for a in ps.host_inputs())
+        dcode = _lib.DTYPE_F64 if src[0].dtype == torch.float64 else _lib.DTYPE_F32
         x64 = torch.empty(n, dtype=f64, device=dev)
         y64, z64, q64 = torch.empty_like(x64), torch.empty_like(x64), torch.empty_like(x64)
         root = torch.empty(8, dtype=f64, device=dev)
@@ -357,6 +379,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         d_body_leaf=body_leaf, d_cells_by_level=pre_of_bfs,
         d_lo=lo, d_hi=hi, d_ctr=ctr, d_bmax=bmax, d_rmax=rmax,
     )
+    tree._host_input = None if ps.on_device else ps
     tree.build_time = time.perf_counter() - t0
     return tree
 

@@ -162,15 +162,19 @@ def test_call_sites_match_abi_arity():
     checked = 0
     for fn in glob.glob(os.path.join(pkg, "*.py")) + [os.path.join(ROOT, "bench.py")]:
         tree = ast.parse(open(fn).read())
-        env = {}
+        seen = {}
         for node in ast.walk(tree):
             if isinstance(node, ast.Assign) and len(node.targets) == 1 and isinstance(node.targets[0], ast.Name):
+                k = None
                 if isinstance(node.value, (ast.Tuple, ast.List)):
-                    env[node.targets[0].id] = len(node.value.elts)
+                    k = len(node.value.elts)
                 elif isinstance(node.value, ast.ListComp) and isinstance(node.value.generators[0].iter, ast.Call):
                     c = node.value.generators[0].iter
                     if getattr(c.func, "id", "") == "range" and c.args and isinstance(c.args[0], ast.Constant):
-                        env[node.targets[0].id] = c.args[0].value
+                        k = c.args[0].value
+                seen.setdefault(node.targets[0].id, set()).add(k)
+        # names bound more than one way are ambiguous: those call sites are skipped
+        env = {n: next(iter(v)) for n, v in seen.items() if len(v) == 1 and None not in v}
         for node in ast.walk(tree):
             if not (isinstance(node, ast.Call) and node.args and isinstance(node.args[0], ast.Constant)
                     and isinstance(node.args[0].value, str) and node.args[0].value.startswith("fmm_")):
