@@ -163,6 +163,20 @@ FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfro
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
                       unsigned long long *dev_counts, void *stream);
 
+/* The whole traversal without host round trips: nsteps breadth-first steps
+ * chained on the device (each step reads its frontier size from the
+ * previous one), frontiers ping-ponging between buffers 0 and 1 (capacity
+ * cap_front each).  dev_log (nsteps + 3 entries) receives {n_p2p, n_m2l,
+ * frontier size entering step 0, 1, ..., nsteps}; the caller reads it once:
+ * a non-zero last entry means nsteps was too small, and any count above its
+ * capacity means buffers must grow (the lists are then incomplete; rerun). */
+FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                 int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                 const double *ctr, const double *bmax, const double *rmax, const int32_t *start,
+                 const int32_t *end, int32_t body_lo, int32_t body_hi, int kind, double th2,
+                 int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
+                 int64_t cap_m2l, unsigned long long *dev_log, void *stream);
+
 /* Sort (t, s) pairs by target then source and build row offsets over all
  * cells: rows[c]..rows[c+1] are the sources of target c (ascending). */
 FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs, int32_t ncells,

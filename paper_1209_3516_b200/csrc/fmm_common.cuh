@@ -23,6 +23,7 @@ struct Tables {
     int deg[NMI];
     double mfact[NMI];
     double ifact[TMAX + 2];                 // 1/k!
+    double rcp[TMAX + 2];                   // 1/k (rcp[0] unused)
     short idx3[TMAX + 2][TMAX + 2][TMAX + 2];
 };
 
@@ -46,6 +47,8 @@ constexpr Tables make_tables() {
     fact[0] = 1.0;
     for (int d = 1; d < TMAX + 2; d++) fact[d] = fact[d - 1] * d;
     for (int d = 0; d < TMAX + 2; d++) t.ifact[d] = 1.0 / fact[d];
+    t.rcp[0] = 0.0;
+    for (int d = 1; d < TMAX + 2; d++) t.rcp[d] = 1.0 / d;
     for (int i = 0; i < n; i++) t.mfact[i] = fact[t.mi[i][0]] * fact[t.mi[i][1]] * fact[t.mi[i][2]];
     return t;
 }

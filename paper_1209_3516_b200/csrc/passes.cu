@@ -10,85 +10,106 @@
 
 namespace fmm {
 
-// x^a / a! for a = 0..deg (recurrence of src/_taylor.py:102-115 per axis)
-__device__ inline void pow_fact_axis(double d, int deg, double *out) {
-    out[0] = 1.0;
-    for (int a = 1; a <= deg; a++) out[a] = out[a - 1] * d / a;
+// ---- P2M: warp per leaf, lane per coefficient ---------------------------
+// M_m = sum_j q_j (x_j - c)^m / m!  (src/_taylor.py:134-143); bodies are
+// broadcast from their loading lane by shuffles, each lane builds its own
+// monomial by repeated multiplication (no tables, no local memory).
+constexpr int kMaxSlots = (NMI + 31) / 32;
+
+__device__ __forceinline__ double mono(double dx, double dy, double dz, int a, int b, int c) {
+    double v = 1.0;
+    for (int i = 0; i < a; i++) v *= dx;
+    for (int i = 0; i < b; i++) v *= dy;
+    for (int i = 0; i < c; i++) v *= dz;
+    return v;
 }
 
-__device__ inline void pow_axis(double d, int deg, double *out) {
-    out[0] = 1.0;
-    for (int a = 1; a <= deg; a++) out[a] = out[a - 1] * d;
-}
-
-// ---- P2M: block per leaf, thread per coefficient; bodies staged in smem --
-constexpr int kP2MTile = 64;
-
+template <int NS>  // coefficient slots per lane: ceil(ncoef(p) / 32)
 __global__ void p2m_kernel(int p, const int32_t *__restrict__ cells, int32_t ncells,
-                           const uint8_t *__restrict__ leaf,
-                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-                           const double *__restrict__ ctr, const double *__restrict__ xs,
-                           const double *__restrict__ ys, const double *__restrict__ zs,
-                           const double *__restrict__ qs, double *M) {
-    __shared__ double sp[kP2MTile][3][TMAX];
-    __shared__ double sq[kP2MTile];
+                           const uint8_t *__restrict__ leaf, const int32_t *__restrict__ start,
+                           const int32_t *__restrict__ end, const double *__restrict__ ctr,
+                           const double *__restrict__ xs, const double *__restrict__ ys,
+                           const double *__restrict__ zs, const double *__restrict__ qs, double *M) {
+    const int lane = threadIdx.x & 31;
     const int nc = ncoef(p);
-    for (int ci = blockIdx.x; ci < ncells; ci += gridDim.x) {
+    for (int ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ci < ncells;
+         ci += (gridDim.x * blockDim.x) >> 5) {
         const int32_t c = cells[ci];
         if (!leaf[c]) continue;
         const double cx = ctr[c * 3], cy = ctr[c * 3 + 1], cz = ctr[c * 3 + 2];
         const int32_t s = start[c], e = end[c];
-        int mx = 0, my = 0, mz = 0;
-        if (threadIdx.x < nc) {
-            mx = d_tab.mi[threadIdx.x][0];
-            my = d_tab.mi[threadIdx.x][1];
-            mz = d_tab.mi[threadIdx.x][2];
+        double acc[NS];
+#pragma unroll
+        for (int k = 0; k < NS; k++) acc[k] = 0.0;
+        int ma[NS], mb[NS], mc[NS];
+        double w[NS];  // 1 / m!
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            const int m = min(lane + 32 * k, nc - 1);
+            ma[k] = d_tab.mi[m][0];
+            mb[k] = d_tab.mi[m][1];
+            mc[k] = d_tab.mi[m][2];
+            w[k] = 1.0 / d_tab.mfact[m];
         }
-        double acc = 0.0;
-        for (int32_t b0 = s; b0 < e; b0 += kP2MTile) {
-            int cnt = min(kP2MTile, e - b0);
-            __syncthreads();
-            for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-                pow_fact_axis(xs[b0 + t] - cx, p - 1, sp[t][0]);
-                pow_fact_axis(ys[b0 + t] - cy, p - 1, sp[t][1]);
-                pow_fact_axis(zs[b0 + t] - cz, p - 1, sp[t][2]);
-                sq[t] = qs[b0 + t];
+        for (int32_t b0 = s; b0 < e; b0 += 32) {
+            const int cnt = min(32, e - b0);
+            double dx = 0.0, dy = 0.0, dz = 0.0, qq = 0.0;
+            if (lane < cnt) {
+                dx = xs[b0 + lane] - cx;
+                dy = ys[b0 + lane] - cy;
+                dz = zs[b0 + lane] - cz;
+                qq = qs[b0 + lane];
             }
-            __syncthreads();
-            if (threadIdx.x < nc)
-                for (int t = 0; t < cnt; t++) acc += sq[t] * (sp[t][0][mx] * sp[t][1][my] * sp[t][2][mz]);
+            for (int j = 0; j < cnt; j++) {
+                const double bx = __shfl_sync(0xffffffffu, dx, j), by = __shfl_sync(0xffffffffu, dy, j);
+                const double bz = __shfl_sync(0xffffffffu, dz, j), bq = __shfl_sync(0xffffffffu, qq, j);
+#pragma unroll
+                for (int k = 0; k < NS; k++)
+                    if (lane + 32 * k < nc) acc[k] += bq * mono(bx, by, bz, ma[k], mb[k], mc[k]);
+            }
         }
-        if (threadIdx.x < nc) M[(int64_t)c * nc + threadIdx.x] = acc;
-        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            const int m = lane + 32 * k;
+            if (m < nc) M[(int64_t)c * nc + m] = acc[k] * w[k];
+        }
     }
 }
 
 // ---- M2M: thread per (internal cell of this level, coefficient m) --------
 // Mdst[m] += sum_child sum_{k<=m} Msrc[k] t^{m-k}/(m-k)!, t = c_child - c_parent
+// (src/_taylor.py:146-166); the powers t^a/a! are carried as running
+// products inside the loops, so nothing spills to local memory.
 __global__ void m2m_level(int p, const int32_t *__restrict__ cells, int32_t count,
                           const uint8_t *__restrict__ leaf, const int32_t *__restrict__ children,
                           const double *__restrict__ ctr, double *M) {
     const int nc = ncoef(p);
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < (int64_t)count * nc;
          it += (int64_t)gridDim.x * blockDim.x) {
-        int32_t c = cells[it / nc];
-        int m = (int)(it % nc);
+        const int32_t c = cells[it / nc];
+        const int m = (int)(it % nc);
         if (leaf[c]) continue;
         const int mx = d_tab.mi[m][0], my = d_tab.mi[m][1], mz = d_tab.mi[m][2];
         double total = 0.0;
         for (int o = 0; o < 8; o++) {
-            int32_t ch = children[c * 8 + o];
+            const int32_t ch = children[c * 8 + o];
             if (ch < 0) continue;
-            double px[TMAX], py[TMAX], pz[TMAX];
-            pow_fact_axis(ctr[ch * 3] - ctr[c * 3], mx, px);
-            pow_fact_axis(ctr[ch * 3 + 1] - ctr[c * 3 + 1], my, py);
-            pow_fact_axis(ctr[ch * 3 + 2] - ctr[c * 3 + 2], mz, pz);
+            const double tx = ctr[ch * 3] - ctr[c * 3], ty = ctr[ch * 3 + 1] - ctr[c * 3 + 1],
+                         tz = ctr[ch * 3 + 2] - ctr[c * 3 + 2];
             const double *Ms = M + (int64_t)ch * nc;
-            double acc = 0.0;
-            for (int kx = 0; kx <= mx; kx++)
-                for (int ky = 0; ky <= my; ky++)
-                    for (int kz = 0; kz <= mz; kz++)
-                        acc += Ms[d_tab.idx3[kx][ky][kz]] * (px[mx - kx] * py[my - ky] * pz[mz - kz]);
+            double acc = 0.0, fx = 1.0;
+            for (int a = 0; a <= mx; a++) {          // a = mx - kx
+                double fy = 1.0;
+                for (int b = 0; b <= my; b++) {      // b = my - ky
+                    double fz = 1.0;
+                    for (int g = 0; g <= mz; g++) {  // g = mz - kz
+                        acc += Ms[d_tab.idx3[mx - a][my - b][mz - g]] * (fx * fy * fz);
+                        fz = fz * tz * d_tab.rcp[g + 1];
+                    }
+                    fy = fy * ty * d_tab.rcp[b + 1];
+                }
+                fx = fx * tx * d_tab.rcp[a + 1];
+            }
             total += acc;
         }
         M[(int64_t)c * nc + m] += total;
@@ -97,31 +118,37 @@ __global__ void m2m_level(int p, const int32_t *__restrict__ cells, int32_t coun
 
 // ---- L2L: thread per (cell of this level, coefficient k), pull from parent
 // Ldst[k] += (1/k!) sum_{n>=k} Lsrc[n] n! t^{n-k}/(n-k)!,  t = c_child - c_parent
+// (src/_taylor.py:220-240), running products as in M2M.
 __global__ void l2l_level(int p, const int32_t *__restrict__ cells, int32_t count,
                           const int32_t *__restrict__ parent, const double *__restrict__ ctr,
                           double *L) {
     const int nc = ncoef(p);
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < (int64_t)count * nc;
          it += (int64_t)gridDim.x * blockDim.x) {
-        int32_t c = cells[it / nc];
-        int k = (int)(it % nc);
-        int32_t pa = parent[c];
+        const int32_t c = cells[it / nc];
+        const int k = (int)(it % nc);
+        const int32_t pa = parent[c];
         if (pa < 0) continue;
         const int kx = d_tab.mi[k][0], ky = d_tab.mi[k][1], kz = d_tab.mi[k][2];
         const int rem = p - 1 - (kx + ky + kz);  // max degree of n-k
-        double px[TMAX], py[TMAX], pz[TMAX];
-        pow_fact_axis(ctr[c * 3] - ctr[pa * 3], rem, px);
-        pow_fact_axis(ctr[c * 3 + 1] - ctr[pa * 3 + 1], rem, py);
-        pow_fact_axis(ctr[c * 3 + 2] - ctr[pa * 3 + 2], rem, pz);
+        const double tx = ctr[c * 3] - ctr[pa * 3], ty = ctr[c * 3 + 1] - ctr[pa * 3 + 1],
+                     tz = ctr[c * 3 + 2] - ctr[pa * 3 + 2];
         const double *Ls = L + (int64_t)pa * nc;
-        double acc = 0.0;
-        for (int ax = 0; ax <= rem; ax++)
-            for (int ay = 0; ay <= rem - ax; ay++)
+        double acc = 0.0, fx = 1.0;
+        for (int ax = 0; ax <= rem; ax++) {
+            double fy = 1.0;
+            for (int ay = 0; ay <= rem - ax; ay++) {
+                double fz = 1.0;
                 for (int az = 0; az <= rem - ax - ay; az++) {
-                    int n = d_tab.idx3[kx + ax][ky + ay][kz + az];
-                    acc += Ls[n] * d_tab.mfact[n] * (px[ax] * py[ay] * pz[az]);
+                    const int n = d_tab.idx3[kx + ax][ky + ay][kz + az];
+                    acc += Ls[n] * d_tab.mfact[n] * (fx * fy * fz);
+                    fz = fz * tz * d_tab.rcp[az + 1];
                 }
-        L[(int64_t)c * nc + k] += acc / d_tab.mfact[k];
+                fy = fy * ty * d_tab.rcp[ay + 1];
+            }
+            fx = fx * tx * d_tab.rcp[ax + 1];
+        }
+        L[(int64_t)c * nc + k] += acc * (d_tab.ifact[kx] * d_tab.ifact[ky] * d_tab.ifact[kz]);
     }
 }
 
@@ -134,20 +161,31 @@ __global__ void l2p_kernel(int p, int64_t b0, int64_t n, const int32_t *__restri
     const int nc = ncoef(p);
     for (int64_t i = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t c = body_leaf[i];
-        double ux[TMAX], uy[TMAX], uz[TMAX];
-        pow_axis(xs[i] - ctr[c * 3], p - 1, ux);
-        pow_axis(ys[i] - ctr[c * 3 + 1], p - 1, uy);
-        pow_axis(zs[i] - ctr[c * 3 + 2], p - 1, uz);
+        const int32_t c = body_leaf[i];
+        const double ux = xs[i] - ctr[c * 3], uy = ys[i] - ctr[c * 3 + 1], uz = zs[i] - ctr[c * 3 + 2];
         const double *Lc = L + (int64_t)c * nc;
         double pot = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-        for (int k = 0; k < nc; k++) {
-            const int a = d_tab.mi[k][0], b = d_tab.mi[k][1], e = d_tab.mi[k][2];
-            double lk = Lc[k];
-            pot += lk * (ux[a] * uy[b] * uz[e]);
-            if (a > 0) gx += lk * a * (ux[a - 1] * uy[b] * uz[e]);
-            if (b > 0) gy += lk * b * (ux[a] * uy[b - 1] * uz[e]);
-            if (e > 0) gz += lk * e * (ux[a] * uy[b] * uz[e - 1]);
+        // walk the graded-lex multi-indices with running powers: for each
+        // (a, b) the z-exponent runs 0..p-1-a-b, u^k = ux^a uy^b uz^c
+        double pa_ = 1.0, pa1 = 0.0;  // ux^a, a*ux^(a-1)
+        for (int a = 0; a < p; a++) {
+            double pb = 1.0, pb1 = 0.0;
+            for (int b = 0; a + b < p; b++) {
+                double pc = 1.0, pc1 = 0.0;
+                for (int g = 0; a + b + g < p; g++) {
+                    const double lk = Lc[d_tab.idx3[a][b][g]];
+                    pot += lk * (pa_ * pb * pc);
+                    gx += lk * (pa1 * pb * pc);
+                    gy += lk * (pa_ * pb1 * pc);
+                    gz += lk * (pa_ * pb * pc1);
+                    pc1 = pc1 * uz + pc;  // d/duz of uz^(g+1) = (g+1) uz^g
+                    pc = pc * uz;
+                }
+                pb1 = pb1 * uy + pb;
+                pb = pb * uy;
+            }
+            pa1 = pa1 * ux + pa_;
+            pa_ = pa_ * ux;
         }
         phi[i] += pot;
         fx[i] -= gx;
@@ -169,11 +207,23 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
     if (p < 1 || p > TMAX) { set_error("expansion order %d outside supported range 1..%d", p, TMAX); return FMM_ERR_INVALID; }
     cudaStream_t s = as_stream(stream);
     const int nc = ncoef(p);
-    int blk = nc <= 32 ? 32 : (nc <= 64 ? 64 : (nc <= 128 ? 128 : (nc <= 256 ? 256 : 384)));
     const int32_t total = host_level_off[nlev];
-    if (total > 0)
-        p2m_kernel<<<grid_for(total, 1, 148 * 32), blk, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr,
-                                                               xs, ys, zs, qs, M); fmm::note_launch();
+    if (total > 0) {
+        const int g = grid_for((int64_t)total * 32, 128, 148 * 16);
+        const int ns = (nc + 31) / 32;
+        if (ns <= 1)
+            p2m_kernel<1><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+        else if (ns <= 2)
+            p2m_kernel<2><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+        else if (ns <= 4)
+            p2m_kernel<4><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+        else if (ns <= 8)
+            p2m_kernel<8><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+        else
+            p2m_kernel<kMaxSlots><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs,
+                                                   M);
+        fmm::note_launch();
+    }
     for (int L = nlev - 2; L >= 0; L--) {
         int32_t off = host_level_off[L], cnt = host_level_off[L + 1] - off;
         if (cnt <= 0) continue;

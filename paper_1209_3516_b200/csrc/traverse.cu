@@ -61,16 +61,23 @@ __device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const uint8_t *__
 // next frontier (the root pair (0, 0) is classified by the first step,
 // which the host launches with `classify_self = 1`).
 __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
-                                     int64_t nfront, int classify_self, const int32_t *__restrict__ children,
+                                     int64_t nfront_host, const unsigned long long *__restrict__ nfront_dev,
+                                     int64_t cap_front, int classify_self, const int32_t *__restrict__ children,
                                      const uint8_t *__restrict__ leaf, const double *__restrict__ ctr,
                                      const double *__restrict__ bmax, const double *__restrict__ rmax,
                                      const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
                                      int32_t blo, int32_t bhi, int kind_mac, double th2, int32_t *p2p_t,
                                      int32_t *p2p_s, int64_t cap_p2p,
                                      int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l, int32_t *na,
-                                     int32_t *nb, int64_t cap_next, unsigned long long *counts) {
+                                     int32_t *nb, int64_t cap_next, unsigned long long *cnt_p2p,
+                                     unsigned long long *cnt_m2l, unsigned long long *cnt_next) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // the frontier size comes from the host or from the previous step's
+    // counter on the device (sync-free chains of steps); entries past the
+    // buffer capacity were never written
+    int64_t nfront = nfront_dev ? (int64_t)*nfront_dev : nfront_host;
+    if (nfront > cap_front) nfront = cap_front;
     // iterate in warp-uniform trip counts so the shuffles see full warps
     const int64_t nround = (nfront + stride - 1) / stride;
     for (int64_t r = 0; r < nround; r++) {
@@ -113,9 +120,9 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
             }
         }
         int op, om, on;
-        const unsigned long long bp = warp_reserve(&counts[0], np, lane, &op);
-        const unsigned long long bm = warp_reserve(&counts[1], nm, lane, &om);
-        const unsigned long long bn = warp_reserve(&counts[2], nn, lane, &on);
+        const unsigned long long bp = warp_reserve(cnt_p2p, np, lane, &op);
+        const unsigned long long bm = warp_reserve(cnt_m2l, nm, lane, &om);
+        const unsigned long long bn = warp_reserve(cnt_next, nn, lane, &on);
         unsigned long long ip = bp + op, im = bm + om, in = bn + on;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
@@ -199,9 +206,36 @@ int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int 
                       unsigned long long *dev_counts, void *stream) {
     if (nfront <= 0) return FMM_OK;
     traverse_step_kernel<<<grid_for(nfront, 256, 148 * 16), 256, 0, as_stream(stream)>>>(
-        fa, fb, nfront, classify_self, children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
-        na, nb, cap_next, dev_counts); fmm::note_launch();
+        fa, fb, nfront, nullptr, nfront, classify_self, children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
+        na, nb, cap_next, dev_counts, dev_counts + 1, dev_counts + 2); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_traverse_step");
+    return FMM_OK;
+}
+
+int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1, int64_t cap_front,
+                 int nsteps, const int32_t *children, const uint8_t *leaf, const double *ctr,
+                 const double *bmax, const double *rmax, const int32_t *start, const int32_t *end,
+                 int32_t body_lo, int32_t body_hi, int kind, double th2, int32_t *p2p_t, int32_t *p2p_s,
+                 int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
+                 unsigned long long *dev_log, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s
+    cudaMemsetAsync(dev_log, 0, sizeof(unsigned long long) * (nsteps + 3), st);
+    const unsigned long long one = 1;
+    cudaMemcpyAsync(dev_log + 2, &one, sizeof(one), cudaMemcpyHostToDevice, st);
+    const int32_t zero = 0;
+    cudaMemcpyAsync(front_a0, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(front_b0, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
+    const int grid = 148 * 8;
+    for (int sidx = 0; sidx < nsteps; sidx++) {
+        const bool even = (sidx & 1) == 0;
+        traverse_step_kernel<<<grid, 256, 0, st>>>(
+            even ? front_a0 : front_a1, even ? front_b0 : front_b1, 0, dev_log + 2 + sidx, cap_front, sidx == 0,
+            children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p,
+            m2l_t, m2l_s, cap_m2l, even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front,
+            dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
+    }
+    FMM_CUDA_CHECK("fmm_traverse");
     return FMM_OK;
 }
 

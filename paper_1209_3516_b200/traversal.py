@@ -135,13 +135,6 @@ class Lists:
 _hint = {}
 
 
-def _grow(buf, used, need, dtype, dev):
-    nb = torch.empty(int(need), dtype=dtype, device=dev)
-    if used:
-        nb[:used].copy_(buf[:used])
-    return nb
-
-
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
@@ -157,51 +150,29 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi)
     cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
                                                  max(4096, tree.ncells * 8)))
-    p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
-    p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
-    m2l_t = torch.empty(cap_m2l, dtype=i32, device=dev)
-    m2l_s = torch.empty(cap_m2l, dtype=i32, device=dev)
-    fa = torch.zeros(max(cap_next, 1), dtype=i32, device=dev)
-    fb = torch.zeros(max(cap_next, 1), dtype=i32, device=dev)
-    na = torch.empty(cap_next, dtype=i32, device=dev)
-    nb = torch.empty(cap_next, dtype=i32, device=dev)
-    counts = torch.zeros(3, dtype=torch.int64, device=dev)
-    done_p2p = done_m2l = 0
-    nfront = 1
-    peak = 1
-    first = 1  # the root pair is classified, later frontier pairs are expanded
-    while nfront > 0:
-        _lib.call("fmm_traverse_step", P(fa), P(fb), nfront, first, P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr),
-                  P(tree.d_bmax), P(tree.d_rmax), P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
-                  cap_m2l, P(na), P(nb), cap_next, P(counts), st)
-        c_p2p, c_m2l, c_next = counts.tolist()
-        if c_p2p > cap_p2p or c_m2l > cap_m2l or c_next > cap_next:
-            if c_p2p > cap_p2p:
-                cap_p2p = int(c_p2p * 1.5) + 4096
-                p2p_t = _grow(p2p_t, done_p2p, cap_p2p, i32, dev)
-                p2p_s = _grow(p2p_s, done_p2p, cap_p2p, i32, dev)
-            if c_m2l > cap_m2l:
-                cap_m2l = int(c_m2l * 1.5) + 4096
-                m2l_t = _grow(m2l_t, done_m2l, cap_m2l, i32, dev)
-                m2l_s = _grow(m2l_s, done_m2l, cap_m2l, i32, dev)
-            if c_next > cap_next:
-                cap_next = int(c_next * 1.5) + 4096
-                na = torch.empty(cap_next, dtype=i32, device=dev)
-                nb = torch.empty(cap_next, dtype=i32, device=dev)
-            counts.copy_(torch.tensor([done_p2p, done_m2l, 0], dtype=torch.int64))
-            continue
-        done_p2p, done_m2l = c_p2p, c_m2l
-        first = 0
-        fa, na = na, fa
-        fb, nb = nb, fb
-        nfront = c_next
-        peak = max(peak, nfront)
-        if na.numel() < cap_next:
-            na = torch.empty(cap_next, dtype=i32, device=dev)
-            nb = torch.empty(cap_next, dtype=i32, device=dev)
-        cap_next_now = na.numel()
-        cap_next = cap_next_now
-        counts[2] = 0
+    # every step opens one side of a pair: at most 2 * depth + 1 steps
+    nsteps = 2 * tree.depth + 2
+    log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
+    while True:
+        p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
+        p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
+        m2l_t = torch.empty(cap_m2l, dtype=i32, device=dev)
+        m2l_s = torch.empty(cap_m2l, dtype=i32, device=dev)
+        fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
+        _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
+                  P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(tree.d_start), P(tree.d_end),
+                  blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s), cap_m2l, P(log), st)
+        hl = log.tolist()  # the one synchronisation of the traversal
+        done_p2p, done_m2l, fronts = hl[0], hl[1], hl[2:]
+        peak = max(fronts)
+        if fronts[-1] != 0:
+            raise RuntimeError("dual traversal did not terminate within 2*depth+2 steps")
+        if done_p2p <= cap_p2p and done_m2l <= cap_m2l and peak <= cap_next:
+            break
+        cap_p2p = max(cap_p2p, int(done_p2p * 1.05) + 4096)
+        cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
+        cap_next = max(cap_next, int(peak * 1.05) + 4096)
+    del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
     ncells = tree.ncells
     m2l_src = torch.empty(max(done_m2l, 1), dtype=i32, device=dev)
@@ -211,7 +182,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     p2p_src = torch.empty(max(done_p2p, 1), dtype=i32, device=dev)
     p2p_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     _lib.call("fmm_pairs_to_csr", P(p2p_t), P(p2p_s), done_p2p, ncells, P(p2p_src), P(p2p_rows), wsp, wsb, st)
-    del p2p_t, p2p_s, m2l_t, m2l_s, fa, fb, na, nb
+    del p2p_t, p2p_s, m2l_t, m2l_s
     # P2P run plan + the reference's pair counters
     leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
     run_off = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
