@@ -353,6 +353,11 @@ __device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, 
         cp_async_commit();
     }
     int32_t it = 0;
+    // the source for iteration it + 1 is read from the ring (LDS) before the
+    // math of iteration it, so its latency hides behind 13*KB/2 packed ops;
+    // the slot a fetch overwrites was consumed two iterations earlier
+    cp_async_wait<kStages - 2>();
+    float4 cur = ring[0];
     for (; it + kStages <= nitc; it += kStages) {
 #pragma unroll
         for (int q = 0; q < kStages; q++) {
@@ -362,8 +367,10 @@ __device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, 
                 stream_seek(rf, jf, rend, nr, srun);
             }
             cp_async_commit();
-            cp_async_wait<kStages - 1>();
-            p2p_f32x2_pairs<KB, false>(ring[q * 32], 0, tx, ty, tz, ap, ax, ay, az);
+            cp_async_wait<kStages - 2>();
+            const float4 nxt = ring[((q + 1) % kStages) * 32];
+            p2p_f32x2_pairs<KB, false>(cur, 0, tx, ty, tz, ap, ax, ay, az);
+            cur = nxt;
         }
     }
     for (; it < nit; it++) {  // <= kStages iterations; the last may be lane-divergent
@@ -373,8 +380,10 @@ __device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, 
             stream_seek(rf, jf, rend, nr, srun);
         }
         cp_async_commit();
-        cp_async_wait<kStages - 1>();
-        p2p_f32x2_pairs<KB, false>(ring[(it % kStages) * 32], 0, tx, ty, tz, ap, ax, ay, az);
+        cp_async_wait<kStages - 2>();
+        const float4 nxt = ring[((it + 1) % kStages) * 32];
+        p2p_f32x2_pairs<KB, false>(cur, 0, tx, ty, tz, ap, ax, ay, az);
+        cur = nxt;
     }
     cp_async_wait<0>();
     float fp[KB], fx_[KB], fy_[KB], fz_[KB];

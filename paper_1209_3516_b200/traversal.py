@@ -135,7 +135,8 @@ class Lists:
 _hint = {}
 
 
-def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None) -> Lists:
+def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
+                      m2l_ready: torch.cuda.Event | None = None) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
@@ -179,6 +180,8 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     m2l_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev)
     _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), wsp, wsb, st)
+    if m2l_ready is not None:
+        m2l_ready.record()  # the M2L list is final: the far field may start
     p2p_src = torch.empty(max(done_p2p, 1), dtype=i32, device=dev)
     p2p_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     _lib.call("fmm_pairs_to_csr", P(p2p_t), P(p2p_s), done_p2p, ncells, P(p2p_src), P(p2p_rows), wsp, wsb, st)
@@ -224,9 +227,25 @@ def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, s
               _lib.stream_handle())
 
 
+_side = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    key = torch.device(dev).index or 0
+    if key not in _side:
+        _side[key] = torch.cuda.Stream(device=dev)
+    return _side[key]
+
+
 def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
                        trace: bool = False) -> EvalReport:
-    """Simultaneous traversal of the tree against itself, on the GPU."""
+    """Simultaneous traversal of the tree against itself, on the GPU.
+
+    Two streams: the main stream builds the lists and runs P2P; a side
+    stream runs the far field (upward pass as soon as the tree exists; M2L
+    and the downward pass as soon as the M2L list is sorted) into separate
+    accumulators, which one combine kernel adds at the end.  The far field
+    (~1 ms at C2) thus hides behind list construction and P2P."""
     if source_tree is not None and source_tree is not tree:
         raise NotImplementedError("separate source trees are outside the B200 hot path")
     if cfg.mutual:
@@ -235,39 +254,59 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         raise ValueError(f"threads must be >= 1, got {threads}")
     stats = KernelStats()
     dev = tree.device
+    p = cfg.p
     with torch.cuda.device(dev):
-        stream = torch.cuda.current_stream(dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        ev[0].record(stream)
-        if tree._M is None or tree.p != cfg.p:
-            upward_pass(tree, cfg.p, stats)
-        tree._L = torch.zeros((tree.ncells, ncoef(cfg.p)), dtype=torch.float64, device=dev)
-        tree.p = cfg.p
-        ev[1].record(stream)
-        lists = interaction_lists(tree, cfg.mac)
+        main = torch.cuda.current_stream(dev)
+        side = _side_stream(dev)
+        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        e0, e_up0, e_up1, e_m2l0, e_m2l1, e_down1, e_l1, e_p0, e_p1, e_end = (E() for _ in range(10))
+        need_up = tree._M is None or tree.p != p
+        nc = ncoef(p)
+        # every buffer the side stream touches is allocated here, on main
+        M = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev) if need_up else tree._M
+        L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
+        far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+        e0.record(main)
+        side.wait_event(e0)
+        with torch.cuda.stream(side):
+            e_up0.record(side)
+            if need_up:
+                upward_pass(tree, p, stats, sync=False, M=M)  # (resets tree._L)
+            e_up1.record(side)
+        tree._M, tree.p, tree._L = M, p, L
+        m2l_ready = torch.cuda.Event()
+        lists = interaction_lists(tree, cfg.mac, m2l_ready=m2l_ready)
         tree.list_cache = lists
-        ev[2].record(stream)
-        run_m2l(tree, lists, cfg.p)
-        ev[3].record(stream)
+        e_l1.record(main)
+        side.wait_event(m2l_ready)
+        with torch.cuda.stream(side):
+            e_m2l0.record(side)
+            run_m2l(tree, lists, p)
+            e_m2l1.record(side)
+            downward_pass(tree, stats, sync=False, out=tuple(far))
+            e_down1.record(side)
+        e_p0.record(main)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
         run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
-        ev[4].record(stream)
+        e_p1.record(main)
         if cfg.precision == "fp32" and int(flag.item()) != 0:
             # two distinct bodies collided in FP32 outside a self run: redo guarded
             run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
-            ev[4].record(stream)
-        ev[5].record(stream)
-        downward_pass(tree, stats, sync=False)
-        ev[6].record(stream)
-        ev[6].synchronize()
+            e_p1.record(main)
+        main.wait_event(e_down1)
+        P = _lib.ptr
+        _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
+                  P(tree.d_fz), _lib.stream_handle())
+        e_end.record(main)
+        e_end.synchronize()
         pairs, skipped = lists.dev_stats.tolist()
     stats.p2p_pairs += int(pairs)
     stats.p2p_skipped += int(skipped)
     stats.p2p_flops += 20 * int(pairs)
     stats.m2l_calls += lists.n_m2l
-    stats.add_time("list", ev[1].elapsed_time(ev[2]) * 1e-3)
-    stats.add_time("m2l", ev[2].elapsed_time(ev[3]) * 1e-3)
-    stats.add_time("p2p", ev[3].elapsed_time(ev[4]) * 1e-3)
+    stats.add_time("list", e0.elapsed_time(e_l1) * 1e-3)
+    stats.add_time("m2l", e_m2l0.elapsed_time(e_m2l1) * 1e-3)
+    stats.add_time("p2p", e_p0.elapsed_time(e_p1) * 1e-3)
     tree._results_changed()
     events = None
     if trace:
@@ -276,11 +315,13 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
-    return EvalReport(strategy="dualtree", n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
+    # phases overlap (far field on the side stream): upward and downward are
+    # their own stream's spans, traversal is the main stream's span
+    return EvalReport(strategy="dualtree", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=False, threads=threads, task_grain=cfg.task_grain, stats=stats,
-                      build_time=tree.build_time, upward_time=ev[0].elapsed_time(ev[1]) * 1e-3,
-                      traversal_time=ev[1].elapsed_time(ev[5]) * 1e-3,
-                      downward_time=ev[5].elapsed_time(ev[6]) * 1e-3, trace=events)
+                      build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
+                      traversal_time=e0.elapsed_time(e_p1) * 1e-3,
+                      downward_time=e_m2l1.elapsed_time(e_down1) * 1e-3, trace=events)
 
 
 def evaluate_on_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,

@@ -384,21 +384,25 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
     return tree
 
 
-def upward_pass(tree: Tree, p: int, stats: KernelStats | None = None) -> None:
+def upward_pass(tree: Tree, p: int, stats: KernelStats | None = None, *, sync: bool = True,
+                M: torch.Tensor | None = None) -> None:
     """P2M at the leaves, M2M up to the root; attaches ``tree.multipole``
-    (src/tree.py:457-472)."""
+    (src/tree.py:457-472).  ``M`` (zeroed, [ncells, ncoef(p)]) may be
+    preallocated by a caller that runs the pass on a side stream."""
     if not 1 <= p <= TMAX:
         raise ValueError(f"expansion order {p} outside supported range 1..{TMAX}")
     t0 = time.perf_counter()
     dev = tree.device
     with torch.cuda.device(dev):
-        M = torch.zeros((tree.ncells, ncoef(p)), dtype=torch.float64, device=dev)
+        if M is None:
+            M = torch.zeros((tree.ncells, ncoef(p)), dtype=torch.float64, device=dev)
         P = _lib.ptr
         _lib.call("fmm_upward", p, tree.ncells, P(tree.d_children), P(tree.d_start), P(tree.d_end),
                   P(tree.d_leaf), P(tree.d_ctr), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_q),
                   P(tree.d_cells_by_level), tree.level_off_c(), len(tree.level_off) - 1, P(M),
                   _lib.stream_handle())
-        torch.cuda.current_stream(dev).synchronize()
+        if sync:
+            torch.cuda.current_stream(dev).synchronize()
     tree._M = M
     tree.p = p
     tree._L = None
@@ -409,12 +413,15 @@ def upward_pass(tree: Tree, p: int, stats: KernelStats | None = None) -> None:
 
 
 def downward_pass(tree: Tree, stats: KernelStats | None = None, *, sync: bool = True,
-                  body_range: tuple[int, int] | None = None) -> None:
+                  body_range: tuple[int, int] | None = None, out=None) -> None:
     """L2L down the tree, L2P into the leaf bodies (src/tree.py:475-488).
 
     Requires local expansions populated by a traversal (``tree.local``).
-    ``body_range=(lo, hi)`` restricts L2P to those bodies (multi-GPU)."""
+    ``body_range=(lo, hi)`` restricts L2P to those bodies (multi-GPU);
+    ``out`` = (phi, fx, fy, fz) accumulates elsewhere than the tree's own
+    accumulators (the overlapped evaluation combines them afterwards)."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
+    acc = out if out is not None else (tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz)
     if tree._L is None or tree.p is None:
         raise ValueError("local expansions not populated; run a traversal first")
     dev = tree.device
@@ -422,8 +429,8 @@ def downward_pass(tree: Tree, stats: KernelStats | None = None, *, sync: bool = 
         P = _lib.ptr
         _lib.call("fmm_downward", tree.p, tree.ncells, P(tree.d_parent), P(tree.d_leaf), P(tree.d_ctr),
                   P(tree.d_cells_by_level), tree.level_off_c(), len(tree.level_off) - 1, blo, bhi,
-                  P(tree.d_body_leaf), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree._L), P(tree.d_phi),
-                  P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), _lib.stream_handle())
+                  P(tree.d_body_leaf), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree._L), *(P(a) for a in acc),
+                  _lib.stream_handle())
         if sync:
             torch.cuda.current_stream(dev).synchronize()
     tree._results_changed()
