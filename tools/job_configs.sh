@@ -1,0 +1,5 @@
+for c in C1 C3 C5; do
+python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -1 gpurun_out/bench_$c.err
+python -c "import json; d=json.load(open('gpurun_out/bench_$c.json')); print('$c', d['value'], d['ms_per_step'], round(d['roofline']['frac'],3), {k: round(v,2) for k,v in d['kernel_ms'].items()}, {k: round(v,2) for k,v in d['phase_ms'].items()})"
+done
+nvidia-smi --query-gpu=memory.used,memory.total --format=csv

@@ -1,0 +1,42 @@
+"""Summarise an ncu --set full report of the P2P kernel into profiles/:
+key throughput metrics, stall breakdown, and DRAM traffic per launch."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h, u, v = rows[0], rows[1], rows[2]
+want = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_active_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_pct",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__warps_active.avg.per_cycle_active": "warps_active_per_sm",
+    "launch__registers_per_thread": "registers",
+    "lts__t_bytes.sum": "l2_bytes",
+    "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+}
+out = {"kernel": rows[2][h.index("Kernel Name")] if "Kernel Name" in h else ""}
+for i, name in enumerate(h):
+    if name in want:
+        out[want[name] + " [" + u[i] + "]"] = v[i]
+stalls = {}
+for i, name in enumerate(h):
+    if name.startswith("smsp__average_warps_issue_stalled_") and name.endswith("_per_issue_active.ratio"):
+        k = name[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]
+        try:
+            f = float(v[i].replace(",", ""))
+        except ValueError:
+            continue
+        if f > 0.02:
+            stalls[k] = f
+out["stall_cycles_per_issued_instruction"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
+print(json.dumps(out, indent=1))
