@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--config", default="C2", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--n", type=int, default=0, help="override N (testing)")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--p", type=int, default=0, help="override the expansion order (C4 sweep)")
+    ap.add_argument("--theta", type=float, default=0.0, help="override theta (C4 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU work for the baseline sample")
@@ -69,6 +71,11 @@ def workload(args):
     gen, n, solver = workloads.CONFIGS[args.config]
     n = args.n or n
     pos, q = gen(n, 0)
+    solver = dict(solver)
+    if args.p:
+        solver["p"] = args.p
+    if args.theta:
+        solver["theta"] = args.theta
     return pos, q, n, solver
 
 

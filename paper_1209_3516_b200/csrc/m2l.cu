@@ -207,6 +207,176 @@ __global__ void __launch_bounds__(kM2LWarps * 32) m2l_warp(int p, int32_t ncells
     }
 }
 
+// ---- block kernel for high orders (p >= 6) -------------------------------
+// The contraction L_n += sum_m (-1)^|m| M_m D_{n+m} has C(p+5, 6) terms
+// (5005 at p = 10).  They are listed n-major, cut into chunks of kChunk
+// terms that never straddle two outputs n, and dealt round-robin to the
+// block's threads: every thread owns a fixed set of chunks, so the work is
+// balanced whatever the output's term count.  Per batch of kWarps pairs,
+// warp g builds pair g's parity-signed moments and D tensor in shared
+// memory; then every thread runs its chunks over the whole batch.  At row
+// end the chunk partials are folded per output in a fixed order
+// (deterministic) and added to L_t once.
+constexpr int kChunk = 8;
+constexpr int kMaxTerms = 12376 + NMI * kChunk;     // C(17,6) + padding, p = 12
+constexpr int kMaxChunks = kMaxTerms / kChunk;
+constexpr int kBlkWarps = 4;
+
+struct TermTable {
+    int p, nchunks, nterms;
+    uint32_t term[kMaxTerms];     // m | (j << 16), chunk-major
+    uint16_t chunk_n[kMaxChunks];  // output of each chunk
+    uint16_t first_chunk[NMI + 1]; // chunks of output n: [first_chunk[n], first_chunk[n+1])
+};
+
+static __device__ TermTable d_terms;
+
+static int build_term_table(int p, TermTable &t) {
+    const Tables &T = kTab;
+    const int nc = ncoef(p);
+    int nt = 0, ch = 0;
+    t.p = p;
+    for (int n = 0; n < nc; n++) {
+        t.first_chunk[n] = (uint16_t)ch;
+        const int lim = ncoef(p - T.deg[n]);
+        int k = 0;
+        for (int m = 0; m < lim; m++) {
+            const int j = T.idx3[T.mi[n][0] + T.mi[m][0]][T.mi[n][1] + T.mi[m][1]][T.mi[n][2] + T.mi[m][2]];
+            t.term[nt++] = (uint32_t)m | ((uint32_t)j << 16);
+            if (++k == kChunk) {
+                t.chunk_n[ch++] = (uint16_t)n;
+                k = 0;
+            }
+        }
+        if (k) {  // pad the last chunk of this output with (m = 0, j = zero slot)
+            for (; k < kChunk; k++) t.term[nt++] = 0u | (0xFFFFu << 16);
+            t.chunk_n[ch++] = (uint16_t)n;
+        }
+    }
+    t.first_chunk[nc] = (uint16_t)ch;
+    t.nchunks = ch;
+    t.nterms = nt;
+    return ch;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) m2l_block(int p, int32_t ncells, const int64_t *__restrict__ rows,
+                                                const int32_t *__restrict__ src, const double *__restrict__ ctr,
+                                                const double *__restrict__ M, double *L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int G = NT / 32;
+    const int nc = ncoef(p);
+    const int nch = d_terms.nchunks;
+    uint32_t *sterm = (uint32_t *)smem_raw;                    // nch * kChunk
+    double *sD = (double *)(sterm + ((nch * kChunk + 1) & ~1)); // G * (nc + 1); slot nc is the zero
+    double *sM = sD + G * (nc + 1);                            // G * nc
+    double *spart = sM + G * nc;                               // nch
+    for (int i = threadIdx.x; i < nch * kChunk; i += NT) {
+        uint32_t v = d_terms.term[i];
+        if ((v >> 16) == 0xFFFFu) v = (v & 0xFFFFu) | ((uint32_t)nc << 16);  // -> zero slot
+        sterm[i] = v;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nslot = (nch + NT - 1) / NT;  // chunks per thread (<= kMaxChunks / NT)
+    for (int t = blockIdx.x; t < ncells; t += gridDim.x) {
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        if (k0 == k1) continue;
+        const double cx = ctr[t * 3], cy = ctr[t * 3 + 1], cz = ctr[t * 3 + 2];
+        double acc[(kMaxChunks + NT - 1) / NT];
+#pragma unroll
+        for (int q = 0; q < (kMaxChunks + NT - 1) / NT; q++) acc[q] = 0.0;
+        for (int64_t kb = k0; kb < k1; kb += G) {
+            __syncthreads();  // previous batch consumed (and srec / sterm loaded)
+            const int gcount = (int)min((int64_t)G, k1 - kb);
+            {   // warp w builds pair w's parity-signed moments and D tensor
+                const int64_t k = kb + w;
+                double *Ms = sM + w * nc;
+                double *D = sD + w * (nc + 1);
+                if (w < gcount) {
+                    const int32_t s = src[k];
+                    for (int m = lane; m < nc; m += 32) {
+                        const double v = M[(int64_t)s * nc + m];
+                        Ms[m] = (d_tab.deg[m] & 1) ? -v : v;
+                    }
+                    const double rx = cx - ctr[s * 3], ry = cy - ctr[s * 3 + 1], rz = cz - ctr[s * 3 + 2];
+                    const double r2 = rx * rx + ry * ry + rz * rz;
+                    const double inv_r2 = 1.0 / r2;
+                    if (lane == 0) {
+                        D[0] = sqrt(inv_r2);
+                        D[nc] = 0.0;
+                    }
+                    __syncwarp();
+                    for (int d = 1; d < p; d++) {
+                        for (int idx = ncoef(d) + lane; idx < ncoef(d + 1); idx += 32) {
+                            const int kx = d_tab.mi[idx][0], ky = d_tab.mi[idx][1], kz = d_tab.mi[idx][2];
+                            double a = 0.0;
+                            if (kx > 0) {
+                                a -= (2.0 * kx - 1.0) * rx * D[d_tab.idx3[kx - 1][ky][kz]];
+                                if (kx > 1) a -= (kx - 1.0) * (kx - 1.0) * D[d_tab.idx3[kx - 2][ky][kz]];
+                                if (ky > 0) {
+                                    a -= 2.0 * ky * ry * D[d_tab.idx3[kx][ky - 1][kz]];
+                                    if (ky > 1) a -= ky * (ky - 1.0) * D[d_tab.idx3[kx][ky - 2][kz]];
+                                }
+                                if (kz > 0) {
+                                    a -= 2.0 * kz * rz * D[d_tab.idx3[kx][ky][kz - 1]];
+                                    if (kz > 1) a -= kz * (kz - 1.0) * D[d_tab.idx3[kx][ky][kz - 2]];
+                                }
+                            } else if (ky > 0) {
+                                a -= (2.0 * ky - 1.0) * ry * D[d_tab.idx3[kx][ky - 1][kz]];
+                                if (ky > 1) a -= (ky - 1.0) * (ky - 1.0) * D[d_tab.idx3[kx][ky - 2][kz]];
+                                if (kz > 0) {
+                                    a -= 2.0 * kz * rz * D[d_tab.idx3[kx][ky][kz - 1]];
+                                    if (kz > 1) a -= kz * (kz - 1.0) * D[d_tab.idx3[kx][ky][kz - 2]];
+                                }
+                            } else {
+                                a -= (2.0 * kz - 1.0) * rz * D[d_tab.idx3[kx][ky][kz - 1]];
+                                if (kz > 1) a -= (kz - 1.0) * (kz - 1.0) * D[d_tab.idx3[kx][ky][kz - 2]];
+                            }
+                            D[idx] = a * inv_r2;
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    for (int m = lane; m < nc; m += 32) Ms[m] = 0.0;
+                    for (int m = lane; m <= nc; m += 32) D[m] = 0.0;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < (kMaxChunks + NT - 1) / NT; q++) {
+                const int c = threadIdx.x + q * NT;
+                if (q < nslot && c < nch) {
+                    const uint32_t *tt = sterm + c * kChunk;
+                    double a = acc[q];
+                    for (int g = 0; g < gcount; g++) {
+                        const double *D = sD + g * (nc + 1);
+                        const double *Ms = sM + g * nc;
+#pragma unroll
+                        for (int e = 0; e < kChunk; e++) {
+                            const uint32_t v = tt[e];
+                            a = fma(Ms[v & 0xFFFFu], D[v >> 16], a);
+                        }
+                    }
+                    acc[q] = a;
+                }
+            }
+        }
+        // fold chunk partials per output in a fixed order; one add per L_n
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < (kMaxChunks + NT - 1) / NT; q++) {
+            const int c = threadIdx.x + q * NT;
+            if (q < nslot && c < nch) spart[c] = acc[q];
+        }
+        __syncthreads();
+        for (int n = threadIdx.x; n < nc; n += NT) {
+            double v = 0.0;
+            for (int c = d_terms.first_chunk[n]; c < d_terms.first_chunk[n + 1]; c++) v += spart[c];
+            L[(int64_t)t * nc + n] += v / d_tab.mfact[n];
+        }
+    }
+}
+
 }  // namespace fmm
 
 using namespace fmm;
@@ -222,9 +392,38 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
         case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
         case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
         case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
-        default:
-            m2l_warp<<<grid_for((int64_t)ncells * 32, kM2LWarps * 32, 148 * 16), kM2LWarps * 32, 0, s>>>(
-                p, ncells, rows, src, ctr, M, L); fmm::note_launch();
+        default: {
+            // high orders: block kernel over a load-balanced term table
+            static int table_p[64];  // per device: the table is a device symbol
+            static bool init = false;
+            static TermTable host_tab;
+            if (!init) {
+                for (int i = 0; i < 64; i++) table_p[i] = -1;
+                init = true;
+            }
+            int dev = 0;
+            cudaGetDevice(&dev);
+            dev &= 63;
+            build_term_table(p, host_tab);
+            if (table_p[dev] != p) {
+                if (cudaMemcpyToSymbolAsync(d_terms, &host_tab, sizeof(TermTable), 0, cudaMemcpyHostToDevice, s) !=
+                    cudaSuccess)
+                    return cuda_status("fmm_m2l_csr table");
+                if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_m2l_csr table sync");
+                table_p[dev] = p;
+            }
+            constexpr int NT = kBlkWarps * 32;
+            const int nc = ncoef(p), nch = host_tab.nchunks;
+            const size_t smem = (size_t)((nch * kChunk + 1) & ~1) * 4 +
+                                (size_t)kBlkWarps * (2 * nc + 1) * 8 + (size_t)nch * 8;
+            static size_t smem_set = 0;
+            if (smem > smem_set) {
+                cudaFuncSetAttribute(m2l_block<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                smem_set = smem;
+            }
+            m2l_block<NT><<<grid_for(ncells, 1, 148 * 4), NT, smem, s>>>(p, ncells, rows, src, ctr, M, L);
+            fmm::note_launch();
+        }
     }
     FMM_CUDA_CHECK("fmm_m2l_csr");
     return FMM_OK;
