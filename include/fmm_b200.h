@@ -185,16 +185,20 @@ FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs,
 /* P2P work decomposition: merge Morton-adjacent source leaves of every
  * target-leaf row into contiguous body runs and split off the self leaf.
  * Rows are the leaves whose bodies lie in [body_lo, body_hi).
- * Outputs the leaf rows (leaf_rows[r] = target leaf), run_off[r..r+1],
- * runs as int4 {bstart, bend, self_flag, 0}; host_nruns = total runs.
+ * Outputs the leaf rows (leaf_rows[r] = target leaf, sized ncells),
+ * run_off[r..r+1] (sized ncells + 1), runs as int4 {bstart, bend,
+ * self_flag, 0}.  Host round trips are optional: with host_nruns and
+ * host_nleaf_rows NULL the call never synchronises (cap_runs must then be
+ * >= the number of P2P pairs, an upper bound on runs); the row count is
+ * written to dev_nrows for fmm_p2p.
  * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
  * into dev_stats[2] (src/_taylor.py:366-407 accounting). */
 FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
                  int32_t body_lo, int32_t body_hi,
                  const int64_t *rows, const int32_t *src_sorted, const double *xs, const double *ys,
                  const double *zs, int32_t *leaf_rows, int64_t *run_off, void *runs, int64_t cap_runs,
-                 int64_t *host_nruns, int32_t *host_nleaf_rows, unsigned long long *dev_stats,
-                 void *ws, size_t ws_bytes, void *stream);
+                 int64_t *host_nruns, int32_t *host_nleaf_rows, int32_t *dev_nrows,
+                 unsigned long long *dev_stats, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- executors (src/traversal.py:500-548) ------------------------------ */
 
@@ -206,9 +210,12 @@ FMM_API int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_
  * body copy b32; FMM_PREC_FP64 reads the float64 SoA.  Results are STORED
  * (not accumulated) into phi/fx/fy/fz for every body of a planned leaf row.
  * use_rsqrt (FP64 only) mirrors src/_taylor.py:318-323.
+ * nrows bounds the grid; when dev_nrows is given the kernels stop at the
+ * device-side row count (written by fmm_p2p_plan) -- no host round trip.
  * dev_flag[0] is set when a non-finite sum was produced (FP32 collision of
  * distinct bodies); the caller reruns with safe=1. */
-FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *leaf_rows,
+FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *dev_nrows,
+            const int32_t *leaf_rows,
             const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
             const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
             const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);

@@ -428,7 +428,7 @@ constexpr int kMaxUnits = 32;
 
 template <bool SAFE, bool ANCHOR>
 __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
-    int32_t nrows, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
+    int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const float4 *__restrict__ b, const float4 *__restrict__ blo, double *phi, double *fx, double *fy,
     double *fz, int *flag) {
@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
     __shared__ int32_t stotal;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float4 *ring = &rings[w][lane];
+    const int32_t nrows = nrows_dev ? *nrows_dev : nrows_host;
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
         const int32_t t = leaf_rows[row];
         const int32_t ts = start[t], cnt = end[t] - ts;
@@ -534,12 +535,13 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
 // ---- FP64 variant (parity mode) ------------------------------------------
 template <int K>
 __global__ void __launch_bounds__(kP2PWarps * 32) p2p_f64_kernel(
-    int32_t nrows, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
+    int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const double *__restrict__ xs, const double *__restrict__ ys, const double *__restrict__ zs,
     const double *__restrict__ qs, int use_rsqrt, double *phi, double *fx, double *fy, double *fz) {
     __shared__ double red[kP2PWarps][4 * K];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int32_t nrows = nrows_dev ? *nrows_dev : nrows_host;
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
         const int32_t t = leaf_rows[row];
         const int32_t ts = start[t], cnt = end[t] - ts;
@@ -640,7 +642,8 @@ __global__ void __launch_bounds__(kP2PWarps * 32) p2p_f64_kernel(
 
 using namespace fmm;
 
-extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *leaf_rows,
+extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *dev_nrows,
+                       const int32_t *leaf_rows,
                        const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
                        const double *xs, const double *ys, const double *zs, const double *qs,
                        const void *b32, const void *b32lo, double *phi, double *fx, double *fy, double *fz,
@@ -654,11 +657,11 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, co
         if (anch && !b32lo) { set_error("anchored fp32 P2P needs the float4 residual copy"); return FMM_ERR_INVALID; }
         auto kern = anch ? (safe ? p2p_f32_kernel<true, true> : p2p_f32_kernel<false, true>)
                          : (safe ? p2p_f32_kernel<true, false> : p2p_f32_kernel<false, false>);
-        kern<<<grid, kP2PWarps * 32, 0, s>>>(nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
+        kern<<<grid, kP2PWarps * 32, 0, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
                                              (const float4 *)b32, (const float4 *)b32lo, phi, fx, fy, fz,
                                              dev_flag); fmm::note_launch();
     } else if (precision == FMM_PREC_FP64) {
-        p2p_f64_kernel<4><<<grid, kP2PWarps * 32, 0, s>>>(nrows, leaf_rows, start, end, run_off,
+        p2p_f64_kernel<4><<<grid, kP2PWarps * 32, 0, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off,
                                                           (const int4 *)runs, xs, ys, zs, qs, use_rsqrt, phi,
                                                           fx, fy, fz); fmm::note_launch();
     } else {

@@ -25,13 +25,19 @@ __device__ inline bool run_start(const int32_t *src, int64_t k, int64_t k0, int3
     return s == t || sp == t || start[s] != end[sp];
 }
 
-__global__ void plan_count(int32_t nrows, const int32_t *__restrict__ leaf_rows,
+__global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells, const int32_t *__restrict__ leaf_rows,
                            const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
                            const int32_t *__restrict__ start, const int32_t *__restrict__ end,
                            int64_t *nr) {
     const int lane = threadIdx.x & 31;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
+    const int32_t nrows = *nrows_dev;
+    // rows past the device count get 0 so one scan over ncells + 1 works
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < ncells;
          r += (gridDim.x * blockDim.x) >> 5) {
+        if (r >= nrows) {
+            if (lane == 0) nr[r] = 0;
+            continue;
+        }
         const int32_t t = leaf_rows[r];
         const int64_t k0 = rows[t], k1 = rows[t + 1];
         int64_t cnt = 0;
@@ -42,14 +48,15 @@ __global__ void plan_count(int32_t nrows, const int32_t *__restrict__ leaf_rows,
         }
         if (lane == 0) nr[r] = cnt;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) nr[nrows] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) nr[ncells] = 0;
 }
 
-__global__ void plan_write(int32_t nrows, const int32_t *__restrict__ leaf_rows,
+__global__ void plan_write(const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
                            const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
                            const int32_t *__restrict__ start, const int32_t *__restrict__ end,
                            const int64_t *__restrict__ run_off, int4 *runs) {
     const int lane = threadIdx.x & 31;
+    const int32_t nrows = *nrows_dev;
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
          r += (gridDim.x * blockDim.x) >> 5) {
         const int32_t t = leaf_rows[r];
@@ -75,12 +82,13 @@ __global__ void plan_write(int32_t nrows, const int32_t *__restrict__ leaf_rows,
 }
 
 // per target row: sum |t| |s| - self |t|, and coincident ordered pairs
-__global__ void plan_stats(int32_t nrows, const int32_t *__restrict__ leaf_rows,
+__global__ void plan_stats(const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
                            const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
                            const int32_t *__restrict__ start, const int32_t *__restrict__ end,
                            const double *__restrict__ xs, const double *__restrict__ ys,
                            const double *__restrict__ zs, unsigned long long *stats) {
     const int lane = threadIdx.x & 31;
+    const int32_t nrows = *nrows_dev;
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
          r += (gridDim.x * blockDim.x) >> 5) {
         const int32_t t = leaf_rows[r];
@@ -128,7 +136,8 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
                             const int64_t *rows, const int32_t *src_sorted, const double *xs,
                             const double *ys, const double *zs, int32_t *leaf_rows, int64_t *run_off,
                             void *runs, int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows,
-                            unsigned long long *dev_stats, void *ws, size_t ws_bytes, void *stream) {
+                            int32_t *dev_nrows, unsigned long long *dev_stats, void *ws, size_t ws_bytes,
+                            void *stream) {
     cudaStream_t s = as_stream(stream);
     Arena ar(ws, ws_bytes);
     int32_t *nsel = ar.take<int32_t>(1);
@@ -141,25 +150,28 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     cub::DeviceSelect::Flagged(nullptr, need, it, flag, leaf_rows, nsel, ncells, s);
     if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
     cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, leaf_rows, nsel, ncells, s);
-    int32_t nrows = 0;
-    cudaMemcpyAsync(&nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
-    *host_nleaf_rows = nrows;
-    const int g = grid_for((int64_t)nrows * 32, 256, 148 * 16);
-    plan_count<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, nr); fmm::note_launch();
+    // leaf_rows is sized ncells: the kernels read the row count on the device
+    const int g = grid_for((int64_t)ncells * 32, 256, 148 * 16);
+    plan_count<<<g, 256, 0, s>>>(nsel, ncells, leaf_rows, rows, src_sorted, start, end, nr); fmm::note_launch();
     need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, nrows + 1, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, ncells + 1, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
-    cub::DeviceScan::ExclusiveSum(ar.rest(), need, nr, run_off, nrows + 1, s);
-    int64_t total = 0;
-    cudaMemcpyAsync(&total, run_off + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
-    *host_nruns = total;
-    if (total > cap_runs) { set_error("run capacity %lld < %lld", (long long)cap_runs, (long long)total); return FMM_ERR_CAPACITY; }
-    plan_write<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs); fmm::note_launch();
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, nr, run_off, ncells + 1, s);
+    if (host_nleaf_rows || host_nruns) {  // optional host view (synchronises)
+        int32_t nrows = 0;
+        int64_t total = 0;
+        cudaMemcpyAsync(&nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&total, run_off + ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
+        if (host_nleaf_rows) *host_nleaf_rows = nrows;
+        if (host_nruns) *host_nruns = total;
+        if (total > cap_runs) { set_error("run capacity %lld < %lld", (long long)cap_runs, (long long)total); return FMM_ERR_CAPACITY; }
+    }
+    if (dev_nrows) cudaMemcpyAsync(dev_nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    plan_write<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs); fmm::note_launch();
     if (dev_stats) {
         cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
-        plan_stats<<<g, 256, 0, s>>>(nrows, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, dev_stats); fmm::note_launch();
+        plan_stats<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, dev_stats); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_p2p_plan");
     return FMM_OK;

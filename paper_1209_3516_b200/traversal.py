@@ -186,25 +186,21 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     p2p_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     _lib.call("fmm_pairs_to_csr", P(p2p_t), P(p2p_s), done_p2p, ncells, P(p2p_src), P(p2p_rows), wsp, wsb, st)
     del p2p_t, p2p_s, m2l_t, m2l_s
-    # P2P run plan + the reference's pair counters
+    # P2P run plan + the reference's pair counters (no host round trip:
+    # runs <= pairs, and the row count stays on the device)
     leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
     run_off = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     dev_stats = torch.zeros(2, dtype=torch.int64, device=dev)
-    cap_runs = min(max(done_p2p, 1), tree.nleaves * 96 + 1024)
-    nruns = C.c_int64(0)
-    nrows = C.c_int32(0)
-    while True:
-        runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
-        try:
-            _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
-                      P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(leaf_rows), P(run_off), P(runs),
-                      cap_runs, C.byref(nruns), C.byref(nrows), P(dev_stats), wsp, wsb, st)
-            break
-        except _lib.CapacityError:
-            cap_runs = int(nruns.value)
+    dev_nrows = torch.empty(1, dtype=i32, device=dev)
+    cap_runs = max(done_p2p, 1)
+    runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
+    _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
+              P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(leaf_rows), P(run_off), P(runs), cap_runs,
+              None, None, P(dev_nrows), P(dev_stats), wsp, wsb, st)
+    nrows_bound = tree.nleaves
     return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
-                 p2p_rows=p2p_rows, leaf_rows=leaf_rows, nrows=int(nrows.value), run_off=run_off, runs=runs,
-                 nruns=int(nruns.value), dev_stats=dev_stats, peak_frontier=peak)
+                 p2p_rows=p2p_rows, leaf_rows=leaf_rows, nrows=nrows_bound, dev_nrows=dev_nrows, run_off=run_off,
+                 runs=runs, dev_stats=dev_stats, peak_frontier=peak)
 
 
 def run_m2l(tree: Tree, lists: Lists, p: int) -> None:
@@ -221,7 +217,8 @@ def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, s
         prec = _lib.PREC_FP32 if tree.fp32_exact else _lib.PREC_FP32_ANCHORED
     else:
         prec = _lib.PREC_FP64
-    _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), lists.nrows, P(lists.leaf_rows), P(tree.d_start),
+    _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), lists.nrows, P(lists.dev_nrows), P(lists.leaf_rows),
+              P(tree.d_start),
               P(tree.d_end), P(lists.run_off), P(lists.runs), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_q),
               P(tree.d_b32), P(tree.d_b32lo), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag),
               _lib.stream_handle())

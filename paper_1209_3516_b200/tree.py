@@ -185,8 +185,9 @@ class Tree:
             h.copy_(a, non_blocking=True)
             host.append(h)
         if self._host_input is not None:
-            src = [np.array(a, dtype=np.float64) for a in
-                   (self._host_input.x, self._host_input.y, self._host_input.z, self._host_input.q)]
+            # the caller's own arrays, in their stored precision (a float32
+            # cloud stays float32 and is upcast lazily on access)
+            src = [np.array(a) for a in self._host_input.host_inputs()]
         else:
             src = None
         torch.cuda.current_stream(self.device).synchronize()

@@ -53,6 +53,6 @@ got = [tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz]
 rel = [float(torch.linalg.norm(g - r) / torch.linalg.norm(r)) for g, r in zip(got, ref)]
 t = float(np.median(times))
 print(json.dumps({"config": args.config, "n": n, "precision": args.precision, "p2p_pairs": pairs,
-                  "nrows": lists.nrows, "nruns": lists.nruns, "ms": 1e3 * t, "min_ms": 1e3 * min(times),
+                  "nrows": int(lists.dev_nrows.item()), "ms": 1e3 * t, "min_ms": 1e3 * min(times),
                   "ginteractions_per_s": pairs / t / 1e9, "tflops_20": 20 * pairs / t / 1e12,
                   "rel_l2_vs_fp64": rel, "lib": os.environ.get("FMM_B200_LIB", "default")}))
