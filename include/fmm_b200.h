@@ -94,27 +94,25 @@ FMM_API int fmm_permute_bodies(const int32_t *perm, const double *x, const doubl
                        const double *q, int64_t n, double *xs, double *ys, double *zs, double *qs,
                        void *b32, void *b32lo, int *dev_inexact, void *stream);
 
-/* One level of the level-synchronous carve (src/tree.py:43-77 _build_rec).
- * node[i] = id of the still-splitting level-`level` cell holding body i, or
- * -1.  Emits the level+1 children as cells [base, base+count) (BFS ids) and
- * updates node[].  host_count receives the number of new cells;
- * FMM_ERR_CAPACITY when base+count > cap (host_count still exact);
- * FMM_ERR_MAX_DEPTH when a depth-21 cell holds > ncrit bodies and
- * !allow_big.  cell arrays are indexed by BFS id. */
-FMM_API int fmm_build_level(const uint64_t *keys, int32_t *node, int64_t n, int level, int32_t ncrit,
-                    int allow_big, int32_t base, int32_t cap, int32_t *c_start, int32_t *c_end,
-                    int32_t *c_parent, int8_t *c_level, uint64_t *c_key, uint8_t *c_split,
-                    int32_t *host_count, void *ws, size_t ws_bytes, void *stream);
+/* Single-pass carve, step 1 (replaces the fmm_build_level loop): per body,
+ * its leaf level and the number of cells it starts; cbase = exclusive scan
+ * of those counts = pre-order id of the first cell starting at that body.
+ * host_level_hist[23] receives cells per level 0..21 and, in slot 22, the
+ * number of leaves; host_ncells the total
+ * (synchronises once).  FMM_ERR_MAX_DEPTH when a depth-21 cell holds more
+ * than ncrit bodies and !allow_big (src/tree.py:419-423). */
+FMM_API int fmm_carve_count(const uint64_t *keys, int64_t n, int32_t ncrit, int allow_big, int32_t *cbase,
+                    int8_t *leaf_level, int32_t *host_level_hist, int32_t *host_ncells, void *ws, size_t ws_bytes,
+                    void *stream);
 
-/* Renumber BFS cells into the reference's pre-order and derive children
- * (indexed by octant, -1 when empty), parent, sub_end, leaf, and the
- * per-body leaf index.  pre_of_bfs[b] = pre-order id of BFS cell b. */
-FMM_API int fmm_finalize_cells(int32_t ncells, int64_t n, const int32_t *b_start, const int32_t *b_end,
-                       const int32_t *b_parent, const int8_t *b_level, const uint64_t *b_key,
-                       const uint8_t *b_split, int32_t *pre_of_bfs, int32_t *children,
-                       int32_t *parent, int8_t *level, uint64_t *key, int32_t *start, int32_t *end,
-                       int32_t *sub_end, uint8_t *leaf, int32_t *body_leaf, void *ws,
-                       size_t ws_bytes, void *stream);
+/* Single-pass carve, step 2: writes every cell array in the reference's
+ * pre-order (children by octant, -1 when empty), cells_by_level grouped by
+ * level using host_level_off[23] (exclusive offsets from the histogram),
+ * and the per-body leaf index. */
+FMM_API int fmm_carve_emit(const uint64_t *keys, int64_t n, const int32_t *cbase, const int8_t *leaf_level,
+                   int32_t ncells, const int32_t *host_level_off, int32_t *children, int32_t *parent,
+                   int8_t *level, uint64_t *key, int32_t *start, int32_t *end, int32_t *sub_end, uint8_t *leaf,
+                   int32_t *cells_by_level, int32_t *body_leaf, void *ws, size_t ws_bytes, void *stream);
 
 /* Cubic/geometric cell geometry, bit-exact (src/tree.py:80-160). */
 FMM_API int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, const int32_t *start,

@@ -38,8 +38,8 @@ SIGNATURES = {
     "fmm_morton_keys": [P, P, P, I64, P, P, P, P],
     "fmm_sort_pairs_u64": [P, P, P, P, I64, INT, P, SZ, P],
     "fmm_permute_bodies": [P, P, P, P, P, I64, P, P, P, P, P, P, P, P],
-    "fmm_build_level": [P, P, I64, INT, I32, INT, I32, I32, P, P, P, P, P, P, P, P, SZ, P],
-    "fmm_finalize_cells": [I32, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
+    "fmm_carve_count": [P, I64, I32, INT, P, P, P, P, P, SZ, P],
+    "fmm_carve_emit": [P, I64, P, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
     "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],

@@ -6,13 +6,11 @@
 //
 // Layout: bodies are float64 SoA in Morton order (plus a float4 copy for
 // the FP32 P2P path); cells are SoA int32/uint64/double arrays indexed by
-// the reference's pre-order cell id.  The carve is level-synchronous: the
-// children of all splitting level-L cells are the runs of equal level-(L+1)
-// key prefix among their bodies, found with one flag pass, one scan and one
-// binary search per child (the reference's searchsorted, tree.py:67).
-// Pre-order numbering is then a sort by (start, level): a cell precedes its
-// descendants (same start, lower level) and every later sibling subtree
-// (larger start).
+// the reference's pre-order cell id.  The carve is a single pass over the
+// sorted keys (see "single-pass carve" below): pre-order is the order by
+// (start, level) -- a cell precedes its descendants (same start, lower
+// level) and every later sibling subtree (larger start) -- so one scan of
+// per-body cell counts numbers every cell.
 #include <cub/cub.cuh>
 #include <atomic>
 #include <stdarg.h>
@@ -165,109 +163,132 @@ __global__ void permute_kernel(const int32_t *__restrict__ perm, const double *_
 }
 
 // ---------------------------------------------------------------------------
-// level-synchronous carve (src/tree.py:43-77)
+// single-pass carve (replaces the level loop): for sorted keys, body i's leaf
+// level l(i) is the first level whose cell around i holds <= ncrit bodies
+// (or 21); i starts a cell at every level in [ldiff(i), l(i)], where
+// ldiff(i) is the first level at which key i differs from key i-1.  An
+// exclusive scan of the per-body counts numbers the cells in (start, level)
+// order -- exactly the reference's pre-order (src/tree.py:43-77).
 // ---------------------------------------------------------------------------
-__global__ void level_flags(const uint64_t *__restrict__ keys, const int32_t *__restrict__ node,
-                            int64_t n, int shift, int32_t *flags) {
+__device__ __forceinline__ int first_diff_level(const uint64_t *keys, int64_t i) {
+    if (i == 0) return 0;
+    const uint64_t x = keys[i] ^ keys[i - 1];
+    if (x == 0) return MAX_LEVEL + 1;  // same depth-21 cell: starts nothing
+    const int b = 63 - __clzll((long long)x);
+    return MAX_LEVEL - b / 3;
+}
+
+// size of the run of equal level-L prefix around i, clipped to the window
+// [i - ncrit, i + ncrit]: <= ncrit exactly when the true cell holds <= ncrit
+__device__ __forceinline__ int64_t run_in_window(const uint64_t *keys, int64_t n, int64_t i, int L, int ncrit) {
+    const int sh = 3 * (MAX_LEVEL - L);
+    const uint64_t pre = sh >= 64 ? 0 : keys[i] >> sh;
+    int64_t wl = i - ncrit < 0 ? 0 : i - ncrit;
+    int64_t wh = i + ncrit + 1 > n ? n : i + ncrit + 1;
+    int64_t a = wl, b = i;  // first index in [wl, i] with the prefix
+    while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if ((sh >= 64 ? 0 : keys[m] >> sh) < pre) a = m + 1;
+        else b = m;
+    }
+    const int64_t lo = a;
+    a = i + 1;
+    b = wh;  // first index in (i, wh) past the prefix
+    while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if ((sh >= 64 ? 0 : keys[m] >> sh) <= pre) a = m + 1;
+        else b = m;
+    }
+    return a - lo;
+}
+
+__global__ void carve_count(const uint64_t *__restrict__ keys, int64_t n, int ncrit, int allow_big,
+                            int32_t *ccount, int8_t *leaf_level, int32_t *level_hist, int *err) {
+    __shared__ int32_t hist[MAX_LEVEL + 2];
+    for (int k = threadIdx.x; k < MAX_LEVEL + 2; k += blockDim.x) hist[k] = 0;
+    __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int f = 0;
-        if (node[i] >= 0) f = (i == 0) || ((keys[i] >> shift) != (keys[i - 1] >> shift));
-        flags[i] = f;
+        // smallest L in [0, 21] with run <= ncrit (monotone in L), else 21
+        int lo = 0, hi = MAX_LEVEL;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (run_in_window(keys, n, i, mid, ncrit) <= ncrit) hi = mid;
+            else lo = mid + 1;
+        }
+        const int leafL = lo;
+        if (leafL == MAX_LEVEL && !allow_big && run_in_window(keys, n, i, MAX_LEVEL, ncrit) > ncrit)
+            atomicExch(err, 1);
+        const int ld = first_diff_level(keys, i);
+        const int c = leafL >= ld ? leafL - ld + 1 : 0;
+        ccount[i] = c;
+        leaf_level[i] = (int8_t)leafL;
+        for (int L = ld; L <= leafL; L++) atomicAdd(&hist[L], 1);
+        if (c > 0) atomicAdd(&hist[MAX_LEVEL + 1], 1);  // body starts a leaf
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < MAX_LEVEL + 2; k += blockDim.x)
+        if (hist[k]) atomicAdd(&level_hist[k], hist[k]);
 }
 
-__device__ inline int64_t lower_bound_u64(const uint64_t *a, int64_t lo, int64_t hi, uint64_t v) {
-    while (lo < hi) {
-        int64_t mid = lo + ((hi - lo) >> 1);
-        if (a[mid] < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-__global__ void level_emit(const uint64_t *__restrict__ keys, const int32_t *__restrict__ node,
-                           const int32_t *__restrict__ flags, const int32_t *__restrict__ incl, int64_t n,
-                           int level, int shift, int32_t ncrit, int allow_big, int32_t base,
-                           int32_t *c_start, int32_t *c_end, int32_t *c_parent, int8_t *c_level,
-                           uint64_t *c_key, uint8_t *c_split, int *err) {
-    const int clev = level + 1;
+__global__ void carve_emit(const uint64_t *__restrict__ keys, int64_t n, const int32_t *__restrict__ cbase,
+                           const int8_t *__restrict__ leaf_level, int32_t *level_cursor, int32_t *children,
+                           int32_t *parent, int8_t *level, uint64_t *key, int32_t *start, int32_t *end,
+                           uint8_t *leaf, int32_t *cells_by_level) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        if (!flags[i]) continue;
-        int32_t c = base + incl[i] - 1;
-        uint64_t pre = shift >= 64 ? 0 : (keys[i] >> shift);
-        int64_t e = (clev == 0) ? n : lower_bound_u64(keys, i, n, (pre + 1) << shift);
-        int64_t cnt = e - i;
-        c_start[c] = (int32_t)i;
-        c_end[c] = (int32_t)e;
-        c_parent[c] = (clev == 0) ? -1 : node[i];
-        c_level[c] = (int8_t)clev;
-        c_key[c] = pre;
-        bool split = cnt > ncrit && clev < MAX_LEVEL;
-        c_split[c] = split ? 1 : 0;
-        if (cnt > ncrit && clev == MAX_LEVEL && !allow_big) atomicExch(err, 1);
+        const int ld = first_diff_level(keys, i);
+        const int leafL = leaf_level[i];
+        for (int L = ld; L <= leafL; L++) {
+            const int32_t c = cbase[i] + (L - ld);
+            const int sh = 3 * (MAX_LEVEL - L);
+            const uint64_t pre = sh >= 64 ? 0 : keys[i] >> sh;
+            int64_t e = n;
+            if (L > 0) {  // first body past this cell's prefix
+                const uint64_t lim = (pre + 1) << sh;
+                int64_t a = i + 1, b = n;
+                while (a < b) {
+                    const int64_t m = (a + b) >> 1;
+                    if (keys[m] < lim) a = m + 1;
+                    else b = m;
+                }
+                e = a;
+            }
+            start[c] = (int32_t)i;
+            end[c] = (int32_t)e;
+            level[c] = (int8_t)L;
+            key[c] = pre;
+            leaf[c] = L == leafL ? 1 : 0;
+            int32_t pc = -1;
+            if (L > 0) {
+                if (L - 1 >= ld) {
+                    pc = c - 1;  // the parent starts at the same body
+                } else {     // the parent starts at the first body of the level-(L-1) prefix
+                    const int psh = 3 * (MAX_LEVEL - (L - 1));
+                    const uint64_t ppre = keys[i] >> psh;
+                    int64_t a = 0, b = i;
+                    while (a < b) {
+                        const int64_t m = (a + b) >> 1;
+                        if ((keys[m] >> psh) < ppre) a = m + 1;
+                        else b = m;
+                    }
+                    pc = cbase[a] + (L - 1 - first_diff_level(keys, a));
+                }
+                children[pc * 8 + (int)(pre & 7ull)] = c;
+            }
+            parent[c] = pc;
+            cells_by_level[atomicAdd(&level_cursor[L], 1)] = c;
+        }
     }
 }
 
-__global__ void level_update(int32_t *node, const int32_t *__restrict__ incl, int64_t n, int32_t base,
-                             const uint8_t *__restrict__ c_split) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (node[i] < 0) continue;
-        int32_t c = base + incl[i] - 1;
-        node[i] = c_split[c] ? c : -1;
-    }
-}
-
-__global__ void fill_i32(int32_t *a, int64_t n, int32_t v) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        a[i] = v;
-}
-
-// ---------------------------------------------------------------------------
-// pre-order renumbering
-// ---------------------------------------------------------------------------
-__global__ void preorder_keys(int32_t ncells, const int32_t *b_start, const int8_t *b_level,
-                              uint64_t *sk, int32_t *iota) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncells; i += gridDim.x * blockDim.x) {
-        sk[i] = ((uint64_t)(uint32_t)b_start[i] << 5) | (uint64_t)(uint8_t)b_level[i];
-        iota[i] = i;
-    }
-}
-
-__global__ void preorder_gather(int32_t ncells, const int32_t *order, const int32_t *b_start,
-                                const int32_t *b_end, const int8_t *b_level, const uint64_t *b_key,
-                                const uint8_t *b_split, int32_t *pre_of_bfs, int8_t *level,
-                                uint64_t *key, int32_t *start, int32_t *end, uint8_t *leaf,
-                                int32_t *children) {
+__global__ void carve_links(int32_t ncells, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                            int32_t *sub_end) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncells; j += gridDim.x * blockDim.x) {
-        int32_t b = order[j];
-        pre_of_bfs[b] = j;
-        level[j] = b_level[b];
-        key[j] = b_key[b];
-        start[j] = b_start[b];
-        end[j] = b_end[b];
-        leaf[j] = b_split[b] ? 0 : 1;
-        for (int o = 0; o < 8; o++) children[j * 8 + o] = -1;
-    }
-}
-
-__global__ void preorder_links(int32_t ncells, const int32_t *order, const int32_t *b_parent,
-                               const int32_t *pre_of_bfs, const uint64_t *key, const int32_t *start,
-                               const int32_t *end, int32_t *parent, int32_t *children,
-                               int32_t *sub_end) {
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncells; j += gridDim.x * blockDim.x) {
-        int32_t pb = b_parent[order[j]];
-        int32_t pj = pb >= 0 ? pre_of_bfs[pb] : -1;
-        parent[j] = pj;
-        if (pj >= 0) children[pj * 8 + (int)(key[j] & 7ull)] = j;
-        // first later cell whose body range starts at or after our end
-        int32_t e = end[j];
+        const int32_t e = end[j];
         int lo = j + 1, hi = ncells;
         while (lo < hi) {
-            int mid = (lo + hi) >> 1;
+            const int mid = (lo + hi) >> 1;
             if (start[mid] < e) lo = mid + 1;
             else hi = mid;
         }
@@ -475,82 +496,56 @@ int fmm_permute_bodies(const int32_t *perm, const double *x, const double *y, co
     return FMM_OK;
 }
 
-int fmm_build_level(const uint64_t *keys, int32_t *node, int64_t n, int level, int32_t ncrit,
-                    int allow_big, int32_t base, int32_t cap, int32_t *c_start, int32_t *c_end,
-                    int32_t *c_parent, int8_t *c_level, uint64_t *c_key, uint8_t *c_split,
-                    int32_t *host_count, void *ws, size_t ws_bytes, void *stream) {
+int fmm_carve_count(const uint64_t *keys, int64_t n, int32_t ncrit, int allow_big, int32_t *cbase,
+                    int8_t *leaf_level, int32_t *host_level_hist, int32_t *host_ncells, void *ws, size_t ws_bytes,
+                    void *stream) {
     cudaStream_t s = as_stream(stream);
     Arena ar(ws, ws_bytes);
-    int32_t *flags = ar.take<int32_t>(n);
-    int32_t *incl = ar.take<int32_t>(n);
-    int *err = ar.take<int>(4);
-    if (!flags || !incl || !err) { set_error("workspace too small"); return FMM_ERR_INVALID; }
-    void *tmp = ar.rest();
-    size_t tmp_bytes = ar.left();
-    int g = grid_for(n, 256);
-    if (level < 0) fill_i32<<<g, 256, 0, s>>>(node, n, 0); fmm::note_launch();
-    const int clev = level + 1;
-    const int shift = 3 * (MAX_LEVEL - clev);
-    level_flags<<<g, 256, 0, s>>>(keys, node, n, shift >= 64 ? 63 : shift, flags); fmm::note_launch();
-    size_t need = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, need, flags, incl, n, s);
-    if (need > tmp_bytes) { set_error("scan workspace"); return FMM_ERR_INVALID; }
-    cub::DeviceScan::InclusiveSum(tmp, need, flags, incl, n, s);
-    int32_t count = 0;
-    cudaMemcpyAsync(&count, incl + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    int32_t *ccount = ar.take<int32_t>(n);
+    int32_t *hist = ar.take<int32_t>(MAX_LEVEL + 2);
+    int *err = ar.take<int>(1);
+    int32_t *last = ar.take<int32_t>(2);
+    if (!ccount || !hist || !err || !last) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    cudaMemsetAsync(hist, 0, sizeof(int32_t) * (MAX_LEVEL + 2), s);
     cudaMemsetAsync(err, 0, sizeof(int), s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_build_level sync");
-    *host_count = count;
-    if (count == 0) return FMM_OK;
-    if ((int64_t)base + count > cap) {
-        set_error("cell capacity %d < %lld", cap, (long long)base + count);
-        return FMM_ERR_CAPACITY;
+    carve_count<<<grid_for(n, 256), 256, 0, s>>>(keys, n, ncrit, allow_big, ccount, leaf_level, hist, err); fmm::note_launch();
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, ccount, cbase, n, s);
+    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, ccount, cbase, n, s);
+    int32_t tail[2] = {0, 0};
+    int herr = 0;
+    cudaMemcpyAsync(&tail[0], cbase + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&tail[1], ccount + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(host_level_hist, hist, sizeof(int32_t) * (MAX_LEVEL + 2), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_carve_count sync");
+    *host_ncells = tail[0] + tail[1];
+    if (herr) {
+        set_error("max depth exceeded: more than ncrit=%d bodies share one depth-%d grid cell "
+                  "(pass allow_oversized_leaves=True to keep them in one leaf)",
+                  ncrit, MAX_LEVEL);
+        return FMM_ERR_MAX_DEPTH;
     }
-    level_emit<<<g, 256, 0, s>>>(keys, node, flags, incl, n, level, shift, ncrit, allow_big, base,
-                                 c_start, c_end, c_parent, c_level, c_key, c_split, err); fmm::note_launch();
-    level_update<<<g, 256, 0, s>>>(node, incl, n, base, c_split); fmm::note_launch();
-    FMM_CUDA_CHECK("fmm_build_level");
-    if (clev == MAX_LEVEL) {
-        int h = 0;
-        cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s);
-        if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_build_level sync");
-        if (h) {
-            set_error("max depth exceeded: more than ncrit=%d bodies share one depth-%d grid cell "
-                      "(pass allow_oversized_leaves=True to keep them in one leaf)",
-                      ncrit, MAX_LEVEL);
-            return FMM_ERR_MAX_DEPTH;
-        }
-    }
+    FMM_CUDA_CHECK("fmm_carve_count");
     return FMM_OK;
 }
 
-int fmm_finalize_cells(int32_t ncells, int64_t n, const int32_t *b_start, const int32_t *b_end,
-                       const int32_t *b_parent, const int8_t *b_level, const uint64_t *b_key,
-                       const uint8_t *b_split, int32_t *pre_of_bfs, int32_t *children, int32_t *parent,
-                       int8_t *level, uint64_t *key, int32_t *start, int32_t *end, int32_t *sub_end,
-                       uint8_t *leaf, int32_t *body_leaf, void *ws, size_t ws_bytes, void *stream) {
+int fmm_carve_emit(const uint64_t *keys, int64_t n, const int32_t *cbase, const int8_t *leaf_level,
+                   int32_t ncells, const int32_t *host_level_off, int32_t *children, int32_t *parent,
+                   int8_t *level, uint64_t *key, int32_t *start, int32_t *end, int32_t *sub_end, uint8_t *leaf,
+                   int32_t *cells_by_level, int32_t *body_leaf, void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t s = as_stream(stream);
     Arena ar(ws, ws_bytes);
-    uint64_t *sk = ar.take<uint64_t>(ncells);
-    uint64_t *sk2 = ar.take<uint64_t>(ncells);
-    int32_t *iota = ar.take<int32_t>(ncells);
-    int32_t *order = ar.take<int32_t>(ncells);
-    if (!sk || !sk2 || !iota || !order) { set_error("workspace too small"); return FMM_ERR_INVALID; }
-    int g = grid_for(ncells, 256);
-    preorder_keys<<<g, 256, 0, s>>>(ncells, b_start, b_level, sk, iota); fmm::note_launch();
-    int end_bit = 5;
-    while (end_bit < 64 && ((uint64_t)n << 5) >> end_bit) end_bit++;
-    size_t need = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, need, sk, sk2, iota, order, ncells, 0, end_bit, s);
-    if (need > ar.left()) { set_error("sort workspace"); return FMM_ERR_INVALID; }
-    cub::DeviceRadixSort::SortPairs(ar.rest(), need, sk, sk2, iota, order, ncells, 0, end_bit, s);
-    preorder_gather<<<g, 256, 0, s>>>(ncells, order, b_start, b_end, b_level, b_key, b_split, pre_of_bfs,
-                                      level, key, start, end, leaf, children); fmm::note_launch();
-    preorder_links<<<g, 256, 0, s>>>(ncells, order, b_parent, pre_of_bfs, key, start, end, parent,
-                                     children, sub_end); fmm::note_launch();
-    body_leaf_kernel<<<grid_for((int64_t)ncells * 32, 256), 256, 0, s>>>(ncells, leaf, start, end,
-                                                                        body_leaf); fmm::note_launch();
-    FMM_CUDA_CHECK("fmm_finalize_cells");
+    int32_t *cursor = ar.take<int32_t>(MAX_LEVEL + 2);
+    if (!cursor) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    cudaMemcpyAsync(cursor, host_level_off, sizeof(int32_t) * (MAX_LEVEL + 2), cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(children, 0xFF, sizeof(int32_t) * 8 * (size_t)ncells, s);  // -1
+    carve_emit<<<grid_for(n, 256), 256, 0, s>>>(keys, n, cbase, leaf_level, cursor, children, parent, level, key,
+                                                start, end, leaf, cells_by_level); fmm::note_launch();
+    carve_links<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, start, end, sub_end); fmm::note_launch();
+    body_leaf_kernel<<<grid_for((int64_t)ncells * 32, 256), 256, 0, s>>>(ncells, leaf, start, end, body_leaf); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_carve_emit");
     return FMM_OK;
 }
 

@@ -16,8 +16,8 @@ materialised on first access, with the reference's dtypes (int64 indices,
 uint64 keys, float64 geometry, bool leaf flags).
 
 Build (csrc/tree_build.cu): ingest + bounds -> depth-21 Morton keys ->
-stable radix sort -> permute -> level-synchronous carve -> pre-order
-renumbering -> geometry.  Bit-exact with src/tree.py:370-454 (keys,
+stable radix sort -> permute -> single-pass carve (cells numbered in
+pre-order by one scan) -> geometry.  Bit-exact with src/tree.py:370-454 (keys,
 permutation and every cell array; tests/test_gpu_parity.py).
 """
 
@@ -313,39 +313,22 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
                   P(qs), P(b32), P(b32lo), P(inexact), st)
         del x64, y64, z64, q64, keys, iota
 
-        # level-synchronous carve (BFS ids), grow-and-retry on capacity
-        cap = max(64, 8 * (n // max(1, ncrit) + 1))
-
-        def alloc(c):
-            return dict(start=torch.empty(c, dtype=i32, device=dev), end=torch.empty(c, dtype=i32, device=dev),
-                        parent=torch.empty(c, dtype=i32, device=dev),
-                        level=torch.empty(c, dtype=torch.int8, device=dev),
-                        key=torch.empty(c, dtype=torch.int64, device=dev),
-                        split=torch.empty(c, dtype=torch.uint8, device=dev))
-
-        bfs = alloc(cap)
-        node = torch.empty(n, dtype=i32, device=dev)
-        base, level, level_off = 0, -1, [0]
-        count = C.c_int32(0)
-        while True:
-            try:
-                _lib.call("fmm_build_level", P(skeys), P(node), n, level, int(ncrit),
-                          int(bool(allow_oversized_leaves)), base, cap, P(bfs["start"]), P(bfs["end"]),
-                          P(bfs["parent"]), P(bfs["level"]), P(bfs["key"]), P(bfs["split"]),
-                          C.byref(count), wsp, wsb, st)
-            except _lib.CapacityError:
-                new_cap = max(cap * 4, base + int(count.value))
-                nb = alloc(new_cap)
-                for k in bfs:
-                    nb[k][:base].copy_(bfs[k][:base])
-                bfs, cap = nb, new_cap
-                continue
-            if count.value == 0:
-                break
-            base += int(count.value)
-            level += 1
-            level_off.append(base)
-        ncells = base
+        # single-pass carve: per-body leaf level, cells numbered in pre-order
+        # by one scan (csrc/tree_build.cu), one host synchronisation
+        cbase = torch.empty(n, dtype=i32, device=dev)
+        leaf_level = torch.empty(n, dtype=torch.int8, device=dev)
+        hist = (C.c_int32 * 23)()
+        nc_host = C.c_int32(0)
+        _lib.call("fmm_carve_count", P(skeys), n, int(ncrit), int(bool(allow_oversized_leaves)), P(cbase),
+                  P(leaf_level), hist, C.byref(nc_host), wsp, wsb, st)
+        ncells = int(nc_host.value)
+        nleaves = int(hist[22])
+        depth = max(L for L in range(22) if hist[L] > 0)
+        off = [0]
+        for L in range(22):
+            off.append(off[-1] + int(hist[L]))
+        level_off = off[:depth + 2]
+        off23 = (C.c_int32 * 23)(*off[:23])
         cc = dict(children=torch.empty((ncells, 8), dtype=i32, device=dev),
                   parent=torch.empty(ncells, dtype=i32, device=dev),
                   level=torch.empty(ncells, dtype=torch.int8, device=dev),
@@ -354,13 +337,12 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
                   end=torch.empty(ncells, dtype=i32, device=dev),
                   sub_end=torch.empty(ncells, dtype=i32, device=dev),
                   leaf=torch.empty(ncells, dtype=torch.uint8, device=dev))
-        pre_of_bfs = torch.empty(ncells, dtype=i32, device=dev)
+        cells_by_level = torch.empty(ncells, dtype=i32, device=dev)
         body_leaf = torch.empty(n, dtype=i32, device=dev)
-        _lib.call("fmm_finalize_cells", ncells, n, P(bfs["start"]), P(bfs["end"]), P(bfs["parent"]),
-                  P(bfs["level"]), P(bfs["key"]), P(bfs["split"]), P(pre_of_bfs), P(cc["children"]),
-                  P(cc["parent"]), P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
-                  P(cc["sub_end"]), P(cc["leaf"]), P(body_leaf), wsp, wsb, st)
-        nleaves = ncells - int(bfs["split"][:ncells].sum())  # leaves = cells that did not split
+        _lib.call("fmm_carve_emit", P(skeys), n, P(cbase), P(leaf_level), ncells, off23, P(cc["children"]),
+                  P(cc["parent"]), P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]), P(cc["sub_end"]),
+                  P(cc["leaf"]), P(cells_by_level), P(body_leaf), wsp, wsb, st)
+        del cbase, leaf_level
         lo = torch.empty((ncells, 3), dtype=f64, device=dev)
         hi, ctr = torch.empty_like(lo), torch.empty_like(lo)
         bmax = torch.empty(ncells, dtype=f64, device=dev)
@@ -377,7 +359,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         d_phi=zeros[0], d_fx=zeros[1], d_fy=zeros[2], d_fz=zeros[3],
         d_children=cc["children"], d_parent=cc["parent"], d_level=cc["level"], d_key=cc["key"],
         d_start=cc["start"], d_end=cc["end"], d_sub_end=cc["sub_end"], d_leaf=cc["leaf"],
-        d_body_leaf=body_leaf, d_cells_by_level=pre_of_bfs,
+        d_body_leaf=body_leaf, d_cells_by_level=cells_by_level,
         d_lo=lo, d_hi=hi, d_ctr=ctr, d_bmax=bmax, d_rmax=rmax,
     )
     tree._host_input = None if ps.on_device else ps
