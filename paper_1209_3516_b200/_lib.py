@@ -133,11 +133,12 @@ def stream_handle(stream=None) -> int:
 _ws = {}
 
 
-def workspace(items: int, device) -> tuple[int, int]:
-    """(pointer, bytes) of a scratch buffer valid for ``items`` elements."""
+def workspace(items: int, device, slot: int = 0) -> tuple[int, int]:
+    """(pointer, bytes) of a scratch buffer valid for ``items`` elements
+    (``slot`` separates buffers used concurrently on different streams)."""
     need = C.c_size_t(0)
     call("fmm_workspace_bytes", int(max(items, 1)), C.byref(need))
-    key = (torch.device(device).index or 0, threading.get_ident())  # per thread: calls may overlap
+    key = (torch.device(device).index or 0, threading.get_ident(), slot)  # per thread: calls may overlap
     buf = _ws.get(key)
     if buf is None or buf.numel() < need.value:
         _ws[key] = None

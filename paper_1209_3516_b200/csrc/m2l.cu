@@ -416,10 +416,10 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
             const int nc = ncoef(p), nch = host_tab.nchunks;
             const size_t smem = (size_t)((nch * kChunk + 1) & ~1) * 4 +
                                 (size_t)kBlkWarps * (2 * nc + 1) * 8 + (size_t)nch * 8;
-            static size_t smem_set = 0;
-            if (smem > smem_set) {
+            static size_t smem_set[64] = {};  // the attribute is per device
+            if (smem > smem_set[dev]) {
                 cudaFuncSetAttribute(m2l_block<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                smem_set = smem;
+                smem_set[dev] = smem;
             }
             m2l_block<NT><<<grid_for(ncells, 1, 148 * 4), NT, smem, s>>>(p, ncells, rows, src, ctr, M, L);
             fmm::note_launch();

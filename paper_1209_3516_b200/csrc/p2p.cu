@@ -243,15 +243,46 @@ __device__ __forceinline__ void p2p_f32_span(int32_t j0, int32_t j1, int step, c
     }
 }
 
+// Fold the warp's 4*KB per-lane partial sums (phi, fx, fy, fz of KB targets)
+// over the 32 lanes by recursive halving: at each step a lane keeps half of
+// its values and receives its partner's copy of that half, so the whole fold
+// takes 4*KB - 1 shuffles (not 4*KB*5).  Lane l ends holding value index
+// l mod 4*KB, i.e. quantity (l mod 4*KB) / KB of target l mod KB.
+template <int KB>
+__device__ __forceinline__ float warp_fold(const f2_t (&ap)[KB / 2], const f2_t (&ax)[KB / 2],
+                                           const f2_t (&ay)[KB / 2], const f2_t (&az)[KB / 2], int lane) {
+    constexpr int N = 4 * KB;
+    float v[N];
+#pragma unroll
+    for (int w = 0; w < KB / 2; w++) {
+        f2_unpack(ap[w], v[0 * KB + 2 * w], v[0 * KB + 2 * w + 1]);
+        f2_unpack(ax[w], v[1 * KB + 2 * w], v[1 * KB + 2 * w + 1]);
+        f2_unpack(ay[w], v[2 * KB + 2 * w], v[2 * KB + 2 * w + 1]);
+        f2_unpack(az[w], v[3 * KB + 2 * w], v[3 * KB + 2 * w + 1]);
+    }
+#pragma unroll
+    for (int n = N; n > 1; n >>= 1) {
+        const int o = n >> 1;  // lane bit that picks the half this lane keeps
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < n / 2; k++) {
+            const float keep = up ? v[k + n / 2] : v[k];
+            const float send = up ? v[k] : v[k + n / 2];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+#pragma unroll
+    for (int o = N; o < 32; o <<= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    return v[0];
+}
+
 // Block of KB consecutive targets starting at i0 (padded with the last
-// valid target), all runs of the row, folded over the warp.  Lane u < KB
-// ends holding target u's sums in (rp, rx, ry, rz).
+// valid target), all runs of the row, folded over the warp (warp_fold).
 template <int KB, bool SAFE, bool ANCHOR>
-__device__ __forceinline__ void p2p_f32_block(int32_t i0, int32_t ilast, int64_t r0, int64_t r1, int part,
+__device__ __forceinline__ float p2p_f32_block(int32_t i0, int32_t ilast, int64_t r0, int64_t r1, int part,
                                               int nparts, int lane, const int4 *__restrict__ runs,
                                               const float4 *__restrict__ b, const float4 *__restrict__ blo,
-                                              const Anchor &an, float4 *ring, float &rp, float &rx, float &ry,
-                                              float &rz) {
+                                              const Anchor &an, float4 *ring) {
     f2_t tx[KB / 2], ty[KB / 2], tz[KB / 2], ap[KB / 2], ax[KB / 2], ay[KB / 2], az[KB / 2];
 #pragma unroll
     for (int v = 0; v < KB / 2; v++) {
@@ -271,52 +302,113 @@ __device__ __forceinline__ void p2p_f32_block(int32_t i0, int32_t ilast, int64_t
         else
             p2p_f32_span<KB, false, ANCHOR>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
     }
-    float fp[KB], fx_[KB], fy_[KB], fz_[KB];
-#pragma unroll
-    for (int v = 0; v < KB / 2; v++) {
-        f2_unpack(ap[v], fp[2 * v], fp[2 * v + 1]);
-        f2_unpack(ax[v], fx_[2 * v], fx_[2 * v + 1]);
-        f2_unpack(ay[v], fy_[2 * v], fy_[2 * v + 1]);
-        f2_unpack(az[v], fz_[2 * v], fz_[2 * v + 1]);
-    }
-#pragma unroll
-    for (int u = 0; u < KB; u++) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            fp[u] += __shfl_xor_sync(0xffffffffu, fp[u], o);
-            fx_[u] += __shfl_xor_sync(0xffffffffu, fx_[u], o);
-            fy_[u] += __shfl_xor_sync(0xffffffffu, fy_[u], o);
-            fz_[u] += __shfl_xor_sync(0xffffffffu, fz_[u], o);
-        }
-        if (lane == u) { rp = fp[u]; rx = fx_[u]; ry = fy_[u]; rz = fz_[u]; }
-    }
+    return warp_fold<KB>(ap, ax, ay, az, lane);
 }
 
-// Streamed block (the fast path): all non-self runs of the row form ONE
-// lane-strided source sequence (the run table sits in shared memory), so the
-// cp.async ring runs continuously across runs -- no per-run prologue or
-// epilogue and no idle lanes at run ends.  The target leaf's own bodies are
-// swept first in a short guarded pass (the only place i == j or r2 == 0 can
-// occur for float32-exact inputs), and the stream then runs unguarded.
+// Streamed rows (the fast path): all non-self runs of the row form ONE
+// source sequence (the run table sits in shared memory).  A unit (target
+// block tb, part p of P) takes the p-th of P equal contiguous shares of the
+// sequence, in chunks of kChunk = 32 * kSPL consecutive sources.  Each warp streams its chunks
+// through a private ring of kWStages shared-memory stages: lane 0 copies a
+// chunk in with one cp.async.bulk per run segment (UBLKCP: one instruction
+// moves up to the whole chunk) that completes on the stage's mbarrier, and
+// the lanes read it back with one LDS.128 per source.  Per source and lane
+// this leaves the LDS next to the 13 * KB / 2 packed FP32 ops -- the
+// per-lane address, run-seek and cp.async bookkeeping of a lane-private
+// stream are gone -- and the warps stay independent of each other.
+// The target leaf's own bodies are swept first in a short guarded pass (the
+// only place i == j or r2 == 0 can occur for float32-exact inputs).
 constexpr int kMaxRuns = 512;
+#ifndef FMM_P2P_SPL
+#define FMM_P2P_SPL 8
+#endif
+#ifndef FMM_P2P_WSTAGES
+#define FMM_P2P_WSTAGES 2
+#endif
+constexpr int kSPL = FMM_P2P_SPL;          // sources per lane per chunk
+constexpr int kWStages = FMM_P2P_WSTAGES;  // chunks in flight per warp
+constexpr int kChunk = 32 * kSPL;          // sources per chunk
 
-__device__ __forceinline__ void stream_seek(int &rf, int32_t &jf, int32_t &rend, int nr, const int2 *srun) {
-    while (rf < nr && jf >= rend) {
-        const int32_t over = jf - rend;
-        if (++rf < nr) {
-            const int2 rr = srun[rf];
-            jf = rr.x + over;
-            rend = rr.y;
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// Lane 0's cursor into the run table: run r starts at sequence position rpos.
+struct RunCursor {
+    int r;
+    int32_t rpos;
+};
+
+// Copy sequence positions [p0, p0 + need) into `dst` (lane 0 only): walk
+// the cursor forward to p0, then one bulk copy per run segment.
+__device__ __forceinline__ void chunk_produce(float4 *dst, uint64_t *bar, int32_t p0, int32_t need, RunCursor &c,
+                                              const int2 *srun, const float4 *__restrict__ b) {
+    mbar_expect_tx(bar, (uint32_t)need * 16u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier LDS of the stage before the copy
+    int2 run = srun[c.r];
+    while (c.rpos + (run.y - run.x) <= p0) {
+        c.rpos += run.y - run.x;
+        run = srun[++c.r];
+    }
+    int32_t off = p0 - c.rpos;
+    while (need > 0) {
+        const int32_t take = min(run.y - run.x - off, need);
+        if (take > 0) bulk_g2s(dst, b + run.x + off, (uint32_t)take * 16u, bar);
+        dst += take;
+        need -= take;
+        if (need > 0) {
+            c.rpos += run.y - run.x;
+            run = srun[++c.r];
+            off = 0;
         }
     }
 }
 
+// One unit of a streamed row: KB targets from i0 (padded with the last
+// valid target) against sources [s0, s1) of the block's source line, which
+// is the target leaf's own cnt bodies (positions [0, cnt), guarded sweep)
+// followed by the run sequence (positions cnt + [0, total)).  `ring` is the
+// warp's kWStages * kChunk stage buffer, `bars` its barriers, `phase` their
+// parity bits (one per stage).
 template <int KB>
-__device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, int32_t ts, int32_t te,
-                                                     const int2 *srun, int nr, int32_t total, int part, int nparts,
-                                                     int lane, const float4 *__restrict__ b, float4 *ring, float &rp,
-                                                     float &rx, float &ry, float &rz) {
+__device__ __forceinline__ float p2p_f32_stream_unit(int32_t i0, int32_t ilast, int32_t ts, int32_t cnt, int32_t s0,
+                                                     int32_t s1, int lane, const float4 *__restrict__ b,
+                                                     float4 *ring, uint64_t *bars, uint32_t &phase,
+                                                     const int2 *srun) {
     f2_t tx[KB / 2], ty[KB / 2], tz[KB / 2], ap[KB / 2], ax[KB / 2], ay[KB / 2], az[KB / 2];
+    // the stream share [lo, hi), cut into chunks from lo; the first chunks
+    // are requested before anything else so they land during the self sweep
+    const int32_t lo = max(s0, cnt) - cnt, hi = max(s1, cnt) - cnt;
+    const int nk = (hi - lo + kChunk - 1) / kChunk;
+    RunCursor cur{0, 0};
+    if (lane == 0)
+        for (int k = 0; k < min(nk, kWStages); k++) {
+            const int32_t p0 = lo + k * kChunk;
+            chunk_produce(ring + k * kChunk, &bars[k], p0, min(kChunk, hi - p0), cur, srun, b);
+        }
 #pragma unroll
     for (int v = 0; v < KB / 2; v++) {
         const float4 e = __ldg(&b[min(i0 + 2 * v, ilast)]);
@@ -326,85 +418,39 @@ __device__ __forceinline__ void p2p_f32_stream_block(int32_t i0, int32_t ilast, 
         tz[v] = f2_fresh(f2_pack(e.z, o.z));
         ap[v] = ax[v] = ay[v] = az[v] = 0ull;
     }
-    const int step = 32 * nparts;
-    // 1) self leaf, guarded
-    for (int32_t j = ts + part * 32 + lane; j < te; j += step)
+    // 1) the self share, guarded
+    for (int32_t j = ts + s0 + lane; j < ts + min(s1, cnt); j += 32)
         p2p_f32x2_pairs<KB, true>(__ldg(&b[j]), j - i0, tx, ty, tz, ap, ax, ay, az);
-    // 2) the stream
-    const int32_t pos0 = part * 32 + lane;
-    const int32_t nit = pos0 < total ? (total - pos0 + step - 1) / step : 0;
-    const int32_t posmax = part * 32 + 31;
-    const int32_t nitc = posmax < total ? (total - posmax + step - 1) / step : 0;  // warp-uniform
-    int rf = 0;
-    int32_t jf = 0, rend = 0;
-    if (nr > 0) {
-        const int2 r0v = srun[0];
-        jf = r0v.x + pos0;
-        rend = r0v.y;
-        stream_seek(rf, jf, rend, nr, srun);
-    }
-#pragma unroll
-    for (int k = 0; k < kStages - 1; k++) {
-        if (k < nit) {
-            cp_async16(&ring[k * 32], &b[jf]);
-            jf += step;
-            stream_seek(rf, jf, rend, nr, srun);
+    // 2) the chunks
+    int st = 0;
+    for (int k = 0; k < nk; k++) {
+        if (k > 0 && lane == 0 && k - 1 + kWStages < nk) {  // refill the stage consumed last iteration
+            const int sp = st == 0 ? kWStages - 1 : st - 1;
+            const int32_t p0 = lo + (k - 1 + kWStages) * kChunk;
+            chunk_produce(ring + sp * kChunk, &bars[sp], p0, min(kChunk, hi - p0), cur, srun, b);
         }
-        cp_async_commit();
-    }
-    int32_t it = 0;
-    // the source for iteration it + 1 is read from the ring (LDS) before the
-    // math of iteration it, so its latency hides behind 13*KB/2 packed ops;
-    // the slot a fetch overwrites was consumed two iterations earlier
-    cp_async_wait<kStages - 2>();
-    float4 cur = ring[0];
-    for (; it + kStages <= nitc; it += kStages) {
+        __syncwarp();
+        mbar_wait(&bars[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const float4 *src = ring + st * kChunk + lane;
+        const int32_t valid = hi - (lo + k * kChunk);
+        if (valid >= kChunk) {
+            float4 s = src[0];
 #pragma unroll
-        for (int q = 0; q < kStages; q++) {
-            if (it + q + kStages - 1 < nit) {
-                cp_async16(&ring[((q + kStages - 1) % kStages) * 32], &b[jf]);
-                jf += step;
-                stream_seek(rf, jf, rend, nr, srun);
+            for (int q = 0; q < kSPL; q++) {
+                const float4 nxt = src[((q + 1) % kSPL) * 32];
+                p2p_f32x2_pairs<KB, false>(s, 0, tx, ty, tz, ap, ax, ay, az);
+                s = nxt;
             }
-            cp_async_commit();
-            cp_async_wait<kStages - 2>();
-            const float4 nxt = ring[((q + 1) % kStages) * 32];
-            p2p_f32x2_pairs<KB, false>(cur, 0, tx, ty, tz, ap, ax, ay, az);
-            cur = nxt;
+        } else {
+#pragma unroll 1
+            for (int q = 0; q < kSPL; q++)
+                if (q * 32 + lane < valid) p2p_f32x2_pairs<KB, false>(src[q * 32], 0, tx, ty, tz, ap, ax, ay, az);
         }
+        __syncwarp();
+        if (++st == kWStages) st = 0;
     }
-    for (; it < nit; it++) {  // <= kStages iterations; the last may be lane-divergent
-        if (it + kStages - 1 < nit) {
-            cp_async16(&ring[((it + kStages - 1) % kStages) * 32], &b[jf]);
-            jf += step;
-            stream_seek(rf, jf, rend, nr, srun);
-        }
-        cp_async_commit();
-        cp_async_wait<kStages - 2>();
-        const float4 nxt = ring[((it + 1) % kStages) * 32];
-        p2p_f32x2_pairs<KB, false>(cur, 0, tx, ty, tz, ap, ax, ay, az);
-        cur = nxt;
-    }
-    cp_async_wait<0>();
-    float fp[KB], fx_[KB], fy_[KB], fz_[KB];
-#pragma unroll
-    for (int v = 0; v < KB / 2; v++) {
-        f2_unpack(ap[v], fp[2 * v], fp[2 * v + 1]);
-        f2_unpack(ax[v], fx_[2 * v], fx_[2 * v + 1]);
-        f2_unpack(ay[v], fy_[2 * v], fy_[2 * v + 1]);
-        f2_unpack(az[v], fz_[2 * v], fz_[2 * v + 1]);
-    }
-#pragma unroll
-    for (int u = 0; u < KB; u++) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            fp[u] += __shfl_xor_sync(0xffffffffu, fp[u], o);
-            fx_[u] += __shfl_xor_sync(0xffffffffu, fx_[u], o);
-            fy_[u] += __shfl_xor_sync(0xffffffffu, fy_[u], o);
-            fz_[u] += __shfl_xor_sync(0xffffffffu, fz_[u], o);
-        }
-        if (lane == u) { rp = fp[u]; rx = fx_[u]; ry = fy_[u]; rz = fz_[u]; }
-    }
+    return warp_fold<KB>(ap, ax, ay, az, lane);
 }
 
 // Target blocks of a leaf: cnt / 8 blocks of 8, then the remainder as one
@@ -424,7 +470,12 @@ __device__ __forceinline__ int gcd_small(int a, int b) {
 // Partial sums of the parts are folded through shared memory in a fixed
 // order (deterministic).  Leaves too large for the fold buffer (oversized
 // leaves) fall back to P = 1 with direct stores.
-constexpr int kMaxUnits = 32;
+constexpr int kMaxUnits = 64;
+
+template <bool SAFE, bool ANCHOR>
+constexpr int p2p_f32_pool_bytes() {
+    return (!SAFE && !ANCHOR ? kP2PWarps * kWStages * kChunk : kP2PWarps * kStages * 32) * (int)sizeof(float4);
+}
 
 template <bool SAFE, bool ANCHOR>
 __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
@@ -432,12 +483,23 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const float4 *__restrict__ b, const float4 *__restrict__ blo, double *phi, double *fx, double *fy,
     double *fz, int *flag) {
+    constexpr bool kStream = !SAFE && !ANCHOR;
+    // the tile ring (streamed rows) and the lane rings (run-by-run rows) share
+    // one pool: a row uses one or the other
+    extern __shared__ __align__(128) float4 pool[];  // p2p_f32_pool_bytes<SAFE, ANCHOR>()
     __shared__ float red[kMaxUnits][4][8];
-    __shared__ float4 rings[kP2PWarps][kStages * 32];
     __shared__ int2 srun[kMaxRuns];
     __shared__ int32_t stotal;
+    __shared__ uint64_t wbars[kP2PWarps][kWStages];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float4 *ring = &rings[w][lane];
+    float4 *ring = &pool[w * kStages * 32 + lane];
+    if (kStream && lane == 0) {
+        for (int k = 0; k < kWStages; k++) mbar_init(&wbars[w][k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    float4 *wring = pool + w * kWStages * kChunk;
+    uint32_t phase = 0;  // parity of each of this warp's stage barriers
     const int32_t nrows = nrows_dev ? *nrows_dev : nrows_host;
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
         const int32_t t = leaf_rows[row];
@@ -445,20 +507,23 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
         const int rem = cnt & 7;
         const int nblk = (cnt >> 3) + (rem ? 1 : 0);
         const bool small_last = rem != 0 && rem <= 4;
-        int P = kP2PWarps / gcd_small(nblk, kP2PWarps);
+        const int64_t r0 = run_off[row], r1 = run_off[row + 1];
+        const int nr = (int)(r1 - r0);
+        // streamed rows split every block's source line over the warps by
+        // weight (P = kP2PWarps partials per block, folded below)
+        const bool streamed = kStream && nr <= kMaxRuns && nblk * kP2PWarps <= kMaxUnits;
+        int P = streamed ? kP2PWarps : kP2PWarps / gcd_small(nblk, kP2PWarps);
         const bool fold = nblk * P <= kMaxUnits;
         if (!fold) P = 1;
         const int nunits = nblk * P;
-        const int64_t r0 = run_off[row], r1 = run_off[row + 1];
         Anchor an{};
         if (ANCHOR) {
             const float4 h = __ldg(&b[ts]), l = __ldg(&blo[ts]);
             an = Anchor{h.x, h.y, h.z, l.x, l.y, l.z};
         }
-        const int nr = (int)(r1 - r0);
-        const bool streamed = !ANCHOR && !SAFE && nr <= kMaxRuns;
         if (streamed) {
             if (threadIdx.x == 0) stotal = 0;
+            for (int k = threadIdx.x; k < nunits * 32; k += blockDim.x) (&red[0][0][0])[k] = 0.f;
             __syncthreads();
             int32_t len = 0;
             for (int k = threadIdx.x; k < nr; k += blockDim.x) {
@@ -471,44 +536,52 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
             if (lane == 0) atomicAdd(&stotal, len);
             __syncthreads();
         }
-        const int32_t total = streamed ? stotal : 0;
-        for (int u = w; u < nunits; u += kP2PWarps) {
-            const int tb = u / P, part = u % P;
-            const int32_t i0 = ts + tb * 8;
-            float rp = 0.f, rx = 0.f, ry = 0.f, rz = 0.f;
-            const bool k4 = tb == nblk - 1 && small_last;
-            if (streamed) {
-                if (k4)
-                    p2p_f32_stream_block<4>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, P, lane, b, ring,
-                                            rp, rx, ry, rz);
-                else
-                    p2p_f32_stream_block<8>(i0, ts + cnt - 1, ts, ts + cnt, srun, nr, total, part, P, lane, b, ring,
-                                            rp, rx, ry, rz);
-            } else {
-                if (k4)
-                    p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring,
-                                                   rp, rx, ry, rz);
-                else
-                    p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring,
-                                                   rp, rx, ry, rz);
-            }
+        // a unit's folded sums: lane l holds quantity q of target uu
+        auto emit = [&](int u, int tb, int32_t i0, bool k4, float val) {
+            const int q = k4 ? (lane >> 2) & 3 : lane >> 3;
+            const int uu = k4 ? lane & 3 : lane & 7;
             if (fold) {
-                if (lane < 8) {
-                    red[u][0][lane] = rp;
-                    red[u][1][lane] = rx;
-                    red[u][2][lane] = ry;
-                    red[u][3][lane] = rz;
-                }
-            } else if (lane < 8 && tb * 8 + lane < cnt) {
-                const int32_t i = i0 + lane;
-                phi[i] = (double)rp;
-                fx[i] = (double)rx;
-                fy[i] = (double)ry;
-                fz[i] = (double)rz;
-                if (!(isfinite(rp) && isfinite(rx) && isfinite(ry) && isfinite(rz))) atomicOr(flag, 1);
+                if (lane < (k4 ? 16 : 32)) red[u][q][uu] = val;
+            } else if (lane < (k4 ? 16 : 32) && tb * 8 + uu < cnt) {
+                double *out = q == 0 ? phi : q == 1 ? fx : q == 2 ? fy : fz;
+                out[i0 + uu] = (double)val;
+                if (!isfinite(val)) atomicOr(flag, 1);
+            }
+        };
+        if (streamed) {
+            // block tb's line: cnt self sources + total stream sources, weight
+            // 2 per source (K8) or 1 (the K4 last block); warp w takes the
+            // w-th quarter of the concatenated weighted lines
+            const int64_t L = (int64_t)cnt + stotal;
+            const int64_t Wl = L * (2 * nblk - (small_last ? 1 : 0));
+            const int64_t A = Wl * w / kP2PWarps, B = Wl * (w + 1) / kP2PWarps;
+            for (int tb = (int)(A / (2 * L)); tb < nblk && 2 * L * tb < B; tb++) {
+                const bool k4 = tb == nblk - 1 && small_last;
+                const int64_t Sb = 2 * L * tb, sc = k4 ? 1 : 2;
+                const int32_t s0 = (int32_t)((max(A, Sb) - Sb) / sc);
+                const int32_t s1 = (int32_t)((min(B, Sb + sc * L) - Sb) / sc);
+                if (s1 <= s0) continue;
+                const int32_t i0 = ts + tb * 8;
+                const float val =
+                    k4 ? p2p_f32_stream_unit<4>(i0, ts + cnt - 1, ts, cnt, s0, s1, lane, b, wring, wbars[w], phase,
+                                                srun)
+                       : p2p_f32_stream_unit<8>(i0, ts + cnt - 1, ts, cnt, s0, s1, lane, b, wring, wbars[w], phase,
+                                                srun);
+                emit(tb * kP2PWarps + w, tb, i0, k4, val);
+            }
+        } else {
+            for (int u = w; u < nunits; u += kP2PWarps) {
+                const int tb = u / P, part = u % P;
+                const int32_t i0 = ts + tb * 8;
+                const bool k4 = tb == nblk - 1 && small_last;
+                const float val =
+                    k4 ? p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring)
+                       : p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an,
+                                                        ring);
+                emit(u, tb, i0, k4, val);
             }
         }
-        __syncthreads();  // partial sums complete; srun may be rewritten after this
+        __syncthreads();  // partial sums complete; srun / pool may be rewritten after this
         if (fold) {
             for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
                 const int tb = k >> 3, l = k & 7;
@@ -657,7 +730,10 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, co
         if (anch && !b32lo) { set_error("anchored fp32 P2P needs the float4 residual copy"); return FMM_ERR_INVALID; }
         auto kern = anch ? (safe ? p2p_f32_kernel<true, true> : p2p_f32_kernel<false, true>)
                          : (safe ? p2p_f32_kernel<true, false> : p2p_f32_kernel<false, false>);
-        kern<<<grid, kP2PWarps * 32, 0, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
+        const int pool = anch ? (safe ? p2p_f32_pool_bytes<true, true>() : p2p_f32_pool_bytes<false, true>())
+                              : (safe ? p2p_f32_pool_bytes<true, false>() : p2p_f32_pool_bytes<false, false>());
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pool);
+        kern<<<grid, kP2PWarps * 32, pool, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
                                              (const float4 *)b32, (const float4 *)b32lo, phi, fx, fy, fz,
                                              dev_flag); fmm::note_launch();
     } else if (precision == FMM_PREC_FP64) {

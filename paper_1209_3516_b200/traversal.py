@@ -136,7 +136,8 @@ _hint = {}
 
 
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
-                      m2l_ready: torch.cuda.Event | None = None) -> Lists:
+                      m2l_ready: torch.cuda.Event | None = None,
+                      side: torch.cuda.Stream | None = None) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
@@ -179,9 +180,23 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     m2l_src = torch.empty(max(done_m2l, 1), dtype=i32, device=dev)
     m2l_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev)
-    _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), wsp, wsb, st)
-    if m2l_ready is not None:
-        m2l_ready.record()  # the M2L list is final: the far field may start
+    if side is None:
+        _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), wsp, wsb, st)
+        if m2l_ready is not None:
+            m2l_ready.record()  # the M2L list is final: the far field may start
+    else:
+        # only the far field reads the M2L list: sort it on the side stream,
+        # off the P2P critical path, with its own scratch buffer
+        traversed = torch.cuda.Event()
+        traversed.record()
+        side.wait_event(traversed)
+        swp, swb = _lib.workspace(max(done_m2l, 1), dev, slot=1)
+        _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), swp, swb,
+                  side.cuda_stream)
+        for a in (m2l_t, m2l_s, m2l_src, m2l_rows):
+            a.record_stream(side)
+        if m2l_ready is not None:
+            m2l_ready.record(side)
     p2p_src = torch.empty(max(done_p2p, 1), dtype=i32, device=dev)
     p2p_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     _lib.call("fmm_pairs_to_csr", P(p2p_t), P(p2p_s), done_p2p, ncells, P(p2p_src), P(p2p_rows), wsp, wsb, st)
@@ -272,7 +287,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             e_up1.record(side)
         tree._M, tree.p, tree._L = M, p, L
         m2l_ready = torch.cuda.Event()
-        lists = interaction_lists(tree, cfg.mac, m2l_ready=m2l_ready)
+        lists = interaction_lists(tree, cfg.mac, m2l_ready=m2l_ready, side=side)
         tree.list_cache = lists
         e_l1.record(main)
         side.wait_event(m2l_ready)
