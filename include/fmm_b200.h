@@ -175,6 +175,24 @@ FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1
                  int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
                  int64_t cap_m2l, unsigned long long *dev_log, void *stream);
 
+/* Treecode lists (replaces _collect_treecode, src/traversal.py:265-313, with
+ * its capacity retry, :944-966): every leaf whose bodies meet
+ * [body_lo, body_hi) walks the source tree from the root; a pair (t, c)
+ * with the MAC accepted is M2P (tested first), else a leaf c is P2P, else
+ * c's children are visited.  Breadth-first, nsteps steps chained on the
+ * device (one source level per step; depth + 1 suffice).  Frontier buffers
+ * hold cap_front >= ncells pairs each; ws holds ncells bytes plus a CUB
+ * select.  dev_log (nsteps + 3 entries) receives {n_p2p, n_m2p, frontier
+ * size entering step 0, ..., nsteps}: read it once, grow and rerun on any
+ * count above its capacity or a non-zero last entry. */
+FMM_API int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                          int64_t cap_front, int nsteps, int32_t ncells, const int32_t *children,
+                          const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                          const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                          double th2, int32_t *m2p_t, int32_t *m2p_s, int64_t cap_m2p, int32_t *p2p_t,
+                          int32_t *p2p_s, int64_t cap_p2p, unsigned long long *dev_log, void *ws,
+                          size_t ws_bytes, void *stream);
+
 /* Sort (t, s) pairs by target then source and build row offsets over all
  * cells: rows[c]..rows[c+1] are the sources of target c (ascending). */
 FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs, int32_t ncells,
@@ -203,6 +221,15 @@ FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *sta
 /* L[t] += sum over row sources of M2L(M[s], ctr[t]-ctr[s]) (src/_taylor.py:169-188). */
 FMM_API int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const double *ctr,
                 const double *M, double *L, void *stream);
+
+/* Treecode far field (replaces _exec_m2p, src/traversal.py:520-528 ->
+ * _m2p, src/_taylor.py:272-307): for every target leaf row t of the CSR M2P
+ * list and every body j of t, phi[j] += sum (-1)^|m| M_m D_m(x_j - c_s) and
+ * f[j] -= the gradient terms (f = -grad phi); bodies at a cell center are
+ * skipped.  Accumulates (+=) into phi/fx/fy/fz; float64; 1 <= p <= 12. */
+FMM_API int fmm_m2p_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const int32_t *start,
+                const int32_t *end, const double *ctr, const double *M, const double *x, const double *y,
+                const double *z, double *phi, double *fx, double *fy, double *fz, void *stream);
 
 /* Near field over the P2P plan.  precision FMM_PREC_FP32 reads the float4
  * body copy b32; FMM_PREC_FP64 reads the float64 SoA.  Results are STORED

@@ -54,6 +54,8 @@ def _declare(L):
     L.orc_downward.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_collect.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _I, _I, _P, _P, _I, _P, _P, _P]
     L.orc_exec_m2l.argtypes = [_I, _P, _P, _P, _P, _P, C.c_int]
+    L.orc_collect_treecode.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _P, _P, _I, _P, _P, _P]
+    L.orc_exec_m2p.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int]
     L.orc_exec_p2p.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_direct_subset.argtypes = [_I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, C.c_int]
     L.orc_fmm.argtypes = [_I, _P, _P, _P, _P, _I, C.c_int, _D, C.c_int, _D,
@@ -205,11 +207,12 @@ def exec_m2l(t: OracleTree, mt, ms, M, p) -> np.ndarray:
     return L
 
 
-def exec_p2p(t: OracleTree, pt, ps, use_rsqrt=False):
-    """src/traversal.py:531-548 on zeroed accumulators; returns
-    (phi, fx, fy, fz, stats[pairs, skipped, flops])."""
+def exec_p2p(t: OracleTree, pt, ps, use_rsqrt=False, acc=None):
+    """src/traversal.py:531-548 on zeroed accumulators (or into ``acc`` =
+    (phi, fx, fy, fz), in place); returns (phi, fx, fy, fz, stats[pairs,
+    skipped, flops])."""
     pt = np.ascontiguousarray(pt, np.int64); ps = np.ascontiguousarray(ps, np.int64)
-    phi, fx, fy, fz = (np.zeros(t.n) for _ in range(4))
+    phi, fx, fy, fz = acc if acc is not None else (np.zeros(t.n) for _ in range(4))
     st = np.zeros(3, np.int64)
     lib().orc_exec_p2p(pt.size, _p(pt), _p(ps), _p(t.cell_start), _p(t.cell_end), _p(t.x), _p(t.y),
                        _p(t.z), _p(t.q), _p(phi), _p(fx), _p(fy), _p(fz), int(use_rsqrt), _p(st))
@@ -234,6 +237,47 @@ def evaluate(t: OracleTree, p: int, theta: float):
     downward(t, Lw, p, phi, fx, fy, fz)
     return dict(phi=phi, fx=fx, fy=fy, fz=fz, M=M, L_m2l=L, m2l=(mt, ms), p2p=(pt, ps),
                 p2p_pairs=int(st[0]), p2p_skipped=int(st[1]), m2l_calls=int(mt.size))
+
+
+def collect_treecode(t: OracleTree, theta: float):
+    """Per-target-leaf walk of the source tree (src/traversal.py:265-313),
+    leaves in pre-order.  Returns (m2p_t, m2p_s, p2p_t, p2p_s)."""
+    leaf_ids = np.ascontiguousarray(np.flatnonzero(t.cell_leaf), np.int64)
+    capm = max(2048, 256 * leaf_ids.size)
+    capp = max(2048, 64 * leaf_ids.size)
+    while True:
+        mt = np.empty(capm, np.int64); ms = np.empty(capm, np.int64)
+        pt = np.empty(capp, np.int64); ps = np.empty(capp, np.int64)
+        out = np.zeros(3, np.int64)
+        lib().orc_collect_treecode(leaf_ids.size, _p(leaf_ids), _p(t.cell_children), _p(t.cell_leaf),
+                                   _p(t.cell_center), _p(t.cell_bmax), float(theta) * float(theta), capm, _p(mt),
+                                   _p(ms), capp, _p(pt), _p(ps), _p(out))
+        if out[2] == 1:
+            capm, capp = int(out[0]) + 1, int(out[1]) + 1
+            continue
+        nm, npp = int(out[0]), int(out[1])
+        return mt[:nm], ms[:nm], pt[:npp], ps[:npp]
+
+
+def exec_m2p(t: OracleTree, mt, ms, M, p, phi=None, fx=None, fy=None, fz=None):
+    """src/traversal.py:520-528 -> src/_taylor.py:272-307, accumulating into
+    (phi, fx, fy, fz) (zeroed when not given); returns them."""
+    mt = np.ascontiguousarray(mt, np.int64); ms = np.ascontiguousarray(ms, np.int64)
+    acc = [np.zeros(t.n) if a is None else a for a in (phi, fx, fy, fz)]
+    lib().orc_exec_m2p(mt.size, _p(mt), _p(ms), _p(t.cell_start), _p(t.cell_end), _p(t.x), _p(t.y), _p(t.z),
+                       *(_p(a) for a in acc), _p(t.cell_center), _p(M), p)
+    return tuple(acc)
+
+
+def evaluate_treecode(t: OracleTree, p: int, theta: float):
+    """evaluate_treecode restated sequentially (src/traversal.py:1002-1046):
+    M2P far field, then the P2P near field, on zeroed accumulators."""
+    M = upward(t, p)
+    mt, ms, pt, ps = collect_treecode(t, theta)
+    acc = exec_m2p(t, mt, ms, M, p)
+    phi, fx, fy, fz, st = exec_p2p(t, pt, ps, acc=acc)  # P2P adds onto the M2P sums
+    return dict(phi=phi, fx=fx, fy=fy, fz=fz, M=M, m2p=(mt, ms), p2p=(pt, ps),
+                p2p_pairs=int(st[0]), p2p_skipped=int(st[1]), m2p_calls=int(mt.size))
 
 
 def direct(x, y, z, q, idx=None, threads=0):

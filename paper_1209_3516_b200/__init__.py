@@ -10,7 +10,8 @@ and forces, computed by hand-written CUDA kernels in ``libfmm_b200.so``
 from .geometry import MAX_LEVEL, Aabb, ParticleSet, compute_bounds
 from .kernels import P2P_FLOPS_PER_PAIR, TMAX, KernelStats, direct, ncoef
 from .mac import MacConfig, accept, error_bound
-from .traversal import EvalConfig, EvalReport, evaluate_dual_tree, evaluate_on_tree, interaction_lists
+from .traversal import (EvalConfig, EvalReport, evaluate_dual_tree, evaluate_on_tree, evaluate_treecode,
+                        interaction_lists, treecode_lists)
 from .tree import Tree, build_tree, check_invariants, downward_pass, upward_pass
 from .tuner import error_sample, sampled_force_error, verify_against_direct
 
@@ -19,7 +20,8 @@ __version__ = "0.1.0"
 __all__ = [
     "MAX_LEVEL", "TMAX", "P2P_FLOPS_PER_PAIR", "Aabb", "ParticleSet", "compute_bounds",
     "KernelStats", "direct", "ncoef", "MacConfig", "accept", "error_bound",
-    "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_on_tree", "interaction_lists",
+    "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_on_tree", "evaluate_treecode", "interaction_lists",
+    "treecode_lists",
     "Tree", "build_tree", "check_invariants", "downward_pass", "upward_pass",
     "error_sample", "sampled_force_error", "verify_against_direct", "__version__",
 ]

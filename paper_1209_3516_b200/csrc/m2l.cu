@@ -14,60 +14,11 @@
 //  * m2l_warp (any p <= 12): one warp per target row, the warp handles one
 //    pair at a time -- lanes split each degree of the D recurrence, then
 //    lanes own output coefficients; D and M_s staged in shared memory.
-#include <type_traits>
-
-#include "fmm_common.cuh"
+#include "taylor.cuh"
 
 namespace fmm {
 
-// ---- register kernel, compile-time multi-indices ------------------------
-// static_for hands each iteration its index as a type, so every table
-// lookup below is a constant expression and D / M / L stay in registers.
-template <int B, int E, class F>
-__device__ __forceinline__ void static_for(F &&f) {
-    if constexpr (B < E) {
-        f(std::integral_constant<int, B>{});
-        static_for<B + 1, E>(f);
-    }
-}
-
-#define IX(a, b, c) (std::integral_constant<int, kTab.idx3[a][b][c]>::value)
-
-template <int P>
-__device__ __forceinline__ void d_tensors_reg(double rx, double ry, double rz, double (&D)[ncoef(P)]) {
-    const double r2 = rx * rx + ry * ry + rz * rz;
-    const double inv_r2 = 1.0 / r2;
-    D[0] = sqrt(inv_r2);
-    static_for<1, ncoef(P)>([&](auto I) {
-        constexpr int idx = decltype(I)::value;
-        constexpr int kx = kTab.mi[idx][0], ky = kTab.mi[idx][1], kz = kTab.mi[idx][2];
-        double acc = 0.0;
-        if constexpr (kx > 0) {
-            acc -= (2.0 * kx - 1.0) * rx * D[IX(kx - 1, ky, kz)];
-            if constexpr (kx > 1) acc -= (kx - 1.0) * (kx - 1.0) * D[IX(kx - 2, ky, kz)];
-            if constexpr (ky > 0) {
-                acc -= 2.0 * ky * ry * D[IX(kx, ky - 1, kz)];
-                if constexpr (ky > 1) acc -= ky * (ky - 1.0) * D[IX(kx, ky - 2, kz)];
-            }
-            if constexpr (kz > 0) {
-                acc -= 2.0 * kz * rz * D[IX(kx, ky, kz - 1)];
-                if constexpr (kz > 1) acc -= kz * (kz - 1.0) * D[IX(kx, ky, kz - 2)];
-            }
-        } else if constexpr (ky > 0) {
-            acc -= (2.0 * ky - 1.0) * ry * D[IX(kx, ky - 1, kz)];
-            if constexpr (ky > 1) acc -= (ky - 1.0) * (ky - 1.0) * D[IX(kx, ky - 2, kz)];
-            if constexpr (kz > 0) {
-                acc -= 2.0 * kz * rz * D[IX(kx, ky, kz - 1)];
-                if constexpr (kz > 1) acc -= kz * (kz - 1.0) * D[IX(kx, ky, kz - 2)];
-            }
-        } else {
-            acc -= (2.0 * kz - 1.0) * rz * D[IX(kx, ky, kz - 1)];
-            if constexpr (kz > 1) acc -= (kz - 1.0) * (kz - 1.0) * D[IX(kx, ky, kz - 2)];
-        }
-        D[idx] = acc * inv_r2;
-    });
-}
-
+// ---- register kernel, compile-time multi-indices (taylor.cuh) -----------
 template <int P>
 __global__ void __launch_bounds__(128) m2l_reg(int32_t ncells, const int64_t *__restrict__ rows,
                                                const int32_t *__restrict__ src,

@@ -1,0 +1,60 @@
+// taylor.cuh -- compile-time Cartesian Taylor machinery shared by the
+// M2L and M2P kernels: D_k = d^k (1/|r|) by the reference's degree-by-degree
+// recurrence (src/_taylor.py:57-95) with every multi-index resolved at
+// compile time, so D stays in registers.
+#pragma once
+
+#include <type_traits>
+
+#include "fmm_common.cuh"
+
+namespace fmm {
+
+// static_for hands each iteration its index as a type, so every table
+// lookup below is a constant expression and D / M / L stay in registers.
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+#define IX(a, b, c) (std::integral_constant<int, kTab.idx3[a][b][c]>::value)
+
+template <int P>
+__device__ __forceinline__ void d_tensors_reg(double rx, double ry, double rz, double (&D)[ncoef(P)]) {
+    const double r2 = rx * rx + ry * ry + rz * rz;
+    const double inv_r2 = 1.0 / r2;
+    D[0] = sqrt(inv_r2);
+    static_for<1, ncoef(P)>([&](auto I) {
+        constexpr int idx = decltype(I)::value;
+        constexpr int kx = kTab.mi[idx][0], ky = kTab.mi[idx][1], kz = kTab.mi[idx][2];
+        double acc = 0.0;
+        if constexpr (kx > 0) {
+            acc -= (2.0 * kx - 1.0) * rx * D[IX(kx - 1, ky, kz)];
+            if constexpr (kx > 1) acc -= (kx - 1.0) * (kx - 1.0) * D[IX(kx - 2, ky, kz)];
+            if constexpr (ky > 0) {
+                acc -= 2.0 * ky * ry * D[IX(kx, ky - 1, kz)];
+                if constexpr (ky > 1) acc -= ky * (ky - 1.0) * D[IX(kx, ky - 2, kz)];
+            }
+            if constexpr (kz > 0) {
+                acc -= 2.0 * kz * rz * D[IX(kx, ky, kz - 1)];
+                if constexpr (kz > 1) acc -= kz * (kz - 1.0) * D[IX(kx, ky, kz - 2)];
+            }
+        } else if constexpr (ky > 0) {
+            acc -= (2.0 * ky - 1.0) * ry * D[IX(kx, ky - 1, kz)];
+            if constexpr (ky > 1) acc -= (ky - 1.0) * (ky - 1.0) * D[IX(kx, ky - 2, kz)];
+            if constexpr (kz > 0) {
+                acc -= 2.0 * kz * rz * D[IX(kx, ky, kz - 1)];
+                if constexpr (kz > 1) acc -= kz * (kz - 1.0) * D[IX(kx, ky, kz - 2)];
+            }
+        } else {
+            acc -= (2.0 * kz - 1.0) * rz * D[IX(kx, ky, kz - 1)];
+            if constexpr (kz > 1) acc -= (kz - 1.0) * (kz - 1.0) * D[IX(kx, ky, kz - 2)];
+        }
+        D[idx] = acc * inv_r2;
+    });
+}
+
+}  // namespace fmm

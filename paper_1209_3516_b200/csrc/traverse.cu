@@ -39,20 +39,25 @@ __device__ inline unsigned long long warp_reserve(unsigned long long *counter, i
 
 // Fate of a pair (src/traversal.py:185-211): 1 = P2P (both leaves, tested
 // before the MAC), 2 = M2L (MAC accepted), 3 = split.
-__device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const uint8_t *__restrict__ leaf,
-                                         const double *__restrict__ ctr, const double *__restrict__ bmax,
-                                         const double *__restrict__ rmax, int kind_mac, double th2) {
-    if (leaf[a] && leaf[b]) return 1;
+// _mac_ok (src/traversal.py:144-156) for target a, source b: 0 = bh,
+// 1 = bmax, 2 = fmm; r2 == 0 rejects.
+__device__ __forceinline__ bool mac_accept(int32_t a, int32_t b, const double *__restrict__ ctr,
+                                           const double *__restrict__ bmax, const double *__restrict__ rmax,
+                                           int kind_mac, double th2) {
     const double dx = ctr[a * 3] - ctr[b * 3];
     const double dy = ctr[a * 3 + 1] - ctr[b * 3 + 1];
     const double dz = ctr[a * 3 + 2] - ctr[b * 3 + 2];
     const double r2 = dx * dx + dy * dy + dz * dz;
-    if (r2 != 0.0) {
-        // src/traversal.py:144-156: 0 = bh, 1 = bmax, 2 = fmm
-        const double s = kind_mac == 2 ? bmax[a] + bmax[b] : (kind_mac == 1 ? bmax[b] : 2.0 * rmax[b]);
-        if (s * s < th2 * r2) return 2;
-    }
-    return 3;
+    if (r2 == 0.0) return false;
+    const double s = kind_mac == 2 ? bmax[a] + bmax[b] : (kind_mac == 1 ? bmax[b] : 2.0 * rmax[b]);
+    return s * s < th2 * r2;
+}
+
+__device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const uint8_t *__restrict__ leaf,
+                                         const double *__restrict__ ctr, const double *__restrict__ bmax,
+                                         const double *__restrict__ rmax, int kind_mac, double th2) {
+    if (leaf[a] && leaf[b]) return 1;
+    return mac_accept(a, b, ctr, bmax, rmax, kind_mac, th2) ? 2 : 3;
 }
 
 // One breadth-first step.  Every frontier pair is a pair already known to
@@ -141,6 +146,77 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
 }
 
 // ---- CSR ----------------------------------------------------------------
+// ---- treecode (src/traversal.py:265-313) ----------------------------------
+// Per target leaf t the reference walks the source tree from the root and
+// classifies each (t, c) it pops: MAC accepted -> M2P (tested FIRST, so a
+// leaf source far enough away is M2P); else c a leaf -> P2P; else push c's
+// non-empty children.  The sets are independent of visiting order, so a
+// breadth-first frontier over (t, c) pairs -- one source level per step --
+// reproduces them.  The seed frontier is every leaf whose bodies meet
+// [blo, bhi), paired with the root.
+__global__ void treecode_seed_flags(int32_t ncells, const uint8_t *__restrict__ leaf,
+                                    const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
+                                    int32_t blo, int32_t bhi, uint8_t *flag, int32_t *fb) {
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+        flag[c] = leaf[c] && cend[c] > blo && cstart[c] < bhi;
+        fb[c] = 0;  // every seed pair starts at the root
+    }
+}
+
+__global__ void treecode_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
+                                     const unsigned long long *__restrict__ nfront_dev, int64_t cap_front,
+                                     const int32_t *__restrict__ children, const uint8_t *__restrict__ leaf,
+                                     const double *__restrict__ ctr, const double *__restrict__ bmax,
+                                     const double *__restrict__ rmax, int kind_mac, double th2,
+                                     int32_t *m2p_t, int32_t *m2p_s, int64_t cap_m2p, int32_t *p2p_t,
+                                     int32_t *p2p_s, int64_t cap_p2p, int32_t *na, int32_t *nb, int64_t cap_next,
+                                     unsigned long long *cnt_p2p, unsigned long long *cnt_m2p,
+                                     unsigned long long *cnt_next) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t nfront = (int64_t)*nfront_dev;
+    if (nfront > cap_front) nfront = cap_front;
+    const int64_t nround = (nfront + stride - 1) / stride;
+    for (int64_t r = 0; r < nround; r++) {
+        const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        int fate = 0;  // 1 = P2P, 2 = M2P, 3 = open the source
+        int32_t t = 0, c = 0;
+        int nch = 0;
+        if (k < nfront) {
+            t = fa[k];
+            c = fb[k];
+            if (mac_accept(t, c, ctr, bmax, rmax, kind_mac, th2)) fate = 2;
+            else if (leaf[c]) fate = 1;
+            else {
+                fate = 3;
+#pragma unroll
+                for (int o = 0; o < 8; o++) nch += children[c * 8 + o] >= 0;
+            }
+        }
+        int op, om, on;
+        const unsigned long long bp = warp_reserve(cnt_p2p, fate == 1, lane, &op);
+        const unsigned long long bm = warp_reserve(cnt_m2p, fate == 2, lane, &om);
+        const unsigned long long bn = warp_reserve(cnt_next, nch, lane, &on);
+        if (fate == 1) {
+            const unsigned long long ip = bp + op;
+            if (ip < (unsigned long long)cap_p2p) { p2p_t[ip] = t; p2p_s[ip] = c; }
+        } else if (fate == 2) {
+            const unsigned long long im = bm + om;
+            if (im < (unsigned long long)cap_m2p) { m2p_t[im] = t; m2p_s[im] = c; }
+        } else if (fate == 3) {
+            unsigned long long in = bn + on;
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int32_t ch = children[c * 8 + o];
+                if (ch >= 0) {
+                    if (in < (unsigned long long)cap_next) { na[in] = t; nb[in] = ch; }
+                    in++;
+                }
+            }
+        }
+    }
+}
+
 __global__ void pack_pairs(const int32_t *t, const int32_t *s, int64_t n, int sbits, uint64_t *keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -236,6 +312,42 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
             dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_traverse");
+    return FMM_OK;
+}
+
+int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                          int64_t cap_front, int nsteps, int32_t ncells, const int32_t *children,
+                          const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                          const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                          double th2, int32_t *m2p_t, int32_t *m2p_s, int64_t cap_m2p, int32_t *p2p_t,
+                          int32_t *p2p_s, int64_t cap_p2p, unsigned long long *dev_log, void *ws,
+                          size_t ws_bytes, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (cap_front < ncells) {
+        set_error("treecode frontier capacity %lld < ncells %d", (long long)cap_front, ncells);
+        return FMM_ERR_INVALID;
+    }
+    Arena ar(ws, ws_bytes);
+    uint8_t *flag = ar.take<uint8_t>((size_t)ncells);
+    if (!flag) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    // dev_log[0] = n_p2p, [1] = n_m2p, [2 + s] = frontier entering step s
+    cudaMemsetAsync(dev_log, 0, sizeof(unsigned long long) * (nsteps + 3), st);
+    treecode_seed_flags<<<grid_for(ncells, 256), 256, 0, st>>>(ncells, leaf, start, end, body_lo, body_hi, flag,
+                                                                front_b0); fmm::note_launch();
+    size_t need = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    cub::DeviceSelect::Flagged(nullptr, need, it, flag, front_a0, dev_log + 2, ncells, st);
+    if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, front_a0, dev_log + 2, ncells, st);
+    const int grid = 148 * 8;
+    for (int sidx = 0; sidx < nsteps; sidx++) {
+        const bool even = (sidx & 1) == 0;
+        treecode_step_kernel<<<grid, 256, 0, st>>>(
+            even ? front_a0 : front_a1, even ? front_b0 : front_b1, dev_log + 2 + sidx, cap_front, children, leaf,
+            ctr, bmax, rmax, kind, th2, m2p_t, m2p_s, cap_m2p, p2p_t, p2p_s, cap_p2p, even ? front_a1 : front_a0,
+            even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
+    }
+    FMM_CUDA_CHECK("fmm_treecode_traverse");
     return FMM_OK;
 }
 

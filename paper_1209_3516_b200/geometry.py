@@ -96,8 +96,9 @@ class ParticleSet:
             for a in (phi, fx, fy, fz):
                 acc.append(np.zeros(n) if a is None else np.ascontiguousarray(a, dtype=np.float64))
             self.phi, self.fx, self.fy, self.fz = acc
-        lengths = {int(a.shape[0]) for a in (self.x, self.y, self.z, self.q, self.phi, self.fx, self.fy,
-                                             self.fz)}
+        # (stored arrays: reading self.x here would upcast a float32 cloud)
+        stored = self.host_inputs() if self._f64 is not None else (self.x, self.y, self.z, self.q)
+        lengths = {int(a.shape[0]) for a in (*stored, self.phi, self.fx, self.fy, self.fz)}
         if lengths != {int(n)}:
             raise ValueError(f"particle arrays disagree on length: {sorted(lengths)}")
 

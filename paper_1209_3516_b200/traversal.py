@@ -16,9 +16,15 @@ downward; ``total_time`` sums them) and are measured with CUDA events on the
 evaluation stream; ``stats.times`` holds the per-kernel-class split
 ("list", "m2l", "p2p").
 
-Scope: ``strategy="dualtree"``, directed (``mutual=False``), one shared
-tree.  ``treecode``/``listfmm``, ``mutual=True`` and ``source_tree`` are
-outside the B200 hot path and raise NotImplementedError.
+``evaluate_treecode`` walks every target leaf against
+the tree (csrc/traverse.cu, bit-exact sets with ``_collect_treecode``),
+evaluates accepted cells' multipoles at the bodies (M2P, csrc/m2p.cu) and
+reuses the P2P plan and kernel for the near field.
+
+Scope: ``strategy="dualtree"`` (directed, ``mutual=False``) and
+``"treecode"``, one shared tree.  ``listfmm``, ``mutual=True`` and
+``source_tree`` are outside the B200 hot path and raise
+NotImplementedError.
 ``precision`` is a new knob: "fp64" (default, the reference's arithmetic)
 or "fp32" (FP32 near field; far field stays float64).
 """
@@ -40,8 +46,8 @@ STRATEGIES = ("treecode", "listfmm", "dualtree")
 PRECISIONS = ("fp64", "fp32")
 REPORT_SCHEMA = "fmmkit-report-v1"
 
-__all__ = ["STRATEGIES", "PRECISIONS", "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_on_tree",
-           "interaction_lists"]
+__all__ = ["STRATEGIES", "PRECISIONS", "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_treecode",
+           "evaluate_on_tree", "interaction_lists", "treecode_lists"]
 
 
 @dataclass
@@ -177,45 +183,60 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
     ncells = tree.ncells
-    m2l_src = torch.empty(max(done_m2l, 1), dtype=i32, device=dev)
-    m2l_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev)
-    if side is None:
-        _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), wsp, wsb, st)
-        if m2l_ready is not None:
-            m2l_ready.record()  # the M2L list is final: the far field may start
-    else:
-        # only the far field reads the M2L list: sort it on the side stream,
-        # off the P2P critical path, with its own scratch buffer
-        traversed = torch.cuda.Event()
-        traversed.record()
-        side.wait_event(traversed)
-        swp, swb = _lib.workspace(max(done_m2l, 1), dev, slot=1)
-        _lib.call("fmm_pairs_to_csr", P(m2l_t), P(m2l_s), done_m2l, ncells, P(m2l_src), P(m2l_rows), swp, swb,
-                  side.cuda_stream)
-        for a in (m2l_t, m2l_s, m2l_src, m2l_rows):
-            a.record_stream(side)
-        if m2l_ready is not None:
-            m2l_ready.record(side)
-    p2p_src = torch.empty(max(done_p2p, 1), dtype=i32, device=dev)
-    p2p_rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
-    _lib.call("fmm_pairs_to_csr", P(p2p_t), P(p2p_s), done_p2p, ncells, P(p2p_src), P(p2p_rows), wsp, wsb, st)
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
+    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
     del p2p_t, p2p_s, m2l_t, m2l_s
-    # P2P run plan + the reference's pair counters (no host round trip:
-    # runs <= pairs, and the row count stays on the device)
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+                 p2p_rows=p2p_rows, peak_frontier=peak,
+                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+
+
+def _csr(t, s, n, ncells, dev, wsp, wsb, stream):
+    """(sources, row offsets) of pairs (t, s) sorted by target then source."""
+    src = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
+    _lib.call("fmm_pairs_to_csr", _lib.ptr(t), _lib.ptr(s), n, ncells, _lib.ptr(src), _lib.ptr(rows), wsp, wsb,
+              stream)
+    return src, rows
+
+
+def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready):
+    """CSR of a far-field list (M2L or M2P).  Only the far field reads it, so
+    with a ``side`` stream it is sorted there, off the P2P critical path,
+    with its own scratch buffer; ``ready`` is recorded once it is final."""
+    if side is None:
+        out = _csr(t, s, n, ncells, dev, wsp, wsb, st)
+        if ready is not None:
+            ready.record()
+        return out
+    traversed = torch.cuda.Event()
+    traversed.record()
+    side.wait_event(traversed)
+    swp, swb = _lib.workspace(max(n, 1), dev, slot=1)
+    out = _csr(t, s, n, ncells, dev, swp, swb, side.cuda_stream)
+    for a in (t, s, *out):
+        a.record_stream(side)
+    if ready is not None:
+        ready.record(side)
+    return out
+
+
+def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st) -> dict:
+    """P2P run plan + the reference's pair counters (no host round trip:
+    runs <= pairs, and the row count stays on the device)."""
+    dev, P, i32, ncells = tree.device, _lib.ptr, torch.int32, tree.ncells
     leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
     run_off = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
     dev_stats = torch.zeros(2, dtype=torch.int64, device=dev)
     dev_nrows = torch.empty(1, dtype=i32, device=dev)
-    cap_runs = max(done_p2p, 1)
+    cap_runs = max(n_p2p, 1)
     runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
     _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
               P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(leaf_rows), P(run_off), P(runs), cap_runs,
               None, None, P(dev_nrows), P(dev_stats), wsp, wsb, st)
-    nrows_bound = tree.nleaves
-    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
-                 p2p_rows=p2p_rows, leaf_rows=leaf_rows, nrows=nrows_bound, dev_nrows=dev_nrows, run_off=run_off,
-                 runs=runs, dev_stats=dev_stats, peak_frontier=peak)
+    return dict(leaf_rows=leaf_rows, nrows=tree.nleaves, dev_nrows=dev_nrows, run_off=run_off, runs=runs,
+                dev_stats=dev_stats)
 
 
 def run_m2l(tree: Tree, lists: Lists, p: int) -> None:
@@ -236,6 +257,64 @@ def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, s
               P(tree.d_start),
               P(tree.d_end), P(lists.run_off), P(lists.runs), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_q),
               P(tree.d_b32), P(tree.d_b32lo), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag),
+              _lib.stream_handle())
+
+
+def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
+                   m2p_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None) -> Lists:
+    """Treecode walk (src/traversal.py:265-313) of every target leaf against
+    the source tree -> target-sorted CSR M2P and P2P lists (bit-exact sets
+    with the reference's ``_collect_treecode``) + the P2P run plan.
+
+    ``body_range=(lo, hi)`` keeps the target leaves whose bodies meet
+    [lo, hi) (a multi-GPU rank's share)."""
+    blo, bhi = body_range if body_range is not None else (0, tree.n)
+    dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
+    th2 = mac.theta * mac.theta
+    ncells = tree.ncells
+    key = ("treecode", ncells, tree.nleaves, mac.kind, th2, blo, bhi)
+    cap_p2p, cap_m2p, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.nleaves * 256),
+                                                 max(4096, ncells * 8)))
+    nsteps = tree.depth + 2  # one source level per step
+    log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
+    wsp, wsb = _lib.workspace(max(ncells, tree.n), dev)
+    while True:
+        cap_front = max(cap_next, ncells)
+        fr = [torch.empty(cap_front, dtype=i32, device=dev) for _ in range(4)]
+        m2p_t = torch.empty(cap_m2p, dtype=i32, device=dev)
+        m2p_s = torch.empty(cap_m2p, dtype=i32, device=dev)
+        p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
+        p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
+        _lib.call("fmm_treecode_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_front, nsteps, ncells,
+                  P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax),
+                  P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(m2p_t), P(m2p_s), cap_m2p, P(p2p_t),
+                  P(p2p_s), cap_p2p, P(log), wsp, wsb, st)
+        hl = log.tolist()  # the one synchronisation of the walk
+        done_p2p, done_m2p, fronts = hl[0], hl[1], hl[2:]
+        peak = max(fronts)
+        if fronts[-1] != 0:
+            raise RuntimeError("treecode walk did not terminate within depth+2 steps")
+        if done_p2p <= cap_p2p and done_m2p <= cap_m2p and peak <= cap_front:
+            break
+        cap_p2p = max(cap_p2p, int(done_p2p * 1.05) + 4096)
+        cap_m2p = max(cap_m2p, int(done_m2p * 1.05) + 4096)
+        cap_next = max(cap_next, int(peak * 1.05) + 4096)
+    del fr
+    _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2p * 1.02) + 4096, int(peak * 1.05) + 4096)
+    wsp, wsb = _lib.workspace(max(done_m2p, done_p2p, tree.n), dev)
+    m2p_src, m2p_rows = _far_csr(m2p_t, m2p_s, done_m2p, ncells, dev, wsp, wsb, st, side, m2p_ready)
+    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    del p2p_t, p2p_s, m2p_t, m2p_s
+    return Lists(n_m2l=0, n_m2p=done_m2p, n_p2p=done_p2p, m2p_src=m2p_src, m2p_rows=m2p_rows, p2p_src=p2p_src,
+                 p2p_rows=p2p_rows, peak_frontier=peak,
+                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+
+
+def run_m2p(tree: Tree, lists: Lists, p: int, out) -> None:
+    """Treecode far field into ``out`` = (phi, fx, fy, fz) (accumulated)."""
+    P = _lib.ptr
+    _lib.call("fmm_m2p_csr", p, tree.ncells, P(lists.m2p_rows), P(lists.m2p_src), P(tree.d_start),
+              P(tree.d_end), P(tree.d_ctr), P(tree._M), P(tree.d_x), P(tree.d_y), P(tree.d_z), *(P(a) for a in out),
               _lib.stream_handle())
 
 
@@ -336,9 +415,88 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                       downward_time=e_m2l1.elapsed_time(e_down1) * 1e-3, trace=events)
 
 
+def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
+                      trace: bool = False) -> EvalReport:
+    """Classic one-tree-at-a-time walk; the far field lands directly on the
+    bodies (src/traversal.py:1002-1046), on the GPU.
+
+    Same two-stream layout as ``evaluate_dual_tree``: the main stream walks
+    the tree and runs P2P; the side stream runs the upward pass and, once
+    the M2P list is sorted, M2P into separate accumulators that one combine
+    kernel adds at the end.  The walk is target-leaf driven, so
+    ``cfg.mutual`` has no effect here (as in the reference)."""
+    if source_tree is not None and source_tree is not tree:
+        raise NotImplementedError("separate source trees are outside the B200 hot path")
+    if threads < 1:
+        raise ValueError(f"threads must be >= 1, got {threads}")
+    stats = KernelStats()
+    dev = tree.device
+    p = cfg.p
+    with torch.cuda.device(dev):
+        main = torch.cuda.current_stream(dev)
+        side = _side_stream(dev)
+        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        e0, e_up0, e_up1, e_m0, e_m1, e_l1, e_p0, e_p1, e_end = (E() for _ in range(9))
+        need_up = tree._M is None or tree.p != p
+        M = torch.zeros((tree.ncells, ncoef(p)), dtype=torch.float64, device=dev) if need_up else tree._M
+        far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+        e0.record(main)
+        side.wait_event(e0)
+        with torch.cuda.stream(side):
+            e_up0.record(side)
+            if need_up:
+                upward_pass(tree, p, stats, sync=False, M=M)  # (resets tree._L)
+            e_up1.record(side)
+        tree._M, tree.p = M, p
+        m2p_ready = torch.cuda.Event()
+        lists = treecode_lists(tree, cfg.mac, m2p_ready=m2p_ready, side=side)
+        tree.list_cache = lists
+        e_l1.record(main)
+        side.wait_event(m2p_ready)
+        with torch.cuda.stream(side):
+            e_m0.record(side)
+            run_m2p(tree, lists, p, tuple(far))
+            e_m1.record(side)
+        e_p0.record(main)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+        e_p1.record(main)
+        if cfg.precision == "fp32" and int(flag.item()) != 0:
+            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+            e_p1.record(main)
+        main.wait_event(e_m1)
+        P = _lib.ptr
+        _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
+                  P(tree.d_fz), _lib.stream_handle())
+        e_end.record(main)
+        e_end.synchronize()
+        pairs, skipped = lists.dev_stats.tolist()
+    stats.p2p_pairs += int(pairs)
+    stats.p2p_skipped += int(skipped)
+    stats.p2p_flops += 20 * int(pairs)
+    stats.m2p_calls += lists.n_m2p
+    stats.add_time("list", e0.elapsed_time(e_l1) * 1e-3)
+    stats.add_time("m2p", e_m0.elapsed_time(e_m1) * 1e-3)
+    stats.add_time("p2p", e_p0.elapsed_time(e_p1) * 1e-3)
+    tree._results_changed()
+    events = None
+    if trace:
+        events = []
+        mt, ms = lists.host_pairs("m2p")
+        events += [("m2p", int(a), int(b)) for a, b in zip(mt, ms)]
+        pt, ps = lists.host_pairs("p2p")
+        events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
+    return EvalReport(strategy="treecode", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
+                      theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain,
+                      stats=stats, build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
+                      traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=0.0, trace=events)
+
+
 def evaluate_on_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
                      trace: bool = False) -> EvalReport:
     """Run ``cfg.strategy`` on the tree; results land in ``tree.bodies``."""
+    if cfg.strategy == "treecode":
+        return evaluate_treecode(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)
     if cfg.strategy != "dualtree":
-        raise NotImplementedError(f"strategy {cfg.strategy!r} is outside the B200 hot path (dualtree only)")
+        raise NotImplementedError(f"strategy {cfg.strategy!r} is outside the B200 hot path")
     return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)

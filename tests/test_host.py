@@ -135,9 +135,11 @@ def test_workload_generators_are_seeded():
 
 
 def test_out_of_scope_paths_raise():
-    cfg = fb.EvalConfig(strategy="treecode")
+    cfg = fb.EvalConfig(strategy="listfmm")
     with pytest.raises(NotImplementedError):
         fb.evaluate_on_tree(object(), cfg)
+    with pytest.raises(NotImplementedError):
+        fb.evaluate_treecode(object(), fb.EvalConfig(strategy="treecode"), source_tree=object())
 
 
 def _static_len(node, env):
