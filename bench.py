@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--p", type=int, default=0, help="override the expansion order (C4 sweep)")
     ap.add_argument("--theta", type=float, default=0.0, help="override theta (C4 sweep)")
+    ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode"],
+                    help="evaluation strategy (the headline is the dual-tree FMM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU work for the baseline sample")
@@ -81,7 +83,7 @@ def workload(args):
 
 def config_block(args, n, solver, extra=None):
     d = {"workload": f"{args.config}: Laplace FMM N={n}", "n": n, "p": solver["p"], "theta": solver["theta"],
-         "ncrit": solver["ncrit"], "mac": "fmm", "strategy": "dualtree",
+         "ncrit": solver["ncrit"], "mac": "fmm", "strategy": getattr(args, "strategy", "dualtree"),
          "distribution": {"C1": "uniform f64", "C2": "uniform f32, q~U[0,1)", "C3": "Plummer a=1 rcut=10a",
                           "C4": "uniform f32, q~U[-1,1)", "C5": "uniform f32, q~U[0,1)"}[args.config],
          "l2": "flushed between timed steps (2x L2 write)"}
@@ -245,7 +247,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pos, q, n, solver = workload(args)
-    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"], precision=args.precision)
+    if args.strategy != "dualtree" and world > 1:
+        raise SystemExit("multi-GPU runs partition the dual-tree FMM only")
+    cfg = fb.EvalConfig(strategy=args.strategy, mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"],
+                        precision=args.precision)
     dev = torch.device("cuda", local)
     dt = torch.float32 if pos.dtype == np.float32 else torch.float64
     dpos = torch.as_tensor(pos, device=dev).to(dt)
@@ -340,7 +345,7 @@ def run_ours(args):
         except Exception:
             traffic = None
     cpu = None
-    if not args.no_cpu_baseline and rank == 0 and world == 1:
+    if not args.no_cpu_baseline and rank == 0 and world == 1 and args.strategy == "dualtree":
         v, d = cpu_run(pos, q, solver, args.cpu_seconds)
         cpu = {"value": v, "unit": "particles/s", "cores": d["threads"], "kind": "port",
                "sample": f"C oracle (restated reference, {d['threads']} threads, {cpu_model()}): full "
@@ -355,7 +360,7 @@ def run_ours(args):
         "data": "synthetic", "config": config_block(args, n, solver, {"precision": args.precision,
                                                                       "parallelism": f"morton-partition x{world}"}),
         "p2p_ginteractions_per_s": rep.stats.p2p_pairs / p2p_s / 1e9,
-        "p2p_pairs": rep.stats.p2p_pairs, "m2l_calls": rep.stats.m2l_calls,
+        "p2p_pairs": rep.stats.p2p_pairs, "m2l_calls": rep.stats.m2l_calls, "m2p_calls": rep.stats.m2p_calls,
         "phase_ms": {"build": 1e3 * rep.build_time, "upward": 1e3 * rep.upward_time,
                      "traversal": 1e3 * rep.traversal_time, "downward": 1e3 * rep.downward_time},
         "kernel_ms": kernel_ms,

@@ -13,7 +13,8 @@ from .mac import MacConfig, accept, error_bound
 from .traversal import (EvalConfig, EvalReport, evaluate_dual_tree, evaluate_on_tree, evaluate_treecode,
                         interaction_lists, treecode_lists)
 from .tree import Tree, build_tree, check_invariants, downward_pass, upward_pass
-from .tuner import error_sample, sampled_force_error, verify_against_direct
+from .tuner import (TuneEntry, TuneResult, error_sample, max_theta_for_error, sampled_force_error, select_p_theta,
+                    verify_against_direct)
 
 __version__ = "0.1.0"
 
@@ -23,5 +24,6 @@ __all__ = [
     "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_on_tree", "evaluate_treecode", "interaction_lists",
     "treecode_lists",
     "Tree", "build_tree", "check_invariants", "downward_pass", "upward_pass",
-    "error_sample", "sampled_force_error", "verify_against_direct", "__version__",
+    "error_sample", "sampled_force_error", "verify_against_direct", "max_theta_for_error", "select_p_theta",
+    "TuneEntry", "TuneResult", "__version__",
 ]

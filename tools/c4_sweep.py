@@ -20,7 +20,8 @@ dpos = torch.as_tensor(pos, device="cuda")
 ps = fb.ParticleSet(dpos[:, 0].contiguous(), dpos[:, 1].contiguous(), dpos[:, 2].contiguous(),
                     torch.as_tensor(q, device="cuda"))
 tree = fb.build_tree(ps, ncrit=64)
-idx, fref, pref = fb.error_sample(tree, 1000, 0)
+from paper_1209_3516_b200.tuner import potential_sample  # noqa: E402
+idx, fref, pref = potential_sample(tree, 1000, 0)
 out = []
 for p in (3, 4, 6, 8, 10):
     for th in (0.3, 0.4, 0.5, 0.6):
