@@ -42,7 +42,9 @@ def test_max_theta_matches_reference(tree, k):
     assert theta == c["theta"]
     fb.evaluate_dual_tree(tree, fb.EvalConfig(mac=fb.MacConfig("fmm", theta), p=c["p"]))
     err = fb.sampled_force_error(tree, *oracle)
-    assert abs(err - c["tuned_error"]) <= 1e-9 * max(c["tuned_error"], 1e-12) + 1e-15
+    # relative 1e-9, with an absolute floor for near-direct configurations
+    # whose error is FP64 rounding (~1e-15, order-dependent)
+    assert abs(err - c["tuned_error"]) <= 1e-9 * c["tuned_error"] + 1e-13
 
 
 def test_select_p_theta_consistent(tree):
