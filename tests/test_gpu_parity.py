@@ -11,6 +11,7 @@ import pytest
 import torch
 
 import paper_1209_3516_b200 as fb
+from paper_1209_3516_b200 import workloads
 from goldens import CASES, Case, canon_pairs, rel_l2, sha
 from oracle import oracle as orc
 
@@ -167,3 +168,36 @@ def test_max_depth_error_message():
     with pytest.raises(ValueError) as ei:
         fb.build_tree(ps, ncrit=8)
     assert str(ei.value) == INDEX["max_depth_message"]
+
+
+def _assert_rows_sorted(rows, src):
+    rows = rows.cpu().numpy()
+    src = src.cpu().numpy()[: rows[-1]].astype(np.int64)
+    d = np.diff(src)  # d[k] compares src[k + 1] with src[k]
+    keep = np.ones(d.size, bool)
+    starts = rows[1:-1]
+    starts = starts[(starts > 0) & (starts < src.size)]
+    keep[starts - 1] = False  # a new row starts at k + 1: no ordering across rows
+    assert np.all(d[keep] > 0)
+
+
+def test_csr_rows_sorted_and_long_rows():
+    """Every CSR row is strictly ascending (the plan merges runs from it),
+    including rows longer than one warp's sort capacity (2048): at tiny theta
+    every leaf pair is P2P, so each row lists all leaves."""
+    pos, q = workloads.uniform_unit(1 << 14, 3)
+    t = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], q), ncrit=4)
+    assert t.nleaves > 2048
+    lists = fb.interaction_lists(t, fb.MacConfig("fmm", 1e-6))
+    assert lists.n_m2l == 0 and lists.n_p2p == t.nleaves ** 2
+    _assert_rows_sorted(lists.p2p_rows, lists.p2p_src)
+    leaves = np.flatnonzero(t.cell_leaf)
+    rows = lists.p2p_rows.cpu().numpy()
+    src = lists.p2p_src.cpu().numpy()
+    for leaf in leaves[:: max(1, leaves.size // 7)]:
+        assert np.array_equal(src[rows[leaf]:rows[leaf + 1]], leaves)
+    c = Case("c1")
+    t2 = build(c)
+    l2 = fb.interaction_lists(t2, fb.MacConfig("fmm", c.theta))
+    _assert_rows_sorted(l2.m2l_rows, l2.m2l_src)
+    _assert_rows_sorted(l2.p2p_rows, l2.p2p_src)
