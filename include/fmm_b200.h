@@ -152,12 +152,16 @@ FMM_API int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uin
  * kind: MAC kind code (0 bh, 1 bmax, 2 fmm; src/mac.py:21-22); th2 = theta*theta
  * computed by the caller exactly as the reference.  Pairs whose target
  * cell's body range misses [body_lo, body_hi) are dropped (a multi-GPU rank
- * keeps only its own targets; [0, n) keeps everything). */
+ * keeps only its own targets; [0, n) keeps everything).  With
+ * m2l_owner_only, an M2L pair is emitted only if its target's FIRST body
+ * lies in [body_lo, body_hi), so chunks of one GPU's targets, cut on leaf
+ * boundaries, partition the M2L list as well as the P2P list. */
 FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int classify_self,
                       const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
                       const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
-                      int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                      int m2l_owner_only, int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
+                      int32_t *m2l_t,
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
                       unsigned long long *dev_counts, void *stream);
 
@@ -171,8 +175,8 @@ FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfro
 FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
                  int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
                  const double *ctr, const double *bmax, const double *rmax, const int32_t *start,
-                 const int32_t *end, int32_t body_lo, int32_t body_hi, int kind, double th2,
-                 int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
+                 const int32_t *end, int32_t body_lo, int32_t body_hi, int m2l_owner_only, int kind,
+                 double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
                  int64_t cap_m2l, unsigned long long *dev_log, void *stream);
 
 /* Treecode lists (replaces _collect_treecode, src/traversal.py:265-313, with

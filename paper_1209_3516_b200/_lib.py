@@ -43,8 +43,9 @@ SIGNATURES = {
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
     "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],
-    "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64, P, P, I64, P, P],
-    "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64, P, P],
+    "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P, P, I64, P, P,
+                          I64, P, P],
+    "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P, P, I64, P, P],
     "fmm_treecode_traverse": [P, P, P, P, I64, INT, I32, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P,
                               I64, P, P, SZ, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
@@ -136,9 +137,12 @@ def stream_handle(stream=None) -> int:
 _ws = {}
 
 
-def workspace(items: int, device, slot: int = 0) -> tuple[int, int]:
+def workspace(items: int, device, slot: int = 0, stream=None) -> tuple[int, int]:
     """(pointer, bytes) of a scratch buffer valid for ``items`` elements
-    (``slot`` separates buffers used concurrently on different streams)."""
+    (``slot`` separates buffers used concurrently on different streams; with
+    ``stream`` (a torch stream other than the allocating one) the buffer is
+    recorded on it, so a later reallocation cannot recycle it under that
+    stream's pending work)."""
     need = C.c_size_t(0)
     call("fmm_workspace_bytes", int(max(items, 1)), C.byref(need))
     key = (torch.device(device).index or 0, threading.get_ident(), slot)  # per thread: calls may overlap
@@ -147,4 +151,6 @@ def workspace(items: int, device, slot: int = 0) -> tuple[int, int]:
         _ws[key] = None
         buf = torch.empty(int(need.value * 1.25) + 4096, dtype=torch.uint8, device=device)
         _ws[key] = buf
+    if stream is not None:
+        buf.record_stream(stream)
     return buf.data_ptr(), buf.numel()

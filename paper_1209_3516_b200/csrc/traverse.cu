@@ -71,7 +71,8 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                                      const uint8_t *__restrict__ leaf, const double *__restrict__ ctr,
                                      const double *__restrict__ bmax, const double *__restrict__ rmax,
                                      const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
-                                     int32_t blo, int32_t bhi, int kind_mac, double th2, int32_t *p2p_t,
+                                     int32_t blo, int32_t bhi, int m2l_owner, int kind_mac, double th2,
+                                     int32_t *p2p_t,
                                      int32_t *p2p_s, int64_t cap_p2p,
                                      int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l, int32_t *na,
                                      int32_t *nb, int64_t cap_next, unsigned long long *cnt_p2p,
@@ -119,6 +120,9 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                 // multi-GPU: only targets whose body range meets [blo, bhi)
                 if (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi) continue;
                 fate[q] = pair_fate(ca[q], cb[q], leaf, ctr, bmax, rmax, kind_mac, th2);
+                // chunked single-GPU runs: an M2L pair belongs to the chunk
+                // holding its target's first body (no pair is emitted twice)
+                if (fate[q] == 2 && m2l_owner && (cstart[ca[q]] < blo || cstart[ca[q]] >= bhi)) fate[q] = 0;
                 np += fate[q] == 1;
                 nm += fate[q] == 2;
                 nn += fate[q] == 3;
@@ -277,12 +281,14 @@ int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int 
                       const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
                       const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
-                      int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                      int m2l_owner_only, int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
+                      int32_t *m2l_t,
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
                       unsigned long long *dev_counts, void *stream) {
     if (nfront <= 0) return FMM_OK;
     traverse_step_kernel<<<grid_for(nfront, 256, 148 * 16), 256, 0, as_stream(stream)>>>(
-        fa, fb, nfront, nullptr, nfront, classify_self, children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
+        fa, fb, nfront, nullptr, nfront, classify_self, children, leaf, ctr, bmax, rmax, start, end, body_lo,
+        body_hi, m2l_owner_only, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
         na, nb, cap_next, dev_counts, dev_counts + 1, dev_counts + 2); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_traverse_step");
     return FMM_OK;
@@ -291,8 +297,8 @@ int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int 
 int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1, int64_t cap_front,
                  int nsteps, const int32_t *children, const uint8_t *leaf, const double *ctr,
                  const double *bmax, const double *rmax, const int32_t *start, const int32_t *end,
-                 int32_t body_lo, int32_t body_hi, int kind, double th2, int32_t *p2p_t, int32_t *p2p_s,
-                 int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
+                 int32_t body_lo, int32_t body_hi, int m2l_owner_only, int kind, double th2, int32_t *p2p_t,
+                 int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
                  unsigned long long *dev_log, void *stream) {
     cudaStream_t st = as_stream(stream);
     // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s
@@ -307,7 +313,8 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
         const bool even = (sidx & 1) == 0;
         traverse_step_kernel<<<grid, 256, 0, st>>>(
             even ? front_a0 : front_a1, even ? front_b0 : front_b1, 0, dev_log + 2 + sidx, cap_front, sidx == 0,
-            children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p,
+            children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, m2l_owner_only, kind, th2, p2p_t,
+            p2p_s, cap_p2p,
             m2l_t, m2l_s, cap_m2l, even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front,
             dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
     }

@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -143,7 +144,7 @@ _hint = {}
 
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
                       m2l_ready: torch.cuda.Event | None = None,
-                      side: torch.cuda.Stream | None = None) -> Lists:
+                      side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
@@ -155,7 +156,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     st = _lib.stream_handle()
     i32 = torch.int32
     th2 = mac.theta * mac.theta
-    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi)
+    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, m2l_owner_only)
     cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
                                                  max(4096, tree.ncells * 8)))
     # every step opens one side of a pair: at most 2 * depth + 1 steps
@@ -169,7 +170,8 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
         _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
                   P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(tree.d_start), P(tree.d_end),
-                  blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s), cap_m2l, P(log), st)
+                  blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
+                  cap_m2l, P(log), st)
         hl = log.tolist()  # the one synchronisation of the traversal
         done_p2p, done_m2l, fronts = hl[0], hl[1], hl[2:]
         peak = max(fronts)
@@ -183,7 +185,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
     ncells = tree.ncells
-    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev)
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
     m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
     p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
     del p2p_t, p2p_s, m2l_t, m2l_s
@@ -213,7 +215,7 @@ def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready):
     traversed = torch.cuda.Event()
     traversed.record()
     side.wait_event(traversed)
-    swp, swb = _lib.workspace(max(n, 1), dev, slot=1)
+    swp, swb = _lib.workspace(max(n, 1), dev, slot=1, stream=side)
     out = _csr(t, s, n, ncells, dev, swp, swb, side.cuda_stream)
     for a in (t, s, *out):
         a.record_stream(side)
@@ -321,22 +323,70 @@ def run_m2p(tree: Tree, lists: Lists, p: int, out) -> None:
 _side = {}
 
 
-def _side_stream(dev) -> torch.cuda.Stream:
-    key = torch.device(dev).index or 0
+def _side_stream(dev, which: int = 0) -> torch.cuda.Stream:
+    """Persistent auxiliary streams per device: 0 = far field, 1 = P2P,
+    2 = list construction (highest priority: its short kernels take SM slots
+    as P2P blocks retire instead of queueing behind the whole P2P grid)."""
+    key = (torch.device(dev).index or 0, which)
     if key not in _side:
-        _side[key] = torch.cuda.Stream(device=dev)
+        prio = torch.cuda.Stream.priority_range()[1] if which == 2 else 0
+        _side[key] = torch.cuda.Stream(device=dev, priority=prio)
     return _side[key]
+
+
+def _nchunks(tree: Tree) -> int:
+    """Target chunks of one evaluation (FMM_B200_CHUNKS; default 1).
+
+    Chunking bounds the list memory of one pass and lets chunk k + 1's lists
+    run beside chunk k's P2P, but measured on B200 it does not pay: the P2P
+    grid already saturates the SMs, so list blocks displace P2P blocks
+    (C2: 14.20 ms at 1 chunk, 14.32 at 2, 14.86 at 4)."""
+    env = os.environ.get("FMM_B200_CHUNKS")
+    return max(1, int(env)) if env else 1
+
+
+def _chunk_cuts(tree: Tree, k: int) -> list[int]:
+    """Body cut points 0 = c0 < ... < ck = n on leaf boundaries (the start of
+    the leaf holding body i * n / k); duplicates collapse."""
+    if k <= 1:
+        return [0, tree.n]
+    at = torch.tensor([i * tree.n // k for i in range(1, k)], dtype=torch.int64, device=tree.device)
+    inner = tree.d_start[tree.d_body_leaf[at].long()].tolist()
+    cuts = [0]
+    for c in inner:
+        if cuts[-1] < c < tree.n:
+            cuts.append(int(c))
+    return cuts + [tree.n]
+
+
+class ChunkedLists:
+    """The lists of a chunked evaluation, viewed as one (trace, tests)."""
+
+    def __init__(self, parts):
+        self.parts = parts
+        self.n_m2l = sum(x.n_m2l for x in parts)
+        self.n_p2p = sum(x.n_p2p for x in parts)
+        self.peak_frontier = max(x.peak_frontier for x in parts)
+
+    def host_pairs(self, which: str):
+        import numpy as np
+        tt, ss = zip(*(x.host_pairs(which) for x in self.parts))
+        return np.concatenate(tt), np.concatenate(ss)
 
 
 def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
                        trace: bool = False) -> EvalReport:
     """Simultaneous traversal of the tree against itself, on the GPU.
 
-    Two streams: the main stream builds the lists and runs P2P; a side
-    stream runs the far field (upward pass as soon as the tree exists; M2L
-    and the downward pass as soon as the M2L list is sorted) into separate
-    accumulators, which one combine kernel adds at the end.  The far field
-    (~1 ms at C2) thus hides behind list construction and P2P."""
+    Three streams.  The targets may be cut into Morton chunks on leaf
+    boundaries (``_nchunks``, default one chunk); a list stream builds each
+    chunk's lists (traversal, P2P CSR and run plan) and a P2P stream runs
+    the chunk's near field as soon as its plan exists.  M2L pairs are
+    emitted only by the chunk owning their target's first body, so the
+    chunks partition both lists exactly.  A side stream runs the far field:
+    the upward pass as soon as the tree exists, each chunk's M2L as soon as
+    its M2L list is sorted, then the downward pass, into separate
+    accumulators that one combine kernel adds at the end."""
     if source_tree is not None and source_tree is not tree:
         raise NotImplementedError("separate source trees are outside the B200 hot path")
     if cfg.mutual:
@@ -349,55 +399,84 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
+        pst = _side_stream(dev, 1)
         E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-        e0, e_up0, e_up1, e_m2l0, e_m2l1, e_down1, e_l1, e_p0, e_p1, e_end = (E() for _ in range(10))
+        e0, e_up0, e_up1, e_down0, e_down1, e_l1, e_pend, e_end = (E() for _ in range(8))
         need_up = tree._M is None or tree.p != p
         nc = ncoef(p)
-        # every buffer the side stream touches is allocated here, on main
+        # every buffer the other streams touch is allocated here, on main
         M = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev) if need_up else tree._M
         L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
         far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
         e0.record(main)
         side.wait_event(e0)
+        pst.wait_event(e0)
         with torch.cuda.stream(side):
             e_up0.record(side)
             if need_up:
                 upward_pass(tree, p, stats, sync=False, M=M)  # (resets tree._L)
             e_up1.record(side)
         tree._M, tree.p, tree._L = M, p, L
-        m2l_ready = torch.cuda.Event()
-        lists = interaction_lists(tree, cfg.mac, m2l_ready=m2l_ready, side=side)
-        tree.list_cache = lists
-        e_l1.record(main)
-        side.wait_event(m2l_ready)
+        cuts = _chunk_cuts(tree, _nchunks(tree))
+        nch = len(cuts) - 1
+        lst = _side_stream(dev, 2) if nch > 1 else main
+        lst.wait_event(e0)
+        parts, m2l_ev, p2p_ev = [], [], []
+        for k in range(nch):
+            rng = (cuts[k], cuts[k + 1]) if nch > 1 else None
+            ready = torch.cuda.Event()
+            with torch.cuda.stream(lst):
+                lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
+                                          m2l_owner_only=nch > 1)
+            parts.append(lists)
+            with torch.cuda.stream(side):  # M2L rows of this chunk: after upward and its sorted list
+                ea, eb = E(), E()
+                ea.record(side)
+                run_m2l(tree, lists, p)
+                eb.record(side)
+                m2l_ev.append((ea, eb))
+            planned = torch.cuda.Event()
+            planned.record(lst)
+            pst.wait_event(planned)
+            with torch.cuda.stream(pst):
+                ea, eb = E(), E()
+                ea.record(pst)
+                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+                eb.record(pst)
+                p2p_ev.append((ea, eb))
+        e_l1.record(lst)
+        main.wait_event(e_l1)
         with torch.cuda.stream(side):
-            e_m2l0.record(side)
-            run_m2l(tree, lists, p)
-            e_m2l1.record(side)
+            e_down0.record(side)
             downward_pass(tree, stats, sync=False, out=tuple(far))
             e_down1.record(side)
-        e_p0.record(main)
-        flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
-        e_p1.record(main)
+        e_pend.record(pst)
+        main.wait_event(e_pend)
         if cfg.precision == "fp32" and int(flag.item()) != 0:
             # two distinct bodies collided in FP32 outside a self run: redo guarded
-            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
-            e_p1.record(main)
+            for lists in parts:
+                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
         main.wait_event(e_down1)
         P = _lib.ptr
         _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
                   P(tree.d_fz), _lib.stream_handle())
         e_end.record(main)
         e_end.synchronize()
-        pairs, skipped = lists.dev_stats.tolist()
+        pairs = skipped = 0
+        for lists in parts:
+            a, b = lists.dev_stats.tolist()
+            pairs += a
+            skipped += b
+    lists = parts[0] if nch == 1 else ChunkedLists(parts)
+    tree.list_cache = lists
     stats.p2p_pairs += int(pairs)
     stats.p2p_skipped += int(skipped)
     stats.p2p_flops += 20 * int(pairs)
     stats.m2l_calls += lists.n_m2l
     stats.add_time("list", e0.elapsed_time(e_l1) * 1e-3)
-    stats.add_time("m2l", e_m2l0.elapsed_time(e_m2l1) * 1e-3)
-    stats.add_time("p2p", e_p0.elapsed_time(e_p1) * 1e-3)
+    stats.add_time("m2l", sum(a.elapsed_time(b) for a, b in m2l_ev) * 1e-3)
+    stats.add_time("p2p", sum(a.elapsed_time(b) for a, b in p2p_ev) * 1e-3)  # kernel time, all chunks
     tree._results_changed()
     events = None
     if trace:
@@ -406,13 +485,14 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
-    # phases overlap (far field on the side stream): upward and downward are
-    # their own stream's spans, traversal is the main stream's span
+    # phases overlap (far field on the side stream, near field on the P2P
+    # stream): upward and downward are their own stream's spans, traversal
+    # is the span from the start to the last P2P chunk
     return EvalReport(strategy="dualtree", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=False, threads=threads, task_grain=cfg.task_grain, stats=stats,
                       build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
-                      traversal_time=e0.elapsed_time(e_p1) * 1e-3,
-                      downward_time=e_m2l1.elapsed_time(e_down1) * 1e-3, trace=events)
+                      traversal_time=e0.elapsed_time(e_pend) * 1e-3,
+                      downward_time=e_down0.elapsed_time(e_down1) * 1e-3, trace=events)
 
 
 def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
