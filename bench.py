@@ -247,8 +247,6 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pos, q, n, solver = workload(args)
-    if args.strategy != "dualtree" and world > 1:
-        raise SystemExit("multi-GPU runs partition the dual-tree FMM only")
     cfg = fb.EvalConfig(strategy=args.strategy, mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"],
                         precision=args.precision)
     dev = torch.device("cuda", local)

@@ -153,12 +153,15 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import EvalReport, interaction_lists, run_m2l, run_p2p
+    from .traversal import EvalReport, interaction_lists, run_m2l, run_m2p, run_p2p, treecode_lists
     from .tree import downward_pass
 
     if world == 1:
-        from .traversal import evaluate_dual_tree
-        return evaluate_dual_tree(tree, cfg)
+        from .traversal import evaluate_on_tree
+        return evaluate_on_tree(tree, cfg)
+    treecode = cfg.strategy == "treecode"
+    if not treecode and cfg.strategy != "dualtree":
+        raise NotImplementedError(f"strategy {cfg.strategy!r} is outside the B200 hot path")
     plan = getattr(tree, "_dist_plan", None)
     if plan is None or len(plan.cuts) != world + 1:
         plan = _Plan(tree, world)
@@ -182,16 +185,28 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     tree._M, tree.p = M, cfg.p
     tree._L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
     ev[1].record(stream)
-    lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi))
-    ev[2].record(stream)
-    run_m2l(tree, lists, cfg.p)
+    if treecode:
+        # the rank's target leaves walk the whole (replicated) tree
+        lists = treecode_lists(tree, cfg.mac, body_range=(lo, hi))
+        ev[2].record(stream)
+        far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+        run_m2p(tree, lists, cfg.p, tuple(far))
+    else:
+        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi))
+        ev[2].record(stream)
+        run_m2l(tree, lists, cfg.p)
     ev[3].record(stream)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
     if cfg.precision == "fp32" and int(flag.item()) != 0:
         run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
     ev[4].record(stream)
-    downward_pass(tree, None, sync=False, body_range=(lo, hi))
+    if treecode:
+        P = _lib.ptr
+        _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
+                  P(tree.d_fz), _lib.stream_handle())
+    else:
+        downward_pass(tree, None, sync=False, body_range=(lo, hi))
     ev[5].record(stream)
     res = torch.stack([tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz], 1)
     comm.allgather_rows(res, plan.cuts, rank, world)
@@ -202,14 +217,15 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     pairs, skipped = lists.dev_stats.tolist()
     stats.p2p_pairs, stats.p2p_skipped, stats.p2p_flops = int(pairs), int(skipped), 20 * int(pairs)
     stats.m2l_calls = lists.n_m2l
+    stats.m2p_calls = getattr(lists, "n_m2p", 0)
     stats.add_time("list", ev[1].elapsed_time(ev[2]) * 1e-3)
-    stats.add_time("m2l", ev[2].elapsed_time(ev[3]) * 1e-3)
+    stats.add_time("m2p" if treecode else "m2l", ev[2].elapsed_time(ev[3]) * 1e-3)
     stats.add_time("p2p", ev[3].elapsed_time(ev[4]) * 1e-3)
     stats.add_time("allgather", ev[5].elapsed_time(ev[6]) * 1e-3)
     tree._results_changed()
     del _lib
-    return EvalReport(strategy="dualtree", n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
+    return EvalReport(strategy=cfg.strategy, n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=False, threads=world, task_grain=cfg.task_grain, stats=stats,
                       build_time=tree.build_time, upward_time=ev[0].elapsed_time(ev[1]) * 1e-3,
                       traversal_time=ev[1].elapsed_time(ev[4]) * 1e-3,
-                      downward_time=ev[4].elapsed_time(ev[6]) * 1e-3)
+                      downward_time=0.0 if treecode else ev[4].elapsed_time(ev[6]) * 1e-3)

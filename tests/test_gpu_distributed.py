@@ -39,11 +39,12 @@ def _ps(c):
     return fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], c.q)
 
 
-@pytest.mark.parametrize("name,world,precision", [("c2_32k", 2, "fp64"), ("plummer_32k", 4, "fp64"),
-                                                  ("c1", 3, "fp64"), ("c2_32k", 8, "fp32")])
-def test_partitioned_equals_single(name, world, precision):
+@pytest.mark.parametrize("name,world,precision,strategy", [
+    ("c2_32k", 2, "fp64", "dualtree"), ("plummer_32k", 4, "fp64", "dualtree"), ("c1", 3, "fp64", "dualtree"),
+    ("c2_32k", 8, "fp32", "dualtree"), ("c1", 3, "fp64", "treecode"), ("c2_32k", 4, "fp32", "treecode")])
+def test_partitioned_equals_single(name, world, precision, strategy):
     c = Case(name)
-    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", c.theta), p=c.p, precision=precision)
+    cfg = fb.EvalConfig(strategy=strategy, mac=fb.MacConfig("fmm", c.theta), p=c.p, precision=precision)
     ref_tree = fb.build_tree(_ps(c), ncrit=c.ncrit)
     ref = fb.evaluate_on_tree(ref_tree, cfg)
     want = [a.clone() for a in (ref_tree.d_phi, ref_tree.d_fx, ref_tree.d_fy, ref_tree.d_fz)]
@@ -71,6 +72,7 @@ def test_partitioned_equals_single(name, world, precision):
     assert sum(rp.stats.p2p_pairs for rp in reps) == ref.stats.p2p_pairs
     assert sum(rp.stats.p2p_skipped for rp in reps) == ref.stats.p2p_skipped
     assert sum(rp.stats.m2l_calls for rp in reps) >= ref.stats.m2l_calls  # shared top rows repeat
+    assert sum(rp.stats.m2p_calls for rp in reps) == ref.stats.m2p_calls  # leaf targets: never shared
     for r in range(world):
         got = (trees[r].d_phi, trees[r].d_fx, trees[r].d_fy, trees[r].d_fz)
         for g, w in zip(got, want):
