@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--p", type=int, default=0, help="override the expansion order (C4 sweep)")
     ap.add_argument("--theta", type=float, default=0.0, help="override theta (C4 sweep)")
-    ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode"],
+    ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode", "listfmm"],
                     help="evaluation strategy (the headline is the dual-tree FMM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -197,6 +197,22 @@ FMM_API int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t 
                           int32_t *p2p_s, int64_t cap_p2p, unsigned long long *dev_log, void *ws,
                           size_t ws_bytes, void *stream);
 
+/* listfmm lists (replaces _collect_vlist / _collect_ulist,
+ * src/traversal.py:341-497, with their capacity retry, :1061-1118): the
+ * V list (M2L: children of the parent's 3x3x3 neighbourhood not adjacent
+ * to the target) of every cell and the U list (P2P: own-level neighbours,
+ * or their descendant leaves, plus leaf cells adjacent to a coarser
+ * ancestor) of every leaf whose bodies meet [body_lo, body_hi).
+ * level_off is a HOST array of the depth + 2 cell-count offsets per level.
+ * dev_counts[2] = {n_p2p, n_m2l}, counting past capacity (grow and rerun).
+ * ws holds the (level, key) table (~25 B per cell) and a CUB sort. */
+FMM_API int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_off, const int8_t *level,
+                      const uint64_t *key, const int32_t *parent, const int32_t *children, const uint8_t *leaf,
+                      const int32_t *sub_end, const int32_t *start, const int32_t *end,
+                      int32_t body_lo, int32_t body_hi, int32_t *m2l_t,
+                      int32_t *m2l_s, int64_t cap_m2l, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
+                      unsigned long long *dev_counts, void *ws, size_t ws_bytes, void *stream);
+
 /* Sort (t, s) pairs by target then source and build row offsets over all
  * cells: rows[c]..rows[c+1] are the sources of target c (ascending). */
 FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs, int32_t ncells,

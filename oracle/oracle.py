@@ -54,6 +54,8 @@ def _declare(L):
     L.orc_downward.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_collect.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _I, _I, _P, _P, _I, _P, _P, _P]
     L.orc_exec_m2l.argtypes = [_I, _P, _P, _P, _P, _P, C.c_int]
+    L.orc_collect_vlist.argtypes = [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P]
+    L.orc_collect_ulist.argtypes = [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P]
     L.orc_collect_treecode.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _P, _P, _I, _P, _P, _P]
     L.orc_exec_m2p.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int]
     L.orc_exec_p2p.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
@@ -278,6 +280,63 @@ def evaluate_treecode(t: OracleTree, p: int, theta: float):
     phi, fx, fy, fz, st = exec_p2p(t, pt, ps, acc=acc)  # P2P adds onto the M2P sums
     return dict(phi=phi, fx=fx, fy=fy, fz=fz, M=M, m2p=(mt, ms), p2p=(pt, ps),
                 p2p_pairs=int(st[0]), p2p_skipped=int(st[1]), m2p_calls=int(mt.size))
+
+
+def level_tables(t: OracleTree):
+    """_level_tables (src/traversal.py:1052-1058): cells sorted by
+    (level, key), their keys, and level offsets."""
+    order = np.ascontiguousarray(np.lexsort((t.cell_key, t.cell_level)).astype(np.int64))
+    sorted_keys = np.ascontiguousarray(t.cell_key[order].astype(np.uint64))
+    depth = int(t.cell_level.max())
+    counts = np.bincount(t.cell_level, minlength=depth + 1)
+    level_off = np.zeros(depth + 2, np.int64)
+    np.cumsum(counts, out=level_off[1:])
+    return order, sorted_keys, level_off
+
+
+def collect_listfmm(t: OracleTree):
+    """V list (src/traversal.py:341-403) over all cells and U list (:406-497)
+    over all leaves: returns (m2l_t, m2l_s, p2p_t, p2p_s)."""
+    order, skeys, loff = level_tables(t)
+    lvl = np.ascontiguousarray(t.cell_level, np.int64)
+    key = np.ascontiguousarray(t.cell_key, np.uint64)
+    par = np.ascontiguousarray(t.cell_parent, np.int64)
+    leaf_ids = np.ascontiguousarray(np.flatnonzero(t.cell_leaf), np.int64)
+    cap = max(4096, 256 * t.ncells)
+    while True:
+        mt = np.empty(cap, np.int64); ms = np.empty(cap, np.int64)
+        out = np.zeros(3, np.int64)
+        lib().orc_collect_vlist(0, t.ncells, _p(lvl), _p(key), _p(par), _p(t.cell_children), _p(order), _p(skeys),
+                                _p(loff), cap, _p(mt), _p(ms), _p(out))
+        if out[2] == 1:
+            cap = int(out[0]) + 1
+            continue
+        nm = int(out[0])
+        break
+    cap = max(4096, 64 * leaf_ids.size)
+    while True:
+        pt = np.empty(cap, np.int64); ps = np.empty(cap, np.int64)
+        out = np.zeros(3, np.int64)
+        lib().orc_collect_ulist(0, leaf_ids.size, _p(leaf_ids), _p(lvl), _p(key), _p(t.cell_leaf),
+                                _p(np.ascontiguousarray(t.cell_sub_end, np.int64)), _p(order), _p(skeys), _p(loff),
+                                cap, _p(pt), _p(ps), _p(out))
+        if out[2] == 1:
+            cap = int(out[1]) + 1
+            continue
+        npp = int(out[1])
+        break
+    return mt[:nm], ms[:nm], pt[:npp], ps[:npp]
+
+
+def evaluate_listfmm(t: OracleTree, p: int):
+    """evaluate_list_fmm restated sequentially (src/traversal.py:1127-1189)."""
+    M = upward(t, p)
+    mt, ms, pt, ps = collect_listfmm(t)
+    L = exec_m2l(t, mt, ms, M, p)
+    phi, fx, fy, fz, st = exec_p2p(t, pt, ps)
+    downward(t, L.copy(), p, phi, fx, fy, fz)
+    return dict(phi=phi, fx=fx, fy=fy, fz=fz, m2l=(mt, ms), p2p=(pt, ps), p2p_pairs=int(st[0]),
+                p2p_skipped=int(st[1]), m2l_calls=int(mt.size))
 
 
 def direct(x, y, z, q, idx=None, threads=0):

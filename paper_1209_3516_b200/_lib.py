@@ -48,6 +48,7 @@ SIGNATURES = {
     "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P, P, I64, P, P],
     "fmm_treecode_traverse": [P, P, P, P, I64, INT, I32, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P,
                               I64, P, P, SZ, P],
+    "fmm_listfmm_lists": [I32, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, I64, P, P, I64, P, P, SZ, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
     "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P],

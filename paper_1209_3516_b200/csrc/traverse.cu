@@ -221,6 +221,178 @@ __global__ void treecode_step_kernel(const int32_t *__restrict__ fa, const int32
     }
 }
 
+// ---- listfmm (src/traversal.py:314-497) ---------------
+// Level-wise lists on the cubic tree, theta-free.  V list: for every cell
+// c, the children of the parent's 3x3x3 neighbourhood that are not adjacent
+// to c (M2L).  U list: for every leaf t, its own-level neighbourhood (a leaf
+// neighbour itself, an internal one all its descendant leaves, swept over
+// the contiguous pre-order subtree) plus the leaf cells of every coarser
+// ancestor's neighbourhood (P2P).  Same-level neighbours are found by binary
+// search in the (level, key) table: the pre-order ids stably sorted by level
+// list each level in pre-order, which is key order.
+// Every thread walks its target twice: count, one warp-aggregated reserve,
+// then write -- the emitted SETS are the reference's.
+__device__ __forceinline__ int64_t level_lookup(const uint64_t *__restrict__ skeys, int64_t lo, int64_t hi,
+                                                uint64_t key) {
+    const int64_t hi0 = hi;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (skeys[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < hi0 && skeys[lo] == key) ? lo : -1;
+}
+
+__device__ __forceinline__ uint64_t interleave3(int64_t ix, int64_t iy, int64_t iz) {
+    return spread21((uint64_t)ix) | (spread21((uint64_t)iy) << 1) | (spread21((uint64_t)iz) << 2);
+}
+
+struct LevelTable {
+    const int32_t *cells;  // cells_by_level
+    const uint64_t *keys;  // key[cells_by_level]
+    const int64_t *off;    // level offsets (depth + 2)
+};
+
+__global__ void fill_iota(int32_t *a, int32_t n) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+__global__ void gather_keys(int32_t n, const int32_t *__restrict__ cells, const uint64_t *__restrict__ key,
+                            uint64_t *out) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = key[cells[i]];
+}
+
+// V list of cell c: calls f(ch) for every well-separated child of the
+// parent's neighbourhood, in the reference's (z, y, x, octant) order.
+template <class F>
+__device__ __forceinline__ void vlist_walk(int32_t c, const int8_t *__restrict__ level,
+                                           const uint64_t *__restrict__ key, const int32_t *__restrict__ parent,
+                                           const int32_t *__restrict__ children, const LevelTable &tab, F &&f) {
+    const int lvl = level[c];
+    if (lvl == 0) return;
+    const uint64_t k = key[c];
+    const int64_t ix = (int64_t)compact21(k), iy = (int64_t)compact21(k >> 1), iz = (int64_t)compact21(k >> 2);
+    const uint64_t pk = key[parent[c]];
+    const int64_t px = (int64_t)compact21(pk), py = (int64_t)compact21(pk >> 1), pz = (int64_t)compact21(pk >> 2);
+    const int plvl = lvl - 1;
+    const int64_t ng = (int64_t)1 << plvl;
+    for (int dz = -1; dz <= 1; dz++) {
+        const int64_t jz = pz + dz;
+        if (jz < 0 || jz >= ng) continue;
+        for (int dy = -1; dy <= 1; dy++) {
+            const int64_t jy = py + dy;
+            if (jy < 0 || jy >= ng) continue;
+            for (int dx = -1; dx <= 1; dx++) {
+                const int64_t jx = px + dx;
+                if (jx < 0 || jx >= ng) continue;
+                const int64_t pos = level_lookup(tab.keys, tab.off[plvl], tab.off[plvl + 1], interleave3(jx, jy, jz));
+                if (pos < 0) continue;
+                const int32_t nc = tab.cells[pos];
+                for (int o = 0; o < 8; o++) {
+                    const int32_t ch = children[nc * 8 + o];
+                    if (ch < 0) continue;
+                    const uint64_t ck = key[ch];
+                    const int64_t ddx = (int64_t)compact21(ck) - ix, ddy = (int64_t)compact21(ck >> 1) - iy,
+                                  ddz = (int64_t)compact21(ck >> 2) - iz;
+                    if (ddx >= -1 && ddx <= 1 && ddy >= -1 && ddy <= 1 && ddz >= -1 && ddz <= 1) continue;
+                    f(ch);
+                }
+            }
+        }
+    }
+}
+
+// U list of leaf t: calls f(s) for every near-field source leaf.
+template <class F>
+__device__ __forceinline__ void ulist_walk(int32_t t, const int8_t *__restrict__ level,
+                                           const uint64_t *__restrict__ key, const uint8_t *__restrict__ leaf,
+                                           const int32_t *__restrict__ sub_end, const LevelTable &tab, F &&f) {
+    const int lvl = level[t];
+    const uint64_t k = key[t];
+    const int64_t ix = (int64_t)compact21(k), iy = (int64_t)compact21(k >> 1), iz = (int64_t)compact21(k >> 2);
+    const int64_t ng = (int64_t)1 << lvl;
+    for (int dz = -1; dz <= 1; dz++) {
+        const int64_t jz = iz + dz;
+        if (jz < 0 || jz >= ng) continue;
+        for (int dy = -1; dy <= 1; dy++) {
+            const int64_t jy = iy + dy;
+            if (jy < 0 || jy >= ng) continue;
+            for (int dx = -1; dx <= 1; dx++) {
+                const int64_t jx = ix + dx;
+                if (jx < 0 || jx >= ng) continue;
+                const int64_t pos = level_lookup(tab.keys, tab.off[lvl], tab.off[lvl + 1], interleave3(jx, jy, jz));
+                if (pos < 0) continue;
+                const int32_t c = tab.cells[pos];
+                if (leaf[c]) f(c);
+                else
+                    for (int32_t d = c; d < sub_end[c]; d++)
+                        if (leaf[d]) f(d);
+            }
+        }
+    }
+    uint64_t ak = k;
+    for (int lv = lvl - 1; lv > 0; lv--) {
+        ak >>= 3;
+        const int64_t ax = (int64_t)compact21(ak), ay = (int64_t)compact21(ak >> 1), az = (int64_t)compact21(ak >> 2);
+        const int64_t ngl = (int64_t)1 << lv;
+        for (int dz = -1; dz <= 1; dz++) {
+            const int64_t jz = az + dz;
+            if (jz < 0 || jz >= ngl) continue;
+            for (int dy = -1; dy <= 1; dy++) {
+                const int64_t jy = ay + dy;
+                if (jy < 0 || jy >= ngl) continue;
+                for (int dx = -1; dx <= 1; dx++) {
+                    if (dx == 0 && dy == 0 && dz == 0) continue;  // the ancestor itself
+                    const int64_t jx = ax + dx;
+                    if (jx < 0 || jx >= ngl) continue;
+                    const int64_t pos =
+                        level_lookup(tab.keys, tab.off[lv], tab.off[lv + 1], interleave3(jx, jy, jz));
+                    if (pos < 0) continue;
+                    const int32_t c = tab.cells[pos];
+                    if (leaf[c]) f(c);
+                }
+            }
+        }
+    }
+}
+
+__global__ void listfmm_kernel(int32_t ncells, const int8_t *__restrict__ level, const uint64_t *__restrict__ key,
+                               const int32_t *__restrict__ parent, const int32_t *__restrict__ children,
+                               const uint8_t *__restrict__ leaf, const int32_t *__restrict__ sub_end,
+                               const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend, int32_t blo,
+                               int32_t bhi, LevelTable tab, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
+                               int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, unsigned long long *cnt_p2p,
+                               unsigned long long *cnt_m2l) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nround = (ncells + stride - 1) / stride;
+    for (int64_t r = 0; r < nround; r++) {
+        const int64_t k = r * stride + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const bool mine = k < ncells && cend[k] > blo && cstart[k] < bhi;
+        const int32_t c = (int32_t)k;
+        int nv = 0, nu = 0;
+        if (mine) {
+            vlist_walk(c, level, key, parent, children, tab, [&](int32_t) { nv++; });
+            if (leaf[c]) ulist_walk(c, level, key, leaf, sub_end, tab, [&](int32_t) { nu++; });
+        }
+        int ov, ou;
+        unsigned long long iv = warp_reserve(cnt_m2l, nv, lane, &ov) + ov;
+        unsigned long long iu = warp_reserve(cnt_p2p, nu, lane, &ou) + ou;
+        if (mine) {
+            vlist_walk(c, level, key, parent, children, tab, [&](int32_t s) {
+                if (iv < (unsigned long long)cap_m2l) { m2l_t[iv] = c; m2l_s[iv] = s; }
+                iv++;
+            });
+            if (leaf[c])
+                ulist_walk(c, level, key, leaf, sub_end, tab, [&](int32_t s) {
+                    if (iu < (unsigned long long)cap_p2p) { p2p_t[iu] = c; p2p_s[iu] = s; }
+                    iu++;
+                });
+        }
+    }
+}
+
 __global__ void pack_pairs(const int32_t *t, const int32_t *s, int64_t n, int sbits, uint64_t *keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -355,6 +527,40 @@ int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a
             even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_treecode_traverse");
+    return FMM_OK;
+}
+
+int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_off, const int8_t *level,
+                      const uint64_t *key, const int32_t *parent, const int32_t *children, const uint8_t *leaf,
+                      const int32_t *sub_end, const int32_t *start, const int32_t *end,
+                      int32_t body_lo, int32_t body_hi, int32_t *m2l_t,
+                      int32_t *m2l_s, int64_t cap_m2l, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
+                      unsigned long long *dev_counts, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (depth < 0 || depth > MAX_LEVEL) { set_error("bad depth %d", depth); return FMM_ERR_INVALID; }
+    Arena ar(ws, ws_bytes);
+    uint64_t *skeys = ar.take<uint64_t>((size_t)ncells);
+    int64_t *doff = ar.take<int64_t>((size_t)depth + 2);
+    int32_t *iota = ar.take<int32_t>((size_t)ncells);
+    int32_t *bylevel = ar.take<int32_t>((size_t)ncells);
+    uint8_t *lv_sorted = ar.take<uint8_t>((size_t)ncells);
+    if (!skeys || !doff || !iota || !bylevel || !lv_sorted) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    cudaMemcpyAsync(doff, level_off, sizeof(int64_t) * ((size_t)depth + 2), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(dev_counts, 0, 2 * sizeof(unsigned long long), st);
+    // (level, key) table: a stable sort of the pre-order ids by level keeps
+    // pre-order, i.e. key order, within each level
+    fill_iota<<<grid_for(ncells, 256), 256, 0, st>>>(iota, ncells); fmm::note_launch();
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, (const uint8_t *)level, lv_sorted, iota, bylevel, ncells, 0, 8, st);
+    if (need > ar.left()) { set_error("sort workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceRadixSort::SortPairs(ar.rest(), need, (const uint8_t *)level, lv_sorted, iota, bylevel, ncells, 0, 8,
+                                    st);
+    gather_keys<<<grid_for(ncells, 256), 256, 0, st>>>(ncells, bylevel, key, skeys); fmm::note_launch();
+    LevelTable tab{bylevel, skeys, doff};
+    listfmm_kernel<<<grid_for(ncells, 128, 148 * 16), 128, 0, st>>>(
+        ncells, level, key, parent, children, leaf, sub_end, start, end, body_lo, body_hi, tab, m2l_t, m2l_s,
+        cap_m2l, p2p_t, p2p_s, cap_p2p, dev_counts, dev_counts + 1); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_listfmm_lists");
     return FMM_OK;
 }
 

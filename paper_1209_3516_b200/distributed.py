@@ -153,15 +153,16 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import EvalReport, interaction_lists, run_m2l, run_m2p, run_p2p, treecode_lists
+    from .traversal import (EvalReport, interaction_lists, listfmm_lists, run_m2l, run_m2p, run_p2p,
+                            treecode_lists)
     from .tree import downward_pass
 
     if world == 1:
         from .traversal import evaluate_on_tree
         return evaluate_on_tree(tree, cfg)
     treecode = cfg.strategy == "treecode"
-    if not treecode and cfg.strategy != "dualtree":
-        raise NotImplementedError(f"strategy {cfg.strategy!r} is outside the B200 hot path")
+    if cfg.mutual and cfg.strategy == "dualtree":
+        raise NotImplementedError("mutual traversal is outside the B200 hot path")
     plan = getattr(tree, "_dist_plan", None)
     if plan is None or len(plan.cuts) != world + 1:
         plan = _Plan(tree, world)
@@ -192,7 +193,10 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
         run_m2p(tree, lists, cfg.p, tuple(far))
     else:
-        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi))
+        if cfg.strategy == "listfmm":
+            lists = listfmm_lists(tree, body_range=(lo, hi))
+        else:
+            lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi))
         ev[2].record(stream)
         run_m2l(tree, lists, cfg.p)
     ev[3].record(stream)

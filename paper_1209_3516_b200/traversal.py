@@ -21,10 +21,13 @@ the tree (csrc/traverse.cu, bit-exact sets with ``_collect_treecode``),
 evaluates accepted cells' multipoles at the bodies (M2P, csrc/m2p.cu) and
 reuses the P2P plan and kernel for the near field.
 
-Scope: ``strategy="dualtree"`` (directed, ``mutual=False``) and
-``"treecode"``, one shared tree.  ``listfmm``, ``mutual=True`` and
-``source_tree`` are outside the B200 hot path and raise
-NotImplementedError.
+``evaluate_list_fmm`` builds the level-wise V/U lists
+(csrc/traverse.cu, bit-exact sets with ``_collect_vlist``/``_collect_ulist``)
+and reuses the M2L, P2P and downward executors.
+
+Scope: all three strategies (``dualtree`` directed, ``treecode``,
+``listfmm``) on one shared tree.  ``mutual=True`` and ``source_tree`` are
+outside the B200 hot path and raise NotImplementedError.
 ``precision`` is a new knob: "fp64" (default, the reference's arithmetic)
 or "fp32" (FP32 near field; far field stays float64).
 """
@@ -47,8 +50,8 @@ STRATEGIES = ("treecode", "listfmm", "dualtree")
 PRECISIONS = ("fp64", "fp32")
 REPORT_SCHEMA = "fmmkit-report-v1"
 
-__all__ = ["STRATEGIES", "PRECISIONS", "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_treecode",
-           "evaluate_on_tree", "interaction_lists", "treecode_lists"]
+__all__ = ["STRATEGIES", "PRECISIONS", "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_list_fmm",
+           "evaluate_treecode", "evaluate_on_tree", "interaction_lists", "listfmm_lists", "treecode_lists"]
 
 
 @dataclass
@@ -312,6 +315,44 @@ def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | Non
                  **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
+def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
+                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None) -> Lists:
+    """Level-wise V (M2L) and U (P2P) lists of the cubic tree
+    (src/traversal.py:341-497; bit-exact sets with the reference's
+    ``_collect_vlist`` / ``_collect_ulist``) -> target-sorted CSR + P2P plan.
+    ``body_range`` keeps the targets whose bodies meet [lo, hi)."""
+    blo, bhi = body_range if body_range is not None else (0, tree.n)
+    dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
+    ncells = tree.ncells
+    key = ("listfmm", ncells, tree.nleaves, blo, bhi)
+    cap_p2p, cap_m2l = _hint.get(key, (max(4096, tree.nleaves * 48), max(4096, ncells * 200)))
+    off = (C.c_int64 * len(tree.level_off))(*tree.level_off)
+    cnt = torch.empty(2, dtype=torch.int64, device=dev)
+    wsp, wsb = _lib.workspace(max(ncells, tree.n), dev, stream=torch.cuda.current_stream())
+    while True:
+        m2l_t = torch.empty(cap_m2l, dtype=i32, device=dev)
+        m2l_s = torch.empty(cap_m2l, dtype=i32, device=dev)
+        p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
+        p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
+        _lib.call("fmm_listfmm_lists", ncells, tree.depth, off, P(tree.d_level), P(tree.d_key), P(tree.d_parent),
+                  P(tree.d_children), P(tree.d_leaf), P(tree.d_sub_end), P(tree.d_start), P(tree.d_end),
+                  blo, bhi, P(m2l_t), P(m2l_s), cap_m2l, P(p2p_t), P(p2p_s), cap_p2p,
+                  P(cnt), wsp, wsb, st)
+        done_p2p, done_m2l = cnt.tolist()  # the one synchronisation
+        if done_p2p <= cap_p2p and done_m2l <= cap_m2l:
+            break
+        cap_p2p = max(cap_p2p, int(done_p2p * 1.05) + 4096)
+        cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
+    _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096)
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
+    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    del p2p_t, p2p_s, m2l_t, m2l_s
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+                 p2p_rows=p2p_rows, peak_frontier=0,
+                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+
+
 def run_m2p(tree: Tree, lists: Lists, p: int, out) -> None:
     """Treecode far field into ``out`` = (phi, fx, fy, fz) (accumulated)."""
     P = _lib.ptr
@@ -572,11 +613,91 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
                       traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=0.0, trace=events)
 
 
+def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
+                      trace: bool = False) -> EvalReport:
+    """Level-wise interaction lists, adjacency-based; theta plays no role
+    (src/traversal.py:1121-1189), on the GPU.
+
+    Same two-stream layout as ``evaluate_dual_tree``: the main stream builds
+    the V/U lists and runs P2P over the U list; the side stream runs the
+    upward pass, M2L over the V list and the downward pass into separate
+    accumulators that one combine kernel adds at the end."""
+    if source_tree is not None and source_tree is not tree:
+        raise ValueError("listfmm evaluates one tree onto itself")
+    if tree.shape != "cubic":
+        raise ValueError("listfmm requires cubic cells; rebuild the tree with shape='cubic'")
+    if threads < 1:
+        raise ValueError(f"threads must be >= 1, got {threads}")
+    stats = KernelStats()
+    dev = tree.device
+    p = cfg.p
+    with torch.cuda.device(dev):
+        main = torch.cuda.current_stream(dev)
+        side = _side_stream(dev)
+        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        e0, e_up0, e_up1, e_m0, e_m1, e_d1, e_l1, e_p0, e_p1, e_end = (E() for _ in range(10))
+        need_up = tree._M is None or tree.p != p
+        nc = ncoef(p)
+        M = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev) if need_up else tree._M
+        L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
+        far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+        e0.record(main)
+        side.wait_event(e0)
+        with torch.cuda.stream(side):
+            e_up0.record(side)
+            if need_up:
+                upward_pass(tree, p, stats, sync=False, M=M)  # (resets tree._L)
+            e_up1.record(side)
+        tree._M, tree.p, tree._L = M, p, L
+        m2l_ready = torch.cuda.Event()
+        lists = listfmm_lists(tree, m2l_ready=m2l_ready, side=side)
+        tree.list_cache = lists
+        e_l1.record(main)
+        side.wait_event(m2l_ready)
+        with torch.cuda.stream(side):
+            e_m0.record(side)
+            run_m2l(tree, lists, p)
+            e_m1.record(side)
+            downward_pass(tree, stats, sync=False, out=tuple(far))
+            e_d1.record(side)
+        e_p0.record(main)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+        e_p1.record(main)
+        if cfg.precision == "fp32" and int(flag.item()) != 0:
+            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+            e_p1.record(main)
+        main.wait_event(e_d1)
+        P = _lib.ptr
+        _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
+                  P(tree.d_fz), _lib.stream_handle())
+        e_end.record(main)
+        e_end.synchronize()
+        pairs, skipped = lists.dev_stats.tolist()
+    stats.p2p_pairs += int(pairs)
+    stats.p2p_skipped += int(skipped)
+    stats.p2p_flops += 20 * int(pairs)
+    stats.m2l_calls += lists.n_m2l
+    stats.add_time("list", e0.elapsed_time(e_l1) * 1e-3)
+    stats.add_time("m2l", e_m0.elapsed_time(e_m1) * 1e-3)
+    stats.add_time("p2p", e_p0.elapsed_time(e_p1) * 1e-3)
+    tree._results_changed()
+    events = None
+    if trace:
+        events = []
+        mt, ms = lists.host_pairs("m2l")
+        events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
+        pt, ps = lists.host_pairs("p2p")
+        events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
+    return EvalReport(strategy="listfmm", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
+                      theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain,
+                      stats=stats, build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
+                      traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=e_m1.elapsed_time(e_d1) * 1e-3,
+                      trace=events)
+
+
 def evaluate_on_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
                      trace: bool = False) -> EvalReport:
     """Run ``cfg.strategy`` on the tree; results land in ``tree.bodies``."""
-    if cfg.strategy == "treecode":
-        return evaluate_treecode(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)
-    if cfg.strategy != "dualtree":
-        raise NotImplementedError(f"strategy {cfg.strategy!r} is outside the B200 hot path")
-    return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)
+    fn = {"treecode": evaluate_treecode, "listfmm": evaluate_list_fmm, "dualtree": evaluate_dual_tree}
+    return fn[cfg.strategy](tree, cfg, source_tree=source_tree, threads=threads, trace=trace)

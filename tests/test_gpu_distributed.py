@@ -41,7 +41,8 @@ def _ps(c):
 
 @pytest.mark.parametrize("name,world,precision,strategy", [
     ("c2_32k", 2, "fp64", "dualtree"), ("plummer_32k", 4, "fp64", "dualtree"), ("c1", 3, "fp64", "dualtree"),
-    ("c2_32k", 8, "fp32", "dualtree"), ("c1", 3, "fp64", "treecode"), ("c2_32k", 4, "fp32", "treecode")])
+    ("c2_32k", 8, "fp32", "dualtree"), ("c1", 3, "fp64", "treecode"), ("c2_32k", 4, "fp32", "treecode"),
+    ("c1", 2, "fp64", "listfmm"), ("plummer_32k", 4, "fp64", "listfmm")])
 def test_partitioned_equals_single(name, world, precision, strategy):
     c = Case(name)
     cfg = fb.EvalConfig(strategy=strategy, mac=fb.MacConfig("fmm", c.theta), p=c.p, precision=precision)

@@ -135,11 +135,12 @@ def test_workload_generators_are_seeded():
 
 
 def test_out_of_scope_paths_raise():
-    cfg = fb.EvalConfig(strategy="listfmm")
     with pytest.raises(NotImplementedError):
-        fb.evaluate_on_tree(object(), cfg)
+        fb.evaluate_on_tree(object(), fb.EvalConfig(mutual=True))
     with pytest.raises(NotImplementedError):
         fb.evaluate_treecode(object(), fb.EvalConfig(strategy="treecode"), source_tree=object())
+    with pytest.raises(ValueError, match="one tree onto itself"):  # the reference's error
+        fb.evaluate_list_fmm(object(), fb.EvalConfig(strategy="listfmm"), source_tree=object())
 
 
 def _static_len(node, env):
