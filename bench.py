@@ -186,11 +186,13 @@ def run_reference(args):
         return
     pos, q, n, solver = workload(args)
     vals = []
+    # bounded: the whole --steps K --warmup W run stays around three minutes
+    per_step = max(2.0, min(args.cpu_seconds, 180.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_run(pos, q, solver, min(args.cpu_seconds, 5.0))
+        cpu_run(pos, q, solver, per_step)
     details = None
     for _ in range(args.steps):
-        v, details = cpu_run(pos, q, solver, args.cpu_seconds)
+        v, details = cpu_run(pos, q, solver, per_step)
         vals.append(v)
     value = float(np.median(vals))
     line = {
