@@ -117,8 +117,8 @@ FMM_API int fmm_carve_emit(const uint64_t *keys, int64_t n, const int32_t *cbase
 /* Cubic/geometric cell geometry, bit-exact (src/tree.py:80-160). */
 FMM_API int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, const int32_t *start,
                       const int32_t *end, const double *xs, const double *ys, const double *zs,
-                      const double *root, double *lo, double *hi, double *ctr, double *bmax,
-                      double *rmax, void *ws, size_t ws_bytes, void *stream);
+                      const double *qs, int rect, int com, const double *root, double *lo, double *hi,
+                      double *ctr, double *bmax, double *rmax, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- vertical passes (src/tree.py:163-189, src/_taylor.py:102-269) ------ */
 

@@ -49,7 +49,8 @@ def _declare(L):
     L.orc_argsort_stable.argtypes = [_I, _P, _P]
     L.orc_build_cells.argtypes = [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]
     L.orc_build_cells.restype = _I
-    L.orc_fill_geometry.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P, _P, _P]
+    L.orc_fill_geometry.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D, _D, C.c_int, C.c_int, _P, _P, _P,
+                                    _P, _P]
     L.orc_upward.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_downward.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_collect.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _I, _I, _P, _P, _I, _P, _P, _P]
@@ -112,7 +113,11 @@ class OracleTree:
     """SoA tree with the reference's ``Tree`` field names (tree.py:275-302)."""
 
 
-def build_tree(pos, q, ncrit=30, allow_oversized_leaves=False) -> OracleTree:
+def build_tree(pos, q, ncrit=30, allow_oversized_leaves=False, shape="cubic",
+               center_mode="geometric") -> OracleTree:
+    """src/tree.py:370-454 (shape "cubic"/"rect", center_mode "geometric"/"com")."""
+    if shape not in ("cubic", "rect") or center_mode not in ("geometric", "com"):
+        raise ValueError("bad shape or center mode")
     pos = np.asarray(pos)
     x, y, z = f64(pos[:, 0]), f64(pos[:, 1]), f64(pos[:, 2])
     q = f64(q)
@@ -165,9 +170,10 @@ def build_tree(pos, q, ncrit=30, allow_oversized_leaves=False) -> OracleTree:
     t.cell_bmax = np.empty(nc)
     t.cell_rmax = np.empty(nc)
     lib().orc_fill_geometry(nc, _p(t.cell_level), _p(t.cell_key), _p(t.cell_start), _p(t.cell_end),
-                            _p(t.x), _p(t.y), _p(t.z), float(lo[0]), float(lo[1]), float(lo[2]), size,
-                            _p(t.cell_lo), _p(t.cell_hi), _p(t.cell_center), _p(t.cell_bmax),
-                            _p(t.cell_rmax))
+                            _p(t.x), _p(t.y), _p(t.z), _p(t.q), float(lo[0]), float(lo[1]), float(lo[2]), size,
+                            int(shape == "rect"), int(center_mode == "com"), _p(t.cell_lo), _p(t.cell_hi),
+                            _p(t.cell_center), _p(t.cell_bmax), _p(t.cell_rmax))
+    t.shape, t.center_mode = shape, center_mode
     return t
 
 

@@ -343,6 +343,61 @@ __global__ void geometry_cells(int32_t ncells, const int8_t *__restrict__ level,
     }
 }
 
+// rect and/or center-of-mass cells (src/tree.py:101-141): the tight box of
+// the cell's bodies and the charge-weighted center, in the reference's
+// sequential body order (bit-exact sums; one thread per cell -- a
+// non-default mode, bounded by the root's N-body chain), then rmax again.
+__global__ void geometry_rect_com(int32_t ncells, const int32_t *__restrict__ start,
+                                  const int32_t *__restrict__ end, const double *__restrict__ xs,
+                                  const double *__restrict__ ys, const double *__restrict__ zs,
+                                  const double *__restrict__ qs, int rect, int com, double *lo, double *hi,
+                                  double *ctr, double *rmax) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+        const int32_t s = start[c], e = end[c];
+        if (rect) {
+            double x0 = xs[s], x1 = xs[s], y0 = ys[s], y1 = ys[s], z0 = zs[s], z1 = zs[s];
+            for (int32_t j = s + 1; j < e; j++) {
+                const double x = xs[j], y = ys[j], z = zs[j];
+                if (x < x0) x0 = x;
+                if (x > x1) x1 = x;
+                if (y < y0) y0 = y;
+                if (y > y1) y1 = y;
+                if (z < z0) z0 = z;
+                if (z > z1) z1 = z;
+            }
+            lo[c * 3] = x0; lo[c * 3 + 1] = y0; lo[c * 3 + 2] = z0;
+            hi[c * 3] = x1; hi[c * 3 + 1] = y1; hi[c * 3 + 2] = z1;
+        }
+        double m[3];
+        bool mid = true;
+        if (com) {
+            double q = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+            for (int32_t j = s; j < e; j++) {
+                const double qj = qs[j];
+                q += qj;
+                cx += qj * xs[j];
+                cy += qj * ys[j];
+                cz += qj * zs[j];
+            }
+            if (q != 0.0) {
+                m[0] = cx / q;
+                m[1] = cy / q;
+                m[2] = cz / q;
+                mid = false;
+            }
+        }
+        double a[3];
+        for (int d = 0; d < 3; d++) {
+            const double l = lo[c * 3 + d], h = hi[c * 3 + d];
+            if (mid) m[d] = 0.5 * (l + h);
+            ctr[c * 3 + d] = m[d];
+            const double u = fabs(l - m[d]), v = fabs(h - m[d]);
+            a[d] = (v > u) ? v : u;
+        }
+        rmax[c] = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    }
+}
+
 __device__ inline int upper_bound_i32(const int32_t *a, int n, int32_t v) {
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -551,8 +606,8 @@ int fmm_carve_emit(const uint64_t *keys, int64_t n, const int32_t *cbase, const 
 
 int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, const int32_t *start,
                       const int32_t *end, const double *xs, const double *ys, const double *zs,
-                      const double *root, double *lo, double *hi, double *ctr, double *bmax,
-                      double *rmax, void *ws, size_t ws_bytes, void *stream) {
+                      const double *qs, int rect, int com, const double *root, double *lo, double *hi,
+                      double *ctr, double *bmax, double *rmax, void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t s = as_stream(stream);
     Arena ar(ws, ws_bytes);
     unsigned long long *b2 = ar.take<unsigned long long>(ncells);
@@ -561,6 +616,11 @@ int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, 
     if (!b2 || !nchunk || !choff) { set_error("workspace too small"); return FMM_ERR_INVALID; }
     int g = grid_for(ncells, 256);
     geometry_cells<<<g, 256, 0, s>>>(ncells, level, key, start, end, root, lo, hi, ctr, rmax, b2, nchunk); fmm::note_launch();
+    if (rect || com) {
+        if (com && !qs) { set_error("center_mode com needs the charges"); return FMM_ERR_INVALID; }
+        geometry_rect_com<<<grid_for(ncells, 64), 64, 0, s>>>(ncells, start, end, xs, ys, zs, qs, rect, com, lo, hi,
+                                                             ctr, rmax); fmm::note_launch();
+    }
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, nchunk, choff, ncells, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }

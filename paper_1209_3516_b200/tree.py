@@ -17,7 +17,8 @@ uint64 keys, float64 geometry, bool leaf flags).
 
 Build (csrc/tree_build.cu): ingest + bounds -> depth-21 Morton keys ->
 stable radix sort -> permute -> single-pass carve (cells numbered in
-pre-order by one scan) -> geometry.  Bit-exact with src/tree.py:370-454 (keys,
+pre-order by one scan) -> geometry (cubic or rect boxes, geometric or
+charge-weighted centers).  Bit-exact with src/tree.py:370-454 (keys,
 permutation and every cell array; tests/test_gpu_parity.py).
 """
 
@@ -263,9 +264,9 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
                allow_oversized_leaves: bool = False, *, device=None) -> Tree:
     """Build the adaptive octree for ``ps`` on the GPU (src/tree.py:370-454).
 
-    Same validation and errors as the reference; ``shape="rect"`` and
-    ``center_mode="com"`` are outside the B200 hot path and raise
-    NotImplementedError.
+    Same validation and errors as the reference, all four geometry modes
+    (``shape`` "cubic"/"rect", ``center_mode`` "geometric"/"com",
+    src/tree.py:80-160) bit-exact.
     """
     t0 = time.perf_counter()
     if shape not in SHAPES:
@@ -276,8 +277,6 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         raise ValueError(f"ncrit must be >= 1, got {ncrit}")
     if ps.n == 0:
         raise ValueError("empty particle set")
-    if shape != "cubic" or center_mode != "geometric":
-        raise NotImplementedError("the B200 path builds cubic trees with geometric centers only")
     _lib.require_cuda()
     if device is None:
         dev = ps.x.device if ps.on_device else torch.device("cuda", torch.cuda.current_device())
@@ -348,7 +347,8 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         bmax = torch.empty(ncells, dtype=f64, device=dev)
         rmax = torch.empty_like(bmax)
         _lib.call("fmm_cell_geometry", ncells, P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
-                  P(xs), P(ys), P(zs), P(root), P(lo), P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
+                  P(xs), P(ys), P(zs), P(qs), int(shape == "rect"), int(center_mode == "com"), P(root), P(lo),
+                  P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
         zeros = [torch.zeros(n, dtype=f64, device=dev) for _ in range(4)]
         fp32_exact = int(inexact.item()) == 0  # synchronises the stream
     tree = Tree(
