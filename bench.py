@@ -335,6 +335,15 @@ def run_ours(args):
                        "(phi, f back in input order as float64); wall clock per step, median"}
         del res
 
+    # accuracy of the last timed step: relative L2 error against direct
+    # summation on the reference's 1000-body sample (tree order, seed 0)
+    acc = None
+    if rank == 0:
+        from paper_1209_3516_b200.tuner import potential_sample, sampled_force_error, sampled_potential_error
+        idx, fref, pref = potential_sample(tree, 1000, 0)
+        acc = {"force_err": sampled_force_error(tree, idx, fref), "pot_err": sampled_potential_error(tree, idx, pref),
+               "sample": int(idx.size), "reference": "direct O(N*S) sums on the GPU, FP64 (src/tuner.py:30-55)"}
+
     peak, peaks = fp32_peak(torch, _lib.call, sh)
     p2p_s = float(np.median(p2p_times))
     achieved = 20.0 * rep.stats.p2p_pairs / p2p_s / 1e12
@@ -369,7 +378,7 @@ def run_ours(args):
                      "peak_source": "FFMA/FFMA2 probe measured live in this run (%s); MEASURED_PEAKS.json has "
                                     "no FP32 figure" % ", ".join(f"{k} {v:.1f}" for k, v in peaks.items()),
                      "kernel": "p2p_f32_kernel", "flop_model": "20 flops/pair (src/_taylor.py:314)"},
-        "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+        "accuracy": acc, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
     }

@@ -228,12 +228,14 @@ FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs,
  * >= the number of P2P pairs, an upper bound on runs); the row count is
  * written to dev_nrows for fmm_p2p.
  * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
- * into dev_stats[2] (src/_taylor.py:366-407 accounting). */
+ * into dev_stats[2] (src/_taylor.py:366-407 accounting).  keys (the sorted
+ * body keys, optional) let leaves without two equal keys skip the
+ * coincident-pair scan (coincident bodies share a key); NULL scans all. */
 FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
                  int32_t body_lo, int32_t body_hi,
                  const int64_t *rows, const int32_t *src_sorted, const double *xs, const double *ys,
-                 const double *zs, int32_t *leaf_rows, int64_t *run_off, void *runs, int64_t cap_runs,
-                 int64_t *host_nruns, int32_t *host_nleaf_rows, int32_t *dev_nrows,
+                 const double *zs, const uint64_t *keys, int32_t *leaf_rows, int64_t *run_off, void *runs,
+                 int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows, int32_t *dev_nrows,
                  unsigned long long *dev_stats, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- executors (src/traversal.py:500-548) ------------------------------ */

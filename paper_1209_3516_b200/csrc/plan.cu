@@ -25,10 +25,18 @@ __device__ inline bool run_start(const int32_t *src, int64_t k, int64_t k0, int3
     return s == t || sp == t || start[s] != end[sp];
 }
 
+// Runs per row (nr) and the reference's pair counters in one pass over the
+// row's sources: pairs = sum |t| |s| - self |t| - coincident, where the
+// coincident ordered pairs (r2 == 0.0 in float64) can only occur inside the
+// target leaf itself, and only between bodies with equal depth-21 keys --
+// with the sorted keys given, leaves without two equal adjacent keys skip
+// the O(|t|^2) scan.
 __global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells, const int32_t *__restrict__ leaf_rows,
                            const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
                            const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-                           int64_t *nr) {
+                           const double *__restrict__ xs, const double *__restrict__ ys,
+                           const double *__restrict__ zs, const uint64_t *__restrict__ keys, int64_t *nr,
+                           unsigned long long *stats) {
     const int lane = threadIdx.x & 31;
     const int32_t nrows = *nrows_dev;
     // rows past the device count get 0 so one scan over ncells + 1 works
@@ -40,13 +48,51 @@ __global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells
         }
         const int32_t t = leaf_rows[r];
         const int64_t k0 = rows[t], k1 = rows[t + 1];
+        const int32_t ts = start[t], te = end[t];
+        const int64_t nt = te - ts;
         int64_t cnt = 0;
+        unsigned long long blocks = 0, skipped = 0;
+        bool self = false;
         for (int64_t kb = k0; kb < k1; kb += 32) {
-            int64_t k = kb + lane;
-            bool f = k < k1 && run_start(src, k, k0, t, start, end);
+            const int64_t k = kb + lane;
+            const bool valid = k < k1;
+            const bool f = valid && run_start(src, k, k0, t, start, end);
             cnt += __popc(__ballot_sync(0xffffffffu, f));
+            if (valid) {
+                const int32_t s = src[k];
+                blocks += (unsigned long long)(nt * (end[s] - start[s]));
+                if (s == t) {
+                    blocks -= (unsigned long long)nt;
+                    self = true;
+                }
+            }
         }
-        if (lane == 0) nr[r] = cnt;
+        // coincident pairs inside the target leaf (only if the self pair is listed)
+        self = __any_sync(0xffffffffu, self);
+        bool dup = keys == nullptr;
+        if (self && !dup)
+            for (int32_t i = ts + lane; i + 1 < te && !dup; i += 32) dup = keys[i] == keys[i + 1];
+        if (self && __any_sync(0xffffffffu, dup)) {
+            for (int64_t i = ts + lane; i < te; i += 32) {
+                for (int64_t j = ts; j < te; j++) {
+                    if (j == i) continue;
+                    const double dx = xs[i] - xs[j], dy = ys[i] - ys[j], dz = zs[i] - zs[j];
+                    const double r2 = dx * dx + dy * dy + dz * dz;
+                    if (r2 == 0.0) skipped++;
+                }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            blocks += __shfl_xor_sync(0xffffffffu, blocks, o);
+            skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
+        }
+        if (lane == 0) {
+            nr[r] = cnt;
+            if (stats) {
+                atomicAdd(&stats[0], blocks - skipped);
+                atomicAdd(&stats[1], skipped);
+            }
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) nr[ncells] = 0;
 }
@@ -81,45 +127,6 @@ __global__ void plan_write(const int32_t *__restrict__ nrows_dev, const int32_t 
     }
 }
 
-// per target row: sum |t| |s| - self |t|, and coincident ordered pairs
-__global__ void plan_stats(const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
-                           const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
-                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-                           const double *__restrict__ xs, const double *__restrict__ ys,
-                           const double *__restrict__ zs, unsigned long long *stats) {
-    const int lane = threadIdx.x & 31;
-    const int32_t nrows = *nrows_dev;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
-         r += (gridDim.x * blockDim.x) >> 5) {
-        const int32_t t = leaf_rows[r];
-        const int64_t k0 = rows[t], k1 = rows[t + 1];
-        const int64_t nt = end[t] - start[t];
-        unsigned long long blocks = 0, skipped = 0;
-        for (int64_t k = k0 + lane; k < k1; k += 32) {
-            int32_t s = src[k];
-            blocks += (unsigned long long)(nt * (end[s] - start[s]));
-            if (s == t) blocks -= (unsigned long long)nt;
-        }
-        // coincident pairs inside the target leaf (only if the self pair is listed)
-        for (int64_t i = start[t] + lane; i < end[t]; i += 32) {
-            for (int64_t j = start[t]; j < end[t]; j++) {
-                if (j == i) continue;
-                double dx = xs[i] - xs[j], dy = ys[i] - ys[j], dz = zs[i] - zs[j];
-                double r2 = dx * dx + dy * dy + dz * dz;
-                if (r2 == 0.0) skipped++;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            blocks += __shfl_xor_sync(0xffffffffu, blocks, o);
-            skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
-        }
-        if (lane == 0) {
-            atomicAdd(&stats[0], blocks - skipped);
-            atomicAdd(&stats[1], skipped);
-        }
-    }
-}
-
 __global__ void leaf_in_range(int32_t ncells, const uint8_t *leaf, const int32_t *start, int32_t lo, int32_t hi,
                               uint8_t *flag) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x)
@@ -134,7 +141,8 @@ using namespace fmm;
 extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
                             int32_t body_lo, int32_t body_hi,
                             const int64_t *rows, const int32_t *src_sorted, const double *xs,
-                            const double *ys, const double *zs, int32_t *leaf_rows, int64_t *run_off,
+                            const double *ys, const double *zs, const uint64_t *keys, int32_t *leaf_rows,
+                            int64_t *run_off,
                             void *runs, int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows,
                             int32_t *dev_nrows, unsigned long long *dev_stats, void *ws, size_t ws_bytes,
                             void *stream) {
@@ -152,7 +160,9 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, leaf_rows, nsel, ncells, s);
     // leaf_rows is sized ncells: the kernels read the row count on the device
     const int g = grid_for((int64_t)ncells * 32, 256, 148 * 16);
-    plan_count<<<g, 256, 0, s>>>(nsel, ncells, leaf_rows, rows, src_sorted, start, end, nr); fmm::note_launch();
+    if (dev_stats) cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
+    plan_count<<<g, 256, 0, s>>>(nsel, ncells, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, keys, nr,
+                                 dev_stats); fmm::note_launch();
     need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, ncells + 1, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
@@ -169,10 +179,6 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     }
     if (dev_nrows) cudaMemcpyAsync(dev_nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
     plan_write<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs); fmm::note_launch();
-    if (dev_stats) {
-        cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
-        plan_stats<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, dev_stats); fmm::note_launch();
-    }
     FMM_CUDA_CHECK("fmm_p2p_plan");
     return FMM_OK;
 }

@@ -238,7 +238,8 @@ def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
     cap_runs = max(n_p2p, 1)
     runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
     _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
-              P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(leaf_rows), P(run_off), P(runs), cap_runs,
+              P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), P(leaf_rows), P(run_off), P(runs),
+              cap_runs,
               None, None, P(dev_nrows), P(dev_stats), wsp, wsb, st)
     return dict(leaf_rows=leaf_rows, nrows=tree.nleaves, dev_nrows=dev_nrows, run_off=run_off, runs=runs,
                 dev_stats=dev_stats)
