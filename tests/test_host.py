@@ -198,3 +198,15 @@ def test_call_sites_match_abi_arity():
             assert n == len(_lib.SIGNATURES[name]), (fn, node.lineno, name, n, len(_lib.SIGNATURES[name]))
             checked += 1
     assert checked >= 15
+
+
+def test_integration_binding_matches_header():
+    """INTEGRATION.md's reference-side ctypes stub declares argtypes with the
+    arity the header declares (the doc cannot drift from the ABI)."""
+    decls = header_decls()
+    txt = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    found = re.findall(r"_lib\.(fmm_\w+)\.argtypes\s*=\s*\[([^\]]*)\]", txt)
+    assert found
+    for name, args in found:
+        n = len([a for a in args.split(",") if a.strip()])
+        assert decls[name] == n, (name, decls[name], n)
