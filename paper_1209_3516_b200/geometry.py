@@ -92,13 +92,17 @@ class ParticleSet:
                 self._raw = None
                 self._f64 = [np.ascontiguousarray(a, dtype=np.float64) for a in raw]
             n = (self._raw or self._f64)[0].shape[0]
-            acc = []
-            for a in (phi, fx, fy, fz):
-                acc.append(np.zeros(n) if a is None else np.ascontiguousarray(a, dtype=np.float64))
-            self.phi, self.fx, self.fy, self.fz = acc
+            self._n = int(n)
+            # zero accumulators are materialised on first access (they are
+            # written on the device; allocating 4 x 8 B x N zeros up front
+            # costs milliseconds per call on large clouds)
+            for name, a in zip(("phi", "fx", "fy", "fz"), (phi, fx, fy, fz)):
+                if a is not None:
+                    object.__setattr__(self, name, np.ascontiguousarray(a, dtype=np.float64))
         # (stored arrays: reading self.x here would upcast a float32 cloud)
         stored = self.host_inputs() if self._f64 is not None else (self.x, self.y, self.z, self.q)
-        lengths = {int(a.shape[0]) for a in (*stored, self.phi, self.fx, self.fy, self.fz)}
+        accs = [self.__dict__[k] for k in ("phi", "fx", "fy", "fz") if k in self.__dict__]
+        lengths = {int(a.shape[0]) for a in (*stored, *accs)}
         if lengths != {int(n)}:
             raise ValueError(f"particle arrays disagree on length: {sorted(lengths)}")
 
@@ -115,7 +119,11 @@ class ParticleSet:
             self._raw = None
         self._f64[k] = np.ascontiguousarray(v, dtype=np.float64)
 
-    def __getattr__(self, name):  # x, y, z, q of the host form
+    def __getattr__(self, name):  # x, y, z, q of the host form; lazy zero accumulators
+        if name in ("phi", "fx", "fy", "fz") and "_n" in self.__dict__:
+            a = np.zeros(self.__dict__["_n"])
+            object.__setattr__(self, name, a)
+            return a
         idx = {"x": 0, "y": 1, "z": 2, "q": 3}.get(name)
         if idx is None or self.__dict__.get("_f64") is None:
             raise AttributeError(name)

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import torch
@@ -38,6 +39,11 @@ SHAPES = ("cubic", "rect")
 CENTER_MODES = ("geometric", "com")
 
 __all__ = ["Tree", "build_tree", "upward_pass", "downward_pass", "check_invariants"]
+
+
+# snapshots of host inputs run here, overlapping the GPU work (numpy copies
+# release the GIL)
+_snap = ThreadPoolExecutor(max_workers=1, thread_name_prefix="fmm-snapshot")
 
 
 def _u64_np(t: torch.Tensor) -> np.ndarray:
@@ -58,6 +64,16 @@ class Tree:
         self.list_cache = None  # interaction lists of the last traversal (csr)
 
     # ---- sizes ---------------------------------------------------------
+    @property
+    def fp32_exact(self) -> bool:
+        """Every float64 input is exactly representable in float32 (read
+        from the device flag on first use -- no synchronisation in the build)."""
+        v = self.__dict__.get("_fp32_exact")
+        if v is None:
+            v = int(self.d_inexact.item()) == 0
+            self._fp32_exact = v
+        return v
+
     @property
     def ncells(self) -> int:
         return int(self._ncells)
@@ -185,10 +201,12 @@ class Tree:
             h = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
             h.copy_(a, non_blocking=True)
             host.append(h)
-        if self._host_input is not None:
-            # the caller's own arrays, in their stored precision (a float32
-            # cloud stays float32 and is upcast lazily on access)
-            src = [np.array(a) for a in self._host_input.host_inputs()]
+        if self._input_snapshot is not None:
+            # the caller's arrays as of build time (the reference's tree holds
+            # its own copy of the bodies), in their stored precision (a
+            # float32 cloud stays float32 and is upcast lazily on access);
+            # copied on a worker thread while the GPU worked
+            src = self._input_snapshot.result()
         else:
             src = None
         torch.cuda.current_stream(self.device).synchronize()
@@ -350,19 +368,18 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
                   P(xs), P(ys), P(zs), P(qs), int(shape == "rect"), int(center_mode == "com"), P(root), P(lo),
                   P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
         zeros = [torch.zeros(n, dtype=f64, device=dev) for _ in range(4)]
-        fp32_exact = int(inexact.item()) == 0  # synchronises the stream
     tree = Tree(
         device=dev, n=n, ncrit=ncrit, shape=shape, center_mode=center_mode,
         allow_oversized_leaves=bool(allow_oversized_leaves), _ncells=ncells, _nleaves=nleaves,
         level_off=level_off, d_root=root, d_keys=skeys, d_perm=perm,
-        d_x=xs, d_y=ys, d_z=zs, d_q=qs, d_b32=b32, d_b32lo=b32lo, fp32_exact=fp32_exact,
+        d_x=xs, d_y=ys, d_z=zs, d_q=qs, d_b32=b32, d_b32lo=b32lo, d_inexact=inexact,
         d_phi=zeros[0], d_fx=zeros[1], d_fy=zeros[2], d_fz=zeros[3],
         d_children=cc["children"], d_parent=cc["parent"], d_level=cc["level"], d_key=cc["key"],
         d_start=cc["start"], d_end=cc["end"], d_sub_end=cc["sub_end"], d_leaf=cc["leaf"],
         d_body_leaf=body_leaf, d_cells_by_level=cells_by_level,
         d_lo=lo, d_hi=hi, d_ctr=ctr, d_bmax=bmax, d_rmax=rmax,
     )
-    tree._host_input = None if ps.on_device else ps
+    tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
     tree.build_time = time.perf_counter() - t0
     return tree
 
