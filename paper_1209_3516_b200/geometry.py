@@ -22,7 +22,8 @@ import torch
 
 MAX_LEVEL = 21  # src/geometry.py:17
 
-__all__ = ["MAX_LEVEL", "Aabb", "ParticleSet", "compute_bounds"]
+__all__ = ["MAX_LEVEL", "Aabb", "ParticleSet", "compute_bounds", "generate_distribution", "load_particles_csv",
+           "save_particles_csv"]
 
 
 def _is_torch(a) -> bool:
@@ -191,3 +192,51 @@ def compute_bounds(ps: ParticleSet) -> Aabb:
     lo = np.array([ps.x.min(), ps.y.min(), ps.z.min()])
     hi = np.array([ps.x.max(), ps.y.max(), ps.z.max()])
     return Aabb(lo, hi)
+
+
+def generate_distribution(kind: str, n: int, seed: int = 0) -> ParticleSet:
+    """Seeded benchmark cloud (src/geometry.py:273-287): ``uniform`` (alias
+    ``cube``) positions in [0, 1)^3 from ``default_rng(seed)``, every charge
+    1/n (total charge one)."""
+    if n <= 0:
+        raise ValueError(f"n must be positive, got {n}")
+    if kind not in ("uniform", "cube"):
+        raise ValueError(f"unknown distribution kind: {kind!r}")
+    pts = np.random.default_rng(seed).random((n, 3))
+    return ParticleSet(pts[:, 0], pts[:, 1], pts[:, 2], np.full(n, 1.0 / n))
+
+
+def save_particles_csv(ps: ParticleSet, path: str) -> None:
+    """Bodies as CSV with header ``x,y,z,q``, full float64 round trip
+    (src/geometry.py:290-297)."""
+    cols = [_np(a) for a in (ps.x, ps.y, ps.z, ps.q)]
+    with open(path, "w", newline="") as fh:
+        fh.write("x,y,z,q\n")
+        for i in range(ps.n):
+            fh.write(",".join(repr(float(c[i])) for c in cols) + "\n")
+
+
+def load_particles_csv(path: str) -> ParticleSet:
+    """Bodies from a CSV with header ``x,y,z,q`` (src/geometry.py:298-318);
+    ValueError with the line number on malformed input."""
+    import csv
+
+    rows = []
+    with open(path, newline="") as fh:
+        reader = csv.reader(fh)
+        header = next(reader, None)
+        if header is None or [h.strip().lower() for h in header] != ["x", "y", "z", "q"]:
+            raise ValueError(f"bad particle CSV header in {path}: expected x,y,z,q")
+        for lineno, row in enumerate(reader, start=2):
+            if not row:
+                continue
+            if len(row) != 4:
+                raise ValueError(f"bad particle CSV row at line {lineno}: expected 4 fields")
+            try:
+                rows.append([float(v) for v in row])
+            except ValueError as exc:
+                raise ValueError(f"bad particle CSV value at line {lineno}: {exc}") from None
+    if not rows:
+        raise ValueError(f"empty particle set in {path}")
+    a = np.asarray(rows, dtype=np.float64)
+    return ParticleSet(a[:, 0], a[:, 1], a[:, 2], a[:, 3])
