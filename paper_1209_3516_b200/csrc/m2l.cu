@@ -14,6 +14,8 @@
 //  * m2l_warp (any p <= 12): one warp per target row, the warp handles one
 //    pair at a time -- lanes split each degree of the D recurrence, then
 //    lanes own output coefficients; D and M_s staged in shared memory.
+#include <stdlib.h>
+
 #include "taylor.cuh"
 
 namespace fmm {
@@ -328,6 +330,112 @@ __global__ void __launch_bounds__(NT) m2l_block(int p, int32_t ncells, const int
     }
 }
 
+// ---- high orders (P >= 6): lanes own outputs ------------------------------
+// One CTA (4 warps) per target row; warp w takes the row's pairs w, w+4, ...
+// Per pair the warp stages the parity-signed moments and D (degrees < P,
+// the reference's recurrence, src/_taylor.py:57-95) in its shared-memory
+// slice.  Lane l owns the outputs n = l + 32 i (graded-lex order, so one
+// slot i spans few degrees) and accumulates them over all its pairs in
+// registers.  For output n the terms group into rows of fixed (|m|, m_x):
+// along a row m steps (m_x, |m|-m_x-t, t) and n + m steps (n_x+m_x, ., n_z+t),
+// so both operands are CONTIGUOUS runs -- idx(v) = ncoef(|v|) + tri(|v| -
+// v_x) + v_z -- and the M run is the same for every lane (broadcast).  Rows
+// and run lengths are compile-time; only each lane's D offset is computed.
+// The four warps' partials are folded in a fixed order: deterministic.
+__host__ __device__ constexpr int tri(int a) { return a * (a + 1) / 2; }
+
+template <int P>
+__global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *__restrict__ rows,
+                                                 const int32_t *__restrict__ src, const double *__restrict__ ctr,
+                                                 const double *__restrict__ M, double *L) {
+    constexpr int NC = ncoef(P);
+    constexpr int NS = (NC + 31) / 32;
+    __shared__ double sM[4][NC];
+    __shared__ double sD[4][NC];
+    __shared__ double red[4][NC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *Ms = sM[w], *D = sD[w];
+    for (int32_t t = blockIdx.x; t < ncells; t += gridDim.x) {
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        if (k0 == k1) continue;
+        const double cx = ctr[t * 3], cy = ctr[t * 3 + 1], cz = ctr[t * 3 + 2];
+        double acc[NS];
+#pragma unroll
+        for (int i = 0; i < NS; i++) acc[i] = 0.0;
+        for (int64_t k = k0 + w; k < k1; k += 4) {
+            const int32_t s = src[k];
+            for (int m = lane; m < NC; m += 32) {
+                const double v = __ldg(&M[(int64_t)s * NC + m]);
+                Ms[m] = (d_tab.deg[m] & 1) ? -v : v;
+            }
+            const double rx = cx - ctr[s * 3], ry = cy - ctr[s * 3 + 1], rz = cz - ctr[s * 3 + 2];
+            const double inv_r2 = 1.0 / (rx * rx + ry * ry + rz * rz);
+            if (lane == 0) D[0] = sqrt(inv_r2);
+            __syncwarp();
+            for (int d = 1; d < P; d++) {
+                for (int idx = ncoef(d) + lane; idx < ncoef(d + 1); idx += 32) {
+                    const int kx = d_tab.mi[idx][0], ky = d_tab.mi[idx][1], kz = d_tab.mi[idx][2];
+                    double a = 0.0;
+                    if (kx > 0) {
+                        a -= (2.0 * kx - 1.0) * rx * D[d_tab.idx3[kx - 1][ky][kz]];
+                        if (kx > 1) a -= (kx - 1.0) * (kx - 1.0) * D[d_tab.idx3[kx - 2][ky][kz]];
+                        if (ky > 0) {
+                            a -= 2.0 * ky * ry * D[d_tab.idx3[kx][ky - 1][kz]];
+                            if (ky > 1) a -= ky * (ky - 1.0) * D[d_tab.idx3[kx][ky - 2][kz]];
+                        }
+                        if (kz > 0) {
+                            a -= 2.0 * kz * rz * D[d_tab.idx3[kx][ky][kz - 1]];
+                            if (kz > 1) a -= kz * (kz - 1.0) * D[d_tab.idx3[kx][ky][kz - 2]];
+                        }
+                    } else if (ky > 0) {
+                        a -= (2.0 * ky - 1.0) * ry * D[d_tab.idx3[kx][ky - 1][kz]];
+                        if (ky > 1) a -= (ky - 1.0) * (ky - 1.0) * D[d_tab.idx3[kx][ky - 2][kz]];
+                        if (kz > 0) {
+                            a -= 2.0 * kz * rz * D[d_tab.idx3[kx][ky][kz - 1]];
+                            if (kz > 1) a -= kz * (kz - 1.0) * D[d_tab.idx3[kx][ky][kz - 2]];
+                        }
+                    } else {
+                        a -= (2.0 * kz - 1.0) * rz * D[d_tab.idx3[kx][ky][kz - 1]];
+                        if (kz > 1) a -= (kz - 1.0) * (kz - 1.0) * D[d_tab.idx3[kx][ky][kz - 2]];
+                    }
+                    D[idx] = a * inv_r2;
+                }
+                __syncwarp();
+            }
+#pragma unroll 1
+            for (int i = 0; i < NS; i++) {
+                const int n = 32 * i + lane;
+                const bool valid = n < NC;
+                const int nn = valid ? n : 0;
+                const int nx = d_tab.mi[nn][0], nz = d_tab.mi[nn][2], dn = valid ? d_tab.deg[nn] : P;
+                double a = 0.0;
+                static_for<0, P>([&](auto Idm) {
+                    constexpr int dm = decltype(Idm)::value;
+                    if (dn + dm <= P - 1) {
+                        const int dv = dn + dm;
+                        static_for<0, dm + 1>([&](auto Imx) {
+                            constexpr int mx = decltype(Imx)::value;
+                            constexpr int bm = ncoef(dm) + tri(dm - mx), len = dm - mx + 1;
+                            const int bd = dv * (dv + 1) * (dv + 2) / 6 + tri(dv - nx - mx) + nz;
+#pragma unroll
+                            for (int u = 0; u < len; u++) a = fma(Ms[bm + u], D[bd + u], a);
+                        });
+                    }
+                });
+                acc[i] += a;
+            }
+            __syncwarp();  // the warp's slices are rewritten by its next pair
+        }
+#pragma unroll
+        for (int i = 0; i < NS; i++)
+            if (32 * i + lane < NC) red[w][32 * i + lane] = acc[i];
+        __syncthreads();
+        for (int n = threadIdx.x; n < NC; n += blockDim.x)
+            L[(int64_t)t * NC + n] += (((red[0][n] + red[1][n]) + red[2][n]) + red[3][n]) / d_tab.mfact[n];
+        __syncthreads();  // red is rewritten by the next row
+    }
+}
+
 }  // namespace fmm
 
 using namespace fmm;
@@ -343,6 +451,22 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
         case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
         case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
         case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
+#define M2L_LANES(PP)                                                                                   \
+    case PP:                                                                                            \
+        if (PP >= 8 && !getenv("FMM_B200_M2L_BLOCK")) {                                                 \
+            m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), 128, 0, s>>>(ncells, rows, src, ctr, M, L);    \
+            fmm::note_launch();                                                                         \
+            break;                                                                                      \
+        }                                                                                               \
+        [[fallthrough]];
+        M2L_LANES(6)
+        M2L_LANES(7)
+        M2L_LANES(8)
+        M2L_LANES(9)
+        M2L_LANES(10)
+        M2L_LANES(11)
+        M2L_LANES(12)
+#undef M2L_LANES
         default: {
             // high orders: block kernel over a load-balanced term table
             static int table_p[64];  // per device: the table is a device symbol
