@@ -422,9 +422,7 @@ __device__ __forceinline__ float p2p_f32_stream_unit(int32_t i0, int32_t ilast, 
     // 1) the self share, guarded
     for (int32_t j = ts + s0 + lane; j < ts + min(s1, cnt); j += 32)
         p2p_f32x2_pairs<KB, true>(__ldg(&b[j]), j - i0, tx, ty, tz, ap, ax, ay, az);
-    // 2) the chunks: full ones in the loop (one straight-line body, so the
-    // accumulators keep their registers across iterations), the tail after
-    const int nfull = (hi - lo) / kChunk;
+    // 2) the chunks
     int st = 0;
     for (int k = 0; k < nk; k++) {
         if (k > 0 && lane == 0 && k - 1 + kWStages < nk) {  // refill the stage consumed last iteration
@@ -432,22 +430,23 @@ __device__ __forceinline__ float p2p_f32_stream_unit(int32_t i0, int32_t ilast, 
             const int32_t p0 = lo + (k - 1 + kWStages) * kChunk;
             chunk_produce(ring + sp * kChunk, &bars[sp], p0, min(kChunk, hi - p0), cur, srun, b);
         }
+        __syncwarp();
         mbar_wait(&bars[st], (phase >> st) & 1u);
         phase ^= 1u << st;
         const float4 *src = ring + st * kChunk + lane;
-        if (k == nfull) {  // the partial last chunk
-            const int32_t valid = hi - (lo + k * kChunk);
+        const int32_t valid = hi - (lo + k * kChunk);
+        if (valid >= kChunk) {
+            float4 s = src[0];
+#pragma unroll
+            for (int q = 0; q < kSPL; q++) {
+                const float4 nxt = src[((q + 1) % kSPL) * 32];
+                p2p_f32x2_pairs<KB, false>(s, 0, tx, ty, tz, ap, ax, ay, az);
+                s = nxt;
+            }
+        } else {
 #pragma unroll 1
             for (int q = 0; q < kSPL; q++)
                 if (q * 32 + lane < valid) p2p_f32x2_pairs<KB, false>(src[q * 32], 0, tx, ty, tz, ap, ax, ay, az);
-            break;
-        }
-        float4 s = src[0];
-#pragma unroll
-        for (int q = 0; q < kSPL; q++) {
-            const float4 nxt = src[((q + 1) % kSPL) * 32];
-            p2p_f32x2_pairs<KB, false>(s, 0, tx, ty, tz, ap, ax, ay, az);
-            s = nxt;
         }
         __syncwarp();  // every lane is done with stage st before lane 0 refills it
         if (++st == kWStages) st = 0;
