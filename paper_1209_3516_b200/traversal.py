@@ -421,11 +421,10 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     """Simultaneous traversal of the tree against itself, on the GPU.
 
     Three streams.  The targets may be cut into Morton chunks on leaf
-    boundaries (``_nchunks``, default one chunk); a high-priority list
-    stream builds each chunk's lists (traversal, P2P CSR and run plan) --
-    its latency-bound kernels get SMs ahead of the far field, since they
-    gate P2P -- and a P2P stream runs the chunk's near field as soon as its
-    plan exists.  M2L pairs are
+    boundaries (``_nchunks``, default one chunk); the main stream (a
+    high-priority list stream when chunked) builds each chunk's lists
+    (traversal, P2P CSR and run plan) and a P2P stream runs the chunk's near
+    field as soon as its plan exists.  M2L pairs are
     emitted only by the chunk owning their target's first body, so the
     chunks partition both lists exactly.  A side stream runs the far field:
     the upward pass as soon as the tree exists, each chunk's M2L as soon as
@@ -464,7 +463,10 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         tree._M, tree.p, tree._L = M, p, L
         cuts = _chunk_cuts(tree, _nchunks(tree))
         nch = len(cuts) - 1
-        lst = _side_stream(dev, 2)  # high priority: the lists gate P2P
+        # chunked runs build lists on a high-priority stream (they gate P2P); with
+        # one chunk the main stream does: a priority stream there starves the
+        # far field behind P2P on some runs (C3 measured 37 ms or 49 ms)
+        lst = _side_stream(dev, 2) if nch > 1 else main
         lst.wait_event(e0)
         parts, m2l_ev, p2p_ev = [], [], []
         for k in range(nch):
