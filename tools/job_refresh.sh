@@ -9,6 +9,7 @@ for c in C1 C3 C5; do
 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 python bench.py --strategy treecode --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_treecode.json 2> gpurun_out/bench_tc.err
+python bench.py --strategy listfmm --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_listfmm.json 2> gpurun_out/bench_lf.err
 CFG=C2 bash tools/job_launches.sh
 CFG=C3 bash tools/job_launches.sh
 for c in C2 C3; do
