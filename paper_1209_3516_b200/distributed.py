@@ -40,17 +40,14 @@ __all__ = ["body_cuts", "cell_chunks", "shared_cells", "allgather_rows", "TorchD
 
 
 def body_cuts(leaf_start: np.ndarray, leaf_end: np.ndarray, n: int, world: int) -> np.ndarray:
-    """Cut points ``cuts[0]=0 < ... < cuts[world]=n`` on leaf boundaries,
-    closest to the equal split ``r * n / world`` (leaves in Morton order)."""
-    bounds = np.concatenate([np.sort(np.asarray(leaf_start, np.int64)), [n]])
+    """Cut points ``cuts[0]=0 <= ... <= cuts[world]=n`` on leaf boundaries:
+    cut r is the start of the leaf holding body ``r * n // world`` (leaves in
+    Morton order), within one leaf of the equal split."""
+    starts = np.sort(np.asarray(leaf_start, np.int64))
     cuts = [0]
     for r in range(1, world):
-        target = r * n / world
-        k = int(np.searchsorted(bounds, target))
-        cand = [bounds[max(0, k - 1)], bounds[min(len(bounds) - 1, k)]]
-        c = int(min(cand, key=lambda v: abs(v - target)))
-        c = max(c, cuts[-1])
-        cuts.append(c)
+        k = int(np.searchsorted(starts, r * n // world, side="right")) - 1
+        cuts.append(max(int(starts[max(k, 0)]), cuts[-1]))
     cuts.append(n)
     return np.asarray(cuts, np.int64)
 
@@ -93,34 +90,48 @@ def allgather_rows(full: torch.Tensor, chunks, rank: int, world: int, group=None
 
 
 class _Plan:
-    """Per-tree partition plan (host arrays + device cell lists)."""
+    """This rank's share of the tree, computed on the device each step
+    (``body_cuts``, ``cell_chunks`` and ``shared_cells`` above state the same
+    rules on NumPy arrays):
 
-    def __init__(self, tree, world: int):
-        from .tree import Tree  # noqa: F401
-        leaf = tree.cell_leaf
-        start, end, level = tree.cell_start, tree.cell_end, tree.cell_level
-        self.cuts = body_cuts(start[leaf], end[leaf], tree.n, world)
-        self.chunks = cell_chunks(start, self.cuts)
-        self.shared = shared_cells(start, end, self.cuts)
-        bfs = tree.d_cells_by_level.cpu().numpy()  # pre-order ids grouped by level
-        nlev = len(tree.level_off) - 1
-        self.owned = []
-        for r in range(world):
-            lo, hi = self.cuts[r], self.cuts[r + 1]
-            own = (start >= lo) & (end <= hi)
-            self.owned.append(self._by_level(bfs, own, tree.level_off, nlev, tree.device))
-        self.top = self._by_level(bfs, self.shared, tree.level_off, nlev, tree.device)
+    * ``cuts``: body cut points on leaf boundaries (the start of the leaf
+      holding body r * n / world), ``chunks``: the cells whose first body
+      lies in each rank's range (pre-order cell starts are non-decreasing);
+    * ``owned``: this rank's cells (body range inside its own), grouped by
+      level, ``top``: cells straddling an interior cut, grouped by level --
+      both as (device id list, host level offsets) for ``fmm_upward``.
+    Three small device-to-host reads, no host copies of cell arrays."""
 
-    @staticmethod
-    def _by_level(bfs, mask, level_off, nlev, dev):
-        ids, off = [], [0]
-        for L in range(nlev):
-            seg = bfs[level_off[L]:level_off[L + 1]]
-            sel = seg[mask[seg]]
-            ids.append(sel)
-            off.append(off[-1] + sel.size)
-        arr = np.concatenate(ids).astype(np.int32) if ids else np.zeros(0, np.int32)
-        return torch.as_tensor(arr, device=dev), off
+    def __init__(self, tree, world: int, rank: int):
+        n, dev = tree.n, tree.device
+        at = torch.tensor([r * n // world for r in range(1, world)], dtype=torch.int64, device=dev)
+        inner = tree.d_start[tree.d_body_leaf[at].long()].tolist() if world > 1 else []
+        cuts = [0]
+        for c in inner:
+            cuts.append(max(int(c), cuts[-1]))
+        cuts.append(n)
+        self.cuts = np.asarray(cuts, np.int64)
+        start = tree.d_start.long()
+        end = tree.d_end.long()
+        bounds = torch.as_tensor(self.cuts, device=dev)
+        self.chunks = torch.searchsorted(start, bounds, side="left").cpu().numpy().astype(np.int64)
+        shared = torch.zeros(tree.ncells, dtype=torch.bool, device=dev)
+        for c in self.cuts[1:-1]:
+            shared |= (start < int(c)) & (end > int(c))
+        lo, hi = int(self.cuts[rank]), int(self.cuts[rank + 1])
+        own = (start >= lo) & (end <= hi)
+        bfs = tree.d_cells_by_level.long()
+        lev = tree.d_level.long()[bfs]
+        depth = len(tree.level_off) - 2
+        counts = []
+        self.lists = []
+        for mask in (own, shared):
+            sel = mask[bfs]
+            self.lists.append(bfs[sel].to(torch.int32))  # level-grouped (bfs is)
+            counts.append(torch.bincount(lev[sel], minlength=depth + 1))
+        both = torch.stack(counts).tolist()
+        self.owned = (self.lists[0], [0] + list(np.cumsum(both[0]).astype(int)))
+        self.top = (self.lists[1], [0] + list(np.cumsum(both[1]).astype(int)))
 
 
 def _upward_cells(tree, p, cells, off, M):
@@ -164,72 +175,82 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     if cfg.mutual and cfg.strategy == "dualtree":
         raise NotImplementedError("mutual traversal is outside the B200 hot path")
     plan = getattr(tree, "_dist_plan", None)
-    if plan is None or len(plan.cuts) != world + 1:
-        plan = _Plan(tree, world)
+    if plan is None or len(plan.cuts) != world + 1 or plan.rank != rank:
+        plan = _Plan(tree, world, rank)
+        plan.rank = rank
         tree._dist_plan = plan
     lo, hi = int(plan.cuts[rank]), int(plan.cuts[rank + 1])
     dev = tree.device
     stats = KernelStats()
-    stream = torch.cuda.current_stream(dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-    ev[0].record(stream)
+    from .traversal import _side_stream
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
+    ev[0].record(main)
     nc = ncoef(cfg.p)
-    # upward: owned cells, all-gather, shared top rebuilt redundantly
     M = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
-    cells, off = plan.owned[rank]
-    _upward_cells(tree, cfg.p, cells, off, M)
-    comm.allgather_rows(M, plan.chunks, rank, world)
-    top, toff = plan.top
-    if top.numel():
-        M[top.long()] = 0.0
-        _upward_cells(tree, cfg.p, top, toff, M)
-    tree._M, tree.p = M, cfg.p
-    tree._L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
-    ev[1].record(stream)
-    if treecode:
-        # the rank's target leaves walk the whole (replicated) tree
-        lists = treecode_lists(tree, cfg.mac, body_range=(lo, hi))
-        ev[2].record(stream)
-        far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
-        run_m2p(tree, lists, cfg.p, tuple(far))
-    else:
-        if cfg.strategy == "listfmm":
-            lists = listfmm_lists(tree, body_range=(lo, hi))
-        else:
-            lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi))
-        ev[2].record(stream)
-        run_m2l(tree, lists, cfg.p)
-    ev[3].record(stream)
+    L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
+    far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    # far field, side stream: owned upward, all-gather, shared top rebuilt
+    # redundantly -- beside the main stream's traversal, which needs no moments
+    side.wait_event(ev[0])
+    with torch.cuda.stream(side):
+        cells, off = plan.owned
+        _upward_cells(tree, cfg.p, cells, off, M)
+        comm.allgather_rows(M, plan.chunks, rank, world)
+        top, toff = plan.top
+        if top.numel():
+            M[top.long()] = 0.0
+            _upward_cells(tree, cfg.p, top, toff, M)
+        ev[1].record(side)
+    tree._M, tree.p, tree._L = M, cfg.p, L
+    ready = torch.cuda.Event()
+    if treecode:  # the rank's target leaves walk the whole (replicated) tree
+        lists = treecode_lists(tree, cfg.mac, body_range=(lo, hi), m2p_ready=ready, side=side)
+    elif cfg.strategy == "listfmm":
+        lists = listfmm_lists(tree, body_range=(lo, hi), m2l_ready=ready, side=side)
+    else:
+        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side)
+    ev[2].record(main)
+    side.wait_event(ready)
+    with torch.cuda.stream(side):
+        ev[3].record(side)
+        if treecode:
+            run_m2p(tree, lists, cfg.p, tuple(far))
+        else:
+            run_m2l(tree, lists, cfg.p)
+        ev[4].record(side)
+        if not treecode:
+            downward_pass(tree, None, sync=False, body_range=(lo, hi), out=tuple(far))
+        ev[5].record(side)
+    ev[6].record(main)
     run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
     if cfg.precision == "fp32" and int(flag.item()) != 0:
         run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
-    ev[4].record(stream)
-    if treecode:
-        P = _lib.ptr
-        _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
-                  P(tree.d_fz), _lib.stream_handle())
-    else:
-        downward_pass(tree, None, sync=False, body_range=(lo, hi))
-    ev[5].record(stream)
+    ev[7].record(main)
+    main.wait_event(ev[5])
+    P = _lib.ptr
+    _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
+              P(tree.d_fz), _lib.stream_handle())
     res = torch.stack([tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz], 1)
     comm.allgather_rows(res, plan.cuts, rank, world)
     for k, a in enumerate((tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz)):
         a.copy_(res[:, k])
-    ev[6].record(stream)
-    ev[6].synchronize()
+    ev[8].record(main)
+    ev[8].synchronize()
     pairs, skipped = lists.dev_stats.tolist()
     stats.p2p_pairs, stats.p2p_skipped, stats.p2p_flops = int(pairs), int(skipped), 20 * int(pairs)
     stats.m2l_calls = lists.n_m2l
     stats.m2p_calls = getattr(lists, "n_m2p", 0)
-    stats.add_time("list", ev[1].elapsed_time(ev[2]) * 1e-3)
-    stats.add_time("m2p" if treecode else "m2l", ev[2].elapsed_time(ev[3]) * 1e-3)
-    stats.add_time("p2p", ev[3].elapsed_time(ev[4]) * 1e-3)
-    stats.add_time("allgather", ev[5].elapsed_time(ev[6]) * 1e-3)
+    stats.add_time("list", ev[0].elapsed_time(ev[2]) * 1e-3)
+    stats.add_time("m2p" if treecode else "m2l", ev[3].elapsed_time(ev[4]) * 1e-3)
+    stats.add_time("p2p", ev[6].elapsed_time(ev[7]) * 1e-3)
+    stats.add_time("allgather", ev[7].elapsed_time(ev[8]) * 1e-3)
     tree._results_changed()
     del _lib
     return EvalReport(strategy=cfg.strategy, n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=False, threads=world, task_grain=cfg.task_grain, stats=stats,
                       build_time=tree.build_time, upward_time=ev[0].elapsed_time(ev[1]) * 1e-3,
-                      traversal_time=ev[1].elapsed_time(ev[4]) * 1e-3,
-                      downward_time=0.0 if treecode else ev[4].elapsed_time(ev[6]) * 1e-3)
+                      traversal_time=ev[0].elapsed_time(ev[7]) * 1e-3,
+                      downward_time=0.0 if treecode else ev[4].elapsed_time(ev[5]) * 1e-3)

@@ -79,3 +79,26 @@ def test_partitioned_equals_single(name, world, precision, strategy):
         for g, w in zip(got, want):
             rel = float(torch.linalg.norm(g - w) / torch.linalg.norm(w))
             assert rel <= 1e-12, (r, rel)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_device_plan_matches_host_rules(world):
+    """The per-step device plan equals the host functions' cuts, chunks,
+    shared top and owned cells (fd.body_cuts / cell_chunks / shared_cells)."""
+    c = Case("plummer_32k")
+    t = fb.build_tree(_ps(c), ncrit=c.ncrit)
+    leaf = t.cell_leaf
+    cuts = fd.body_cuts(t.cell_start[leaf], t.cell_end[leaf], t.n, world)
+    chunks = fd.cell_chunks(t.cell_start, cuts)
+    shared = fd.shared_cells(t.cell_start, t.cell_end, cuts)
+    for rank in range(world):
+        plan = fd._Plan(t, world, rank)
+        assert np.array_equal(plan.cuts, cuts) and np.array_equal(plan.chunks, chunks)
+        lo, hi = cuts[rank], cuts[rank + 1]
+        own = np.flatnonzero((t.cell_start >= lo) & (t.cell_end <= hi))
+        ids, off = plan.owned
+        assert sorted(ids.cpu().tolist()) == own.tolist() and off[-1] == own.size
+        tids, toff = plan.top
+        assert sorted(tids.cpu().tolist()) == np.flatnonzero(shared).tolist() and toff[-1] == shared.sum()
+        lev = t.cell_level[ids.cpu().numpy()]
+        assert np.all(np.diff(lev) >= 0)  # grouped by level, as fmm_upward needs
