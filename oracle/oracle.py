@@ -55,6 +55,10 @@ def _declare(L):
     L.orc_downward.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_collect.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _I, _I, _P, _P, _I, _P, _P, _P]
     L.orc_exec_m2l.argtypes = [_I, _P, _P, _P, _P, _P, C.c_int]
+    L.orc_collect2.argtypes = [_P] * 10 + [_D, _I, _I, _I, _P, _P, _I, _P, _P, _P]
+    L.orc_collect_treecode2.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _I, _P, _P, _P]
+    L.orc_exec_m2l2.argtypes = [_I, _P, _P, _P, _P, _P, _P, C.c_int]
+    L.orc_exec_p2p_cross.argtypes = [_I] + [_P] * 17 + [C.c_int, _P]
     L.orc_collect_vlist.argtypes = [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P]
     L.orc_collect_ulist.argtypes = [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P]
     L.orc_collect_treecode.argtypes = [_I, _P, _P, _P, _P, _P, _D, _I, _P, _P, _I, _P, _P, _P]
@@ -343,6 +347,80 @@ def evaluate_listfmm(t: OracleTree, p: int):
     downward(t, L.copy(), p, phi, fx, fy, fz)
     return dict(phi=phi, fx=fx, fy=fy, fz=fz, m2l=(mt, ms), p2p=(pt, ps), p2p_pairs=int(st[0]),
                 p2p_skipped=int(st[1]), m2l_calls=int(mt.size))
+
+
+# ---- cross-tree evaluation (targets of A, sources of B) -------------------
+def collect_cross(A: OracleTree, B: OracleTree, theta: float):
+    """Dual traversal from (root_A, root_B) (src/traversal.py:159-262 with a
+    source tree): (m2l_t, m2l_s, p2p_t, p2p_s), targets in A, sources in B."""
+    capm = capp = max(2048, 64 * (A.ncells + B.ncells))
+    while True:
+        mt = np.empty(capm, np.int64); ms = np.empty(capm, np.int64)
+        pt = np.empty(capp, np.int64); ps = np.empty(capp, np.int64)
+        out = np.zeros(3, np.int64)
+        lib().orc_collect2(*(_p(a) for a in (A.cell_children, A.cell_leaf, A.cell_center, A.cell_bmax, A.cell_rmax,
+                                              B.cell_children, B.cell_leaf, B.cell_center, B.cell_bmax, B.cell_rmax)),
+                           float(theta) * float(theta), 0, 0, capm, _p(mt), _p(ms), capp, _p(pt), _p(ps), _p(out))
+        if out[2] == 1:
+            capm, capp = int(out[0]) + 1, int(out[1]) + 1
+            continue
+        return mt[:int(out[0])], ms[:int(out[0])], pt[:int(out[1])], ps[:int(out[1])]
+
+
+def collect_treecode_cross(A: OracleTree, B: OracleTree, theta: float):
+    """Treecode walk of A's leaves over B's tree (src/traversal.py:265-313)."""
+    leaf_ids = np.ascontiguousarray(np.flatnonzero(A.cell_leaf), np.int64)
+    capm = max(2048, 256 * leaf_ids.size)
+    capp = max(2048, 64 * leaf_ids.size)
+    while True:
+        mt = np.empty(capm, np.int64); ms = np.empty(capm, np.int64)
+        pt = np.empty(capp, np.int64); ps = np.empty(capp, np.int64)
+        out = np.zeros(3, np.int64)
+        lib().orc_collect_treecode2(leaf_ids.size, _p(leaf_ids), _p(A.cell_center), _p(A.cell_bmax),
+                                    _p(B.cell_children), _p(B.cell_leaf), _p(B.cell_center), _p(B.cell_bmax),
+                                    float(theta) * float(theta), capm, _p(mt), _p(ms), capp, _p(pt), _p(ps), _p(out))
+        if out[2] == 1:
+            capm, capp = int(out[0]) + 1, int(out[1]) + 1
+            continue
+        return mt[:int(out[0])], ms[:int(out[0])], pt[:int(out[1])], ps[:int(out[1])]
+
+
+def exec_p2p_cross(A: OracleTree, B: OracleTree, pt, ps, acc=None, use_rsqrt=False):
+    """src/traversal.py:560-597 into (phi, fx, fy, fz) of A (zeroed unless
+    given); returns them and stats[pairs, skipped, flops]."""
+    pt = np.ascontiguousarray(pt, np.int64); ps = np.ascontiguousarray(ps, np.int64)
+    phi, fx, fy, fz = acc if acc is not None else (np.zeros(A.n) for _ in range(4))
+    st = np.zeros(3, np.int64)
+    lib().orc_exec_p2p_cross(pt.size, _p(pt), _p(ps), _p(A.cell_start), _p(A.cell_end), _p(A.x), _p(A.y), _p(A.z),
+                             _p(phi), _p(fx), _p(fy), _p(fz), _p(B.cell_start), _p(B.cell_end), _p(B.x), _p(B.y),
+                             _p(B.z), _p(B.q), int(use_rsqrt), _p(st))
+    return phi, fx, fy, fz, st
+
+
+def evaluate_cross(A: OracleTree, B: OracleTree, p: int, theta: float):
+    """evaluate_dual_tree(A, source_tree=B) restated sequentially."""
+    MB = upward(B, p)
+    mt, ms, pt, ps = collect_cross(A, B, theta)
+    L = np.zeros((A.ncells, ncoef(p)))
+    mt64, ms64 = np.ascontiguousarray(mt, np.int64), np.ascontiguousarray(ms, np.int64)
+    lib().orc_exec_m2l2(mt.size, _p(mt64), _p(ms64), _p(A.cell_center), _p(B.cell_center), _p(MB), _p(L), p)
+    phi, fx, fy, fz, st = exec_p2p_cross(A, B, pt, ps)
+    downward(A, L.copy(), p, phi, fx, fy, fz)
+    return dict(phi=phi, fx=fx, fy=fy, fz=fz, m2l=(mt, ms), p2p=(pt, ps), p2p_pairs=int(st[0]),
+                p2p_skipped=int(st[1]))
+
+
+def evaluate_treecode_cross(A: OracleTree, B: OracleTree, p: int, theta: float):
+    """evaluate_treecode(A, source_tree=B) restated sequentially."""
+    MB = upward(B, p)
+    mt, ms, pt, ps = collect_treecode_cross(A, B, theta)
+    acc = [np.zeros(A.n) for _ in range(4)]
+    mt64, ms64 = np.ascontiguousarray(mt, np.int64), np.ascontiguousarray(ms, np.int64)
+    lib().orc_exec_m2p(mt.size, _p(mt64), _p(ms64), _p(A.cell_start), _p(A.cell_end), _p(A.x), _p(A.y), _p(A.z),
+                       *(_p(a) for a in acc), _p(B.cell_center), _p(MB), p)
+    phi, fx, fy, fz, st = exec_p2p_cross(A, B, pt, ps, acc=acc)
+    return dict(phi=phi, fx=fx, fy=fy, fz=fz, m2p=(mt, ms), p2p=(pt, ps), p2p_pairs=int(st[0]),
+                p2p_skipped=int(st[1]))
 
 
 def direct(x, y, z, q, idx=None, threads=0):
