@@ -159,6 +159,8 @@ FMM_API int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uin
 FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int classify_self,
                       const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                      const int32_t *children_b, const uint8_t *leaf_b, const double *ctr_b, const double *bmax_b,
+                      const double *rmax_b,
                       const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
                       int m2l_owner_only, int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
                       int32_t *m2l_t,
@@ -174,7 +176,9 @@ FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfro
  * capacity means buffers must grow (the lists are then incomplete; rerun). */
 FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
                  int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
-                 const double *ctr, const double *bmax, const double *rmax, const int32_t *start,
+                 const double *ctr, const double *bmax, const double *rmax, const int32_t *children_b,
+                 const uint8_t *leaf_b, const double *ctr_b, const double *bmax_b, const double *rmax_b,
+                 const int32_t *start,
                  const int32_t *end, int32_t body_lo, int32_t body_hi, int m2l_owner_only, int kind,
                  double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
                  int64_t cap_m2l, unsigned long long *dev_log, void *stream);
@@ -192,6 +196,8 @@ FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1
 FMM_API int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
                           int64_t cap_front, int nsteps, int32_t ncells, const int32_t *children,
                           const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                          const int32_t *children_b, const uint8_t *leaf_b, const double *ctr_b,
+                          const double *bmax_b, const double *rmax_b,
                           const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
                           double th2, int32_t *m2p_t, int32_t *m2p_s, int64_t cap_m2p, int32_t *p2p_t,
                           int32_t *p2p_s, int64_t cap_p2p, unsigned long long *dev_log, void *ws,
@@ -230,19 +236,26 @@ FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs,
  * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
  * into dev_stats[2] (src/_taylor.py:366-407 accounting).  keys (the sorted
  * body keys, optional) let leaves without two equal keys skip the
- * coincident-pair scan (coincident bodies share a key); NULL scans all. */
+ * coincident-pair scan (coincident bodies share a key); NULL scans all.
+ * Cross-tree plans (src_start given): the sources are the source tree's
+ * leaves, their body runs shifted by src_offset (where the source bodies
+ * sit in the P2P body arrays); no self leaf, no coincident scan (see
+ * fmm_p2p_coincident). */
 FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
                  int32_t body_lo, int32_t body_hi,
                  const int64_t *rows, const int32_t *src_sorted, const double *xs, const double *ys,
-                 const double *zs, const uint64_t *keys, int32_t *leaf_rows, int64_t *run_off, void *runs,
+                 const double *zs, const uint64_t *keys, const int32_t *src_start, const int32_t *src_end,
+                 int32_t src_offset, int32_t *leaf_rows, int64_t *run_off, void *runs,
                  int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows, int32_t *dev_nrows,
                  unsigned long long *dev_stats, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- executors (src/traversal.py:500-548) ------------------------------ */
 
-/* L[t] += sum over row sources of M2L(M[s], ctr[t]-ctr[s]) (src/_taylor.py:169-188). */
+/* L[t] += sum over row sources of M2L(M[s], ctr[t]-ctr_src[s]) (src/_taylor.py:169-188).
+ * ctr_src and M are the source tree's (a cross-tree evaluation); ctr_src
+ * NULL means the same tree. */
 FMM_API int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const double *ctr,
-                const double *M, double *L, void *stream);
+                const double *ctr_src, const double *M, double *L, void *stream);
 
 /* Treecode far field (replaces _exec_m2p, src/traversal.py:520-528 ->
  * _m2p, src/_taylor.py:272-307): for every target leaf row t of the CSR M2P
@@ -260,12 +273,23 @@ FMM_API int fmm_m2p_csr(int p, int32_t ncells, const int64_t *rows, const int32_
  * nrows bounds the grid; when dev_nrows is given the kernels stop at the
  * device-side row count (written by fmm_p2p_plan) -- no host round trip.
  * dev_flag[0] is set when a non-finite sum was produced (FP32 collision of
- * distinct bodies); the caller reruns with safe=1. */
-FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *dev_nrows,
+ * distinct bodies); the caller reruns with safe=1.
+ * cross: the sources are another tree's bodies (src/traversal.py:552-597),
+ * appended after the targets in the body arrays (the plan's runs point
+ * there): the target leaf's own bodies are then not swept as sources. */
+FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_t nrows, const int32_t *dev_nrows,
             const int32_t *leaf_rows,
             const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
             const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
             const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);
+
+/* Coincident (target, source) pairs of a cross-tree P2P plan (r2 == 0.0 in
+ * float64, which the reference skips and counts as p2p_skipped,
+ * src/traversal.py:552-597), added into *count. */
+FMM_API int fmm_p2p_coincident(int32_t nrows, const int32_t *dev_nrows, const int32_t *leaf_rows,
+                       const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
+                       const double *xs, const double *ys, const double *zs, unsigned long long *count,
+                       void *stream);
 
 /* Scatter four Morton-ordered arrays back to input order:
  * b_k[perm[i]] = a_k[i] (Tree.results_in_input_order, src/tree.py:344-348). */

@@ -386,7 +386,7 @@ def collect_treecode_cross(A: OracleTree, B: OracleTree, theta: float):
 
 
 def exec_p2p_cross(A: OracleTree, B: OracleTree, pt, ps, acc=None, use_rsqrt=False):
-    """src/traversal.py:560-597 into (phi, fx, fy, fz) of A (zeroed unless
+    """src/traversal.py:552-597 into (phi, fx, fy, fz) of A (zeroed unless
     given); returns them and stats[pairs, skipped, flops]."""
     pt = np.ascontiguousarray(pt, np.int64); ps = np.ascontiguousarray(ps, np.int64)
     phi, fx, fy, fz = acc if acc is not None else (np.zeros(A.n) for _ in range(4))

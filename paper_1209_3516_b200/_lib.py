@@ -43,17 +43,19 @@ SIGNATURES = {
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, INT, INT, P, P, P, P, P, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
     "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],
-    "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P, P, I64, P, P,
-                          I64, P, P],
-    "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P, P, I64, P, P],
-    "fmm_treecode_traverse": [P, P, P, P, I64, INT, I32, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P,
-                              I64, P, P, SZ, P],
+    "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64,
+                          P, P, I64, P, P, I64, P, P],
+    "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P,
+                     P, I64, P, P],
+    "fmm_treecode_traverse": [P, P, P, P, I64, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P,
+                              I64, P, P, I64, P, P, SZ, P],
     "fmm_listfmm_lists": [I32, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, I64, P, P, I64, P, P, SZ, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
-    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, SZ, P],
-    "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P],
+    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, I32, P, P, P, I64, P, P, P, P, P, SZ, P],
+    "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P, P],
     "fmm_m2p_csr": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
-    "fmm_p2p": [INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "fmm_p2p_coincident": [I32, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_unpermute": [P, I64, P, P, P, P, P, P, P, P, P],
     "fmm_combine": [I64, P, P, P, P, P, P, P, P, P],
     "fmm_direct": [I64, P, P, P, P, I64, P, P, P, P, P, P],

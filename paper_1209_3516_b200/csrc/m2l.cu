@@ -24,6 +24,7 @@ template <int P>
 __global__ void __launch_bounds__(128) m2l_reg(int32_t ncells, const int64_t *__restrict__ rows,
                                                const int32_t *__restrict__ src,
                                                const double *__restrict__ ctr,
+                                               const double *__restrict__ cs,
                                                const double *__restrict__ M, double *L) {
     constexpr int NC = ncoef(P);
     const int lane = threadIdx.x & 31;
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(128) m2l_reg(int32_t ncells, const int64_t *__
         for (int64_t k = k0 + lane; k < k1; k += 32) {
             const int32_t s = src[k];
             double D[NC];
-            d_tensors_reg<P>(cx - ctr[s * 3], cy - ctr[s * 3 + 1], cz - ctr[s * 3 + 2], D);
+            d_tensors_reg<P>(cx - cs[s * 3], cy - cs[s * 3 + 1], cz - cs[s * 3 + 2], D);
             double Ms[NC];
 #pragma unroll
             for (int m = 0; m < NC; m++) Ms[m] = __ldg(&M[(int64_t)s * NC + m]);
@@ -120,7 +121,8 @@ __device__ inline DRecipe make_recipe(int idx) {
 template <int P>
 __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *__restrict__ rows,
                                                  const int32_t *__restrict__ src, const double *__restrict__ ctr,
-                                                 const double *__restrict__ M, double *L) {
+                                                 const double *__restrict__ cs, const double *__restrict__ M,
+                                                 double *L) {
     constexpr int NC = ncoef(P);
     constexpr int NS = (NC + 31) / 32;
     __shared__ double sM[4][NC];
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *
         for (int64_t k = k0 + w; k < k1; k += 4) {
             const int32_t s = src[k];
             for (int m = lane; m < NC; m += 32) Ms[m] = sgn[m] * __ldg(&M[(int64_t)s * NC + m]);
-            const double r[3] = {cx - ctr[s * 3], cy - ctr[s * 3 + 1], cz - ctr[s * 3 + 2]};
+            const double r[3] = {cx - cs[s * 3], cy - cs[s * 3 + 1], cz - cs[s * 3 + 2]};
             const double inv_r2 = 1.0 / (r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
             if (lane == 0) D[0] = sqrt(inv_r2);
             __syncwarp();
@@ -207,19 +209,20 @@ __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *
 using namespace fmm;
 
 extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src,
-                           const double *ctr, const double *M, double *L, void *stream) {
+                           const double *ctr, const double *ctr_src, const double *M, double *L, void *stream) {
+    if (!ctr_src) ctr_src = ctr;  // one tree
     if (p < 1 || p > TMAX) { set_error("expansion order %d outside supported range 1..%d", p, TMAX); return FMM_ERR_INVALID; }
     cudaStream_t s = as_stream(stream);
     const int grid = grid_for((int64_t)ncells * 32, 128, 148 * 16);
     switch (p) {
-        case 1: m2l_reg<1><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
-        case 2: m2l_reg<2><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
-        case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
-        case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
-        case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, M, L); fmm::note_launch(); break;
+        case 1: m2l_reg<1><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        case 2: m2l_reg<2><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
 #define M2L_LANES(PP)                                                                                 \
     case PP:                                                                                          \
-        m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), 128, 0, s>>>(ncells, rows, src, ctr, M, L);      \
+        m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); \
         fmm::note_launch();                                                                           \
         break;
         M2L_LANES(6)

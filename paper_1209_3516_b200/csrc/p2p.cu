@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
     int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const float4 *__restrict__ b, const float4 *__restrict__ blo, double *phi, double *fx, double *fy,
-    double *fz, int *flag) {
+    double *fz, int *flag, int cross) {
     constexpr bool kStream = !SAFE && !ANCHOR;
     // the tile ring (streamed rows) and the lane rings (run-by-run rows) share
     // one pool: a row uses one or the other
@@ -553,7 +553,8 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
             // block tb's line: cnt self sources + total stream sources, weight
             // 2 per source (K8) or 1 (the K4 last block); warp w takes the
             // w-th quarter of the concatenated weighted lines
-            const int64_t L = (int64_t)cnt + stotal;
+            const int32_t scnt = cross ? 0 : cnt;  // cross-tree rows have no self leaf
+            const int64_t L = (int64_t)scnt + stotal;
             const int64_t Wl = L * (2 * nblk - (small_last ? 1 : 0));
             const int64_t A = Wl * w / kP2PWarps, B = Wl * (w + 1) / kP2PWarps;
             for (int tb = (int)(A / (2 * L)); tb < nblk && 2 * L * tb < B; tb++) {
@@ -564,9 +565,9 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
                 if (s1 <= s0) continue;
                 const int32_t i0 = ts + tb * 8;
                 const float val =
-                    k4 ? p2p_f32_stream_unit<4>(i0, ts + cnt - 1, ts, cnt, s0, s1, lane, b, wring, wbars[w], phase,
+                    k4 ? p2p_f32_stream_unit<4>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w], phase,
                                                 srun)
-                       : p2p_f32_stream_unit<8>(i0, ts + cnt - 1, ts, cnt, s0, s1, lane, b, wring, wbars[w], phase,
+                       : p2p_f32_stream_unit<8>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w], phase,
                                                 srun);
                 emit(tb * kP2PWarps + w, tb, i0, k4, val);
             }
@@ -712,11 +713,40 @@ __global__ void __launch_bounds__(kP2PWarps * 32) p2p_f64_kernel(
     }
 }
 
+// Coincident (target, source) pairs of a cross-tree plan: r2 == 0.0 in
+// float64 -- the reference skips and counts them (src/traversal.py:552-597).
+// A block per row, threads over the row's (target, source) pairs.
+__global__ void p2p_coincident_kernel(int32_t nrows_host, const int32_t *__restrict__ nrows_dev,
+                                      const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
+                                      const int32_t *__restrict__ end, const int64_t *__restrict__ run_off,
+                                      const int4 *__restrict__ runs, const double *__restrict__ xs,
+                                      const double *__restrict__ ys, const double *__restrict__ zs,
+                                      unsigned long long *count) {
+    const int32_t nrows = nrows_dev ? *nrows_dev : nrows_host;
+    unsigned long long local = 0;
+    for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const int32_t t = leaf_rows[row];
+        const int32_t ts = start[t], cnt = end[t] - ts;
+        for (int64_t r = run_off[row]; r < run_off[row + 1]; r++) {
+            const int4 run = runs[r];
+            const int64_t len = run.y - run.x, tot = len * cnt;
+            for (int64_t k = threadIdx.x; k < tot; k += blockDim.x) {
+                const int32_t i = ts + (int32_t)(k / len), j = run.x + (int32_t)(k % len);
+                const double dx = __dsub_rn(xs[i], xs[j]), dy = __dsub_rn(ys[i], ys[j]), dz = __dsub_rn(zs[i], zs[j]);
+                const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                local += r2 == 0.0;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
 }  // namespace fmm
 
 using namespace fmm;
 
-extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, const int32_t *dev_nrows,
+extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_t nrows, const int32_t *dev_nrows,
                        const int32_t *leaf_rows,
                        const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
                        const double *xs, const double *ys, const double *zs, const double *qs,
@@ -736,7 +766,7 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, co
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pool);
         kern<<<grid, kP2PWarps * 32, pool, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
                                              (const float4 *)b32, (const float4 *)b32lo, phi, fx, fy, fz,
-                                             dev_flag); fmm::note_launch();
+                                             dev_flag, cross); fmm::note_launch();
     } else if (precision == FMM_PREC_FP64) {
         p2p_f64_kernel<4><<<grid, kP2PWarps * 32, 0, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off,
                                                           (const int4 *)runs, xs, ys, zs, qs, use_rsqrt, phi,
@@ -746,5 +776,16 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int32_t nrows, co
         return FMM_ERR_INVALID;
     }
     FMM_CUDA_CHECK("fmm_p2p");
+    return FMM_OK;
+}
+
+extern "C" int fmm_p2p_coincident(int32_t nrows, const int32_t *dev_nrows, const int32_t *leaf_rows,
+                                  const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
+                                  const double *xs, const double *ys, const double *zs, unsigned long long *count,
+                                  void *stream) {
+    if (nrows <= 0) return FMM_OK;
+    p2p_coincident_kernel<<<grid_for(nrows, 1, 148 * 8), 256, 0, as_stream(stream)>>>(
+        nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs, xs, ys, zs, count); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_p2p_coincident");
     return FMM_OK;
 }

@@ -18,11 +18,14 @@
 
 namespace fmm {
 
+// Source leaves of a target row merge into one body run when adjacent; in
+// a one-tree evaluation the target's own leaf always stands alone (self).
+// cross: sources belong to another tree (no self leaf).
 __device__ inline bool run_start(const int32_t *src, int64_t k, int64_t k0, int32_t t,
-                                 const int32_t *start, const int32_t *end) {
+                                 const int32_t *sstart, const int32_t *send, int cross) {
     if (k == k0) return true;
     int32_t s = src[k], sp = src[k - 1];
-    return s == t || sp == t || start[s] != end[sp];
+    return (!cross && (s == t || sp == t)) || sstart[s] != send[sp];
 }
 
 // Runs per row (nr) and the reference's pair counters in one pass over the
@@ -34,6 +37,7 @@ __device__ inline bool run_start(const int32_t *src, int64_t k, int64_t k0, int3
 __global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells, const int32_t *__restrict__ leaf_rows,
                            const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
                            const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                           const int32_t *__restrict__ sstart, const int32_t *__restrict__ send, int cross,
                            const double *__restrict__ xs, const double *__restrict__ ys,
                            const double *__restrict__ zs, const uint64_t *__restrict__ keys, int64_t *nr,
                            unsigned long long *stats) {
@@ -56,12 +60,12 @@ __global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells
         for (int64_t kb = k0; kb < k1; kb += 32) {
             const int64_t k = kb + lane;
             const bool valid = k < k1;
-            const bool f = valid && run_start(src, k, k0, t, start, end);
+            const bool f = valid && run_start(src, k, k0, t, sstart, send, cross);
             cnt += __popc(__ballot_sync(0xffffffffu, f));
             if (valid) {
                 const int32_t s = src[k];
-                blocks += (unsigned long long)(nt * (end[s] - start[s]));
-                if (s == t) {
+                blocks += (unsigned long long)(nt * (send[s] - sstart[s]));
+                if (!cross && s == t) {
                     blocks -= (unsigned long long)nt;
                     self = true;
                 }
@@ -99,8 +103,8 @@ __global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells
 
 __global__ void plan_write(const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
                            const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
-                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-                           const int64_t *__restrict__ run_off, int4 *runs) {
+                           const int32_t *__restrict__ sstart, const int32_t *__restrict__ send, int cross,
+                           int32_t soff, const int64_t *__restrict__ run_off, int4 *runs) {
     const int lane = threadIdx.x & 31;
     const int32_t nrows = *nrows_dev;
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
@@ -111,17 +115,17 @@ __global__ void plan_write(const int32_t *__restrict__ nrows_dev, const int32_t 
         for (int64_t kb = k0; kb < k1; kb += 32) {
             int64_t k = kb + lane;
             bool valid = k < k1;
-            bool f = valid && run_start(src, k, k0, t, start, end);
-            bool last = valid && (k + 1 == k1 || run_start(src, k + 1, k0, t, start, end));
+            bool f = valid && run_start(src, k, k0, t, sstart, send, cross);
+            bool last = valid && (k + 1 == k1 || run_start(src, k + 1, k0, t, sstart, send, cross));
             unsigned m = __ballot_sync(0xffffffffu, f);
             int64_t idx = base + __popc(m & ((2u << lane) - 1u));
             if (f) {
                 int32_t s = src[k];
-                runs[idx].x = start[s];
-                runs[idx].z = (s == t) ? 1 : 0;
+                runs[idx].x = sstart[s] + soff;
+                runs[idx].z = (!cross && s == t) ? 1 : 0;
                 runs[idx].w = 0;
             }
-            if (last) runs[idx].y = end[src[k]];
+            if (last) runs[idx].y = send[src[k]] + soff;
             base += __popc(m);
         }
     }
@@ -141,8 +145,8 @@ using namespace fmm;
 extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
                             int32_t body_lo, int32_t body_hi,
                             const int64_t *rows, const int32_t *src_sorted, const double *xs,
-                            const double *ys, const double *zs, const uint64_t *keys, int32_t *leaf_rows,
-                            int64_t *run_off,
+                            const double *ys, const double *zs, const uint64_t *keys, const int32_t *src_start,
+                            const int32_t *src_end, int32_t src_offset, int32_t *leaf_rows, int64_t *run_off,
                             void *runs, int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows,
                             int32_t *dev_nrows, unsigned long long *dev_stats, void *ws, size_t ws_bytes,
                             void *stream) {
@@ -161,8 +165,10 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     // leaf_rows is sized ncells: the kernels read the row count on the device
     const int g = grid_for((int64_t)ncells * 32, 256, 148 * 16);
     if (dev_stats) cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
-    plan_count<<<g, 256, 0, s>>>(nsel, ncells, leaf_rows, rows, src_sorted, start, end, xs, ys, zs, keys, nr,
-                                 dev_stats); fmm::note_launch();
+    const int cross = src_start != nullptr;
+    const int32_t *ss = cross ? src_start : start, *se = cross ? src_end : end;
+    plan_count<<<g, 256, 0, s>>>(nsel, ncells, leaf_rows, rows, src_sorted, start, end, ss, se, cross, xs, ys, zs,
+                                 keys, nr, dev_stats); fmm::note_launch();
     need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, ncells + 1, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
@@ -178,7 +184,8 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
         if (total > cap_runs) { set_error("run capacity %lld < %lld", (long long)cap_runs, (long long)total); return FMM_ERR_CAPACITY; }
     }
     if (dev_nrows) cudaMemcpyAsync(dev_nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
-    plan_write<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, start, end, run_off, (int4 *)runs); fmm::note_launch();
+    plan_write<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, ss, se, cross, cross ? src_offset : 0, run_off,
+                                 (int4 *)runs); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_p2p_plan");
     return FMM_OK;
 }

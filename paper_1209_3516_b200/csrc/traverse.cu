@@ -39,25 +39,31 @@ __device__ inline unsigned long long warp_reserve(unsigned long long *counter, i
 
 // Fate of a pair (src/traversal.py:185-211): 1 = P2P (both leaves, tested
 // before the MAC), 2 = M2L (MAC accepted), 3 = split.
-// _mac_ok (src/traversal.py:144-156) for target a, source b: 0 = bh,
-// 1 = bmax, 2 = fmm; r2 == 0 rejects.
-__device__ __forceinline__ bool mac_accept(int32_t a, int32_t b, const double *__restrict__ ctr,
-                                           const double *__restrict__ bmax, const double *__restrict__ rmax,
-                                           int kind_mac, double th2) {
-    const double dx = ctr[a * 3] - ctr[b * 3];
-    const double dy = ctr[a * 3 + 1] - ctr[b * 3 + 1];
-    const double dz = ctr[a * 3 + 2] - ctr[b * 3 + 2];
+// One tree's cell arrays as the traversals read them: the target tree A
+// and the source tree B are the same arrays for a one-tree evaluation.
+struct Cells {
+    const int32_t *children;
+    const uint8_t *leaf;
+    const double *ctr, *bmax, *rmax;
+};
+
+// _mac_ok (src/traversal.py:144-156) for target a of A, source b of B:
+// 0 = bh, 1 = bmax, 2 = fmm; r2 == 0 rejects.
+__device__ __forceinline__ bool mac_accept(int32_t a, int32_t b, const Cells &A, const Cells &B, int kind_mac,
+                                           double th2) {
+    const double dx = A.ctr[a * 3] - B.ctr[b * 3];
+    const double dy = A.ctr[a * 3 + 1] - B.ctr[b * 3 + 1];
+    const double dz = A.ctr[a * 3 + 2] - B.ctr[b * 3 + 2];
     const double r2 = dx * dx + dy * dy + dz * dz;
     if (r2 == 0.0) return false;
-    const double s = kind_mac == 2 ? bmax[a] + bmax[b] : (kind_mac == 1 ? bmax[b] : 2.0 * rmax[b]);
+    const double s = kind_mac == 2 ? A.bmax[a] + B.bmax[b] : (kind_mac == 1 ? B.bmax[b] : 2.0 * B.rmax[b]);
     return s * s < th2 * r2;
 }
 
-__device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const uint8_t *__restrict__ leaf,
-                                         const double *__restrict__ ctr, const double *__restrict__ bmax,
-                                         const double *__restrict__ rmax, int kind_mac, double th2) {
-    if (leaf[a] && leaf[b]) return 1;
-    return mac_accept(a, b, ctr, bmax, rmax, kind_mac, th2) ? 2 : 3;
+__device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const Cells &A, const Cells &B, int kind_mac,
+                                         double th2) {
+    if (A.leaf[a] && B.leaf[b]) return 1;
+    return mac_accept(a, b, A, B, kind_mac, th2) ? 2 : 3;
 }
 
 // One breadth-first step.  Every frontier pair is a pair already known to
@@ -67,9 +73,7 @@ __device__ __forceinline__ int pair_fate(int32_t a, int32_t b, const uint8_t *__
 // which the host launches with `classify_self = 1`).
 __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
                                      int64_t nfront_host, const unsigned long long *__restrict__ nfront_dev,
-                                     int64_t cap_front, int classify_self, const int32_t *__restrict__ children,
-                                     const uint8_t *__restrict__ leaf, const double *__restrict__ ctr,
-                                     const double *__restrict__ bmax, const double *__restrict__ rmax,
+                                     int64_t cap_front, int classify_self, Cells A, Cells B,
                                      const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
                                      int32_t blo, int32_t bhi, int m2l_owner, int kind_mac, double th2,
                                      int32_t *p2p_t,
@@ -98,12 +102,12 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                 cb[0] = b;
                 n = 1;
             } else {
-                const bool la = leaf[a], lb = leaf[b];
-                const bool open_a = la ? false : (lb ? true : (rmax[a] >= rmax[b]));
-                const int32_t who = open_a ? a : b;
+                const bool la = A.leaf[a], lb = B.leaf[b];
+                const bool open_a = la ? false : (lb ? true : (A.rmax[a] >= B.rmax[b]));
+                const int32_t *kids = open_a ? A.children + a * 8 : B.children + b * 8;
 #pragma unroll
                 for (int o = 0; o < 8; o++) {
-                    const int32_t ch = children[who * 8 + o];
+                    const int32_t ch = kids[o];
                     if (ch >= 0) {
                         ca[n] = open_a ? ch : a;
                         cb[n] = open_a ? b : ch;
@@ -119,7 +123,7 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
             if (q < n) {
                 // multi-GPU: only targets whose body range meets [blo, bhi)
                 if (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi) continue;
-                fate[q] = pair_fate(ca[q], cb[q], leaf, ctr, bmax, rmax, kind_mac, th2);
+                fate[q] = pair_fate(ca[q], cb[q], A, B, kind_mac, th2);
                 // chunked single-GPU runs: an M2L pair belongs to the chunk
                 // holding its target's first body (no pair is emitted twice)
                 if (fate[q] == 2 && m2l_owner && (cstart[ca[q]] < blo || cstart[ca[q]] >= bhi)) fate[q] = 0;
@@ -168,10 +172,8 @@ __global__ void treecode_seed_flags(int32_t ncells, const uint8_t *__restrict__ 
 }
 
 __global__ void treecode_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
-                                     const unsigned long long *__restrict__ nfront_dev, int64_t cap_front,
-                                     const int32_t *__restrict__ children, const uint8_t *__restrict__ leaf,
-                                     const double *__restrict__ ctr, const double *__restrict__ bmax,
-                                     const double *__restrict__ rmax, int kind_mac, double th2,
+                                     const unsigned long long *__restrict__ nfront_dev, int64_t cap_front, Cells A,
+                                     Cells B, int kind_mac, double th2,
                                      int32_t *m2p_t, int32_t *m2p_s, int64_t cap_m2p, int32_t *p2p_t,
                                      int32_t *p2p_s, int64_t cap_p2p, int32_t *na, int32_t *nb, int64_t cap_next,
                                      unsigned long long *cnt_p2p, unsigned long long *cnt_m2p,
@@ -189,12 +191,12 @@ __global__ void treecode_step_kernel(const int32_t *__restrict__ fa, const int32
         if (k < nfront) {
             t = fa[k];
             c = fb[k];
-            if (mac_accept(t, c, ctr, bmax, rmax, kind_mac, th2)) fate = 2;
-            else if (leaf[c]) fate = 1;
+            if (mac_accept(t, c, A, B, kind_mac, th2)) fate = 2;
+            else if (B.leaf[c]) fate = 1;
             else {
                 fate = 3;
 #pragma unroll
-                for (int o = 0; o < 8; o++) nch += children[c * 8 + o] >= 0;
+                for (int o = 0; o < 8; o++) nch += B.children[c * 8 + o] >= 0;
             }
         }
         int op, om, on;
@@ -211,7 +213,7 @@ __global__ void treecode_step_kernel(const int32_t *__restrict__ fa, const int32
             unsigned long long in = bn + on;
 #pragma unroll
             for (int o = 0; o < 8; o++) {
-                const int32_t ch = children[c * 8 + o];
+                const int32_t ch = B.children[c * 8 + o];
                 if (ch >= 0) {
                     if (in < (unsigned long long)cap_next) { na[in] = t; nb[in] = ch; }
                     in++;
@@ -447,19 +449,33 @@ __global__ void fill_i64(int64_t *a, int64_t n, int64_t v) {
 
 using namespace fmm;
 
+// The source tree's arrays default to the target tree's (one-tree evaluation).
+static Cells cells_of(const int32_t *children, const uint8_t *leaf, const double *ctr, const double *bmax,
+                      const double *rmax) {
+    return Cells{children, leaf, ctr, bmax, rmax};
+}
+static Cells source_cells(const Cells &A, const int32_t *children_b, const uint8_t *leaf_b, const double *ctr_b,
+                          const double *bmax_b, const double *rmax_b) {
+    return children_b ? Cells{children_b, leaf_b, ctr_b, bmax_b, rmax_b} : A;
+}
+
 extern "C" {
 
 int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int classify_self,
                       const int32_t *children,
                       const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                      const int32_t *children_b, const uint8_t *leaf_b, const double *ctr_b, const double *bmax_b,
+                      const double *rmax_b,
                       const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi,
                       int m2l_owner_only, int kind, double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
                       int32_t *m2l_t,
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
                       unsigned long long *dev_counts, void *stream) {
     if (nfront <= 0) return FMM_OK;
+    const Cells A = cells_of(children, leaf, ctr, bmax, rmax);
+    const Cells B = source_cells(A, children_b, leaf_b, ctr_b, bmax_b, rmax_b);
     traverse_step_kernel<<<grid_for(nfront, 256, 148 * 16), 256, 0, as_stream(stream)>>>(
-        fa, fb, nfront, nullptr, nfront, classify_self, children, leaf, ctr, bmax, rmax, start, end, body_lo,
+        fa, fb, nfront, nullptr, nfront, classify_self, A, B, start, end, body_lo,
         body_hi, m2l_owner_only, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
         na, nb, cap_next, dev_counts, dev_counts + 1, dev_counts + 2); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_traverse_step");
@@ -468,11 +484,14 @@ int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int 
 
 int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1, int64_t cap_front,
                  int nsteps, const int32_t *children, const uint8_t *leaf, const double *ctr,
-                 const double *bmax, const double *rmax, const int32_t *start, const int32_t *end,
+                 const double *bmax, const double *rmax, const int32_t *children_b, const uint8_t *leaf_b,
+                 const double *ctr_b, const double *bmax_b, const double *rmax_b, const int32_t *start, const int32_t *end,
                  int32_t body_lo, int32_t body_hi, int m2l_owner_only, int kind, double th2, int32_t *p2p_t,
                  int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
                  unsigned long long *dev_log, void *stream) {
     cudaStream_t st = as_stream(stream);
+    const Cells A = cells_of(children, leaf, ctr, bmax, rmax);
+    const Cells B = source_cells(A, children_b, leaf_b, ctr_b, bmax_b, rmax_b);
     // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s
     cudaMemsetAsync(dev_log, 0, sizeof(unsigned long long) * (nsteps + 3), st);
     const unsigned long long one = 1;
@@ -485,7 +504,7 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
         const bool even = (sidx & 1) == 0;
         traverse_step_kernel<<<grid, 256, 0, st>>>(
             even ? front_a0 : front_a1, even ? front_b0 : front_b1, 0, dev_log + 2 + sidx, cap_front, sidx == 0,
-            children, leaf, ctr, bmax, rmax, start, end, body_lo, body_hi, m2l_owner_only, kind, th2, p2p_t,
+            A, B, start, end, body_lo, body_hi, m2l_owner_only, kind, th2, p2p_t,
             p2p_s, cap_p2p,
             m2l_t, m2l_s, cap_m2l, even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front,
             dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
@@ -497,11 +516,15 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
 int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
                           int64_t cap_front, int nsteps, int32_t ncells, const int32_t *children,
                           const uint8_t *leaf, const double *ctr, const double *bmax, const double *rmax,
+                          const int32_t *children_b, const uint8_t *leaf_b, const double *ctr_b,
+                          const double *bmax_b, const double *rmax_b,
                           const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
                           double th2, int32_t *m2p_t, int32_t *m2p_s, int64_t cap_m2p, int32_t *p2p_t,
                           int32_t *p2p_s, int64_t cap_p2p, unsigned long long *dev_log, void *ws,
                           size_t ws_bytes, void *stream) {
     cudaStream_t st = as_stream(stream);
+    const Cells A = cells_of(children, leaf, ctr, bmax, rmax);
+    const Cells B = source_cells(A, children_b, leaf_b, ctr_b, bmax_b, rmax_b);
     if (cap_front < ncells) {
         set_error("treecode frontier capacity %lld < ncells %d", (long long)cap_front, ncells);
         return FMM_ERR_INVALID;
@@ -522,8 +545,8 @@ int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a
     for (int sidx = 0; sidx < nsteps; sidx++) {
         const bool even = (sidx & 1) == 0;
         treecode_step_kernel<<<grid, 256, 0, st>>>(
-            even ? front_a0 : front_a1, even ? front_b0 : front_b1, dev_log + 2 + sidx, cap_front, children, leaf,
-            ctr, bmax, rmax, kind, th2, m2p_t, m2p_s, cap_m2p, p2p_t, p2p_s, cap_p2p, even ? front_a1 : front_a0,
+            even ? front_a0 : front_a1, even ? front_b0 : front_b1, dev_log + 2 + sidx, cap_front, A, B,
+            kind, th2, m2p_t, m2p_s, cap_m2p, p2p_t, p2p_s, cap_p2p, even ? front_a1 : front_a0,
             even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_treecode_traverse");

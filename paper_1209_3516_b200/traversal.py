@@ -26,8 +26,12 @@ reuses the P2P plan and kernel for the near field.
 and reuses the M2L, P2P and downward executors.
 
 Scope: all three strategies (``dualtree`` directed, ``treecode``,
-``listfmm``) on one shared tree.  ``mutual=True`` and ``source_tree`` are
-outside the B200 hot path and raise NotImplementedError.
+``listfmm``) on one shared tree, and ``dualtree`` / ``treecode`` with a
+separate ``source_tree``: the source bodies are appended
+after the targets in one set of P2P body arrays, the traversals read the two
+trees' cell arrays, M2L/M2P read the source tree's multipoles and the P2P
+plan's runs point past the targets.  ``mutual=True`` on one tree is outside
+the B200 hot path and raises NotImplementedError.
 ``precision`` is a new knob: "fp64" (default, the reference's arithmetic)
 or "fp32" (FP32 near field; far field stays float64).
 """
@@ -147,23 +151,29 @@ _hint = {}
 
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
                       m2l_ready: torch.cuda.Event | None = None,
-                      side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False) -> Lists:
+                      side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False,
+                      src: Tree | None = None) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
     ``body_range=(lo, hi)`` keeps only pairs whose target cell holds bodies
-    in [lo, hi) (a multi-GPU rank's share); the default keeps all."""
+    in [lo, hi) (a multi-GPU rank's share); the default keeps all.
+    ``src`` is a separate source tree (cross-tree lists: sources index its
+    cells, the P2P plan points at its bodies appended after the targets)."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev = tree.device
     P = _lib.ptr
     st = _lib.stream_handle()
     i32 = torch.int32
     th2 = mac.theta * mac.theta
-    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, m2l_owner_only)
+    cross = src is not None and src is not tree
+    sb = src if cross else tree
+    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, m2l_owner_only, sb.ncells if cross else 0)
     cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
                                                  max(4096, tree.ncells * 8)))
-    # every step opens one side of a pair: at most 2 * depth + 1 steps
-    nsteps = 2 * tree.depth + 2
+    # every step opens one side of a pair: at most depth_A + depth_B + 1 steps
+    nsteps = tree.depth + sb.depth + 2
+    bcells = _source_cells(tree, src)
     log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
     while True:
         p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
@@ -172,8 +182,8 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         m2l_s = torch.empty(cap_m2l, dtype=i32, device=dev)
         fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
         _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
-                  P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(tree.d_start), P(tree.d_end),
-                  blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
+                  P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), *bcells, P(tree.d_start),
+                  P(tree.d_end), blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
                   cap_m2l, P(log), st)
         hl = log.tolist()  # the one synchronisation of the traversal
         done_p2p, done_m2l, fronts = hl[0], hl[1], hl[2:]
@@ -187,14 +197,24 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         cap_next = max(cap_next, int(peak * 1.05) + 4096)
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
-    ncells = tree.ncells
+    # the CSR key packs (target, source) ids: size it for the larger tree
+    ncells = max(tree.ncells, sb.ncells)
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
     m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
     p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
     del p2p_t, p2p_s, m2l_t, m2l_s
     return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
                  p2p_rows=p2p_rows, peak_frontier=peak,
-                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
+
+
+def _source_cells(tree: Tree, src: Tree | None) -> tuple:
+    """The source tree's cell arrays for the traversal ABI (NULLs: the
+    target tree is its own source)."""
+    if src is None or src is tree:
+        return (None,) * 5
+    P = _lib.ptr
+    return P(src.d_children), P(src.d_leaf), P(src.d_ctr), P(src.d_bmax), P(src.d_rmax)
 
 
 def _csr(t, s, n, ncells, dev, wsp, wsb, stream):
@@ -227,9 +247,12 @@ def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready):
     return out
 
 
-def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st) -> dict:
+def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st,
+              src: Tree | None = None) -> dict:
     """P2P run plan + the reference's pair counters (no host round trip:
-    runs <= pairs, and the row count stays on the device)."""
+    runs <= pairs, and the row count stays on the device).  With a separate
+    source tree the runs address its bodies at offset ``tree.n`` of the
+    concatenated body arrays (``CrossBodies``)."""
     dev, P, i32, ncells = tree.device, _lib.ptr, torch.int32, tree.ncells
     leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
     run_off = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
@@ -237,51 +260,91 @@ def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
     dev_nrows = torch.empty(1, dtype=i32, device=dev)
     cap_runs = max(n_p2p, 1)
     runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
+    cross = src is not None and src is not tree
+    sstart, send = (P(src.d_start), P(src.d_end)) if cross else (None, None)
     _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
-              P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), P(leaf_rows), P(run_off), P(runs),
-              cap_runs,
+              P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), sstart, send,
+              tree.n if cross else 0, P(leaf_rows), P(run_off), P(runs), cap_runs,
               None, None, P(dev_nrows), P(dev_stats), wsp, wsb, st)
     return dict(leaf_rows=leaf_rows, nrows=tree.nleaves, dev_nrows=dev_nrows, run_off=run_off, runs=runs,
                 dev_stats=dev_stats)
 
 
-def run_m2l(tree: Tree, lists: Lists, p: int) -> None:
+def run_m2l(tree: Tree, lists: Lists, p: int, src: Tree | None = None) -> None:
+    """M2L over the target CSR into ``tree``'s locals; the multipoles and
+    centres are ``src``'s when it is a separate source tree
+    (src/traversal.py:500-517 with ``MA``/``ctrB`` of the source)."""
     P = _lib.ptr
-    _lib.call("fmm_m2l_csr", p, tree.ncells, P(lists.m2l_rows), P(lists.m2l_src), P(tree.d_ctr), P(tree._M),
-              P(tree._L), _lib.stream_handle())
+    cross = src is not None and src is not tree
+    _lib.call("fmm_m2l_csr", p, tree.ncells, P(lists.m2l_rows), P(lists.m2l_src), P(tree.d_ctr),
+              P(src.d_ctr) if cross else None, P(src._M if cross else tree._M), P(tree._L), _lib.stream_handle())
+
+
+class CrossBodies:
+    """P2P body arrays of a cross-tree evaluation: the target tree's bodies
+    followed by the source tree's, so one plan's runs address both
+    (``_p2p_plan`` shifts source runs by ``tree.n``).  Results land in the
+    target tree's accumulators."""
+
+    def __init__(self, tree: Tree, src: Tree):
+        cat = lambda a, b: torch.cat((a, b))  # noqa: E731
+        self.d_x, self.d_y, self.d_z, self.d_q = (cat(getattr(tree, k), getattr(src, k))
+                                                  for k in ("d_x", "d_y", "d_z", "d_q"))
+        self.d_b32 = cat(tree.d_b32, src.d_b32)
+        self.d_b32lo = cat(tree.d_b32lo, src.d_b32lo)
+        self.fp32_exact = tree.fp32_exact and src.fp32_exact
 
 
 def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, safe: bool = False,
-            flag=None) -> None:
+            flag=None, bodies: CrossBodies | None = None) -> None:
+    """P2P over the plan into ``tree``'s accumulators; ``bodies`` holds the
+    concatenated body arrays of a cross-tree plan (the target leaf then
+    sweeps only the source runs)."""
     P = _lib.ptr
+    b = tree if bodies is None else bodies
     if precision == "fp32":
         # float32 cannot hold these float64 inputs: anchor offsets per row
-        prec = _lib.PREC_FP32 if tree.fp32_exact else _lib.PREC_FP32_ANCHORED
+        prec = _lib.PREC_FP32 if b.fp32_exact else _lib.PREC_FP32_ANCHORED
     else:
         prec = _lib.PREC_FP64
-    _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), lists.nrows, P(lists.dev_nrows), P(lists.leaf_rows),
-              P(tree.d_start),
-              P(tree.d_end), P(lists.run_off), P(lists.runs), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_q),
-              P(tree.d_b32), P(tree.d_b32lo), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag),
+    _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), int(bodies is not None), lists.nrows,
+              P(lists.dev_nrows), P(lists.leaf_rows), P(tree.d_start), P(tree.d_end), P(lists.run_off),
+              P(lists.runs), P(b.d_x), P(b.d_y), P(b.d_z), P(b.d_q), P(b.d_b32), P(b.d_b32lo), P(tree.d_phi),
+              P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag), _lib.stream_handle())
+
+
+def count_coincident(tree: Tree, lists: Lists, bodies: CrossBodies) -> torch.Tensor:
+    """Device count of the cross-tree P2P pairs at distance 0.0 (float64),
+    which the reference skips and counts as ``p2p_skipped``
+    (src/traversal.py:552-597)."""
+    P = _lib.ptr
+    n = torch.zeros(1, dtype=torch.int64, device=tree.device)
+    _lib.call("fmm_p2p_coincident", lists.nrows, P(lists.dev_nrows), P(lists.leaf_rows), P(tree.d_start),
+              P(tree.d_end), P(lists.run_off), P(lists.runs), P(bodies.d_x), P(bodies.d_y), P(bodies.d_z), P(n),
               _lib.stream_handle())
+    return n
 
 
 def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
-                   m2p_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None) -> Lists:
+                   m2p_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
+                   src: Tree | None = None) -> Lists:
     """Treecode walk (src/traversal.py:265-313) of every target leaf against
     the source tree -> target-sorted CSR M2P and P2P lists (bit-exact sets
     with the reference's ``_collect_treecode``) + the P2P run plan.
 
     ``body_range=(lo, hi)`` keeps the target leaves whose bodies meet
-    [lo, hi) (a multi-GPU rank's share)."""
+    [lo, hi) (a multi-GPU rank's share); ``src`` is a separate source tree."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
     th2 = mac.theta * mac.theta
     ncells = tree.ncells
-    key = ("treecode", ncells, tree.nleaves, mac.kind, th2, blo, bhi)
+    cross = src is not None and src is not tree
+    sb = src if cross else tree
+    key = ("treecode", ncells, tree.nleaves, mac.kind, th2, blo, bhi, sb.ncells if cross else 0)
     cap_p2p, cap_m2p, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.nleaves * 256),
                                                  max(4096, ncells * 8)))
-    nsteps = tree.depth + 2  # one source level per step
+    nsteps = sb.depth + 2  # one source level per step
+    bcells = _source_cells(tree, src)
     log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
     wsp, wsb = _lib.workspace(max(ncells, tree.n), dev)
     while True:
@@ -292,7 +355,7 @@ def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | Non
         p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
         p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
         _lib.call("fmm_treecode_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_front, nsteps, ncells,
-                  P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax),
+                  P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), *bcells,
                   P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(m2p_t), P(m2p_s), cap_m2p, P(p2p_t),
                   P(p2p_s), cap_p2p, P(log), wsp, wsb, st)
         hl = log.tolist()  # the one synchronisation of the walk
@@ -308,12 +371,13 @@ def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | Non
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2p * 1.02) + 4096, int(peak * 1.05) + 4096)
     wsp, wsb = _lib.workspace(max(done_m2p, done_p2p, tree.n), dev)
-    m2p_src, m2p_rows = _far_csr(m2p_t, m2p_s, done_m2p, ncells, dev, wsp, wsb, st, side, m2p_ready)
-    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    kcells = max(ncells, sb.ncells)  # the CSR key packs ids of both trees
+    m2p_src, m2p_rows = _far_csr(m2p_t, m2p_s, done_m2p, kcells, dev, wsp, wsb, st, side, m2p_ready)
+    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, kcells, dev, wsp, wsb, st)
     del p2p_t, p2p_s, m2p_t, m2p_s
     return Lists(n_m2l=0, n_m2p=done_m2p, n_p2p=done_p2p, m2p_src=m2p_src, m2p_rows=m2p_rows, p2p_src=p2p_src,
                  p2p_rows=p2p_rows, peak_frontier=peak,
-                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
 
 
 def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
@@ -354,11 +418,13 @@ def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
                  **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
-def run_m2p(tree: Tree, lists: Lists, p: int, out) -> None:
-    """Treecode far field into ``out`` = (phi, fx, fy, fz) (accumulated)."""
+def run_m2p(tree: Tree, lists: Lists, p: int, out, src: Tree | None = None) -> None:
+    """Treecode far field into ``out`` = (phi, fx, fy, fz) (accumulated);
+    the accepted cells (centres, multipoles) are ``src``'s when given."""
     P = _lib.ptr
+    sb = tree if src is None else src
     _lib.call("fmm_m2p_csr", p, tree.ncells, P(lists.m2p_rows), P(lists.m2p_src), P(tree.d_start),
-              P(tree.d_end), P(tree.d_ctr), P(tree._M), P(tree.d_x), P(tree.d_y), P(tree.d_z), *(P(a) for a in out),
+              P(tree.d_end), P(sb.d_ctr), P(sb._M), P(tree.d_x), P(tree.d_y), P(tree.d_z), *(P(a) for a in out),
               _lib.stream_handle())
 
 
@@ -429,13 +495,22 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     chunks partition both lists exactly.  A side stream runs the far field:
     the upward pass as soon as the tree exists, each chunk's M2L as soon as
     its M2L list is sorted, then the downward pass, into separate
-    accumulators that one combine kernel adds at the end."""
-    if source_tree is not None and source_tree is not tree:
-        raise NotImplementedError("separate source trees are outside the B200 hot path")
+    accumulators that one combine kernel adds at the end.
+
+    With a separate ``source_tree`` (src/traversal.py:864-932) the upward
+    pass runs on the source tree, the traversal pairs target cells with
+    source cells, and P2P sweeps the source bodies (``CrossBodies``);
+    coincident target/source bodies are skipped and counted as the
+    reference does."""
+    src = tree if source_tree is None else source_tree
+    cross = src is not tree
+    if cfg.mutual and cross:
+        raise ValueError("mutual traversal needs target and source to share one tree")
     if cfg.mutual:
         raise NotImplementedError("mutual traversal is outside the B200 hot path")
     if threads < 1:
         raise ValueError(f"threads must be >= 1, got {threads}")
+    _same_device(tree, src)
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
@@ -445,22 +520,24 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         pst = _side_stream(dev, 1)
         E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
         e0, e_up0, e_up1, e_down0, e_down1, e_l1, e_pend, e_end = (E() for _ in range(8))
-        need_up = tree._M is None or tree.p != p
+        need_up = src._M is None or src.p != p
         nc = ncoef(p)
         # every buffer the other streams touch is allocated here, on main
-        M = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev) if need_up else tree._M
+        M = torch.zeros((src.ncells, nc), dtype=torch.float64, device=dev) if need_up else src._M
         L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
         far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        bodies = CrossBodies(tree, src) if cross else None
         e0.record(main)
         side.wait_event(e0)
         pst.wait_event(e0)
         with torch.cuda.stream(side):
             e_up0.record(side)
             if need_up:
-                upward_pass(tree, p, stats, sync=False, M=M)  # (resets tree._L)
+                upward_pass(src, p, stats, sync=False, M=M)  # (resets src._L)
             e_up1.record(side)
-        tree._M, tree.p, tree._L = M, p, L
+        src._M, src.p = M, p
+        _attach_locals(tree, p, L)
         cuts = _chunk_cuts(tree, _nchunks(tree))
         nch = len(cuts) - 1
         # chunked runs build lists on a high-priority stream (they gate P2P); with
@@ -474,12 +551,12 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             ready = torch.cuda.Event()
             with torch.cuda.stream(lst):
                 lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
-                                          m2l_owner_only=nch > 1)
+                                          m2l_owner_only=nch > 1, src=src)
             parts.append(lists)
             with torch.cuda.stream(side):  # M2L rows of this chunk: after upward and its sorted list
                 ea, eb = E(), E()
                 ea.record(side)
-                run_m2l(tree, lists, p)
+                run_m2l(tree, lists, p, src)
                 eb.record(side)
                 m2l_ev.append((ea, eb))
             planned = torch.cuda.Event()
@@ -488,7 +565,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             with torch.cuda.stream(pst):
                 ea, eb = E(), E()
                 ea.record(pst)
-                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag, bodies)
                 eb.record(pst)
                 p2p_ev.append((ea, eb))
         e_l1.record(lst)
@@ -499,10 +576,14 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             e_down1.record(side)
         e_pend.record(pst)
         main.wait_event(e_pend)
-        if cfg.precision == "fp32" and int(flag.item()) != 0:
+        redo = cfg.precision == "fp32" and int(flag.item()) != 0
+        if redo:
             # two distinct bodies collided in FP32 outside a self run: redo guarded
             for lists in parts:
-                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag, bodies)
+        # cross-tree: float64-coincident pairs (none unless FP32 saw one)
+        coinc = [count_coincident(tree, x, bodies) for x in parts] if cross and (redo or cfg.precision == "fp64") \
+            else []
         main.wait_event(e_down1)
         P = _lib.ptr
         _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
@@ -514,6 +595,10 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             a, b = lists.dev_stats.tolist()
             pairs += a
             skipped += b
+        for c in coinc:
+            k = int(c.item())
+            pairs -= k
+            skipped += k
     lists = parts[0] if nch == 1 else ChunkedLists(parts)
     tree.list_cache = lists
     stats.p2p_pairs += int(pairs)
@@ -534,9 +619,9 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     # phases overlap (far field on the side stream, near field on the P2P
     # stream): upward and downward are their own stream's spans, traversal
     # is the span from the start to the last P2P chunk
-    return EvalReport(strategy="dualtree", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
+    return EvalReport(strategy="dualtree", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=False, threads=threads, task_grain=cfg.task_grain, stats=stats,
-                      build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
+                      build_time=_build_time(tree, src), upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
                       traversal_time=e0.elapsed_time(e_pend) * 1e-3,
                       downward_time=e_down0.elapsed_time(e_down1) * 1e-3, trace=events)
 
@@ -550,11 +635,14 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
     the tree and runs P2P; the side stream runs the upward pass and, once
     the M2P list is sorted, M2P into separate accumulators that one combine
     kernel adds at the end.  The walk is target-leaf driven, so
-    ``cfg.mutual`` has no effect here (as in the reference)."""
-    if source_tree is not None and source_tree is not tree:
-        raise NotImplementedError("separate source trees are outside the B200 hot path")
+    ``cfg.mutual`` has no effect here (as in the reference).  A separate
+    ``source_tree`` (src/traversal.py:1002-1046) is walked from every target
+    leaf; its multipoles and bodies are the sources."""
+    src = tree if source_tree is None else source_tree
+    cross = src is not tree
     if threads < 1:
         raise ValueError(f"threads must be >= 1, got {threads}")
+    _same_device(tree, src)
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
@@ -563,33 +651,36 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         side = _side_stream(dev)
         E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
         e0, e_up0, e_up1, e_m0, e_m1, e_l1, e_p0, e_p1, e_end = (E() for _ in range(9))
-        need_up = tree._M is None or tree.p != p
-        M = torch.zeros((tree.ncells, ncoef(p)), dtype=torch.float64, device=dev) if need_up else tree._M
+        need_up = src._M is None or src.p != p
+        M = torch.zeros((src.ncells, ncoef(p)), dtype=torch.float64, device=dev) if need_up else src._M
         far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+        bodies = CrossBodies(tree, src) if cross else None
         e0.record(main)
         side.wait_event(e0)
         with torch.cuda.stream(side):
             e_up0.record(side)
             if need_up:
-                upward_pass(tree, p, stats, sync=False, M=M)  # (resets tree._L)
+                upward_pass(src, p, stats, sync=False, M=M)  # (resets src._L)
             e_up1.record(side)
-        tree._M, tree.p = M, p
+        src._M, src.p = M, p
         m2p_ready = torch.cuda.Event()
-        lists = treecode_lists(tree, cfg.mac, m2p_ready=m2p_ready, side=side)
+        lists = treecode_lists(tree, cfg.mac, m2p_ready=m2p_ready, side=side, src=src)
         tree.list_cache = lists
         e_l1.record(main)
         side.wait_event(m2p_ready)
         with torch.cuda.stream(side):
             e_m0.record(side)
-            run_m2p(tree, lists, p, tuple(far))
+            run_m2p(tree, lists, p, tuple(far), src)
             e_m1.record(side)
         e_p0.record(main)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag, bodies)
         e_p1.record(main)
-        if cfg.precision == "fp32" and int(flag.item()) != 0:
-            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+        redo = cfg.precision == "fp32" and int(flag.item()) != 0
+        if redo:
+            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag, bodies)
             e_p1.record(main)
+        coinc = count_coincident(tree, lists, bodies) if cross and (redo or cfg.precision == "fp64") else None
         main.wait_event(e_m1)
         P = _lib.ptr
         _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
@@ -597,6 +688,10 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         e_end.record(main)
         e_end.synchronize()
         pairs, skipped = lists.dev_stats.tolist()
+        if coinc is not None:
+            k = int(coinc.item())
+            pairs -= k
+            skipped += k
     stats.p2p_pairs += int(pairs)
     stats.p2p_skipped += int(skipped)
     stats.p2p_flops += 20 * int(pairs)
@@ -612,9 +707,9 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         events += [("m2p", int(a), int(b)) for a, b in zip(mt, ms)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
-    return EvalReport(strategy="treecode", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
+    return EvalReport(strategy="treecode", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain,
-                      stats=stats, build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
+                      stats=stats, build_time=_build_time(tree, src), upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
                       traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=0.0, trace=events)
 
 
@@ -699,6 +794,24 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
                       stats=stats, build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
                       traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=e_m1.elapsed_time(e_d1) * 1e-3,
                       trace=events)
+
+
+def _same_device(tree: Tree, src: Tree) -> None:
+    if src is not tree and torch.device(src.device) != torch.device(tree.device):
+        raise ValueError(f"source tree on {src.device}, target tree on {tree.device}")
+
+
+def _build_time(tree: Tree, src: Tree) -> float:
+    """Both trees' build times (src/traversal.py:922)."""
+    return tree.build_time + (src.build_time if src is not tree else 0.0)
+
+
+def _attach_locals(tree: Tree, p: int, L: torch.Tensor) -> None:
+    """Fresh order-p locals on the target tree (src/traversal.py:614-618); its
+    multipoles stay valid only if they are of order p."""
+    if tree._M is not None and tree.p != p:
+        tree._M = None
+    tree.p, tree._L = p, L
 
 
 def evaluate_on_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,

@@ -137,8 +137,8 @@ def test_workload_generators_are_seeded():
 def test_out_of_scope_paths_raise():
     with pytest.raises(NotImplementedError):
         fb.evaluate_on_tree(object(), fb.EvalConfig(mutual=True))
-    with pytest.raises(NotImplementedError):
-        fb.evaluate_treecode(object(), fb.EvalConfig(strategy="treecode"), source_tree=object())
+    with pytest.raises(ValueError, match="share one tree"):  # the reference's error
+        fb.evaluate_dual_tree(object(), fb.EvalConfig(mutual=True), source_tree=object())
     with pytest.raises(ValueError, match="one tree onto itself"):  # the reference's error
         fb.evaluate_list_fmm(object(), fb.EvalConfig(strategy="listfmm"), source_tree=object())
 
