@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--theta", type=float, default=0.0, help="override theta (C4 sweep)")
     ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode", "listfmm"],
                     help="evaluation strategy (the headline is the dual-tree FMM)")
+    ap.add_argument("--mutual", action="store_true", help="mutual dual traversal (EvalConfig.mutual)")
+    ap.add_argument("--task-grain", type=int, default=5000, help="EvalConfig.task_grain (mutual partition)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true", help="skip the 1000-sample direct-sum check")
@@ -88,6 +90,8 @@ def config_block(args, n, solver, extra=None):
          "distribution": {"C1": "uniform f64", "C2": "uniform f32, q~U[0,1)", "C3": "Plummer a=1 rcut=10a",
                           "C4": "uniform f32, q~U[-1,1)", "C5": "uniform f32, q~U[0,1)"}[args.config],
          "l2": "flushed between timed steps (2x L2 write)"}
+    if getattr(args, "mutual", False):
+        d.update(mutual=True, task_grain=args.task_grain)
     if extra:
         d.update(extra)
     return d
@@ -251,7 +255,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pos, q, n, solver = workload(args)
     cfg = fb.EvalConfig(strategy=args.strategy, mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"],
-                        precision=args.precision)
+                        precision=args.precision, mutual=args.mutual, task_grain=args.task_grain)
     dev = torch.device("cuda", local)
     dt = torch.float32 if pos.dtype == np.float32 else torch.float64
     dpos = torch.as_tensor(pos, device=dev).to(dt)
@@ -368,7 +372,7 @@ def run_ours(args):
         except Exception:
             traffic = None
     cpu = None
-    if not args.no_cpu_baseline and rank == 0 and world == 1 and args.strategy == "dualtree":
+    if not args.no_cpu_baseline and rank == 0 and world == 1 and args.strategy == "dualtree" and not args.mutual:
         v, d = cpu_run(pos, q, solver, args.cpu_seconds)
         cpu = {"value": v, "unit": "particles/s", "cores": d["threads"], "kind": "port",
                "sample": f"C oracle (restated reference, {d['threads']} threads, {cpu_model()}): full "

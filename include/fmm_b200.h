@@ -183,6 +183,30 @@ FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1
                  double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
                  int64_t cap_m2l, unsigned long long *dev_log, void *stream);
 
+/* Partition owners of the mutual traversal (replaces _partition_roots +
+ * _owner_map, src/traversal.py:621-640): owner[c] = the partition root
+ * (maximal subtree with < grain bodies, leaves included) holding cell c,
+ * -1 above the partition.  grain >= 1 (EvalConfig.task_grain). */
+FMM_API int fmm_partition_owner(int32_t ncells, const int32_t *parent, const uint8_t *leaf, const int32_t *start,
+                        const int32_t *end, int64_t grain, int32_t *owner, void *stream);
+
+/* Mutual dual traversal (replaces _dual_driver + _collect_units with mutual
+ * units, src/traversal.py:159-262, :704-791, and their retries): from the
+ * mutual root pair, a mutual pair straddling two owners is demoted to the
+ * directed pairs (a, b) and (b, a); pairs are classified with the unit
+ * rules (MAC in both directions when mutual; a mutual self pair splits
+ * into (ci, ci) and (ci, cj), i < j).  The lists are written DIRECTED:
+ * a mutual entry (a, b) as (a, b) and, for a != b, (b, a) (the reference's
+ * trace expansion), for the directed M2L/P2P executors; only targets whose
+ * bodies meet [body_lo, body_hi).  Frontier and dev_log as fmm_traverse
+ * (2 * depth + 2 steps suffice). */
+FMM_API int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                        int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                        const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
+                        const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                        double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                        int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, void *stream);
+
 /* Treecode lists (replaces _collect_treecode, src/traversal.py:265-313, with
  * its capacity retry, :944-966): every leaf whose bodies meet
  * [body_lo, body_hi) walks the source tree from the root; a pair (t, c)

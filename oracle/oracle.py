@@ -65,6 +65,12 @@ def _declare(L):
     L.orc_exec_m2p.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int]
     L.orc_exec_p2p.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_direct_subset.argtypes = [_I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, C.c_int]
+    L.orc_partition_roots.argtypes = [_I, _P, _P, _P, _P, _P, _I, _P, _P]
+    L.orc_partition_roots.restype = _I
+    L.orc_collect_mutual.argtypes = [_I, _P, _P, _P, _P, _P, _P, C.c_int, _D, C.c_int, _I, _P, _P, _P, _I, _P, _P,
+                                     _P, _P]
+    L.orc_exec_m2l_mut.argtypes = [_I, _P, _P, _P, _P, _P, _P, C.c_int]
+    L.orc_exec_p2p_mut.argtypes = [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P]
     L.orc_fmm.argtypes = [_I, _P, _P, _P, _P, _I, C.c_int, _D, C.c_int, _D,
                           _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
     L.orc_fmm.restype = C.c_int
@@ -462,3 +468,65 @@ def fmm(pos, q, ncrit, p, theta, threads=0, tfrac=1.0):
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+# ---------------------------------------------------------------------------
+# mutual dual traversal
+# ---------------------------------------------------------------------------
+MAC_CODES = {"bh": 0, "bmax": 1, "fmm": 2}
+
+
+def partition_roots(t: OracleTree, grain: int):
+    """src/traversal.py:621-640: (sorted partition roots, owner map)."""
+    roots = np.empty(t.ncells, np.int64)
+    owner = np.empty(t.ncells, np.int64)
+    nr = lib().orc_partition_roots(t.ncells, _p(t.cell_children), _p(t.cell_leaf), _p(t.cell_start),
+                                   _p(t.cell_end), _p(np.ascontiguousarray(t.cell_sub_end, np.int64)), int(grain),
+                                   _p(roots), _p(owner))
+    return roots[:nr].copy(), owner
+
+
+def collect_mutual(t: OracleTree, theta: float, grain: int, mac: str = "fmm", mutual: bool = True):
+    """Driver + per-bucket _collect_units with (target, source, mut) entries
+    (src/traversal.py:159-262, :704-791).  Returns (mt, ms, mm, pt, ps, pm)
+    in the reference's execution order."""
+    _, owner = partition_roots(t, grain)
+    capm = capp = max(2048, 64 * t.ncells)
+    while True:
+        mt = np.empty(capm, np.int64); ms = np.empty(capm, np.int64); mm = np.empty(capm, np.uint8)
+        pt = np.empty(capp, np.int64); ps = np.empty(capp, np.int64); pm = np.empty(capp, np.uint8)
+        out = np.zeros(3, np.int64)
+        lib().orc_collect_mutual(t.ncells, _p(t.cell_children), _p(t.cell_leaf), _p(t.cell_center),
+                                 _p(t.cell_bmax), _p(t.cell_rmax), _p(owner), MAC_CODES[mac],
+                                 float(theta) * float(theta), int(mutual), capm, _p(mt), _p(ms), _p(mm), capp,
+                                 _p(pt), _p(ps), _p(pm), _p(out))
+        if out[2] == 1:
+            capm, capp = int(out[0]) + 1, int(out[1]) + 1
+            continue
+        nm, npp = int(out[0]), int(out[1])
+        return mt[:nm], ms[:nm], mm[:nm], pt[:npp], ps[:npp], pm[:npp]
+
+
+def expand_mutual(t, s, m):
+    """Directed events of (target, source, mut) entries, as the reference's
+    trace lists them (src/traversal.py:644-650): a mutual entry (a, b),
+    a != b, also stands for (b, a)."""
+    t, s, m = (np.asarray(a) for a in (t, s, m))
+    rev = (m != 0) & (t != s)
+    return np.concatenate([t, s[rev]]), np.concatenate([s, t[rev]])
+
+
+def evaluate_mutual(t: OracleTree, p: int, theta: float, grain: int, mac: str = "fmm"):
+    """evaluate_dual_tree(..., mutual=True) restated sequentially."""
+    M = upward(t, p)
+    mt, ms, mm, pt, ps, pm = collect_mutual(t, theta, grain, mac)
+    L = np.zeros_like(M)
+    lib().orc_exec_m2l_mut(mt.size, _p(mt), _p(ms), _p(mm), _p(t.cell_center), _p(M), _p(L), p)
+    phi, fx, fy, fz = (np.zeros(t.n) for _ in range(4))
+    st = np.zeros(3, np.int64)
+    lib().orc_exec_p2p_mut(pt.size, _p(pt), _p(ps), _p(pm), _p(t.cell_start), _p(t.cell_end), _p(t.x), _p(t.y),
+                           _p(t.z), _p(t.q), _p(phi), _p(fx), _p(fy), _p(fz), 0, _p(st))
+    downward(t, L.copy(), p, phi, fx, fy, fz)
+    m2l = expand_mutual(mt, ms, mm)
+    return dict(phi=phi, fx=fx, fy=fy, fz=fz, m2l=m2l, p2p=expand_mutual(pt, ps, pm), p2p_pairs=int(st[0]),
+                p2p_skipped=int(st[1]), m2l_calls=int(m2l[0].size))

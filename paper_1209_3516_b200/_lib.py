@@ -47,6 +47,9 @@ SIGNATURES = {
                           P, P, I64, P, P, I64, P, P],
     "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P,
                      P, I64, P, P],
+    "fmm_partition_owner": [I32, P, P, P, P, I64, P, P],
+    "fmm_traverse_mutual": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64,
+                            P, P],
     "fmm_treecode_traverse": [P, P, P, P, I64, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P,
                               I64, P, P, I64, P, P, SZ, P],
     "fmm_listfmm_lists": [I32, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, I64, P, P, I64, P, P, SZ, P],

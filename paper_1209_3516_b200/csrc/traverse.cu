@@ -450,6 +450,145 @@ __global__ void fill_i64(int64_t *a, int64_t n, int64_t v) {
 using namespace fmm;
 
 // The source tree's arrays default to the target tree's (one-tree evaluation).
+// ---- mutual traversal ---------------------------------
+// Partition owner (src/traversal.py:621-640): the reference's partition
+// roots are the maximal subtrees holding fewer than `grain` bodies (leaves
+// included), so a cell is unowned (-1) iff it is internal with >= grain
+// bodies, and otherwise owned by its highest ancestor-or-self whose parent
+// is unowned.
+__global__ void partition_owner_kernel(int32_t ncells, const int32_t *__restrict__ parent,
+                                       const uint8_t *__restrict__ leaf, const int32_t *__restrict__ cstart,
+                                       const int32_t *__restrict__ cend, int64_t grain, int32_t *owner) {
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+        int32_t r = -1;
+        if (leaf[c] || (int64_t)(cend[c] - cstart[c]) < grain) {
+            r = c;
+            while (r != 0) {
+                const int32_t up = parent[r];
+                if ((int64_t)(cend[up] - cstart[up]) >= grain) break;
+                r = up;
+            }
+        }
+        owner[c] = r;
+    }
+}
+
+// Children pairs of an unresolved pair (src/traversal.py:222-256): a leaf
+// -> b's children; b leaf -> a's; a mutual self pair -> (ci, ci) and
+// (ci, cj), i < j; else the larger rmax opens (ties: the target).
+template <class F>
+__device__ __forceinline__ void for_split(int32_t a, int32_t b, int m, const Cells &C, F &&f) {
+    const int32_t *ka = C.children + (int64_t)a * 8, *kb = C.children + (int64_t)b * 8;
+    if (C.leaf[a]) {
+        for (int o = 0; o < 8; o++) if (kb[o] >= 0) f(a, kb[o]);
+    } else if (C.leaf[b]) {
+        for (int o = 0; o < 8; o++) if (ka[o] >= 0) f(ka[o], b);
+    } else if (m && a == b) {
+        for (int i = 0; i < 8; i++) {
+            const int32_t ci = ka[i];
+            if (ci < 0) continue;
+            f(ci, ci);
+            for (int j = i + 1; j < 8; j++) if (ka[j] >= 0) f(ci, ka[j]);
+        }
+    } else if (C.rmax[a] >= C.rmax[b]) {
+        for (int o = 0; o < 8; o++) if (ka[o] >= 0) f(ka[o], b);
+    } else {
+        for (int o = 0; o < 8; o++) if (kb[o] >= 0) f(a, kb[o]);
+    }
+}
+
+// One breadth-first step of the mutual traversal.  Frontier entries are
+// UNCLASSIFIED (a, b, mut) pairs, mut in bit 31 of fb.  A mutual pair whose
+// cells have different partition owners is first demoted to the directed
+// pairs (a, b) and (b, a) (the reference's driver, src/traversal.py:727-738);
+// every pair is then classified with the unit rules (both leaves -> P2P;
+// MAC, both directions when mutual -> M2L; else split).  Emitted lists are
+// DIRECTED: a mutual entry (a, b) is written as (a, b) and, when a != b,
+// (b, a) -- the reference's trace expansion (src/traversal.py:644-650) --
+// so the directed M2L / P2P executors run them unchanged.  Only targets
+// whose bodies meet [blo, bhi) are emitted.
+__global__ void mutual_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
+                                   const unsigned long long *__restrict__ nfront_dev, int64_t cap_front, Cells C,
+                                   const int32_t *__restrict__ owner, const int32_t *__restrict__ cstart,
+                                   const int32_t *__restrict__ cend, int32_t blo, int32_t bhi, int kind_mac,
+                                   double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                                   int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
+                                   unsigned long long *cnt_p2p, unsigned long long *cnt_m2l,
+                                   unsigned long long *cnt_next) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t nfront = (int64_t)*nfront_dev;
+    if (nfront > cap_front) nfront = cap_front;
+    const int64_t nround = (nfront + stride - 1) / stride;
+    auto keep = [&](int32_t c) { return cend[c] > blo && cstart[c] < bhi; };
+    for (int64_t r = 0; r < nround; r++) {
+        const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        int32_t ia[2], ib[2];
+        int im_[2], fate[2];
+        int nitem = 0;
+        if (k < nfront) {
+            const int32_t a = fa[k];
+            const int32_t b = fb[k] & 0x7fffffff;
+            const int m = (int)((uint32_t)fb[k] >> 31);
+            if (m && owner[a] >= 0 && owner[b] >= 0 && owner[a] != owner[b]) {
+                ia[0] = a; ib[0] = b; im_[0] = 0;
+                ia[1] = b; ib[1] = a; im_[1] = 0;
+                nitem = 2;
+            } else {
+                ia[0] = a; ib[0] = b; im_[0] = m;
+                nitem = 1;
+            }
+        }
+        int np = 0, nm = 0, nn = 0;
+        for (int q = 0; q < 2; q++) {
+            fate[q] = 0;
+            if (q >= nitem) continue;
+            const int32_t a = ia[q], b = ib[q];
+            const int m = im_[q];
+            if (C.leaf[a] && C.leaf[b]) {
+                fate[q] = 1;
+                np += keep(a) + (m && a != b && keep(b));
+            } else if (mac_accept(a, b, C, C, kind_mac, th2) && (!m || mac_accept(b, a, C, C, kind_mac, th2))) {
+                fate[q] = 2;
+                nm += keep(a) + (m && keep(b));
+            } else {
+                fate[q] = 3;
+                for_split(a, b, m, C, [&](int32_t x, int32_t y) { nn += keep(x) || (m && keep(y)); });
+            }
+        }
+        int op, om, on;
+        const unsigned long long bp = warp_reserve(cnt_p2p, np, lane, &op);
+        const unsigned long long bm = warp_reserve(cnt_m2l, nm, lane, &om);
+        const unsigned long long bn = warp_reserve(cnt_next, nn, lane, &on);
+        unsigned long long ip = bp + op, im = bm + om, in = bn + on;
+        for (int q = 0; q < 2; q++) {
+            const int32_t a = ia[q], b = ib[q];
+            const int m = im_[q];
+            if (fate[q] == 1 || fate[q] == 2) {
+                int32_t *tt = fate[q] == 1 ? p2p_t : m2l_t, *ss = fate[q] == 1 ? p2p_s : m2l_s;
+                const unsigned long long cap = (unsigned long long)(fate[q] == 1 ? cap_p2p : cap_m2l);
+                unsigned long long &at = fate[q] == 1 ? ip : im;
+                if (keep(a)) {
+                    if (at < cap) { tt[at] = a; ss[at] = b; }
+                    at++;
+                }
+                if (m && a != b && keep(b)) {
+                    if (at < cap) { tt[at] = b; ss[at] = a; }
+                    at++;
+                }
+            } else if (fate[q] == 3) {
+                const int32_t mbit = m ? (int32_t)0x80000000u : 0;
+                for_split(a, b, m, C, [&](int32_t x, int32_t y) {
+                    if (keep(x) || (m && keep(y))) {
+                        if (in < (unsigned long long)cap_next) { na[in] = x; nb[in] = y | mbit; }
+                        in++;
+                    }
+                });
+            }
+        }
+    }
+}
+
 static Cells cells_of(const int32_t *children, const uint8_t *leaf, const double *ctr, const double *bmax,
                       const double *rmax) {
     return Cells{children, leaf, ctr, bmax, rmax};
@@ -550,6 +689,45 @@ int fmm_treecode_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a
             even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_treecode_traverse");
+    return FMM_OK;
+}
+
+int fmm_partition_owner(int32_t ncells, const int32_t *parent, const uint8_t *leaf, const int32_t *start,
+                        const int32_t *end, int64_t grain, int32_t *owner, void *stream) {
+    if (grain < 1) { set_error("task_grain must be >= 1, got %lld", (long long)grain); return FMM_ERR_INVALID; }
+    partition_owner_kernel<<<grid_for(ncells, 256), 256, 0, as_stream(stream)>>>(ncells, parent, leaf, start, end,
+                                                                                grain, owner); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_partition_owner");
+    return FMM_OK;
+}
+
+int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                        int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                        const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
+                        const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                        double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                        int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (cap_front < 1) { set_error("frontier capacity must be >= 1"); return FMM_ERR_INVALID; }
+    const Cells C = cells_of(children, leaf, ctr, bmax, rmax);
+    // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s;
+    // the seed is the unclassified mutual root pair (0, 0)
+    cudaMemsetAsync(dev_log, 0, sizeof(unsigned long long) * (nsteps + 3), st);
+    const unsigned long long one = 1;
+    cudaMemcpyAsync(dev_log + 2, &one, sizeof(one), cudaMemcpyHostToDevice, st);
+    const int32_t zero = 0, root_mut = (int32_t)0x80000000u;
+    cudaMemcpyAsync(front_a0, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(front_b0, &root_mut, sizeof(root_mut), cudaMemcpyHostToDevice, st);
+    const int grid = 148 * 8;
+    for (int sidx = 0; sidx < nsteps; sidx++) {
+        const bool even = (sidx & 1) == 0;
+        mutual_step_kernel<<<grid, 256, 0, st>>>(
+            even ? front_a0 : front_a1, even ? front_b0 : front_b1, dev_log + 2 + sidx, cap_front, C, owner, start,
+            end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
+            even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1,
+            dev_log + 3 + sidx); fmm::note_launch();
+    }
+    FMM_CUDA_CHECK("fmm_traverse_mutual");
     return FMM_OK;
 }
 

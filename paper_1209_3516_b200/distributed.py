@@ -164,7 +164,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import (EvalReport, interaction_lists, listfmm_lists, run_m2l, run_m2p, run_p2p,
+    from .traversal import (EvalReport, interaction_lists, listfmm_lists, mutual_lists, run_m2l, run_m2p, run_p2p,
                             treecode_lists)
     from .tree import downward_pass
 
@@ -172,8 +172,6 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         from .traversal import evaluate_on_tree
         return evaluate_on_tree(tree, cfg)
     treecode = cfg.strategy == "treecode"
-    if cfg.mutual and cfg.strategy == "dualtree":
-        raise NotImplementedError("mutual traversal is outside the B200 hot path")
     plan = getattr(tree, "_dist_plan", None)
     if plan is None or len(plan.cuts) != world + 1 or plan.rank != rank:
         plan = _Plan(tree, world, rank)
@@ -210,6 +208,8 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         lists = treecode_lists(tree, cfg.mac, body_range=(lo, hi), m2p_ready=ready, side=side)
     elif cfg.strategy == "listfmm":
         lists = listfmm_lists(tree, body_range=(lo, hi), m2l_ready=ready, side=side)
+    elif cfg.mutual:  # the rank's targets of the mutual lists (directed-expanded)
+        lists = mutual_lists(tree, cfg.mac, cfg.task_grain, body_range=(lo, hi), m2l_ready=ready, side=side)
     else:
         lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side)
     ev[2].record(main)
@@ -250,7 +250,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     tree._results_changed()
     del _lib
     return EvalReport(strategy=cfg.strategy, n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
-                      theta=cfg.mac.theta, mutual=False, threads=world, task_grain=cfg.task_grain, stats=stats,
+                      theta=cfg.mac.theta, mutual=cfg.mutual, threads=world, task_grain=cfg.task_grain, stats=stats,
                       build_time=tree.build_time, upward_time=ev[0].elapsed_time(ev[1]) * 1e-3,
                       traversal_time=ev[0].elapsed_time(ev[7]) * 1e-3,
                       downward_time=0.0 if treecode else ev[4].elapsed_time(ev[5]) * 1e-3)

@@ -30,8 +30,10 @@ Scope: all three strategies (``dualtree`` directed, ``treecode``,
 separate ``source_tree``: the source bodies are appended
 after the targets in one set of P2P body arrays, the traversals read the two
 trees' cell arrays, M2L/M2P read the source tree's multipoles and the P2P
-plan's runs point past the targets.  ``mutual=True`` on one tree is outside
-the B200 hot path and raises NotImplementedError.
+plan's runs point past the targets.  ``mutual=True``
+runs the mutual traversal (``mutual_lists``): the reference's mutual list
+sets, partition demotion included, written directed so the same M2L / P2P
+executors evaluate them.
 ``precision`` is a new knob: "fp64" (default, the reference's arithmetic)
 or "fp32" (FP32 near field; far field stays float64).
 """
@@ -215,6 +217,73 @@ def _source_cells(tree: Tree, src: Tree | None) -> tuple:
         return (None,) * 5
     P = _lib.ptr
     return P(src.d_children), P(src.d_leaf), P(src.d_ctr), P(src.d_bmax), P(src.d_rmax)
+
+
+def partition_owner(tree: Tree, grain: int) -> torch.Tensor:
+    """Device owner map of the mutual traversal's target partition
+    (src/traversal.py:621-640): the partition root holding each cell, -1
+    above the partition."""
+    if grain < 1:
+        raise ValueError(f"task_grain must be >= 1, got {grain}")
+    cache = tree.__dict__.setdefault("_owner_cache", {})
+    if grain not in cache:
+        owner = torch.empty(tree.ncells, dtype=torch.int32, device=tree.device)
+        P = _lib.ptr
+        _lib.call("fmm_partition_owner", tree.ncells, P(tree.d_parent), P(tree.d_leaf), P(tree.d_start),
+                  P(tree.d_end), int(grain), P(owner), _lib.stream_handle())
+        cache.clear()
+        cache[grain] = owner
+    return cache[grain]
+
+
+def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[int, int] | None = None,
+                 m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None) -> Lists:
+    """Mutual dual traversal (src/traversal.py:159-262 with mutual units,
+    :704-791 driver) -> DIRECTED target-sorted CSR M2L/P2P lists: each
+    mutual entry (a, b) contributes (a, b) and (b, a), the reference's trace
+    expansion, so the lists equal the reference's trace sets and feed the
+    directed executors.  The sets depend on ``task_grain`` through the
+    partition: a mutual pair straddling two partition roots is demoted to
+    two directed pairs."""
+    blo, bhi = body_range if body_range is not None else (0, tree.n)
+    dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
+    th2 = mac.theta * mac.theta
+    owner = partition_owner(tree, task_grain)
+    key = ("mutual", tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, task_grain)
+    cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
+                                                 max(4096, tree.ncells * 16)))
+    nsteps = 2 * tree.depth + 2
+    log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
+    while True:
+        p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
+        p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
+        m2l_t = torch.empty(cap_m2l, dtype=i32, device=dev)
+        m2l_s = torch.empty(cap_m2l, dtype=i32, device=dev)
+        fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
+        _lib.call("fmm_traverse_mutual", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps,
+                  P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(owner),
+                  P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t),
+                  P(m2l_s), cap_m2l, P(log), st)
+        hl = log.tolist()  # the one synchronisation of the traversal
+        done_p2p, done_m2l, fronts = hl[0], hl[1], hl[2:]
+        peak = max(fronts)
+        if done_p2p <= cap_p2p and done_m2l <= cap_m2l and peak <= cap_next:
+            if fronts[-1] != 0:
+                raise RuntimeError("mutual traversal did not terminate within 2*depth+2 steps")
+            break
+        cap_p2p = max(cap_p2p, int(done_p2p * 1.05) + 4096)
+        cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
+        cap_next = max(cap_next, int(peak * 1.05) + 4096)
+    del fr
+    _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
+    ncells = tree.ncells
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
+    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    del p2p_t, p2p_s, m2l_t, m2l_s
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+                 p2p_rows=p2p_rows, peak_frontier=peak,
+                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
 def _csr(t, s, n, ncells, dev, wsp, wsb, stream):
@@ -506,8 +575,6 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     cross = src is not tree
     if cfg.mutual and cross:
         raise ValueError("mutual traversal needs target and source to share one tree")
-    if cfg.mutual:
-        raise NotImplementedError("mutual traversal is outside the B200 hot path")
     if threads < 1:
         raise ValueError(f"threads must be >= 1, got {threads}")
     _same_device(tree, src)
@@ -538,7 +605,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             e_up1.record(side)
         src._M, src.p = M, p
         _attach_locals(tree, p, L)
-        cuts = _chunk_cuts(tree, _nchunks(tree))
+        cuts = _chunk_cuts(tree, 1 if cfg.mutual else _nchunks(tree))
         nch = len(cuts) - 1
         # chunked runs build lists on a high-priority stream (they gate P2P); with
         # one chunk the main stream does: a priority stream there starves the
@@ -550,8 +617,11 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             rng = (cuts[k], cuts[k + 1]) if nch > 1 else None
             ready = torch.cuda.Event()
             with torch.cuda.stream(lst):
-                lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
-                                          m2l_owner_only=nch > 1, src=src)
+                if cfg.mutual:
+                    lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side)
+                else:
+                    lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
+                                              m2l_owner_only=nch > 1, src=src)
             parts.append(lists)
             with torch.cuda.stream(side):  # M2L rows of this chunk: after upward and its sorted list
                 ea, eb = E(), E()
@@ -620,7 +690,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     # stream): upward and downward are their own stream's spans, traversal
     # is the span from the start to the last P2P chunk
     return EvalReport(strategy="dualtree", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
-                      theta=cfg.mac.theta, mutual=False, threads=threads, task_grain=cfg.task_grain, stats=stats,
+                      theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain, stats=stats,
                       build_time=_build_time(tree, src), upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
                       traversal_time=e0.elapsed_time(e_pend) * 1e-3,
                       downward_time=e_down0.elapsed_time(e_down1) * 1e-3, trace=events)

@@ -30,8 +30,7 @@ def test_bad_config_files_exit_2(tmp_path, text, capsys):
 
 
 def test_usage_errors_exit_2(capsys):
-    assert cli.main(["scaling", "--mutual", "--n-list", "10"]) == 2  # outside the B200 path
-    assert cli.main(["scaling", "--n-list", "10,-3", "--mutual"]) == 2
+    assert cli.main(["scaling", "--n-list=-3,10", "--mutual"]) == 2
     assert cli.main(["run", "--n", "0"]) == 2
     assert cli.main(["run", "--input", "/nonexistent.csv"]) == 2
     with pytest.raises(SystemExit) as e:

@@ -42,10 +42,13 @@ def _ps(c):
 @pytest.mark.parametrize("name,world,precision,strategy", [
     ("c2_32k", 2, "fp64", "dualtree"), ("plummer_32k", 4, "fp64", "dualtree"), ("c1", 3, "fp64", "dualtree"),
     ("c2_32k", 8, "fp32", "dualtree"), ("c1", 3, "fp64", "treecode"), ("c2_32k", 4, "fp32", "treecode"),
-    ("c1", 2, "fp64", "listfmm"), ("plummer_32k", 4, "fp64", "listfmm")])
+    ("c1", 2, "fp64", "listfmm"), ("plummer_32k", 4, "fp64", "listfmm"), ("c1", 3, "fp64", "mutual"),
+    ("c2_32k", 4, "fp32", "mutual")])
 def test_partitioned_equals_single(name, world, precision, strategy):
     c = Case(name)
-    cfg = fb.EvalConfig(strategy=strategy, mac=fb.MacConfig("fmm", c.theta), p=c.p, precision=precision)
+    mutual = strategy == "mutual"
+    cfg = fb.EvalConfig(strategy="dualtree" if mutual else strategy, mac=fb.MacConfig("fmm", c.theta), p=c.p,
+                        precision=precision, mutual=mutual, task_grain=1500)
     ref_tree = fb.build_tree(_ps(c), ncrit=c.ncrit)
     ref = fb.evaluate_on_tree(ref_tree, cfg)
     want = [a.clone() for a in (ref_tree.d_phi, ref_tree.d_fx, ref_tree.d_fy, ref_tree.d_fz)]

@@ -134,9 +134,7 @@ def test_workload_generators_are_seeded():
     assert abs(q1.mean()) < 1e-15
 
 
-def test_out_of_scope_paths_raise():
-    with pytest.raises(NotImplementedError):
-        fb.evaluate_on_tree(object(), fb.EvalConfig(mutual=True))
+def test_reference_argument_errors():
     with pytest.raises(ValueError, match="share one tree"):  # the reference's error
         fb.evaluate_dual_tree(object(), fb.EvalConfig(mutual=True), source_tree=object())
     with pytest.raises(ValueError, match="one tree onto itself"):  # the reference's error
