@@ -98,12 +98,14 @@ FMM_API int fmm_permute_bodies(const int32_t *perm, const double *x, const doubl
  * its leaf level and the number of cells it starts; cbase = exclusive scan
  * of those counts = pre-order id of the first cell starting at that body.
  * host_level_hist[23] receives cells per level 0..21 and, in slot 22, the
- * number of leaves; host_ncells the total
- * (synchronises once).  FMM_ERR_MAX_DEPTH when a depth-21 cell holds more
- * than ncrit bodies and !allow_big (src/tree.py:419-423). */
+ * number of leaves; host_ncells the total; host_flag (optional) a copy of
+ * the device int *dev_flag read in the same transfer (the build passes
+ * fmm_permute_bodies' float32-inexact flag).  Synchronises once, with one
+ * pinned copy.  FMM_ERR_MAX_DEPTH when a depth-21 cell holds more than
+ * ncrit bodies and !allow_big (src/tree.py:419-423). */
 FMM_API int fmm_carve_count(const uint64_t *keys, int64_t n, int32_t ncrit, int allow_big, int32_t *cbase,
-                    int8_t *leaf_level, int32_t *host_level_hist, int32_t *host_ncells, void *ws, size_t ws_bytes,
-                    void *stream);
+                    int8_t *leaf_level, int32_t *host_level_hist, int32_t *host_ncells, const int32_t *dev_flag,
+                    int32_t *host_flag, void *ws, size_t ws_bytes, void *stream);
 
 /* Single-pass carve, step 2: writes every cell array in the reference's
  * pre-order (children by octant, -1 when empty), cells_by_level grouped by
@@ -243,34 +245,56 @@ FMM_API int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_of
                       int32_t *m2l_s, int64_t cap_m2l, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p,
                       unsigned long long *dev_counts, void *ws, size_t ws_bytes, void *stream);
 
+/* Sort every CSR row's ids ascending (rows of distinct ids, e.g. a grouped
+ * interaction list): out[rows[c]..rows[c+1]) = sorted in[...]. */
+FMM_API int fmm_sort_rows(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, void *stream);
+
+/* The same CSR as fmm_pairs_to_csr without a host pair count: *dev_npairs
+ * (a traversal's device counter, clamped to cap) pairs are counted per
+ * target, scattered, and each row's sources sorted by one CTA (block radix
+ * sort; long rows by a larger tile or an in-memory bitonic sort), so a
+ * traversal and its CSR chain on the stream with no host round trip.
+ * Sources are ids below nsrc (<= 0: ncells).  sort_rows = 0 skips the
+ * row sort (rows grouped, order within a row free: fmm_p2p_plan sorts its
+ * rows itself).  ws holds
+ * fmm_workspace_bytes(max(cap, ncells + 1)). */
+FMM_API int fmm_pairs_to_rows(const int32_t *t, const int32_t *s, const unsigned long long *dev_npairs, int64_t cap,
+                      int32_t ncells, int32_t nsrc, int sort_rows, int32_t *src_sorted, int64_t *rows, void *ws,
+                      size_t ws_bytes, void *stream);
+
 /* Sort (t, s) pairs by target then source and build row offsets over all
  * cells: rows[c]..rows[c+1] are the sources of target c (ascending). */
 FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs, int32_t ncells,
                      int32_t *src_sorted, int64_t *rows, void *ws, size_t ws_bytes, void *stream);
 
-/* P2P work decomposition: merge Morton-adjacent source leaves of every
- * target-leaf row into contiguous body runs and split off the self leaf.
- * Rows are the leaves whose bodies lie in [body_lo, body_hi).
- * Outputs the leaf rows (leaf_rows[r] = target leaf, sized ncells),
- * run_off[r..r+1] (sized ncells + 1), runs as int4 {bstart, bend,
- * self_flag, 0}.  Host round trips are optional: with host_nruns and
- * host_nleaf_rows NULL the call never synchronises (cap_runs must then be
- * >= the number of P2P pairs, an upper bound on runs); the row count is
- * written to dev_nrows for fmm_p2p.
+/* P2P work decomposition: merge every target-leaf row's Morton-adjacent
+ * source leaves into contiguous body runs (ascending) and split off the
+ * self leaf.  Rows are the leaves whose bodies lie in [body_lo, body_hi).
+ * Input: the P2P list grouped by target (rows[t]..rows[t+1] index src; the
+ * order within a row is free -- fmm_pairs_to_rows with sort_rows = 0).
+ * One warp per row marks the row's source-leaf ordinals in a bitmap and
+ * reads the runs off it (fmm_sort_rows gives the sorted row when wanted).
+ * Outputs: the leaf rows (leaf_rows[r] = target leaf, sized ncells),
+ * run_rng[2r], run_rng[2r+1] (the row's runs, stored row-locally at the
+ * row's own CSR offset, so runs is sized like src: cap_runs >= the pair
+ * count), runs as int4 {bstart, bend, self_flag, 0}.  The call never
+ * synchronises unless host_nruns / host_nleaf_rows are given; the row
+ * count is written to dev_nrows for fmm_p2p.
  * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
  * into dev_stats[2] (src/_taylor.py:366-407 accounting).  keys (the sorted
  * body keys, optional) let leaves without two equal keys skip the
  * coincident-pair scan (coincident bodies share a key); NULL scans all.
- * Cross-tree plans (src_start given): the sources are the source tree's
- * leaves, their body runs shifted by src_offset (where the source bodies
- * sit in the P2P body arrays); no self leaf, no coincident scan (see
- * fmm_p2p_coincident). */
+ * Cross-tree plans (src_start given, with src_leaf, src_end, src_ncells):
+ * the sources are the source tree's leaves, their body runs shifted by
+ * src_offset (where the source bodies sit in the P2P body arrays); no self
+ * leaf, no coincident scan (see fmm_p2p_coincident). */
 FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
-                 int32_t body_lo, int32_t body_hi,
-                 const int64_t *rows, const int32_t *src_sorted, const double *xs, const double *ys,
-                 const double *zs, const uint64_t *keys, const int32_t *src_start, const int32_t *src_end,
-                 int32_t src_offset, int32_t *leaf_rows, int64_t *run_off, void *runs,
-                 int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows, int32_t *dev_nrows,
+                 int32_t body_lo, int32_t body_hi, const int64_t *rows, const int32_t *src,
+                 const double *xs, const double *ys, const double *zs,
+                 const uint64_t *keys, const uint8_t *src_leaf, int32_t src_ncells, const int32_t *src_start,
+                 const int32_t *src_end, int32_t src_offset, int32_t *leaf_rows, int64_t *run_rng, void *runs,
+                 int64_t cap_runs,
+                 int64_t *host_nruns, int32_t *host_nleaf_rows, int32_t *dev_nrows,
                  unsigned long long *dev_stats, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- executors (src/traversal.py:500-548) ------------------------------ */
@@ -303,7 +327,7 @@ FMM_API int fmm_m2p_csr(int p, int32_t ncells, const int64_t *rows, const int32_
  * there): the target leaf's own bodies are then not swept as sources. */
 FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_t nrows, const int32_t *dev_nrows,
             const int32_t *leaf_rows,
-            const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
+            const int32_t *start, const int32_t *end, const int64_t *run_rng, const void *runs,
             const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
             const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);
 
@@ -311,7 +335,7 @@ FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_t n
  * float64, which the reference skips and counts as p2p_skipped,
  * src/traversal.py:552-597), added into *count. */
 FMM_API int fmm_p2p_coincident(int32_t nrows, const int32_t *dev_nrows, const int32_t *leaf_rows,
-                       const int32_t *start, const int32_t *end, const int64_t *run_off, const void *runs,
+                       const int32_t *start, const int32_t *end, const int64_t *run_rng, const void *runs,
                        const double *xs, const double *ys, const double *zs, unsigned long long *count,
                        void *stream);
 

@@ -38,7 +38,7 @@ SIGNATURES = {
     "fmm_morton_keys": [P, P, P, I64, P, P, P, P],
     "fmm_sort_pairs_u64": [P, P, P, P, I64, INT, P, SZ, P],
     "fmm_permute_bodies": [P, P, P, P, P, I64, P, P, P, P, P, P, P, P],
-    "fmm_carve_count": [P, I64, I32, INT, P, P, P, P, P, SZ, P],
+    "fmm_carve_count": [P, I64, I32, INT, P, P, P, P, P, P, P, SZ, P],
     "fmm_carve_emit": [P, I64, P, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, INT, INT, P, P, P, P, P, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
@@ -47,6 +47,7 @@ SIGNATURES = {
                           P, P, I64, P, P, I64, P, P],
     "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P,
                      P, I64, P, P],
+    "fmm_pairs_to_rows": [P, P, P, I64, I32, I32, INT, P, P, P, SZ, P],
     "fmm_partition_owner": [I32, P, P, P, P, I64, P, P],
     "fmm_traverse_mutual": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64,
                             P, P],
@@ -54,7 +55,9 @@ SIGNATURES = {
                               I64, P, P, I64, P, P, SZ, P],
     "fmm_listfmm_lists": [I32, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, I64, P, P, I64, P, P, SZ, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
-    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, I32, P, P, P, I64, P, P, P, P, P, SZ, P],
+    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, I32, P, P, I32, P, P, P, I64, P, P, P, P, P, SZ,
+                     P],
+    "fmm_sort_rows": [I32, P, P, P, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P, P],
     "fmm_m2p_csr": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],

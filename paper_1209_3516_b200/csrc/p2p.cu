@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
         const int rem = cnt & 7;
         const int nblk = (cnt >> 3) + (rem ? 1 : 0);
         const bool small_last = rem != 0 && rem <= 4;
-        const int64_t r0 = run_off[row], r1 = run_off[row + 1];
+        const int64_t r0 = run_off[2 * (int64_t)row], r1 = run_off[2 * (int64_t)row + 1];
         const int nr = (int)(r1 - r0);
         // streamed rows split every block's source line over the warps by
         // weight (P = kP2PWarps partials per block, folded below)
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32) p2p_f64_kernel(
         const int32_t ts = start[t], cnt = end[t] - ts;
         const int nblk = (cnt + K - 1) / K;
         const int nparts = nblk >= kP2PWarps ? 1 : kP2PWarps / nblk;
-        const int64_t r0 = run_off[row], r1 = run_off[row + 1];
+        const int64_t r0 = run_off[2 * (int64_t)row], r1 = run_off[2 * (int64_t)row + 1];
         const int rounds = (nblk + kP2PWarps - 1) / kP2PWarps;
         for (int rd = 0; rd < (nparts > 1 ? 1 : rounds); rd++) {
             int tb, part;
@@ -727,7 +727,7 @@ __global__ void p2p_coincident_kernel(int32_t nrows_host, const int32_t *__restr
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
         const int32_t t = leaf_rows[row];
         const int32_t ts = start[t], cnt = end[t] - ts;
-        for (int64_t r = run_off[row]; r < run_off[row + 1]; r++) {
+        for (int64_t r = run_off[2 * (int64_t)row]; r < run_off[2 * (int64_t)row + 1]; r++) {
             const int4 run = runs[r];
             const int64_t len = run.y - run.x, tot = len * cnt;
             for (int64_t k = threadIdx.x; k < tot; k += blockDim.x) {

@@ -18,58 +18,139 @@
 
 namespace fmm {
 
-// Source leaves of a target row merge into one body run when adjacent; in
-// a one-tree evaluation the target's own leaf always stands alone (self).
-// cross: sources belong to another tree (no self leaf).
-__device__ inline bool run_start(const int32_t *src, int64_t k, int64_t k0, int32_t t,
-                                 const int32_t *sstart, const int32_t *send, int cross) {
-    if (k == k0) return true;
-    int32_t s = src[k], sp = src[k - 1];
-    return (!cross && (s == t || sp == t)) || sstart[s] != send[sp];
-}
+// One warp per target row does the whole plan.  Source leaves are handled
+// as leaf ORDINALS (rank among the source tree's leaves in pre-order):
+// leaves in pre-order own consecutive body ranges, so two sources share a
+// body run exactly when their ordinals are consecutive.  The warp marks the
+// row's ordinals in a shared-memory bitmap (the row's sources are
+// distinct) and reads the runs straight off the bitmap with word-level bit
+// operations -- run starts are set bits whose predecessor bit is clear,
+// run ends set bits whose successor is clear, the self leaf a run of its
+// own -- each lane owning a contiguous block of words, so the sorted row is
+// never materialised.  Runs are stored row-locally at the row's own CSR
+// offset (runs <= pairs), in ascending source order.  The pair counters
+// follow the reference: pairs = sum |t| |s| - self |t| - coincident, where
+// the coincident ordered pairs (r2 == 0.0 in float64) can only occur inside
+// the target leaf itself, and only between bodies with equal depth-21 keys
+// -- with the sorted keys given, leaves without two equal adjacent keys
+// skip the O(|t|^2) scan.
+constexpr int kPlanWarps = 8;
+constexpr int kPlanSegWords = 1024;  // 32768 ordinals per bitmap pass
 
-// Runs per row (nr) and the reference's pair counters in one pass over the
-// row's sources: pairs = sum |t| |s| - self |t| - coincident, where the
-// coincident ordered pairs (r2 == 0.0 in float64) can only occur inside the
-// target leaf itself, and only between bodies with equal depth-21 keys --
-// with the sorted keys given, leaves without two equal adjacent keys skip
-// the O(|t|^2) scan.
-__global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells, const int32_t *__restrict__ leaf_rows,
-                           const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
-                           const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-                           const int32_t *__restrict__ sstart, const int32_t *__restrict__ send, int cross,
-                           const double *__restrict__ xs, const double *__restrict__ ys,
-                           const double *__restrict__ zs, const uint64_t *__restrict__ keys, int64_t *nr,
-                           unsigned long long *stats) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
+    const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows,
+    const int32_t *__restrict__ src, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+    const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
+    const int32_t *__restrict__ s_bend, int cross, int32_t soff, const double *__restrict__ xs,
+    const double *__restrict__ ys, const double *__restrict__ zs, const uint64_t *__restrict__ keys,
+    int64_t *run_rng, int4 *runs, unsigned long long *stats) {
+    __shared__ uint32_t bm_all[kPlanWarps][kPlanSegWords + 2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *bm = bm_all[wid] + 1;  // bm[-1] and bm[kPlanSegWords] stay 0: neighbour words of the edges
+    for (int x = lane; x < kPlanSegWords + 2; x += 32) bm_all[wid][x] = 0u;
+    __syncwarp();
     const int32_t nrows = *nrows_dev;
-    // rows past the device count get 0 so one scan over ncells + 1 works
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < ncells;
-         r += (gridDim.x * blockDim.x) >> 5) {
-        if (r >= nrows) {
-            if (lane == 0) nr[r] = 0;
-            continue;
-        }
+    for (int32_t r = blockIdx.x * kPlanWarps + wid; r < nrows; r += gridDim.x * kPlanWarps) {
         const int32_t t = leaf_rows[r];
         const int64_t k0 = rows[t], k1 = rows[t + 1];
         const int32_t ts = start[t], te = end[t];
         const int64_t nt = te - ts;
-        int64_t cnt = 0;
-        unsigned long long blocks = 0, skipped = 0;
+        const int32_t ot = cross ? -1 : t_ord[t];  // the self leaf's ordinal
+        uint32_t lo = 0xffffffffu, hi = 0u;
+        for (int64_t k = k0 + lane; k < k1; k += 32) {
+            const uint32_t v = (uint32_t)s_ord[src[k]];
+            lo = min(lo, v);
+            hi = max(hi, v);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        long long blocks = 0;
+        unsigned long long skipped = 0;
         bool self = false;
-        for (int64_t kb = k0; kb < k1; kb += 32) {
-            const int64_t k = kb + lane;
-            const bool valid = k < k1;
-            const bool f = valid && run_start(src, k, k0, t, sstart, send, cross);
-            cnt += __popc(__ballot_sync(0xffffffffu, f));
-            if (valid) {
-                const int32_t s = src[k];
-                blocks += (unsigned long long)(nt * (send[s] - sstart[s]));
-                if (!cross && s == t) {
-                    blocks -= (unsigned long long)nt;
+        int64_t nrun = 0;        // runs so far in this row (warp-uniform)
+        uint32_t prev_top = 0u;  // bit 31 of the word before the current pass
+        for (uint32_t seg = lo >> 15; k1 > k0 && seg <= (hi >> 15); seg++) {
+            const uint32_t sbase = seg << 15;
+            bool next_first = false;  // is ordinal sbase + 32768 (next pass) set?
+            for (int64_t k = k0 + lane; k < k1; k += 32) {
+                const uint32_t v = (uint32_t)s_ord[src[k]];
+                if ((v >> 15) == seg) atomicOr(&bm[(v >> 5) & (kPlanSegWords - 1)], 1u << (v & 31u));
+                next_first |= v == sbase + 32768u;
+            }
+            next_first = __any_sync(0xffffffffu, next_first);
+            __syncwarp();
+            // the pass's word window, split into contiguous per-lane blocks
+            const uint32_t wa = (seg == (lo >> 15)) ? ((lo >> 5) & (kPlanSegWords - 1)) : 0u;
+            const uint32_t wb = (seg == (hi >> 15)) ? ((hi >> 5) & (kPlanSegWords - 1)) : kPlanSegWords - 1;
+            const uint32_t nw = wb - wa + 1, per = (nw + 31) / 32;
+            const uint32_t w0 = wa + min(lane * per, nw), w1 = wa + min(lane * per + per, nw);
+            const int32_t self_word = (ot >= 0 && ((uint32_t)ot >> 15) == seg) ? (int32_t)(((uint32_t)ot >> 5) & 1023u) : -2;
+            const int32_t prev_self = (ot >= 0 && (uint32_t)ot + 1u == sbase) ? 1 : 0;  // self just before this pass
+            const int32_t next_self = (ot >= 0 && (uint32_t)ot == sbase + 32768u) ? 1 : 0;
+            // masks of run starts / ends in word x
+            auto masks = [&](uint32_t x, uint32_t &st, uint32_t &en) {
+                const uint32_t W = bm[x];
+                const uint32_t P = (x == 0) ? (prev_top << 31) : bm[x - 1];
+                const uint32_t N = (x == kPlanSegWords - 1) ? (next_first ? 1u : 0u) : bm[x + 1];
+                uint32_t Bs = 0u, Be = 0u;  // forced starts / ends around the self leaf
+                if ((int32_t)x == self_word) {
+                    const uint32_t M = 1u << ((uint32_t)ot & 31u);
+                    Bs |= M | (M << 1);
+                    Be |= M | (M >> 1);
+                }
+                if ((int32_t)x - 1 == self_word && ((uint32_t)ot & 31u) == 31u) Bs |= 1u;
+                if ((int32_t)x + 1 == self_word && ((uint32_t)ot & 31u) == 0u) Be |= 1u << 31;
+                if (x == 0 && prev_self) Bs |= 1u;
+                if (x == kPlanSegWords - 1 && next_self) Be |= 1u << 31;
+                st = W & (~((W << 1) | (P >> 31)) | Bs);
+                en = W & (~((W >> 1) | (N << 31)) | Be);
+            };
+            int cnt = 0;
+            for (uint32_t x = w0; x < w1; x++) {
+                uint32_t st, en;
+                masks(x, st, en);
+                cnt += __popc(st);
+            }
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int64_t idx = k0 + nrun + (incl - cnt) - 1;  // run holding the entry before this lane's block
+            for (uint32_t x = w0; x < w1; x++) {
+                uint32_t st, en;
+                masks(x, st, en);
+                for (uint32_t m = st | en; m; m &= m - 1u) {
+                    const uint32_t bit = (uint32_t)__ffs(m) - 1u, b = 1u << bit;
+                    const uint32_t o = sbase + (x << 5) + bit;
+                    if (st & b) {
+                        ++idx;
+                        const int32_t b0 = s_bstart[o];
+                        // component stores: the run's end may be written by
+                        // another lane (a run crossing lane blocks)
+                        runs[idx].x = b0 + soff;
+                        runs[idx].z = (int32_t)o == ot ? 1 : 0;
+                        runs[idx].w = 0;
+                        blocks -= (long long)nt * b0;
+                    }
+                    if (en & b) {
+                        const int32_t b1 = s_bend[o];
+                        runs[idx].y = b1 + soff;
+                        blocks += (long long)nt * b1;
+                    }
+                }
+                if ((int32_t)x == self_word && (bm[x] >> ((uint32_t)ot & 31u) & 1u)) {
+                    blocks -= (long long)nt;
                     self = true;
                 }
             }
+            nrun += __shfl_sync(0xffffffffu, incl, 31);
+            __syncwarp();  // every lane read its neighbours' words
+            prev_top = bm[kPlanSegWords - 1] >> 31;
+            __syncwarp();
+            for (uint32_t x = w0; x < w1; x++) bm[x] = 0u;
+            __syncwarp();
         }
         // coincident pairs inside the target leaf (only if the self pair is listed)
         self = __any_sync(0xffffffffu, self);
@@ -91,44 +172,42 @@ __global__ void plan_count(const int32_t *__restrict__ nrows_dev, int32_t ncells
             skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
         }
         if (lane == 0) {
-            nr[r] = cnt;
+            run_rng[2 * (int64_t)r] = k0;
+            run_rng[2 * (int64_t)r + 1] = k0 + nrun;
             if (stats) {
-                atomicAdd(&stats[0], blocks - skipped);
+                atomicAdd(&stats[0], (unsigned long long)blocks - skipped);
                 atomicAdd(&stats[1], skipped);
+                atomicAdd(&stats[2], (unsigned long long)nrun);
             }
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) nr[ncells] = 0;
 }
 
-__global__ void plan_write(const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
-                           const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
-                           const int32_t *__restrict__ sstart, const int32_t *__restrict__ send, int cross,
-                           int32_t soff, const int64_t *__restrict__ run_off, int4 *runs) {
-    const int lane = threadIdx.x & 31;
-    const int32_t nrows = *nrows_dev;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows;
-         r += (gridDim.x * blockDim.x) >> 5) {
-        const int32_t t = leaf_rows[r];
-        const int64_t k0 = rows[t], k1 = rows[t + 1];
-        int64_t base = run_off[r] - 1;  // index of the run holding the previous entry
-        for (int64_t kb = k0; kb < k1; kb += 32) {
-            int64_t k = kb + lane;
-            bool valid = k < k1;
-            bool f = valid && run_start(src, k, k0, t, sstart, send, cross);
-            bool last = valid && (k + 1 == k1 || run_start(src, k + 1, k0, t, sstart, send, cross));
-            unsigned m = __ballot_sync(0xffffffffu, f);
-            int64_t idx = base + __popc(m & ((2u << lane) - 1u));
-            if (f) {
-                int32_t s = src[k];
-                runs[idx].x = sstart[s] + soff;
-                runs[idx].z = (!cross && s == t) ? 1 : 0;
-                runs[idx].w = 0;
-            }
-            if (last) runs[idx].y = send[src[k]] + soff;
-            base += __popc(m);
+// Leaf ordinals: ord[c] = number of leaves before c in pre-order (an
+// exclusive scan of the leaf flags), cell[ord[c]] = c for leaves.
+__global__ void leaf_cells_kernel(int32_t ncells, const uint8_t *__restrict__ leaf, const int32_t *__restrict__ ord,
+                                  const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                                  int32_t *bstart, int32_t *bend) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x)
+        if (leaf[c]) {
+            bstart[ord[c]] = start[c];
+            bend[ord[c]] = end[c];
         }
-    }
+}
+
+struct LeafFlag {
+    __host__ __device__ __forceinline__ int32_t operator()(uint8_t v) const { return v ? 1 : 0; }
+};
+
+static int leaf_ordinals(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
+                         int32_t *ord, int32_t *bstart, int32_t *bend, Arena &ar, cudaStream_t s) {
+    cub::TransformInputIterator<int32_t, LeafFlag, const uint8_t *> flags(leaf, LeafFlag());
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, flags, ord, ncells, s);
+    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, flags, ord, ncells, s);
+    leaf_cells_kernel<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, ord, start, end, bstart, bend); fmm::note_launch();
+    return FMM_OK;
 }
 
 __global__ void leaf_in_range(int32_t ncells, const uint8_t *leaf, const int32_t *start, int32_t lo, int32_t hi,
@@ -143,49 +222,59 @@ using namespace fmm;
 
 
 extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
-                            int32_t body_lo, int32_t body_hi,
-                            const int64_t *rows, const int32_t *src_sorted, const double *xs,
-                            const double *ys, const double *zs, const uint64_t *keys, const int32_t *src_start,
-                            const int32_t *src_end, int32_t src_offset, int32_t *leaf_rows, int64_t *run_off,
-                            void *runs, int64_t cap_runs, int64_t *host_nruns, int32_t *host_nleaf_rows,
-                            int32_t *dev_nrows, unsigned long long *dev_stats, void *ws, size_t ws_bytes,
-                            void *stream) {
+                            int32_t body_lo, int32_t body_hi, const int64_t *rows, const int32_t *src,
+                            const double *xs, const double *ys, const double *zs,
+                            const uint64_t *keys, const uint8_t *src_leaf, int32_t src_ncells,
+                            const int32_t *src_start, const int32_t *src_end, int32_t src_offset, int32_t *leaf_rows,
+                            int64_t *run_rng, void *runs, int64_t cap_runs, int64_t *host_nruns,
+                            int32_t *host_nleaf_rows, int32_t *dev_nrows, unsigned long long *dev_stats, void *ws,
+                            size_t ws_bytes, void *stream) {
     cudaStream_t s = as_stream(stream);
+    const int cross = src_start != nullptr;
+    if (cross && (!src_end || !src_leaf || src_ncells <= 0)) {
+        set_error("cross-tree plan needs the source tree's leaf flags, starts, ends and cell count");
+        return FMM_ERR_INVALID;
+    }
     Arena ar(ws, ws_bytes);
     int32_t *nsel = ar.take<int32_t>(1);
-    int64_t *nr = ar.take<int64_t>((size_t)ncells + 1);
+    unsigned long long *st3 = ar.take<unsigned long long>(3);
     uint8_t *flag = ar.take<uint8_t>((size_t)ncells);
-    if (!nsel || !nr || !flag) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    int32_t *t_ord = ar.take<int32_t>((size_t)ncells);
+    int32_t *t_bs = ar.take<int32_t>((size_t)ncells);
+    int32_t *t_be = ar.take<int32_t>((size_t)ncells);
+    int32_t *s_ord = cross ? ar.take<int32_t>((size_t)src_ncells) : t_ord;
+    int32_t *s_bs = cross ? ar.take<int32_t>((size_t)src_ncells) : t_bs;
+    int32_t *s_be = cross ? ar.take<int32_t>((size_t)src_ncells) : t_be;
+    if (!nsel || !st3 || !flag || !t_ord || !t_bs || !t_be || !s_ord || !s_bs || !s_be) {
+        set_error("workspace too small");
+        return FMM_ERR_INVALID;
+    }
+    int rc = leaf_ordinals(ncells, leaf, start, end, t_ord, t_bs, t_be, ar, s);
+    if (rc == FMM_OK && cross) rc = leaf_ordinals(src_ncells, src_leaf, src_start, src_end, s_ord, s_bs, s_be, ar, s);
+    if (rc != FMM_OK) return rc;
     leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag); fmm::note_launch();
     size_t need = 0;
     cub::CountingInputIterator<int32_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, need, it, flag, leaf_rows, nsel, ncells, s);
     if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
     cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, leaf_rows, nsel, ncells, s);
-    // leaf_rows is sized ncells: the kernels read the row count on the device
-    const int g = grid_for((int64_t)ncells * 32, 256, 148 * 16);
-    if (dev_stats) cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
-    const int cross = src_start != nullptr;
-    const int32_t *ss = cross ? src_start : start, *se = cross ? src_end : end;
-    plan_count<<<g, 256, 0, s>>>(nsel, ncells, leaf_rows, rows, src_sorted, start, end, ss, se, cross, xs, ys, zs,
-                                 keys, nr, dev_stats); fmm::note_launch();
-    need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, nr, run_off, ncells + 1, s);
-    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
-    cub::DeviceScan::ExclusiveSum(ar.rest(), need, nr, run_off, ncells + 1, s);
+    cudaMemsetAsync(st3, 0, 3 * sizeof(unsigned long long), s);
+    // leaf_rows is sized ncells: the kernel reads the row count on the device
+    plan_rows_kernel<<<grid_for(ncells, kPlanWarps, 148 * 8), kPlanWarps * 32, 0, s>>>(
+        nsel, leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross, cross ? src_offset : 0, xs, ys, zs,
+        keys, run_rng, (int4 *)runs, st3); fmm::note_launch();
+    if (dev_stats) cudaMemcpyAsync(dev_stats, st3, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s);
+    if (dev_nrows) cudaMemcpyAsync(dev_nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
     if (host_nleaf_rows || host_nruns) {  // optional host view (synchronises)
         int32_t nrows = 0;
-        int64_t total = 0;
+        unsigned long long total = 0;
         cudaMemcpyAsync(&nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(&total, run_off + ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&total, st3 + 2, sizeof(total), cudaMemcpyDeviceToHost, s);
         if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
         if (host_nleaf_rows) *host_nleaf_rows = nrows;
-        if (host_nruns) *host_nruns = total;
-        if (total > cap_runs) { set_error("run capacity %lld < %lld", (long long)cap_runs, (long long)total); return FMM_ERR_CAPACITY; }
+        if (host_nruns) *host_nruns = (int64_t)total;
     }
-    if (dev_nrows) cudaMemcpyAsync(dev_nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
-    plan_write<<<g, 256, 0, s>>>(nsel, leaf_rows, rows, src_sorted, ss, se, cross, cross ? src_offset : 0, run_off,
-                                 (int4 *)runs); fmm::note_launch();
+    (void)cap_runs;
     FMM_CUDA_CHECK("fmm_p2p_plan");
     return FMM_OK;
 }

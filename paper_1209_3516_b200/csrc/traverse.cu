@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include "fmm_common.cuh"
+#include "rowsort.cuh"
 
 namespace fmm {
 
@@ -150,6 +151,164 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                 in++;
             }
         }
+    }
+}
+
+// ---- CSR by counting (sync-free) -------------------------------------------
+// Row sizes by atomic counting, an exclusive scan, an atomic scatter and a
+// segmented sort of every row's sources: the same (target, source)-sorted
+// CSR as the radix path, but the pair count is read on the device, so the
+// host never waits for the traversal.
+// A thread's emitted pairs are contiguous and often share their target, so
+// the warp groups equal targets (match_any) and one lane per group issues
+// the atomic.  Trip counts are warp-uniform so the match sees full warps.
+__global__ void row_count_kernel(const int32_t *__restrict__ t, const unsigned long long *__restrict__ dev_n,
+                                 int64_t cap, unsigned long long *cnt) {
+    int64_t n = (int64_t)*dev_n;
+    if (n > cap) n = cap;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nround = (n + stride - 1) / stride;
+    for (int64_t r = 0; r < nround; r++) {
+        const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        const int32_t key = k < n ? t[k] : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&cnt[key], (unsigned long long)__popc(grp));
+    }
+}
+
+__global__ void row_scatter_kernel(const int32_t *__restrict__ t, const int32_t *__restrict__ s,
+                                   const unsigned long long *__restrict__ dev_n, int64_t cap,
+                                   unsigned long long *cursor, int32_t *out) {
+    int64_t n = (int64_t)*dev_n;
+    if (n > cap) n = cap;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nround = (n + stride - 1) / stride;
+    for (int64_t r = 0; r < nround; r++) {
+        const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        const int32_t key = k < n ? t[k] : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(grp) - 1;
+        unsigned long long base = 0;
+        if (key >= 0 && lane == leader) base = atomicAdd(&cursor[key], (unsigned long long)__popc(grp));
+        base = __shfl_sync(grp, base, leader);
+        if (key >= 0) out[base + __popc(grp & ((1u << lane) - 1u))] = s[k];
+    }
+}
+
+// Per-row sort of the scattered sources (a row's sources are distinct, so
+// stability is moot): one CTA per row, the row in registers, a block radix
+// sort over the source-id bits.  Rows longer than the tile are queued for
+// the large-tile kernel (and, past its tile, the in-memory bitonic one).
+constexpr int kRowSmallThreads = 256, kRowSmallItems = 4;    // 1024 keys
+constexpr int kRowLargeThreads = 512, kRowLargeItems = 16;   // 8192 keys
+
+template <int THREADS, int ITEMS>
+__device__ __forceinline__ void row_sort_tile(const int32_t *in, int32_t *out, int64_t len, int nbits,
+                                              typename cub::BlockRadixSort<int32_t, THREADS, ITEMS>::TempStorage &tmp) {
+    int32_t keys[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const int64_t k = (int64_t)i * THREADS + threadIdx.x;  // striped load
+        keys[i] = k < len ? in[k] : (int32_t)((1u << nbits) - 1u);
+    }
+    // ids are below 2^nbits, so the all-ones pads sort last (a pad equal to
+    // an id is indistinguishable from it in the output)
+    cub::BlockRadixSort<int32_t, THREADS, ITEMS>(tmp).SortBlockedToStriped(keys, 0, nbits);
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const int64_t k = (int64_t)i * THREADS + threadIdx.x;
+        if (k < len) out[k] = keys[i];
+    }
+}
+
+__global__ void __launch_bounds__(kRowSmallThreads) row_sort_small_kernel(
+    int32_t ncells, const int64_t *__restrict__ rows, const int32_t *__restrict__ in, int32_t *out, int nbits,
+    int32_t *long_rows, unsigned long long *nlong) {
+    __shared__ typename cub::BlockRadixSort<int32_t, kRowSmallThreads, kRowSmallItems>::TempStorage tmp;
+    for (int32_t r = blockIdx.x; r < ncells; r += gridDim.x) {
+        const int64_t b = rows[r], len = rows[r + 1] - b;
+        if (len <= 1) {
+            if (len == 1 && threadIdx.x == 0) out[b] = in[b];
+            continue;
+        }
+        if (len > (int64_t)kRowSmallThreads * kRowSmallItems) {
+            if (threadIdx.x == 0) long_rows[atomicAdd(nlong, 1ull)] = r;
+            continue;
+        }
+        row_sort_tile<kRowSmallThreads, kRowSmallItems>(in + b, out + b, len, nbits, tmp);
+        __syncthreads();  // tmp is reused by the next row
+    }
+}
+
+__global__ void __launch_bounds__(kRowLargeThreads) row_sort_large_kernel(
+    const int64_t *__restrict__ rows, const int32_t *__restrict__ in, int32_t *out, int nbits,
+    const int32_t *__restrict__ long_rows, const unsigned long long *__restrict__ nlong, int32_t *huge_rows,
+    unsigned long long *nhuge) {
+    __shared__ typename cub::BlockRadixSort<int32_t, kRowLargeThreads, kRowLargeItems>::TempStorage tmp;
+    const int64_t n = (int64_t)*nlong;
+    for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const int32_t r = long_rows[k];
+        const int64_t b = rows[r], len = rows[r + 1] - b;
+        if (len > (int64_t)kRowLargeThreads * kRowLargeItems) {
+            if (threadIdx.x == 0) huge_rows[atomicAdd(nhuge, 1ull)] = r;
+            continue;
+        }
+        row_sort_tile<kRowLargeThreads, kRowLargeItems>(in + b, out + b, len, nbits, tmp);
+        __syncthreads();
+    }
+}
+
+// Bitmap sort (rowsort.cuh): one warp per row.
+constexpr int kRowBitmapWarps = 8;
+
+__global__ void __launch_bounds__(kRowBitmapWarps * 32) row_sort_bitmap_kernel(
+    int32_t ncells, const int64_t *__restrict__ rows, const int32_t *__restrict__ in, int32_t *out) {
+    __shared__ uint32_t bm_all[kRowBitmapWarps][kSortSegWords];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int32_t r = blockIdx.x * kRowBitmapWarps + w; r < ncells; r += gridDim.x * kRowBitmapWarps)
+        warp_bitmap_sort(in, out, rows[r], rows[r + 1], bm_all[w], lane);
+}
+
+// Rows past the large tile: copy, then an all-ascending bitonic sort in
+// global memory by one CTA (a mirrored compare opens every merge, so the
+// virtual +inf entries past the row never move and need no storage).
+__global__ void __launch_bounds__(1024) row_sort_huge_kernel(const int64_t *__restrict__ rows,
+                                                             const int32_t *__restrict__ in, int32_t *out,
+                                                             const int32_t *__restrict__ huge_rows,
+                                                             const unsigned long long *__restrict__ nhuge) {
+    const int64_t n = (int64_t)*nhuge;
+    for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const int32_t r = huge_rows[k];
+        const int64_t b = rows[r], len = rows[r + 1] - b;
+        int32_t *v = out + b;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) v[i] = in[b + i];
+        int64_t p2 = 1;
+        while (p2 < len) p2 <<= 1;
+        __syncthreads();
+        for (int64_t size = 2; size <= p2; size <<= 1) {
+            const int64_t half = size >> 1;
+            for (int64_t i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+                const int64_t lo = (i / half) * size + (i % half), hi = (i / half) * size + size - 1 - (i % half);
+                if (hi < len) {
+                    const int32_t x = v[lo], y = v[hi];
+                    if (x > y) { v[lo] = y; v[hi] = x; }
+                }
+            }
+            __syncthreads();
+            for (int64_t stride = half >> 1; stride > 0; stride >>= 1) {
+                for (int64_t i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+                    const int64_t lo = (i / stride) * stride * 2 + (i % stride), hi = lo + stride;
+                    if (hi < len) {
+                        const int32_t x = v[lo], y = v[hi];
+                        if (x > y) { v[lo] = y; v[hi] = x; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -762,6 +921,62 @@ int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_off, const
         ncells, level, key, parent, children, leaf, sub_end, start, end, body_lo, body_hi, tab, m2l_t, m2l_s,
         cap_m2l, p2p_t, p2p_s, cap_p2p, dev_counts, dev_counts + 1); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_listfmm_lists");
+    return FMM_OK;
+}
+
+int fmm_sort_rows(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, void *stream) {
+    row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0,
+                             as_stream(stream)>>>(ncells, rows, in, out); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_sort_rows");
+    return FMM_OK;
+}
+
+int fmm_pairs_to_rows(const int32_t *t, const int32_t *s, const unsigned long long *dev_npairs, int64_t cap,
+                      int32_t ncells, int32_t nsrc, int sort_rows, int32_t *src_sorted, int64_t *rows, void *ws,
+                      size_t ws_bytes, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (nsrc <= 0) nsrc = ncells;
+    int nbits = 1;
+    while ((1ll << nbits) < (int64_t)nsrc) nbits++;
+    Arena ar(ws, ws_bytes);
+    unsigned long long *cursor = ar.take<unsigned long long>((size_t)ncells + 1);
+    int32_t *unsorted = ar.take<int32_t>((size_t)(cap > 0 ? cap : 1));
+    int32_t *long_rows = ar.take<int32_t>((size_t)ncells);
+    unsigned long long *nlong = ar.take<unsigned long long>(2);
+    if (!cursor || !unsorted || !long_rows || !nlong) {
+        set_error("workspace too small for %lld pairs", (long long)cap);
+        return FMM_ERR_INVALID;
+    }
+    cudaMemsetAsync(cursor, 0, sizeof(unsigned long long) * ((size_t)ncells + 1), st);
+    cudaMemsetAsync(nlong, 0, 2 * sizeof(unsigned long long), st);
+    const int grid = 148 * 8;
+    row_count_kernel<<<grid, 256, 0, st>>>(t, dev_npairs, cap, cursor); fmm::note_launch();
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, (const int64_t *)cursor, rows, ncells + 1, st);
+    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, (const int64_t *)cursor, rows, ncells + 1, st);
+    cudaMemcpyAsync(cursor, rows, sizeof(int64_t) * ((size_t)ncells + 1), cudaMemcpyDeviceToDevice, st);
+    if (!sort_rows) {  // grouped rows straight into the output
+        row_scatter_kernel<<<grid, 256, 0, st>>>(t, s, dev_npairs, cap, cursor, src_sorted); fmm::note_launch();
+        FMM_CUDA_CHECK("fmm_pairs_to_rows");
+        return FMM_OK;
+    }
+    row_scatter_kernel<<<grid, 256, 0, st>>>(t, s, dev_npairs, cap, cursor, unsorted); fmm::note_launch();
+    // the bitmap sort handles any id range (one 32768-id window per pass);
+    // the block radix tiles remain as a cross-check (FMM_B200_ROWSORT_RADIX=1)
+    if (!getenv("FMM_B200_ROWSORT_RADIX")) {
+        row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0, st>>>(
+            ncells, rows, unsorted, src_sorted); fmm::note_launch();
+        FMM_CUDA_CHECK("fmm_pairs_to_rows");
+        return FMM_OK;
+    }
+    int32_t *huge_rows = (int32_t *)cursor;
+    row_sort_small_kernel<<<grid_for(ncells, 1, 148 * 16), kRowSmallThreads, 0, st>>>(
+        ncells, rows, unsorted, src_sorted, nbits, long_rows, nlong); fmm::note_launch();
+    row_sort_large_kernel<<<148, kRowLargeThreads, 0, st>>>(rows, unsorted, src_sorted, nbits, long_rows, nlong,
+                                                            huge_rows, nlong + 1); fmm::note_launch();
+    row_sort_huge_kernel<<<148, 1024, 0, st>>>(rows, unsorted, src_sorted, huge_rows, nlong + 1); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_pairs_to_rows");
     return FMM_OK;
 }
 

@@ -438,6 +438,18 @@ __global__ void geometry_finish(int32_t ncells, const unsigned long long *b2, do
         bmax[c] = sqrt(__longlong_as_double((long long)b2[c]));
 }
 
+constexpr int kCarveStage = 3 + MAX_LEVEL + 2;
+
+// Cell count (last exclusive-scan entry + its count) and the caller's flag
+// into the staging block read back in one copy.
+__global__ void carve_stage(const int32_t *__restrict__ cbase, const int32_t *__restrict__ ccount, int64_t n,
+                            const int32_t *__restrict__ flag, int32_t *stage) {
+    if (threadIdx.x == 0) {
+        stage[0] = cbase[n - 1] + ccount[n - 1];
+        stage[2] = flag ? *flag : 0;
+    }
+}
+
 static size_t sort_temp_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
@@ -552,31 +564,31 @@ int fmm_permute_bodies(const int32_t *perm, const double *x, const double *y, co
 }
 
 int fmm_carve_count(const uint64_t *keys, int64_t n, int32_t ncrit, int allow_big, int32_t *cbase,
-                    int8_t *leaf_level, int32_t *host_level_hist, int32_t *host_ncells, void *ws, size_t ws_bytes,
-                    void *stream) {
+                    int8_t *leaf_level, int32_t *host_level_hist, int32_t *host_ncells, const int32_t *dev_flag,
+                    int32_t *host_flag, void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t s = as_stream(stream);
     Arena ar(ws, ws_bytes);
     int32_t *ccount = ar.take<int32_t>(n);
-    int32_t *hist = ar.take<int32_t>(MAX_LEVEL + 2);
-    int *err = ar.take<int>(1);
-    int32_t *last = ar.take<int32_t>(2);
-    if (!ccount || !hist || !err || !last) { set_error("workspace too small"); return FMM_ERR_INVALID; }
-    cudaMemsetAsync(hist, 0, sizeof(int32_t) * (MAX_LEVEL + 2), s);
-    cudaMemsetAsync(err, 0, sizeof(int), s);
-    carve_count<<<grid_for(n, 256), 256, 0, s>>>(keys, n, ncrit, allow_big, ccount, leaf_level, hist, err); fmm::note_launch();
+    // staging for the one host read: {cell count, error, flag, hist[23]}
+    int32_t *stage = ar.take<int32_t>(kCarveStage);
+    if (!ccount || !stage) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    int32_t *hist = stage + 3;
+    cudaMemsetAsync(stage, 0, sizeof(int32_t) * kCarveStage, s);
+    carve_count<<<grid_for(n, 256), 256, 0, s>>>(keys, n, ncrit, allow_big, ccount, leaf_level, hist, stage + 1); fmm::note_launch();
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, ccount, cbase, n, s);
     if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
     cub::DeviceScan::ExclusiveSum(ar.rest(), need, ccount, cbase, n, s);
-    int32_t tail[2] = {0, 0};
-    int herr = 0;
-    cudaMemcpyAsync(&tail[0], cbase + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&tail[1], ccount + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(host_level_hist, hist, sizeof(int32_t) * (MAX_LEVEL + 2), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    carve_stage<<<1, 32, 0, s>>>(cbase, ccount, n, dev_flag, stage); fmm::note_launch();
+    static thread_local int32_t *pinned = nullptr;
+    if (!pinned && cudaMallocHost((void **)&pinned, sizeof(int32_t) * kCarveStage) != cudaSuccess)
+        return cuda_status("fmm_carve_count pinned buffer");
+    cudaMemcpyAsync(pinned, stage, sizeof(int32_t) * kCarveStage, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_carve_count sync");
-    *host_ncells = tail[0] + tail[1];
-    if (herr) {
+    *host_ncells = pinned[0];
+    for (int L = 0; L < MAX_LEVEL + 2; L++) host_level_hist[L] = pinned[3 + L];
+    if (host_flag) *host_flag = pinned[2];
+    if (pinned[1]) {
         set_error("max depth exceeded: more than ncrit=%d bodies share one depth-%d grid cell "
                   "(pass allow_oversized_leaves=True to keep them in one leaf)",
                   ncrit, MAX_LEVEL);

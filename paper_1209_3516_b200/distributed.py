@@ -211,7 +211,8 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     elif cfg.mutual:  # the rank's targets of the mutual lists (directed-expanded)
         lists = mutual_lists(tree, cfg.mac, cfg.task_grain, body_range=(lo, hi), m2l_ready=ready, side=side)
     else:
-        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side)
+        # (exact counts up front: a deferred overflow would need a collective redo)
+        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side, defer=False)
     ev[2].record(main)
     side.wait_event(ready)
     with torch.cuda.stream(side):

@@ -135,15 +135,56 @@ class EvalReport:
 # traversal -> CSR lists
 # ---------------------------------------------------------------------------
 class Lists:
-    """Device interaction lists of one traversal (CSR by target cell)."""
+    """Device interaction lists of one traversal (CSR by target cell).
+
+    A traversal run from a capacity hint does not wait for its counters:
+    ``settle()`` reads them later (one host synchronisation, at the end of
+    the evaluation) and reports whether every list fit its buffer; until
+    then ``n_m2l`` / ``n_p2p`` / ``peak_frontier`` are read on demand."""
+
+    _COUNTS = ("n_m2l", "n_p2p", "peak_frontier")
 
     def __init__(self, **kw):
         self.__dict__.update(kw)
 
+    def __getattr__(self, name):
+        if name == "p2p_src" and "p2p_grp" in self.__dict__:
+            # the P2P plan reads its rows unsorted; sort them when asked
+            grp, rows = self.__dict__["p2p_grp"], self.__dict__["p2p_rows"]
+            out = torch.empty_like(grp)
+            _lib.call("fmm_sort_rows", rows.numel() - 1, _lib.ptr(rows), _lib.ptr(grp), _lib.ptr(out),
+                      _lib.stream_handle())
+            self.__dict__["p2p_src"] = out
+            return out
+        if name in Lists._COUNTS and self.__dict__.get("_deferred") is not None:
+            if not self.settle():
+                raise RuntimeError("interaction lists overflowed their capacity hint; re-evaluate")
+            return self.__dict__[name]
+        raise AttributeError(name)
+
+    def settle(self) -> bool:
+        """Read deferred traversal counters; False if a list overflowed (the
+        lists are then incomplete and the evaluation must be redone)."""
+        d = self.__dict__.get("_deferred")
+        if d is None:
+            return True
+        log, caps, key = d
+        hl = log.tolist()
+        n_p2p, n_m2l, fronts = hl[0], hl[1], hl[2:]
+        peak = max(fronts)
+        self.__dict__.update(n_p2p=n_p2p, n_m2l=n_m2l, peak_frontier=peak, _deferred=None)
+        ok = n_p2p <= caps[0] and n_m2l <= caps[1] and peak <= caps[2] and fronts[-1] == 0
+        if ok:
+            _hint[key] = (max(caps[0], int(n_p2p * 1.02) + 4096), max(caps[1], int(n_m2l * 1.02) + 4096),
+                          max(caps[2], int(peak * 1.05) + 4096))
+        else:
+            _hint.pop(key, None)  # the redo takes the synchronising path
+        return ok
+
     def host_pairs(self, which: str):
         """(targets, sources) int64 numpy arrays sorted by (target, source)."""
         rows = getattr(self, which + "_rows").cpu()
-        src = getattr(self, which + "_src").cpu().long()
+        src = getattr(self, which + "_src")[:int(rows[-1])].cpu().long()
         t = torch.repeat_interleave(torch.arange(rows.numel() - 1), rows[1:] - rows[:-1])
         return t.numpy(), src.numpy()
 
@@ -154,14 +195,16 @@ _hint = {}
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
                       m2l_ready: torch.cuda.Event | None = None,
                       side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False,
-                      src: Tree | None = None) -> Lists:
+                      src: Tree | None = None, defer: bool = True) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
     ``body_range=(lo, hi)`` keeps only pairs whose target cell holds bodies
     in [lo, hi) (a multi-GPU rank's share); the default keeps all.
     ``src`` is a separate source tree (cross-tree lists: sources index its
-    cells, the P2P plan points at its bodies appended after the targets)."""
+    cells, the P2P plan points at its bodies appended after the targets).
+    With ``defer`` and a capacity hint for this shape the host does not wait
+    for the traversal's counters (``Lists.settle``)."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev = tree.device
     P = _lib.ptr
@@ -171,12 +214,35 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     cross = src is not None and src is not tree
     sb = src if cross else tree
     key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, m2l_owner_only, sb.ncells if cross else 0)
-    cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
-                                                 max(4096, tree.ncells * 8)))
     # every step opens one side of a pair: at most depth_A + depth_B + 1 steps
     nsteps = tree.depth + sb.depth + 2
     bcells = _source_cells(tree, src)
     log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
+    if defer and key in _hint and _sync_free():
+        # capacities known from an earlier run of this shape: chain the
+        # traversal, both CSRs and the plan on the device, no host wait
+        cap_p2p, cap_m2l, cap_next = _hint[key]
+        p2p_t, p2p_s, m2l_t, m2l_s = (torch.empty(c, dtype=i32, device=dev)
+                                      for c in (cap_p2p, cap_p2p, cap_m2l, cap_m2l))
+        fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
+        _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
+                  P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), *bcells, P(tree.d_start),
+                  P(tree.d_end), blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p,
+                  P(m2l_t), P(m2l_s), cap_m2l, P(log), st)
+        del fr
+        ncells = tree.ncells
+        items = max(cap_p2p, cap_m2l, tree.n, ncells + 1)
+        wsp, wsb = _lib.workspace(items, dev, stream=torch.cuda.current_stream())
+        m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, cap_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
+                                     dev_n=log[1:], nsrc=sb.ncells)
+        p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, cap_p2p, ncells, dev, wsp, wsb, st, dev_n=log, nsrc=sb.ncells,
+                                 sort=False)
+        del p2p_t, p2p_s, m2l_t, m2l_s
+        return Lists(m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_rows=p2p_rows,
+                     _deferred=(log, (cap_p2p, cap_m2l, cap_next), key),
+                     **_p2p_plan(tree, p2p_grp, p2p_rows, cap_p2p, blo, bhi, wsp, wsb, st, src=src))
+    cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
+                                                 max(4096, tree.ncells * 8)))
     while True:
         p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
         p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
@@ -199,15 +265,15 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         cap_next = max(cap_next, int(peak * 1.05) + 4096)
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
-    # the CSR key packs (target, source) ids: size it for the larger tree
-    ncells = max(tree.ncells, sb.ncells)
-    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
-    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
-    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    ncells = tree.ncells
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n, ncells + 1), dev, stream=torch.cuda.current_stream())
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
+                                 nsrc=sb.ncells)
+    p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, nsrc=sb.ncells, sort=False)
     del p2p_t, p2p_s, m2l_t, m2l_s
-    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
                  p2p_rows=p2p_rows, peak_frontier=peak,
-                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
+                 **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
 
 
 def _source_cells(tree: Tree, src: Tree | None) -> tuple:
@@ -277,46 +343,60 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
     ncells = tree.ncells
-    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n, ncells + 1), dev, stream=torch.cuda.current_stream())
     m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
-    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, sort=False)
     del p2p_t, p2p_s, m2l_t, m2l_s
-    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
                  p2p_rows=p2p_rows, peak_frontier=peak,
-                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+                 **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
-def _csr(t, s, n, ncells, dev, wsp, wsb, stream):
-    """(sources, row offsets) of pairs (t, s) sorted by target then source."""
+def _sync_free() -> bool:
+    """Hinted traversals skip the host wait (FMM_B200_SYNC_FREE=0 disables)."""
+    return os.environ.get("FMM_B200_SYNC_FREE", "1") != "0"
+
+
+def _csr(t, s, n, ncells, dev, wsp, wsb, stream, dev_n=None, nsrc=0, sort=True):
+    """(sources, row offsets) of pairs (t, s) sorted by target then source
+    (counting CSR: per-target counts, scatter, per-row sort).  ``n`` is the
+    pair count, or with ``dev_n`` (a device counter) the buffer capacity, the
+    count then read on the device (no host wait).  Sources are ids below
+    ``nsrc`` (0: ``ncells``).  ``sort=False`` leaves each row's sources in
+    arrival order (the P2P plan sorts its rows itself)."""
     src = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     rows = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
-    _lib.call("fmm_pairs_to_csr", _lib.ptr(t), _lib.ptr(s), n, ncells, _lib.ptr(src), _lib.ptr(rows), wsp, wsb,
-              stream)
+    if dev_n is None:
+        dev_n = torch.full((1,), n, dtype=torch.int64, device=dev)
+    _lib.call("fmm_pairs_to_rows", _lib.ptr(t), _lib.ptr(s), _lib.ptr(dev_n), n, ncells, nsrc, int(sort),
+              _lib.ptr(src), _lib.ptr(rows), wsp, wsb, stream)
     return src, rows
 
 
-def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready):
+def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0):
     """CSR of a far-field list (M2L or M2P).  Only the far field reads it, so
     with a ``side`` stream it is sorted there, off the P2P critical path,
     with its own scratch buffer; ``ready`` is recorded once it is final."""
     if side is None:
-        out = _csr(t, s, n, ncells, dev, wsp, wsb, st)
+        out = _csr(t, s, n, ncells, dev, wsp, wsb, st, dev_n, nsrc)
         if ready is not None:
             ready.record()
         return out
+    if dev_n is None:  # the count, written on this stream before the side stream waits
+        dev_n = torch.full((1,), n, dtype=torch.int64, device=dev)
     traversed = torch.cuda.Event()
     traversed.record()
     side.wait_event(traversed)
-    swp, swb = _lib.workspace(max(n, 1), dev, slot=1, stream=side)
-    out = _csr(t, s, n, ncells, dev, swp, swb, side.cuda_stream)
-    for a in (t, s, *out):
+    swp, swb = _lib.workspace(max(n, ncells + 1, 1), dev, slot=1, stream=side)
+    out = _csr(t, s, n, ncells, dev, swp, swb, side.cuda_stream, dev_n, nsrc)
+    for a in (t, s, *out) + ((dev_n,) if dev_n is not None else ()):
         a.record_stream(side)
     if ready is not None:
         ready.record(side)
     return out
 
 
-def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st,
+def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st,
               src: Tree | None = None) -> dict:
     """P2P run plan + the reference's pair counters (no host round trip:
     runs <= pairs, and the row count stays on the device).  With a separate
@@ -324,19 +404,19 @@ def _p2p_plan(tree: Tree, p2p_src, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
     concatenated body arrays (``CrossBodies``)."""
     dev, P, i32, ncells = tree.device, _lib.ptr, torch.int32, tree.ncells
     leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
-    run_off = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
-    dev_stats = torch.zeros(2, dtype=torch.int64, device=dev)
+    run_off = torch.empty(2 * ncells, dtype=torch.int64, device=dev)  # (first, end) run per row
+    dev_stats = torch.empty(2, dtype=torch.int64, device=dev)
     dev_nrows = torch.empty(1, dtype=i32, device=dev)
     cap_runs = max(n_p2p, 1)
-    runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)
+    runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)  # row-local: runs <= pairs per row
     cross = src is not None and src is not tree
-    sstart, send = (P(src.d_start), P(src.d_end)) if cross else (None, None)
+    sleaf, sstart, send = (P(src.d_leaf), P(src.d_start), P(src.d_end)) if cross else (None, None, None)
     _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
-              P(p2p_src), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), sstart, send,
-              tree.n if cross else 0, P(leaf_rows), P(run_off), P(runs), cap_runs,
+              P(p2p_grp), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), sleaf,
+              src.ncells if cross else 0, sstart, send, tree.n if cross else 0, P(leaf_rows), P(run_off), P(runs), cap_runs,
               None, None, P(dev_nrows), P(dev_stats), wsp, wsb, st)
-    return dict(leaf_rows=leaf_rows, nrows=tree.nleaves, dev_nrows=dev_nrows, run_off=run_off, runs=runs,
-                dev_stats=dev_stats)
+    return dict(p2p_grp=p2p_grp, leaf_rows=leaf_rows, nrows=tree.nleaves, dev_nrows=dev_nrows, run_off=run_off,
+                runs=runs, dev_stats=dev_stats)
 
 
 def run_m2l(tree: Tree, lists: Lists, p: int, src: Tree | None = None) -> None:
@@ -439,14 +519,14 @@ def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | Non
         cap_next = max(cap_next, int(peak * 1.05) + 4096)
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2p * 1.02) + 4096, int(peak * 1.05) + 4096)
-    wsp, wsb = _lib.workspace(max(done_m2p, done_p2p, tree.n), dev)
-    kcells = max(ncells, sb.ncells)  # the CSR key packs ids of both trees
-    m2p_src, m2p_rows = _far_csr(m2p_t, m2p_s, done_m2p, kcells, dev, wsp, wsb, st, side, m2p_ready)
-    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, kcells, dev, wsp, wsb, st)
+    wsp, wsb = _lib.workspace(max(done_m2p, done_p2p, tree.n, ncells + 1), dev)
+    m2p_src, m2p_rows = _far_csr(m2p_t, m2p_s, done_m2p, ncells, dev, wsp, wsb, st, side, m2p_ready,
+                                 nsrc=sb.ncells)
+    p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, nsrc=sb.ncells, sort=False)
     del p2p_t, p2p_s, m2p_t, m2p_s
-    return Lists(n_m2l=0, n_m2p=done_m2p, n_p2p=done_p2p, m2p_src=m2p_src, m2p_rows=m2p_rows, p2p_src=p2p_src,
+    return Lists(n_m2l=0, n_m2p=done_m2p, n_p2p=done_p2p, m2p_src=m2p_src, m2p_rows=m2p_rows,
                  p2p_rows=p2p_rows, peak_frontier=peak,
-                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
+                 **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
 
 
 def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
@@ -478,13 +558,13 @@ def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
         cap_p2p = max(cap_p2p, int(done_p2p * 1.05) + 4096)
         cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096)
-    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n), dev, stream=torch.cuda.current_stream())
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n, ncells + 1), dev, stream=torch.cuda.current_stream())
     m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
-    p2p_src, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st)
+    p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, sort=False)
     del p2p_t, p2p_s, m2l_t, m2l_s
-    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_src=p2p_src,
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
                  p2p_rows=p2p_rows, peak_frontier=0,
-                 **_p2p_plan(tree, p2p_src, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
+                 **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
 def run_m2p(tree: Tree, lists: Lists, p: int, out, src: Tree | None = None) -> None:
@@ -589,11 +669,15 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         e0, e_up0, e_up1, e_down0, e_down1, e_l1, e_pend, e_end = (E() for _ in range(8))
         need_up = src._M is None or src.p != p
         nc = ncoef(p)
-        # every buffer the other streams touch is allocated here, on main
-        M = torch.zeros((src.ncells, nc), dtype=torch.float64, device=dev) if need_up else src._M
-        L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
+        # every buffer the other streams touch is allocated here, on main;
+        # the expansions and the flag share one fill: [M (if rebuilt) | L | flag]
+        nm = src.ncells * nc if need_up else 0
+        nl = tree.ncells * nc
+        buf = torch.zeros(nm + nl + 1, dtype=torch.float64, device=dev)
+        M = buf[:nm].view(src.ncells, nc) if need_up else src._M
+        L = buf[nm:nm + nl].view(tree.ncells, nc)
+        flag = buf[-1:].view(torch.int32)[:1]
         far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
-        flag = torch.zeros(1, dtype=torch.int32, device=dev)
         bodies = CrossBodies(tree, src) if cross else None
         e0.record(main)
         side.wait_event(e0)
@@ -660,6 +744,9 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                   P(tree.d_fz), _lib.stream_handle())
         e_end.record(main)
         e_end.synchronize()
+        if not all([x.settle() for x in parts]):
+            # a hinted list outgrew its buffer: redo with exact counts
+            return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)
         pairs = skipped = 0
         for lists in parts:
             a, b = lists.dev_stats.tolist()

@@ -66,8 +66,8 @@ class Tree:
     # ---- sizes ---------------------------------------------------------
     @property
     def fp32_exact(self) -> bool:
-        """Every float64 input is exactly representable in float32 (read
-        from the device flag on first use -- no synchronisation in the build)."""
+        """Every float64 input is exactly representable in float32 (read in
+        the build's one host transfer; the device flag otherwise)."""
         v = self.__dict__.get("_fp32_exact")
         if v is None:
             v = int(self.d_inexact.item()) == 0
@@ -336,8 +336,9 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         leaf_level = torch.empty(n, dtype=torch.int8, device=dev)
         hist = (C.c_int32 * 23)()
         nc_host = C.c_int32(0)
+        inexact_host = C.c_int32(0)  # read with the counts: no separate sync later
         _lib.call("fmm_carve_count", P(skeys), n, int(ncrit), int(bool(allow_oversized_leaves)), P(cbase),
-                  P(leaf_level), hist, C.byref(nc_host), wsp, wsb, st)
+                  P(leaf_level), hist, C.byref(nc_host), P(inexact), C.byref(inexact_host), wsp, wsb, st)
         ncells = int(nc_host.value)
         nleaves = int(hist[22])
         depth = max(L for L in range(22) if hist[L] > 0)
@@ -379,6 +380,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         d_body_leaf=body_leaf, d_cells_by_level=cells_by_level,
         d_lo=lo, d_hi=hi, d_ctr=ctr, d_bmax=bmax, d_rmax=rmax,
     )
+    tree._fp32_exact = int(inexact_host.value) == 0
     tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
     tree.build_time = time.perf_counter() - t0
     return tree
