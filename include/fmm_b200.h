@@ -246,8 +246,12 @@ FMM_API int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_of
                       unsigned long long *dev_counts, void *ws, size_t ws_bytes, void *stream);
 
 /* Sort every CSR row's ids ascending (rows of distinct ids, e.g. a grouped
- * interaction list): out[rows[c]..rows[c+1]) = sorted in[...]. */
-FMM_API int fmm_sort_rows(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, void *stream);
+ * interaction list): out[rows[c]..rows[c+1]) = sorted in[...].  One warp
+ * per row: a shared-memory bitmap when the row's ids fit one 32768-id
+ * window, a register bitonic sort for wider rows of up to 1024 ids.  ws
+ * holds fmm_workspace_bytes(ncells + 1). */
+FMM_API int fmm_sort_rows(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, void *ws,
+                  size_t ws_bytes, void *stream);
 
 /* The same CSR as fmm_pairs_to_csr without a host pair count: *dev_npairs
  * (a traversal's device counter, clamped to cap) pairs are counted per

@@ -57,7 +57,7 @@ SIGNATURES = {
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
     "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, I32, P, P, I32, P, P, P, I64, P, P, P, P, P, SZ,
                      P],
-    "fmm_sort_rows": [I32, P, P, P, P],
+    "fmm_sort_rows": [I32, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P, P],
     "fmm_m2p_csr": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],

@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include "fmm_common.cuh"
+#include "rowsort.cuh"
 
 namespace fmm {
 
@@ -37,13 +38,56 @@ namespace fmm {
 constexpr int kPlanWarps = 8;
 constexpr int kPlanSegWords = 1024;  // 32768 ordinals per bitmap pass
 
+struct LeafOrd {
+    const int32_t *ord;
+    __device__ __forceinline__ uint32_t operator()(int32_t c) const { return (uint32_t)ord[c]; }
+};
+
+// A row's coincident-pair scan, counters and run range (one warp).
+__device__ __forceinline__ void plan_row_finish(int32_t r, int32_t t, int64_t k0, int64_t nrun, long long blocks,
+                                                bool self, int32_t ts, int32_t te, const double *__restrict__ xs,
+                                                const double *__restrict__ ys, const double *__restrict__ zs,
+                                                const uint64_t *__restrict__ keys, int64_t *run_rng,
+                                                unsigned long long *stats, unsigned long long *nruns_total, int lane) {
+    // coincident pairs inside the target leaf (only if the self pair is listed)
+    unsigned long long skipped = 0;
+    self = __any_sync(0xffffffffu, self);
+    bool dup = keys == nullptr;
+    if (self && !dup)
+        for (int32_t i = ts + lane; i + 1 < te && !dup; i += 32) dup = keys[i] == keys[i + 1];
+    if (self && __any_sync(0xffffffffu, dup)) {
+        for (int64_t i = ts + lane; i < te; i += 32) {
+            for (int64_t j = ts; j < te; j++) {
+                if (j == i) continue;
+                const double dx = xs[i] - xs[j], dy = ys[i] - ys[j], dz = zs[i] - zs[j];
+                const double r2 = dx * dx + dy * dy + dz * dz;
+                if (r2 == 0.0) skipped++;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        blocks += __shfl_xor_sync(0xffffffffu, blocks, o);
+        skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
+    }
+    if (lane == 0) {
+        run_rng[2 * (int64_t)r] = k0;
+        run_rng[2 * (int64_t)r + 1] = k0 + nrun;
+        if (stats) {
+            atomicAdd(&stats[0], (unsigned long long)blocks - skipped);
+            atomicAdd(&stats[1], skipped);
+            atomicAdd(nruns_total, (unsigned long long)nrun);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
     const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows,
     const int32_t *__restrict__ src, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
     const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
     const int32_t *__restrict__ s_bend, int cross, int32_t soff, const double *__restrict__ xs,
     const double *__restrict__ ys, const double *__restrict__ zs, const uint64_t *__restrict__ keys,
-    int64_t *run_rng, int4 *runs, unsigned long long *stats) {
+    int64_t *run_rng, int4 *runs, unsigned long long *stats, unsigned long long *nruns_total, int32_t *wide,
+    unsigned long long *nwide) {
     __shared__ uint32_t bm_all[kPlanWarps][kPlanSegWords + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *bm = bm_all[wid] + 1;  // bm[-1] and bm[kPlanSegWords] stay 0: neighbour words of the edges
@@ -64,8 +108,11 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
+        if (k1 - k0 <= 1024 && (hi >> 15) != (lo >> 15)) {  // several bitmap passes: register sort instead
+            if (lane == 0) wide[atomicAdd(nwide, 1ull)] = r;
+            continue;
+        }
         long long blocks = 0;
-        unsigned long long skipped = 0;
         bool self = false;
         int64_t nrun = 0;        // runs so far in this row (warp-uniform)
         uint32_t prev_top = 0u;  // bit 31 of the word before the current pass
@@ -152,34 +199,100 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
             for (uint32_t x = w0; x < w1; x++) bm[x] = 0u;
             __syncwarp();
         }
-        // coincident pairs inside the target leaf (only if the self pair is listed)
-        self = __any_sync(0xffffffffu, self);
-        bool dup = keys == nullptr;
-        if (self && !dup)
-            for (int32_t i = ts + lane; i + 1 < te && !dup; i += 32) dup = keys[i] == keys[i + 1];
-        if (self && __any_sync(0xffffffffu, dup)) {
-            for (int64_t i = ts + lane; i < te; i += 32) {
-                for (int64_t j = ts; j < te; j++) {
-                    if (j == i) continue;
-                    const double dx = xs[i] - xs[j], dy = ys[i] - ys[j], dz = zs[i] - zs[j];
-                    const double r2 = dx * dx + dy * dy + dz * dz;
-                    if (r2 == 0.0) skipped++;
-                }
-            }
+        plan_row_finish(r, t, k0, nrun, blocks, self, ts, te, xs, ys, zs, keys, run_rng, stats, nruns_total, lane);
+    }
+}
+
+// Rows whose ordinals span several bitmap passes (and hold <= 1024
+// sources): the ordinals are sorted in registers (rowsort.cuh, lane-major:
+// lane l holds sorted positions [l * ITEMS, (l + 1) * ITEMS)), then each
+// lane walks its block with its neighbours' edge values.
+template <int ITEMS>
+__device__ __forceinline__ void plan_row_wide(int32_t r, int32_t t, int64_t k0, int64_t len,
+                                              const int32_t *__restrict__ src, const int32_t *__restrict__ start,
+                                              const int32_t *__restrict__ end, const int32_t *__restrict__ t_ord,
+                                              const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
+                                              const int32_t *__restrict__ s_bend, int cross, int32_t soff,
+                                              const double *__restrict__ xs, const double *__restrict__ ys,
+                                              const double *__restrict__ zs, const uint64_t *__restrict__ keys,
+                                              int64_t *run_rng, int4 *runs, unsigned long long *stats,
+                                              unsigned long long *nruns_total, int lane) {
+    uint32_t v[ITEMS];
+    warp_bitonic_load_sort<ITEMS>(src, k0, len, v, lane, LeafOrd{s_ord});
+    const int32_t ts = start[t], te = end[t];
+    const int64_t nt = te - ts;
+    const uint32_t ot = cross ? 0xfffffffeu : (uint32_t)t_ord[t];
+    uint32_t prev = __shfl_up_sync(0xffffffffu, v[ITEMS - 1], 1);
+    uint32_t next = __shfl_down_sync(0xffffffffu, v[0], 1);
+    if (lane == 0) prev = 0xfffffffdu;   // no predecessor
+    if (lane == 31) next = 0xfffffffdu;  // no successor
+    auto is_start = [&](int i) {
+        const uint32_t o = v[i], p = i ? v[i - 1] : prev;
+        return o == ot || p == ot || o != p + 1u || p == 0xfffffffdu;
+    };
+    auto is_end = [&](int i) {
+        const uint32_t o = v[i], nx = i + 1 < ITEMS ? v[i + 1] : next;
+        return o == ot || nx == ot || nx != o + 1u || nx == 0xffffffffu || nx == 0xfffffffdu;
+    };
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++)
+        if ((int64_t)lane * ITEMS + i < len && is_start(i)) cnt++;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    int64_t idx = k0 + (incl - cnt) - 1;
+    long long blocks = 0;
+    bool self = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        if ((int64_t)lane * ITEMS + i >= len) continue;
+        const uint32_t o = v[i];
+        if (is_start(i)) {
+            ++idx;
+            const int32_t b0 = s_bstart[o];
+            runs[idx].x = b0 + soff;  // component stores: the end may come from another lane
+            runs[idx].z = o == ot ? 1 : 0;
+            runs[idx].w = 0;
+            blocks -= (long long)nt * b0;
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            blocks += __shfl_xor_sync(0xffffffffu, blocks, o);
-            skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
+        if (is_end(i)) {
+            const int32_t b1 = s_bend[o];
+            runs[idx].y = b1 + soff;
+            blocks += (long long)nt * b1;
         }
-        if (lane == 0) {
-            run_rng[2 * (int64_t)r] = k0;
-            run_rng[2 * (int64_t)r + 1] = k0 + nrun;
-            if (stats) {
-                atomicAdd(&stats[0], (unsigned long long)blocks - skipped);
-                atomicAdd(&stats[1], skipped);
-                atomicAdd(&stats[2], (unsigned long long)nrun);
-            }
+        if (o == ot) {
+            blocks -= (long long)nt;
+            self = true;
         }
+    }
+    const int64_t nrun = __shfl_sync(0xffffffffu, incl, 31);
+    plan_row_finish(r, t, k0, nrun, blocks, self, ts, te, xs, ys, zs, keys, run_rng, stats, nruns_total, lane);
+}
+
+__global__ void __launch_bounds__(128) plan_rows_wide_kernel(
+    const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
+    const int32_t *__restrict__ start, const int32_t *__restrict__ end, const int32_t *__restrict__ t_ord,
+    const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart, const int32_t *__restrict__ s_bend,
+    int cross, int32_t soff, const double *__restrict__ xs, const double *__restrict__ ys,
+    const double *__restrict__ zs, const uint64_t *__restrict__ keys, int64_t *run_rng, int4 *runs,
+    unsigned long long *stats, unsigned long long *nruns_total, const int32_t *__restrict__ wide,
+    const unsigned long long *__restrict__ nwide) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = (int64_t)*nwide;
+    for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < n;
+         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t r = wide[q], t = leaf_rows[r];
+        const int64_t k0 = rows[t], len = rows[t + 1] - k0;
+#define FMM_PLAN_WIDE(IT) plan_row_wide<IT>(r, t, k0, len, src, start, end, t_ord, s_ord, s_bstart, s_bend, cross, soff, xs, ys, zs, keys, run_rng, runs, stats, nruns_total, lane)
+        if (len <= 128) FMM_PLAN_WIDE(4);
+        else if (len <= 256) FMM_PLAN_WIDE(8);
+        else if (len <= 512) FMM_PLAN_WIDE(16);
+        else FMM_PLAN_WIDE(32);
+#undef FMM_PLAN_WIDE
     }
 }
 
@@ -236,8 +349,9 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
         return FMM_ERR_INVALID;
     }
     Arena ar(ws, ws_bytes);
-    int32_t *nsel = ar.take<int32_t>(1);
-    unsigned long long *st3 = ar.take<unsigned long long>(3);
+    int32_t *nsel_ws = ar.take<int32_t>(1);
+    unsigned long long *st3 = ar.take<unsigned long long>(4);  // {pairs, skipped, runs, wide rows}
+    int32_t *wide = ar.take<int32_t>((size_t)ncells);
     uint8_t *flag = ar.take<uint8_t>((size_t)ncells);
     int32_t *t_ord = ar.take<int32_t>((size_t)ncells);
     int32_t *t_bs = ar.take<int32_t>((size_t)ncells);
@@ -245,26 +359,31 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     int32_t *s_ord = cross ? ar.take<int32_t>((size_t)src_ncells) : t_ord;
     int32_t *s_bs = cross ? ar.take<int32_t>((size_t)src_ncells) : t_bs;
     int32_t *s_be = cross ? ar.take<int32_t>((size_t)src_ncells) : t_be;
-    if (!nsel || !st3 || !flag || !t_ord || !t_bs || !t_be || !s_ord || !s_bs || !s_be) {
+    if (!nsel_ws || !st3 || !wide || !flag || !t_ord || !t_bs || !t_be || !s_ord || !s_bs || !s_be) {
         set_error("workspace too small");
         return FMM_ERR_INVALID;
     }
     int rc = leaf_ordinals(ncells, leaf, start, end, t_ord, t_bs, t_be, ar, s);
     if (rc == FMM_OK && cross) rc = leaf_ordinals(src_ncells, src_leaf, src_start, src_end, s_ord, s_bs, s_be, ar, s);
     if (rc != FMM_OK) return rc;
+    // the row count and the counters go straight to the caller's buffers
+    int32_t *nsel = dev_nrows ? dev_nrows : nsel_ws;
+    unsigned long long *stats = dev_stats ? dev_stats : st3;
     leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag); fmm::note_launch();
     size_t need = 0;
     cub::CountingInputIterator<int32_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, need, it, flag, leaf_rows, nsel, ncells, s);
     if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
     cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, leaf_rows, nsel, ncells, s);
-    cudaMemsetAsync(st3, 0, 3 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(st3, 0, 4 * sizeof(unsigned long long), s);
+    if (dev_stats) cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
     // leaf_rows is sized ncells: the kernel reads the row count on the device
     plan_rows_kernel<<<grid_for(ncells, kPlanWarps, 148 * 8), kPlanWarps * 32, 0, s>>>(
         nsel, leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross, cross ? src_offset : 0, xs, ys, zs,
-        keys, run_rng, (int4 *)runs, st3); fmm::note_launch();
-    if (dev_stats) cudaMemcpyAsync(dev_stats, st3, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s);
-    if (dev_nrows) cudaMemcpyAsync(dev_nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        keys, run_rng, (int4 *)runs, stats, st3 + 2, wide, st3 + 3); fmm::note_launch();
+    plan_rows_wide_kernel<<<148 * 4, 128, 0, s>>>(leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross,
+                                                  cross ? src_offset : 0, xs, ys, zs, keys, run_rng, (int4 *)runs,
+                                                  stats, st3 + 2, wide, st3 + 3); fmm::note_launch();
     if (host_nleaf_rows || host_nruns) {  // optional host view (synchronises)
         int32_t nrows = 0;
         unsigned long long total = 0;

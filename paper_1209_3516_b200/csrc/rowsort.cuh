@@ -14,6 +14,10 @@ namespace fmm {
 
 constexpr int kSortSegWords = 1024;  // 32768 ids per pass
 
+struct IdentityIds {
+    __device__ __forceinline__ uint32_t operator()(int32_t v) const { return (uint32_t)v; }
+};
+
 // Sorts in[k0..k1) (distinct ids) into out[k0..k1).
 __device__ __forceinline__ void warp_bitmap_sort(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t k1,
                                                  uint32_t *bm, int lane) {
@@ -53,6 +57,88 @@ __device__ __forceinline__ void warp_bitmap_sort(const int32_t *__restrict__ in,
         pos += __shfl_sync(0xffffffffu, incl, 31);
         __syncwarp();  // bm is rewritten by the next pass; out is read after return
     }
+}
+
+// ---- rows spread over several bitmap passes: sort in registers -----------
+// Bitonic network over N = 32 * ITEMS keys held lane-major (lane l owns
+// elements [l * ITEMS, (l + 1) * ITEMS)); pads are 0xffffffff.  Its cost
+// does not depend on the id window, which is what makes it the choice when
+// a row's ids spread over several 32768-id bitmap passes.
+template <int ITEMS>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[ITEMS], int lane) {
+    constexpr int N = 32 * ITEMS;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= ITEMS) {  // partner in lane ^ (j / ITEMS), same slot
+                const int lm = j / ITEMS;
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++) {
+                    const bool asc = ((lane * ITEMS + i) & k) == 0;
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[i], lm);
+                    v[i] = (lower == asc) ? min(v[i], o) : max(v[i], o);
+                }
+            } else {  // partner in this lane's registers
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++) {
+                    if ((i & j) == 0) {
+                        const bool asc = ((lane * ITEMS + i) & k) == 0;
+                        const uint32_t a = v[i], b = v[i | j];
+                        v[i] = asc ? min(a, b) : max(a, b);
+                        v[i | j] = asc ? max(a, b) : min(a, b);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Load row [k0, k1) (len <= 32 * ITEMS) lane-major through `map`, sort.
+template <int ITEMS, class Map>
+__device__ __forceinline__ void warp_bitonic_load_sort(const int32_t *__restrict__ in, int64_t k0, int64_t len,
+                                                       uint32_t (&v)[ITEMS], int lane, Map map) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const int64_t e = (int64_t)lane * ITEMS + i;
+        v[i] = e < len ? map(in[k0 + e]) : 0xffffffffu;
+    }
+    warp_bitonic_sort<ITEMS>(v, lane);
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_bitonic_row(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t len,
+                                                 int lane) {
+    uint32_t v[ITEMS];
+    warp_bitonic_load_sort<ITEMS>(in, k0, len, v, lane, IdentityIds());
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const int64_t e = (int64_t)lane * ITEMS + i;
+        if (e < len) out[k0 + e] = (int32_t)v[i];
+    }
+}
+
+// Row [k0, k1) of up to 1024 ids, in registers, dispatched on its length.
+__device__ __forceinline__ void warp_bitonic_any(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t len,
+                                                 int lane) {
+    if (len <= 128) warp_bitonic_row<4>(in, out, k0, len, lane);
+    else if (len <= 256) warp_bitonic_row<8>(in, out, k0, len, lane);
+    else if (len <= 512) warp_bitonic_row<16>(in, out, k0, len, lane);
+    else warp_bitonic_row<32>(in, out, k0, len, lane);
+}
+
+// True when the row's ids [lo, hi] need more than one bitmap pass.
+__device__ __forceinline__ bool row_is_wide(const int32_t *__restrict__ in, int64_t k0, int64_t k1, int lane) {
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int64_t k = k0 + lane; k < k1; k += 32) {
+        const uint32_t v = (uint32_t)in[k];
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    return k1 > k0 && (hi >> 5) - (lo >> 5) >= (uint32_t)kSortSegWords;
 }
 
 }  // namespace fmm

@@ -263,12 +263,45 @@ __global__ void __launch_bounds__(kRowLargeThreads) row_sort_large_kernel(
 // Bitmap sort (rowsort.cuh): one warp per row.
 constexpr int kRowBitmapWarps = 8;
 
+// Rows whose ids fit one bitmap pass (or are too long for the register
+// sort) are sorted here; wide rows of up to 1024 ids are queued for the
+// register bitonic kernel, whose register footprint would otherwise cap
+// this latency-bound kernel's occupancy.
 __global__ void __launch_bounds__(kRowBitmapWarps * 32) row_sort_bitmap_kernel(
-    int32_t ncells, const int64_t *__restrict__ rows, const int32_t *__restrict__ in, int32_t *out) {
+    int32_t ncells, const int64_t *__restrict__ rows, const int32_t *__restrict__ in, int32_t *out,
+    int32_t *wide_rows, unsigned long long *nwide) {
     __shared__ uint32_t bm_all[kRowBitmapWarps][kSortSegWords];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int32_t r = blockIdx.x * kRowBitmapWarps + w; r < ncells; r += gridDim.x * kRowBitmapWarps)
-        warp_bitmap_sort(in, out, rows[r], rows[r + 1], bm_all[w], lane);
+    for (int32_t r = blockIdx.x * kRowBitmapWarps + w; r < ncells; r += gridDim.x * kRowBitmapWarps) {
+        const int64_t k0 = rows[r], k1 = rows[r + 1];
+        if (k1 - k0 <= 1024 && row_is_wide(in, k0, k1, lane)) {
+            if (lane == 0) wide_rows[atomicAdd(nwide, 1ull)] = r;
+            continue;
+        }
+        warp_bitmap_sort(in, out, k0, k1, bm_all[w], lane);
+    }
+}
+
+__global__ void __launch_bounds__(128) row_sort_bitonic_kernel(const int64_t *__restrict__ rows,
+                                                               const int32_t *__restrict__ in, int32_t *out,
+                                                               const int32_t *__restrict__ wide_rows,
+                                                               const unsigned long long *__restrict__ nwide) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = (int64_t)*nwide;
+    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < n;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t r = wide_rows[k];
+        warp_bitonic_any(in, out, rows[r], rows[r + 1] - rows[r], lane);
+    }
+}
+
+static int sort_rows_launch(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, int32_t *wide_rows,
+                            unsigned long long *nwide, cudaStream_t st) {
+    cudaMemsetAsync(nwide, 0, sizeof(unsigned long long), st);
+    row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0, st>>>(
+        ncells, rows, in, out, wide_rows, nwide); fmm::note_launch();
+    row_sort_bitonic_kernel<<<148 * 4, 128, 0, st>>>(rows, in, out, wide_rows, nwide); fmm::note_launch();
+    return FMM_OK;
 }
 
 // Rows past the large tile: copy, then an all-ascending bitonic sort in
@@ -924,9 +957,13 @@ int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_off, const
     return FMM_OK;
 }
 
-int fmm_sort_rows(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, void *stream) {
-    row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0,
-                             as_stream(stream)>>>(ncells, rows, in, out); fmm::note_launch();
+int fmm_sort_rows(int32_t ncells, const int64_t *rows, const int32_t *in, int32_t *out, void *ws, size_t ws_bytes,
+                  void *stream) {
+    Arena ar(ws, ws_bytes);
+    int32_t *wide_rows = ar.take<int32_t>((size_t)ncells + 1);
+    unsigned long long *nwide = ar.take<unsigned long long>(1);
+    if (!wide_rows || !nwide) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    sort_rows_launch(ncells, rows, in, out, wide_rows, nwide, as_stream(stream));
     FMM_CUDA_CHECK("fmm_sort_rows");
     return FMM_OK;
 }
@@ -965,8 +1002,7 @@ int fmm_pairs_to_rows(const int32_t *t, const int32_t *s, const unsigned long lo
     // the bitmap sort handles any id range (one 32768-id window per pass);
     // the block radix tiles remain as a cross-check (FMM_B200_ROWSORT_RADIX=1)
     if (!getenv("FMM_B200_ROWSORT_RADIX")) {
-        row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0, st>>>(
-            ncells, rows, unsorted, src_sorted); fmm::note_launch();
+        sort_rows_launch(ncells, rows, unsorted, src_sorted, long_rows, nlong, st);
         FMM_CUDA_CHECK("fmm_pairs_to_rows");
         return FMM_OK;
     }

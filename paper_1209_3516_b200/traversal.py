@@ -152,7 +152,8 @@ class Lists:
             # the P2P plan reads its rows unsorted; sort them when asked
             grp, rows = self.__dict__["p2p_grp"], self.__dict__["p2p_rows"]
             out = torch.empty_like(grp)
-            _lib.call("fmm_sort_rows", rows.numel() - 1, _lib.ptr(rows), _lib.ptr(grp), _lib.ptr(out),
+            wsp, wsb = _lib.workspace(rows.numel(), grp.device)
+            _lib.call("fmm_sort_rows", rows.numel() - 1, _lib.ptr(rows), _lib.ptr(grp), _lib.ptr(out), wsp, wsb,
                       _lib.stream_handle())
             self.__dict__["p2p_src"] = out
             return out
@@ -691,10 +692,11 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         _attach_locals(tree, p, L)
         cuts = _chunk_cuts(tree, 1 if cfg.mutual else _nchunks(tree))
         nch = len(cuts) - 1
-        # chunked runs build lists on a high-priority stream (they gate P2P); with
-        # one chunk the main stream does: a priority stream there starves the
-        # far field behind P2P on some runs (C3 measured 37 ms or 49 ms)
-        lst = _side_stream(dev, 2) if nch > 1 else main
+        # the lists gate P2P, so they build on a high-priority stream: the
+        # far field's M2L blocks then yield SM slots to the CSR and plan
+        # kernels (C2: 13.05-13.10 ms against 13.09-13.35 on the main stream;
+        # C3 and C5 unchanged).  FMM_B200_LIST_PRIORITY=0 builds them on main.
+        lst = _side_stream(dev, 2) if os.environ.get("FMM_B200_LIST_PRIORITY", "1") == "1" else main
         lst.wait_event(e0)
         parts, m2l_ev, p2p_ev = [], [], []
         for k in range(nch):

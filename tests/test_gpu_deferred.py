@@ -107,3 +107,28 @@ def test_pairs_to_rows_matches_lexsort(shape, nsrc, method, monkeypatch):
     want_rows = np.concatenate([[0], np.cumsum(np.bincount(t, minlength=ncells))])
     assert np.array_equal(rows.cpu().numpy(), want_rows)
     assert np.array_equal(src[:t.size].cpu().numpy(), s[order])
+
+
+def test_plan_with_wide_rows_matches_oracle_p2p():
+    """A tree with more than 32768 leaves: rows whose source-leaf ordinals
+    span several bitmap windows take the register-sort plan path.  The P2P
+    sums over the plan equal the oracle's over the same leaf pairs."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1209_3516_b200 import workloads as wl
+    from paper_1209_3516_b200.traversal import run_p2p
+    pos, q = wl.plummer(120000, 3)
+    pos = np.asarray(pos, np.float64)
+    q = np.asarray(q, np.float64)
+    t = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], q), ncrit=3)
+    assert t.nleaves > 40000
+    lists = fb.interaction_lists(t, fb.MacConfig("fmm", 0.5))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    run_p2p(t, lists, "fp64", flag=flag)
+    got = t.d_phi.cpu().numpy()
+    pt, ps = lists.host_pairs("p2p")
+    ot = orc.build_tree(pos, q, 3)
+    phi, fx, fy, fz, st = orc.exec_p2p(ot, pt, ps)
+    assert np.linalg.norm(got - phi) <= 1e-12 * np.linalg.norm(phi)
+    pairs, skipped = lists.dev_stats.tolist()
+    assert (pairs, skipped) == (int(st[0]), int(st[1]))
