@@ -781,6 +781,16 @@ __global__ void mutual_step_kernel(const int32_t *__restrict__ fa, const int32_t
     }
 }
 
+// The traversal's seed in one launch (no host-to-device copies): the log
+// zeroed with one root pair entering step 0, the frontier (0, root_b).
+__global__ void traverse_seed(unsigned long long *log, int nlog, int32_t *fa, int32_t *fb, int32_t root_b) {
+    for (int i = threadIdx.x; i < nlog; i += blockDim.x) log[i] = i == 2 ? 1ull : 0ull;
+    if (threadIdx.x == 0) {
+        fa[0] = 0;
+        fb[0] = root_b;
+    }
+}
+
 static Cells cells_of(const int32_t *children, const uint8_t *leaf, const double *ctr, const double *bmax,
                       const double *rmax) {
     return Cells{children, leaf, ctr, bmax, rmax};
@@ -824,12 +834,7 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
     const Cells A = cells_of(children, leaf, ctr, bmax, rmax);
     const Cells B = source_cells(A, children_b, leaf_b, ctr_b, bmax_b, rmax_b);
     // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s
-    cudaMemsetAsync(dev_log, 0, sizeof(unsigned long long) * (nsteps + 3), st);
-    const unsigned long long one = 1;
-    cudaMemcpyAsync(dev_log + 2, &one, sizeof(one), cudaMemcpyHostToDevice, st);
-    const int32_t zero = 0;
-    cudaMemcpyAsync(front_a0, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(front_b0, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
+    traverse_seed<<<1, 32, 0, st>>>(dev_log, nsteps + 3, front_a0, front_b0, 0); fmm::note_launch();
     const int grid = 148 * 8;
     for (int sidx = 0; sidx < nsteps; sidx++) {
         const bool even = (sidx & 1) == 0;
@@ -904,12 +909,7 @@ int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1,
     const Cells C = cells_of(children, leaf, ctr, bmax, rmax);
     // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s;
     // the seed is the unclassified mutual root pair (0, 0)
-    cudaMemsetAsync(dev_log, 0, sizeof(unsigned long long) * (nsteps + 3), st);
-    const unsigned long long one = 1;
-    cudaMemcpyAsync(dev_log + 2, &one, sizeof(one), cudaMemcpyHostToDevice, st);
-    const int32_t zero = 0, root_mut = (int32_t)0x80000000u;
-    cudaMemcpyAsync(front_a0, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(front_b0, &root_mut, sizeof(root_mut), cudaMemcpyHostToDevice, st);
+    traverse_seed<<<1, 32, 0, st>>>(dev_log, nsteps + 3, front_a0, front_b0, (int32_t)0x80000000u); fmm::note_launch();
     const int grid = 148 * 8;
     for (int sidx = 0; sidx < nsteps; sidx++) {
         const bool even = (sidx & 1) == 0;

@@ -223,9 +223,9 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         # capacities known from an earlier run of this shape: chain the
         # traversal, both CSRs and the plan on the device, no host wait
         cap_p2p, cap_m2l, cap_next = _hint[key]
-        p2p_t, p2p_s, m2l_t, m2l_s = (torch.empty(c, dtype=i32, device=dev)
-                                      for c in (cap_p2p, cap_p2p, cap_m2l, cap_m2l))
-        fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
+        # one allocation for the pair buffers and the four frontiers
+        pool = torch.empty(2 * cap_p2p + 2 * cap_m2l + 4 * cap_next, dtype=i32, device=dev)
+        p2p_t, p2p_s, m2l_t, m2l_s, *fr = torch.split(pool, [cap_p2p, cap_p2p, cap_m2l, cap_m2l] + [cap_next] * 4)
         _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
                   P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), *bcells, P(tree.d_start),
                   P(tree.d_end), blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p,
@@ -584,7 +584,8 @@ _side = {}
 def _side_stream(dev, which: int = 0) -> torch.cuda.Stream:
     """Persistent auxiliary streams per device: 0 = far field, 1 = P2P,
     2 = list construction (highest priority: its short kernels take SM slots
-    as P2P blocks retire instead of queueing behind the whole P2P grid)."""
+    as far-field blocks retire instead of queueing behind them), 3 = the
+    upward pass."""
     key = (torch.device(dev).index or 0, which)
     if key not in _side:
         prio = torch.cuda.Stream.priority_range()[1] if which == 2 else 0
@@ -683,12 +684,22 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         e0.record(main)
         side.wait_event(e0)
         pst.wait_event(e0)
-        with torch.cuda.stream(side):
-            e_up0.record(side)
-            if need_up:
-                upward_pass(src, p, stats, sync=False, M=M)  # (resets src._L)
-            e_up1.record(side)
-        src._M, src.p = M, p
+        ust = _side_stream(dev, 3)  # the upward pass: launched after the first lists
+        ust.wait_event(e0)
+
+        def launch_upward():
+            # after the traversal's launches, so its host cost is off the
+            # critical path; on its own stream, so it runs beside the lists
+            with torch.cuda.stream(ust):
+                e_up0.record(ust)
+                if need_up:
+                    upward_pass(src, p, stats, sync=False, M=M)  # (resets src._L)
+                e_up1.record(ust)
+            src._M, src.p = M, p
+            _attach_locals(tree, p, L)
+            side.wait_event(e_up1)
+
+        src._M, src.p = (M, p) if need_up else (src._M, src.p)
         _attach_locals(tree, p, L)
         cuts = _chunk_cuts(tree, 1 if cfg.mutual else _nchunks(tree))
         nch = len(cuts) - 1
@@ -709,6 +720,8 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                     lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
                                               m2l_owner_only=nch > 1, src=src)
             parts.append(lists)
+            if k == 0:
+                launch_upward()
             with torch.cuda.stream(side):  # M2L rows of this chunk: after upward and its sorted list
                 ea, eb = E(), E()
                 ea.record(side)

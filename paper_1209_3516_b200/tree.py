@@ -368,7 +368,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         _lib.call("fmm_cell_geometry", ncells, P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
                   P(xs), P(ys), P(zs), P(qs), int(shape == "rect"), int(center_mode == "com"), P(root), P(lo),
                   P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
-        zeros = [torch.zeros(n, dtype=f64, device=dev) for _ in range(4)]
+        zeros = torch.zeros((4, n), dtype=f64, device=dev).unbind(0)  # one fill
     tree = Tree(
         device=dev, n=n, ncrit=ncrit, shape=shape, center_mode=center_mode,
         allow_oversized_leaves=bool(allow_oversized_leaves), _ncells=ncells, _nleaves=nleaves,
