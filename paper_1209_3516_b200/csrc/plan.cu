@@ -15,7 +15,6 @@
 #include <cub/cub.cuh>
 
 #include "fmm_common.cuh"
-#include "rowsort.cuh"
 
 namespace fmm {
 
@@ -37,11 +36,8 @@ namespace fmm {
 // skip the O(|t|^2) scan.
 constexpr int kPlanWarps = 8;
 constexpr int kPlanSegWords = 1024;  // 32768 ordinals per bitmap pass
-
-struct LeafOrd {
-    const int32_t *ord;
-    __device__ __forceinline__ uint32_t operator()(int32_t c) const { return (uint32_t)ord[c]; }
-};
+constexpr int kWideWarps = 4;       // plan_rows_wide_kernel: warps per block
+constexpr int kWideMax = 1024;      // longest row it takes (ordinals staged in shared memory)
 
 // A row's coincident-pair scan, counters and run range (one warp).
 __device__ __forceinline__ void plan_row_finish(int32_t r, int32_t t, int64_t k0, int64_t nrun, long long blocks,
@@ -80,6 +76,91 @@ __device__ __forceinline__ void plan_row_finish(int32_t r, int32_t t, int64_t k0
     }
 }
 
+// Runs of one bitmap pass.  bm (the warp's window, bm[-1] and
+// bm[kPlanSegWords] zero) holds the row's ordinals in [seg << 15, (seg + 1)
+// << 15); words [wa, wb] are the touched ones.  prev_top: is ordinal
+// (seg << 15) - 1 in the row; next_first: is (seg + 1) << 15.  Appends the
+// pass's runs after the row's first nrun, updates the counters, clears the
+// window and returns bit 31 of the pass's last word (the next pass's
+// prev_top when that pass is seg + 1).
+__device__ __forceinline__ uint32_t plan_pass(uint32_t *bm, uint32_t seg, uint32_t wa, uint32_t wb, uint32_t prev_top,
+                                              bool next_first, int32_t ot, int64_t k0, int64_t nt, int64_t &nrun,
+                                              long long &blocks, bool &self, const int32_t *__restrict__ s_bstart,
+                                              const int32_t *__restrict__ s_bend, int32_t soff, int4 *runs, int lane) {
+    const uint32_t sbase = seg << 15;
+    // the pass's word window, split into contiguous per-lane blocks
+    const uint32_t nw = wb - wa + 1, per = (nw + 31) / 32;
+    const uint32_t w0 = wa + min(lane * per, nw), w1 = wa + min(lane * per + per, nw);
+    const int32_t self_word = (ot >= 0 && ((uint32_t)ot >> 15) == seg) ? (int32_t)(((uint32_t)ot >> 5) & 1023u) : -2;
+    const int32_t prev_self = (ot >= 0 && (uint32_t)ot + 1u == sbase) ? 1 : 0;  // self just before this pass
+    const int32_t next_self = (ot >= 0 && (uint32_t)ot == sbase + 32768u) ? 1 : 0;
+    // masks of run starts / ends in word x
+    auto masks = [&](uint32_t x, uint32_t &st, uint32_t &en) {
+        const uint32_t W = bm[x];
+        const uint32_t P = (x == 0) ? (prev_top << 31) : bm[x - 1];
+        const uint32_t N = (x == kPlanSegWords - 1) ? (next_first ? 1u : 0u) : bm[x + 1];
+        uint32_t Bs = 0u, Be = 0u;  // forced starts / ends around the self leaf
+        if ((int32_t)x == self_word) {
+            const uint32_t M = 1u << ((uint32_t)ot & 31u);
+            Bs |= M | (M << 1);
+            Be |= M | (M >> 1);
+        }
+        if ((int32_t)x - 1 == self_word && ((uint32_t)ot & 31u) == 31u) Bs |= 1u;
+        if ((int32_t)x + 1 == self_word && ((uint32_t)ot & 31u) == 0u) Be |= 1u << 31;
+        if (x == 0 && prev_self) Bs |= 1u;
+        if (x == kPlanSegWords - 1 && next_self) Be |= 1u << 31;
+        st = W & (~((W << 1) | (P >> 31)) | Bs);
+        en = W & (~((W >> 1) | (N << 31)) | Be);
+    };
+    int cnt = 0;
+    for (uint32_t x = w0; x < w1; x++) {
+        uint32_t st, en;
+        masks(x, st, en);
+        cnt += __popc(st);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    int64_t idx = k0 + nrun + (incl - cnt) - 1;  // run holding the entry before this lane's block
+    for (uint32_t x = w0; x < w1; x++) {
+        uint32_t st, en;
+        masks(x, st, en);
+        for (uint32_t m = st | en; m; m &= m - 1u) {
+            const uint32_t bit = (uint32_t)__ffs(m) - 1u, b = 1u << bit;
+            const uint32_t o = sbase + (x << 5) + bit;
+            if (st & b) {
+                ++idx;
+                const int32_t b0 = s_bstart[o];
+                // component stores: the run's end may be written by
+                // another lane (a run crossing lane blocks)
+                runs[idx].x = b0 + soff;
+                runs[idx].z = (int32_t)o == ot ? 1 : 0;
+                runs[idx].w = 0;
+                blocks -= (long long)nt * b0;
+            }
+            if (en & b) {
+                const int32_t b1 = s_bend[o];
+                runs[idx].y = b1 + soff;
+                blocks += (long long)nt * b1;
+            }
+        }
+        if ((int32_t)x == self_word && (bm[x] >> ((uint32_t)ot & 31u) & 1u)) {
+            blocks -= (long long)nt;
+            self = true;
+        }
+    }
+    nrun += __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();  // every lane read its neighbours' words
+    const uint32_t top = bm[kPlanSegWords - 1] >> 31;
+    __syncwarp();
+    for (uint32_t x = w0; x < w1; x++) bm[x] = 0u;
+    __syncwarp();
+    return top;
+}
+
 __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
     const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows,
     const int32_t *__restrict__ src, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
@@ -108,7 +189,7 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
-        if (k1 - k0 <= 1024 && (hi >> 15) != (lo >> 15)) {  // several bitmap passes: register sort instead
+        if (k1 - k0 <= kWideMax && (hi >> 15) != (lo >> 15)) {  // several bitmap windows: plan_rows_wide_kernel
             if (lane == 0) wide[atomicAdd(nwide, 1ull)] = r;
             continue;
         }
@@ -126,154 +207,79 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
             }
             next_first = __any_sync(0xffffffffu, next_first);
             __syncwarp();
-            // the pass's word window, split into contiguous per-lane blocks
             const uint32_t wa = (seg == (lo >> 15)) ? ((lo >> 5) & (kPlanSegWords - 1)) : 0u;
             const uint32_t wb = (seg == (hi >> 15)) ? ((hi >> 5) & (kPlanSegWords - 1)) : kPlanSegWords - 1;
-            const uint32_t nw = wb - wa + 1, per = (nw + 31) / 32;
-            const uint32_t w0 = wa + min(lane * per, nw), w1 = wa + min(lane * per + per, nw);
-            const int32_t self_word = (ot >= 0 && ((uint32_t)ot >> 15) == seg) ? (int32_t)(((uint32_t)ot >> 5) & 1023u) : -2;
-            const int32_t prev_self = (ot >= 0 && (uint32_t)ot + 1u == sbase) ? 1 : 0;  // self just before this pass
-            const int32_t next_self = (ot >= 0 && (uint32_t)ot == sbase + 32768u) ? 1 : 0;
-            // masks of run starts / ends in word x
-            auto masks = [&](uint32_t x, uint32_t &st, uint32_t &en) {
-                const uint32_t W = bm[x];
-                const uint32_t P = (x == 0) ? (prev_top << 31) : bm[x - 1];
-                const uint32_t N = (x == kPlanSegWords - 1) ? (next_first ? 1u : 0u) : bm[x + 1];
-                uint32_t Bs = 0u, Be = 0u;  // forced starts / ends around the self leaf
-                if ((int32_t)x == self_word) {
-                    const uint32_t M = 1u << ((uint32_t)ot & 31u);
-                    Bs |= M | (M << 1);
-                    Be |= M | (M >> 1);
-                }
-                if ((int32_t)x - 1 == self_word && ((uint32_t)ot & 31u) == 31u) Bs |= 1u;
-                if ((int32_t)x + 1 == self_word && ((uint32_t)ot & 31u) == 0u) Be |= 1u << 31;
-                if (x == 0 && prev_self) Bs |= 1u;
-                if (x == kPlanSegWords - 1 && next_self) Be |= 1u << 31;
-                st = W & (~((W << 1) | (P >> 31)) | Bs);
-                en = W & (~((W >> 1) | (N << 31)) | Be);
-            };
-            int cnt = 0;
-            for (uint32_t x = w0; x < w1; x++) {
-                uint32_t st, en;
-                masks(x, st, en);
-                cnt += __popc(st);
-            }
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            int64_t idx = k0 + nrun + (incl - cnt) - 1;  // run holding the entry before this lane's block
-            for (uint32_t x = w0; x < w1; x++) {
-                uint32_t st, en;
-                masks(x, st, en);
-                for (uint32_t m = st | en; m; m &= m - 1u) {
-                    const uint32_t bit = (uint32_t)__ffs(m) - 1u, b = 1u << bit;
-                    const uint32_t o = sbase + (x << 5) + bit;
-                    if (st & b) {
-                        ++idx;
-                        const int32_t b0 = s_bstart[o];
-                        // component stores: the run's end may be written by
-                        // another lane (a run crossing lane blocks)
-                        runs[idx].x = b0 + soff;
-                        runs[idx].z = (int32_t)o == ot ? 1 : 0;
-                        runs[idx].w = 0;
-                        blocks -= (long long)nt * b0;
-                    }
-                    if (en & b) {
-                        const int32_t b1 = s_bend[o];
-                        runs[idx].y = b1 + soff;
-                        blocks += (long long)nt * b1;
-                    }
-                }
-                if ((int32_t)x == self_word && (bm[x] >> ((uint32_t)ot & 31u) & 1u)) {
-                    blocks -= (long long)nt;
-                    self = true;
-                }
-            }
-            nrun += __shfl_sync(0xffffffffu, incl, 31);
-            __syncwarp();  // every lane read its neighbours' words
-            prev_top = bm[kPlanSegWords - 1] >> 31;
-            __syncwarp();
-            for (uint32_t x = w0; x < w1; x++) bm[x] = 0u;
-            __syncwarp();
+            prev_top = plan_pass(bm, seg, wa, wb, prev_top, next_first, ot, k0, nt, nrun, blocks, self, s_bstart,
+                                 s_bend, soff, runs, lane);
         }
         plan_row_finish(r, t, k0, nrun, blocks, self, ts, te, xs, ys, zs, keys, run_rng, stats, nruns_total, lane);
     }
 }
 
-// Rows whose ordinals span several bitmap passes (and hold <= 1024
-// sources): the ordinals are sorted in registers (rowsort.cuh, lane-major:
-// lane l holds sorted positions [l * ITEMS, (l + 1) * ITEMS)), then each
-// lane walks its block with its neighbours' edge values.
-template <int ITEMS>
-__device__ __forceinline__ void plan_row_wide(int32_t r, int32_t t, int64_t k0, int64_t len,
-                                              const int32_t *__restrict__ src, const int32_t *__restrict__ start,
-                                              const int32_t *__restrict__ end, const int32_t *__restrict__ t_ord,
-                                              const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
-                                              const int32_t *__restrict__ s_bend, int cross, int32_t soff,
-                                              const double *__restrict__ xs, const double *__restrict__ ys,
-                                              const double *__restrict__ zs, const uint64_t *__restrict__ keys,
-                                              int64_t *run_rng, int4 *runs, unsigned long long *stats,
-                                              unsigned long long *nruns_total, int lane) {
-    uint32_t v[ITEMS];
-    warp_bitonic_load_sort<ITEMS>(src, k0, len, v, lane, LeafOrd{s_ord});
+// Rows whose ordinals span several bitmap windows (and hold <= 1024
+// sources): the ordinals are staged once in the warp's shared-memory slab
+// and the passes visit only the windows that hold some -- a row of leaf
+// neighbours in an adaptive tree clusters into a few dense groups of
+// ordinals far apart -- each pass scanning only the words between its
+// smallest and largest ordinal.
+__device__ __forceinline__ void plan_row_wide(int32_t r, int32_t t, int64_t k0, int64_t len, uint32_t *bm,
+                                              uint32_t *ent, const int32_t *__restrict__ src,
+                                              const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                                              const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord,
+                                              const int32_t *__restrict__ s_bstart, const int32_t *__restrict__ s_bend,
+                                              int cross, int32_t soff, const double *__restrict__ xs,
+                                              const double *__restrict__ ys, const double *__restrict__ zs,
+                                              const uint64_t *__restrict__ keys, int64_t *run_rng, int4 *runs,
+                                              unsigned long long *stats, unsigned long long *nruns_total, int lane) {
+    constexpr uint32_t kNone = 0xffffffffu;
+    const int n = (int)len;
+    uint32_t seg = kNone;
+    for (int e = lane; e < n; e += 32) {
+        const uint32_t v = (uint32_t)s_ord[src[k0 + e]];
+        ent[e] = v;
+        seg = min(seg, v >> 15);
+    }
+    seg = __reduce_min_sync(0xffffffffu, seg);
+    __syncwarp();
     const int32_t ts = start[t], te = end[t];
     const int64_t nt = te - ts;
-    const uint32_t ot = cross ? 0xfffffffeu : (uint32_t)t_ord[t];
-    uint32_t prev = __shfl_up_sync(0xffffffffu, v[ITEMS - 1], 1);
-    uint32_t next = __shfl_down_sync(0xffffffffu, v[0], 1);
-    if (lane == 0) prev = 0xfffffffdu;   // no predecessor
-    if (lane == 31) next = 0xfffffffdu;  // no successor
-    auto is_start = [&](int i) {
-        const uint32_t o = v[i], p = i ? v[i - 1] : prev;
-        return o == ot || p == ot || o != p + 1u || p == 0xfffffffdu;
-    };
-    auto is_end = [&](int i) {
-        const uint32_t o = v[i], nx = i + 1 < ITEMS ? v[i + 1] : next;
-        return o == ot || nx == ot || nx != o + 1u || nx == 0xffffffffu || nx == 0xfffffffdu;
-    };
-    int cnt = 0;
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++)
-        if ((int64_t)lane * ITEMS + i < len && is_start(i)) cnt++;
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
-    }
-    int64_t idx = k0 + (incl - cnt) - 1;
+    const int32_t ot = cross ? -1 : t_ord[t];
     long long blocks = 0;
     bool self = false;
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        if ((int64_t)lane * ITEMS + i >= len) continue;
-        const uint32_t o = v[i];
-        if (is_start(i)) {
-            ++idx;
-            const int32_t b0 = s_bstart[o];
-            runs[idx].x = b0 + soff;  // component stores: the end may come from another lane
-            runs[idx].z = o == ot ? 1 : 0;
-            runs[idx].w = 0;
-            blocks -= (long long)nt * b0;
+    int64_t nrun = 0;
+    uint32_t prev_seg = kNone, prev_top = 0u;
+    while (seg != kNone) {
+        const uint32_t sbase = seg << 15;
+        uint32_t wa = kNone, wb = 0u, nseg = kNone;
+        bool next_first = false;
+        for (int e = lane; e < n; e += 32) {
+            const uint32_t v = ent[e], g = v >> 15;
+            if (g == seg) {
+                const uint32_t wd = (v >> 5) & (kPlanSegWords - 1);
+                atomicOr(&bm[wd], 1u << (v & 31u));
+                wa = min(wa, wd);
+                wb = max(wb, wd);
+            } else if (g > seg) {
+                nseg = min(nseg, g);
+            }
+            next_first |= v == sbase + 32768u;
         }
-        if (is_end(i)) {
-            const int32_t b1 = s_bend[o];
-            runs[idx].y = b1 + soff;
-            blocks += (long long)nt * b1;
-        }
-        if (o == ot) {
-            blocks -= (long long)nt;
-            self = true;
-        }
+        wa = __reduce_min_sync(0xffffffffu, wa);
+        wb = __reduce_max_sync(0xffffffffu, wb);
+        nseg = __reduce_min_sync(0xffffffffu, nseg);
+        next_first = __any_sync(0xffffffffu, next_first);
+        __syncwarp();
+        const uint32_t top = plan_pass(bm, seg, wa, wb, prev_seg + 1u == seg ? prev_top : 0u, next_first, ot, k0, nt,
+                                       nrun, blocks, self, s_bstart, s_bend, soff, runs, lane);
+        prev_seg = seg;
+        prev_top = top;
+        seg = nseg;
     }
-    const int64_t nrun = __shfl_sync(0xffffffffu, incl, 31);
     plan_row_finish(r, t, k0, nrun, blocks, self, ts, te, xs, ys, zs, keys, run_rng, stats, nruns_total, lane);
+    __syncwarp();  // ent is rewritten by the warp's next row
 }
 
-__global__ void __launch_bounds__(128) plan_rows_wide_kernel(
+__global__ void __launch_bounds__(kWideWarps * 32) plan_rows_wide_kernel(
     const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
     const int32_t *__restrict__ start, const int32_t *__restrict__ end, const int32_t *__restrict__ t_ord,
     const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart, const int32_t *__restrict__ s_bend,
@@ -281,18 +287,18 @@ __global__ void __launch_bounds__(128) plan_rows_wide_kernel(
     const double *__restrict__ zs, const uint64_t *__restrict__ keys, int64_t *run_rng, int4 *runs,
     unsigned long long *stats, unsigned long long *nruns_total, const int32_t *__restrict__ wide,
     const unsigned long long *__restrict__ nwide) {
-    const int lane = threadIdx.x & 31;
+    __shared__ uint32_t bm_all[kWideWarps][kPlanSegWords + 2];
+    __shared__ uint32_t ent_all[kWideWarps][kWideMax];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *bm = bm_all[wid] + 1;  // bm[-1] and bm[kPlanSegWords] stay 0
+    for (int x = lane; x < kPlanSegWords + 2; x += 32) bm_all[wid][x] = 0u;
+    __syncwarp();
     const int64_t n = (int64_t)*nwide;
-    for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < n;
-         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t q = (int64_t)blockIdx.x * kWideWarps + wid; q < n; q += (int64_t)gridDim.x * kWideWarps) {
         const int32_t r = wide[q], t = leaf_rows[r];
         const int64_t k0 = rows[t], len = rows[t + 1] - k0;
-#define FMM_PLAN_WIDE(IT) plan_row_wide<IT>(r, t, k0, len, src, start, end, t_ord, s_ord, s_bstart, s_bend, cross, soff, xs, ys, zs, keys, run_rng, runs, stats, nruns_total, lane)
-        if (len <= 128) FMM_PLAN_WIDE(4);
-        else if (len <= 256) FMM_PLAN_WIDE(8);
-        else if (len <= 512) FMM_PLAN_WIDE(16);
-        else FMM_PLAN_WIDE(32);
-#undef FMM_PLAN_WIDE
+        plan_row_wide(r, t, k0, len, bm, ent_all[wid], src, start, end, t_ord, s_ord, s_bstart, s_bend, cross, soff,
+                      xs, ys, zs, keys, run_rng, runs, stats, nruns_total, lane);
     }
 }
 
@@ -381,7 +387,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     plan_rows_kernel<<<grid_for(ncells, kPlanWarps, 148 * 8), kPlanWarps * 32, 0, s>>>(
         nsel, leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross, cross ? src_offset : 0, xs, ys, zs,
         keys, run_rng, (int4 *)runs, stats, st3 + 2, wide, st3 + 3); fmm::note_launch();
-    plan_rows_wide_kernel<<<148 * 4, 128, 0, s>>>(leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross,
+    plan_rows_wide_kernel<<<148 * 6, kWideWarps * 32, 0, s>>>(leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross,
                                                   cross ? src_offset : 0, xs, ys, zs, keys, run_rng, (int4 *)runs,
                                                   stats, st3 + 2, wide, st3 + 3); fmm::note_launch();
     if (host_nleaf_rows || host_nruns) {  // optional host view (synchronises)

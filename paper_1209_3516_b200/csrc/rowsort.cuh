@@ -14,10 +14,6 @@ namespace fmm {
 
 constexpr int kSortSegWords = 1024;  // 32768 ids per pass
 
-struct IdentityIds {
-    __device__ __forceinline__ uint32_t operator()(int32_t v) const { return (uint32_t)v; }
-};
-
 // Sorts in[k0..k1) (distinct ids) into out[k0..k1).
 __device__ __forceinline__ void warp_bitmap_sort(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t k1,
                                                  uint32_t *bm, int lane) {
@@ -59,73 +55,65 @@ __device__ __forceinline__ void warp_bitmap_sort(const int32_t *__restrict__ in,
     }
 }
 
-// ---- rows spread over several bitmap passes: sort in registers -----------
-// Bitonic network over N = 32 * ITEMS keys held lane-major (lane l owns
-// elements [l * ITEMS, (l + 1) * ITEMS)); pads are 0xffffffff.  Its cost
-// does not depend on the id window, which is what makes it the choice when
-// a row's ids spread over several 32768-id bitmap passes.
-template <int ITEMS>
-__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[ITEMS], int lane) {
-    constexpr int N = 32 * ITEMS;
-#pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= ITEMS) {  // partner in lane ^ (j / ITEMS), same slot
-                const int lm = j / ITEMS;
-                const bool lower = (lane & lm) == 0;
-#pragma unroll
-                for (int i = 0; i < ITEMS; i++) {
-                    const bool asc = ((lane * ITEMS + i) & k) == 0;
-                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[i], lm);
-                    v[i] = (lower == asc) ? min(v[i], o) : max(v[i], o);
-                }
-            } else {  // partner in this lane's registers
-#pragma unroll
-                for (int i = 0; i < ITEMS; i++) {
-                    if ((i & j) == 0) {
-                        const bool asc = ((lane * ITEMS + i) & k) == 0;
-                        const uint32_t a = v[i], b = v[i | j];
-                        v[i] = asc ? min(a, b) : max(a, b);
-                        v[i | j] = asc ? max(a, b) : min(a, b);
-                    }
-                }
+// ---- rows of <= kSparseMax ids spread over several windows -----------------
+// The ids are staged once in the warp's shared slab `ent`; each pass marks
+// one NON-EMPTY 32768-id window (the rows of an adaptive tree cluster into a
+// few dense groups far apart) and compacts only the words between its
+// smallest and largest id.  `bm` (kSortSegWords words) is zero on entry and
+// on return.
+constexpr int kSparseMax = 1024;
+
+__device__ __forceinline__ void warp_bitmap_sort_sparse(const int32_t *__restrict__ in, int32_t *out, int64_t k0,
+                                                        int64_t len, uint32_t *bm, uint32_t *ent, int lane) {
+    constexpr uint32_t kNone = 0xffffffffu;
+    const int n = (int)len;
+    uint32_t seg = kNone;
+    for (int e = lane; e < n; e += 32) {
+        const uint32_t v = (uint32_t)in[k0 + e];
+        ent[e] = v;
+        seg = min(seg, v >> 15);
+    }
+    seg = __reduce_min_sync(0xffffffffu, seg);
+    __syncwarp();
+    int64_t pos = k0;
+    while (seg != kNone) {
+        uint32_t wa = kNone, wb = 0u, nseg = kNone;
+        for (int e = lane; e < n; e += 32) {
+            const uint32_t v = ent[e], g = v >> 15;
+            if (g == seg) {
+                const uint32_t wd = (v >> 5) & (kSortSegWords - 1);
+                atomicOr(&bm[wd], 1u << (v & 31u));
+                wa = min(wa, wd);
+                wb = max(wb, wd);
+            } else if (g > seg) {
+                nseg = min(nseg, g);
             }
         }
-    }
-}
-
-// Load row [k0, k1) (len <= 32 * ITEMS) lane-major through `map`, sort.
-template <int ITEMS, class Map>
-__device__ __forceinline__ void warp_bitonic_load_sort(const int32_t *__restrict__ in, int64_t k0, int64_t len,
-                                                       uint32_t (&v)[ITEMS], int lane, Map map) {
+        wa = __reduce_min_sync(0xffffffffu, wa);
+        wb = __reduce_max_sync(0xffffffffu, wb);
+        nseg = __reduce_min_sync(0xffffffffu, nseg);
+        __syncwarp();
+        const uint32_t nw = wb - wa + 1, per = (nw + 31) / 32;
+        const uint32_t w0 = wa + min(lane * per, nw), w1 = wa + min(lane * per + per, nw);
+        int cnt = 0;
+        for (uint32_t x = w0; x < w1; x++) cnt += __popc(bm[x]);
+        int incl = cnt;
 #pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        const int64_t e = (int64_t)lane * ITEMS + i;
-        v[i] = e < len ? map(in[k0 + e]) : 0xffffffffu;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int64_t at = pos + incl - cnt;
+        for (uint32_t x = w0; x < w1; x++) {
+            for (uint32_t bits = bm[x]; bits; bits &= bits - 1u)
+                out[at++] = (int32_t)((seg << 15) + (x << 5) + (uint32_t)(__ffs(bits) - 1));
+            bm[x] = 0u;
+        }
+        pos += __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        seg = nseg;
     }
-    warp_bitonic_sort<ITEMS>(v, lane);
-}
-
-template <int ITEMS>
-__device__ __forceinline__ void warp_bitonic_row(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t len,
-                                                 int lane) {
-    uint32_t v[ITEMS];
-    warp_bitonic_load_sort<ITEMS>(in, k0, len, v, lane, IdentityIds());
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        const int64_t e = (int64_t)lane * ITEMS + i;
-        if (e < len) out[k0 + e] = (int32_t)v[i];
-    }
-}
-
-// Row [k0, k1) of up to 1024 ids, in registers, dispatched on its length.
-__device__ __forceinline__ void warp_bitonic_any(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t len,
-                                                 int lane) {
-    if (len <= 128) warp_bitonic_row<4>(in, out, k0, len, lane);
-    else if (len <= 256) warp_bitonic_row<8>(in, out, k0, len, lane);
-    else if (len <= 512) warp_bitonic_row<16>(in, out, k0, len, lane);
-    else warp_bitonic_row<32>(in, out, k0, len, lane);
+    __syncwarp();  // ent is rewritten by the warp's next row
 }
 
 // True when the row's ids [lo, hi] need more than one bitmap pass.

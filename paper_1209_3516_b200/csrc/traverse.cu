@@ -262,11 +262,12 @@ __global__ void __launch_bounds__(kRowLargeThreads) row_sort_large_kernel(
 
 // Bitmap sort (rowsort.cuh): one warp per row.
 constexpr int kRowBitmapWarps = 8;
+constexpr int kRowSparseWarps = 4;
 
-// Rows whose ids fit one bitmap pass (or are too long for the register
-// sort) are sorted here; wide rows of up to 1024 ids are queued for the
-// register bitonic kernel, whose register footprint would otherwise cap
-// this latency-bound kernel's occupancy.
+// Rows whose ids fit one bitmap pass (or are too long to stage) are sorted
+// here; wide rows of up to kSparseMax ids are queued for the sparse kernel,
+// which stages them in shared memory and visits only their non-empty
+// windows.
 __global__ void __launch_bounds__(kRowBitmapWarps * 32) row_sort_bitmap_kernel(
     int32_t ncells, const int64_t *__restrict__ rows, const int32_t *__restrict__ in, int32_t *out,
     int32_t *wide_rows, unsigned long long *nwide) {
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kRowBitmapWarps * 32) row_sort_bitmap_kernel(
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int32_t r = blockIdx.x * kRowBitmapWarps + w; r < ncells; r += gridDim.x * kRowBitmapWarps) {
         const int64_t k0 = rows[r], k1 = rows[r + 1];
-        if (k1 - k0 <= 1024 && row_is_wide(in, k0, k1, lane)) {
+        if (k1 - k0 <= kSparseMax && row_is_wide(in, k0, k1, lane)) {
             if (lane == 0) wide_rows[atomicAdd(nwide, 1ull)] = r;
             continue;
         }
@@ -282,16 +283,20 @@ __global__ void __launch_bounds__(kRowBitmapWarps * 32) row_sort_bitmap_kernel(
     }
 }
 
-__global__ void __launch_bounds__(128) row_sort_bitonic_kernel(const int64_t *__restrict__ rows,
-                                                               const int32_t *__restrict__ in, int32_t *out,
-                                                               const int32_t *__restrict__ wide_rows,
-                                                               const unsigned long long *__restrict__ nwide) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kRowSparseWarps * 32) row_sort_sparse_kernel(const int64_t *__restrict__ rows,
+                                                                             const int32_t *__restrict__ in,
+                                                                             int32_t *out,
+                                                                             const int32_t *__restrict__ wide_rows,
+                                                                             const unsigned long long *__restrict__ nwide) {
+    __shared__ uint32_t bm_all[kRowSparseWarps][kSortSegWords];
+    __shared__ uint32_t ent_all[kRowSparseWarps][kSparseMax];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int x = lane; x < kSortSegWords; x += 32) bm_all[w][x] = 0u;
+    __syncwarp();
     const int64_t n = (int64_t)*nwide;
-    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < n;
-         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t k = (int64_t)blockIdx.x * kRowSparseWarps + w; k < n; k += (int64_t)gridDim.x * kRowSparseWarps) {
         const int32_t r = wide_rows[k];
-        warp_bitonic_any(in, out, rows[r], rows[r + 1] - rows[r], lane);
+        warp_bitmap_sort_sparse(in, out, rows[r], rows[r + 1] - rows[r], bm_all[w], ent_all[w], lane);
     }
 }
 
@@ -300,7 +305,7 @@ static int sort_rows_launch(int32_t ncells, const int64_t *rows, const int32_t *
     cudaMemsetAsync(nwide, 0, sizeof(unsigned long long), st);
     row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0, st>>>(
         ncells, rows, in, out, wide_rows, nwide); fmm::note_launch();
-    row_sort_bitonic_kernel<<<148 * 4, 128, 0, st>>>(rows, in, out, wide_rows, nwide); fmm::note_launch();
+    row_sort_sparse_kernel<<<148 * 6, kRowSparseWarps * 32, 0, st>>>(rows, in, out, wide_rows, nwide); fmm::note_launch();
     return FMM_OK;
 }
 

@@ -579,6 +579,7 @@ def run_m2p(tree: Tree, lists: Lists, p: int, out, src: Tree | None = None) -> N
 
 
 _side = {}
+last_events = None
 
 
 def _side_stream(dev, which: int = 0) -> torch.cuda.Stream:
@@ -773,6 +774,8 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             skipped += k
     lists = parts[0] if nch == 1 else ChunkedLists(parts)
     tree.list_cache = lists
+    global last_events  # (start, P2P chunk (begin, end) events, end): tools/step_probe.py
+    last_events = (e0, p2p_ev, e_end)
     stats.p2p_pairs += int(pairs)
     stats.p2p_skipped += int(skipped)
     stats.p2p_flops += 20 * int(pairs)
