@@ -11,29 +11,34 @@
 namespace fmm {
 
 // ---- P2M: warp per leaf, lane per coefficient ---------------------------
-// M_m = sum_j q_j (x_j - c)^m / m!  (src/_taylor.py:134-143); bodies are
-// broadcast from their loading lane by shuffles, each lane builds its own
-// monomial by repeated multiplication (no tables, no local memory).
+// M_m = sum_j q_j (x_j - c)^m / m!  (src/_taylor.py:134-143).  The warp
+// takes the leaf's bodies 32 at a time: lane j tabulates its body's scaled
+// powers dx^a / a!, dy^b / b!, dz^c / c! (a, b, c < p) and charge in the
+// warp's shared slab, then lane m accumulates q_j * px[a_m] * py[b_m] *
+// pz[c_m] over the chunk -- three shared loads and three FP64 ops per body
+// and coefficient, no per-lane monomial loops.
 constexpr int kMaxSlots = (NMI + 31) / 32;
-
-__device__ __forceinline__ double mono(double dx, double dy, double dz, int a, int b, int c) {
-    double v = 1.0;
-    for (int i = 0; i < a; i++) v *= dx;
-    for (int i = 0; i < b; i++) v *= dy;
-    for (int i = 0; i < c; i++) v *= dz;
-    return v;
-}
+constexpr int kP2MWarps = 4;
 
 template <int NS>  // coefficient slots per lane: ceil(ncoef(p) / 32)
-__global__ void p2m_kernel(int p, const int32_t *__restrict__ cells, int32_t ncells,
-                           const uint8_t *__restrict__ leaf, const int32_t *__restrict__ start,
-                           const int32_t *__restrict__ end, const double *__restrict__ ctr,
-                           const double *__restrict__ xs, const double *__restrict__ ys,
-                           const double *__restrict__ zs, const double *__restrict__ qs, double *M) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kP2MWarps * 32) p2m_kernel(
+    int p, const int32_t *__restrict__ cells, int32_t ncells, const uint8_t *__restrict__ leaf,
+    const int32_t *__restrict__ start, const int32_t *__restrict__ end, const double *__restrict__ ctr,
+    const double *__restrict__ xs, const double *__restrict__ ys, const double *__restrict__ zs,
+    const double *__restrict__ qs, double *M) {
+    __shared__ double pw_all[kP2MWarps][32][3 * TMAX + 1];  // [body][axis * TMAX + power | charge]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double (*pw)[3 * TMAX + 1] = pw_all[w];
     const int nc = ncoef(p);
-    for (int ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ci < ncells;
-         ci += (gridDim.x * blockDim.x) >> 5) {
+    int ia[NS], ib[NS], ic[NS];
+#pragma unroll
+    for (int k = 0; k < NS; k++) {
+        const int m = min(lane + 32 * k, nc - 1);
+        ia[k] = d_tab.mi[m][0];
+        ib[k] = TMAX + d_tab.mi[m][1];
+        ic[k] = 2 * TMAX + d_tab.mi[m][2];
+    }
+    for (int ci = blockIdx.x * kP2MWarps + w; ci < ncells; ci += gridDim.x * kP2MWarps) {
         const int32_t c = cells[ci];
         if (!leaf[c]) continue;
         const double cx = ctr[c * 3], cy = ctr[c * 3 + 1], cz = ctr[c * 3 + 2];
@@ -41,37 +46,34 @@ __global__ void p2m_kernel(int p, const int32_t *__restrict__ cells, int32_t nce
         double acc[NS];
 #pragma unroll
         for (int k = 0; k < NS; k++) acc[k] = 0.0;
-        int ma[NS], mb[NS], mc[NS];
-        double w[NS];  // 1 / m!
-#pragma unroll
-        for (int k = 0; k < NS; k++) {
-            const int m = min(lane + 32 * k, nc - 1);
-            ma[k] = d_tab.mi[m][0];
-            mb[k] = d_tab.mi[m][1];
-            mc[k] = d_tab.mi[m][2];
-            w[k] = 1.0 / d_tab.mfact[m];
-        }
         for (int32_t b0 = s; b0 < e; b0 += 32) {
             const int cnt = min(32, e - b0);
-            double dx = 0.0, dy = 0.0, dz = 0.0, qq = 0.0;
             if (lane < cnt) {
-                dx = xs[b0 + lane] - cx;
-                dy = ys[b0 + lane] - cy;
-                dz = zs[b0 + lane] - cz;
-                qq = qs[b0 + lane];
+                const double dx = xs[b0 + lane] - cx, dy = ys[b0 + lane] - cy, dz = zs[b0 + lane] - cz;
+                double vx = 1.0, vy = 1.0, vz = 1.0;
+                for (int a = 0; a < p; a++) {
+                    pw[lane][a] = vx;
+                    pw[lane][TMAX + a] = vy;
+                    pw[lane][2 * TMAX + a] = vz;
+                    const double r = d_tab.rcp[a + 1];
+                    vx = vx * dx * r;
+                    vy = vy * dy * r;
+                    vz = vz * dz * r;
+                }
+                pw[lane][3 * TMAX] = qs[b0 + lane];
             }
+            __syncwarp();
             for (int j = 0; j < cnt; j++) {
-                const double bx = __shfl_sync(0xffffffffu, dx, j), by = __shfl_sync(0xffffffffu, dy, j);
-                const double bz = __shfl_sync(0xffffffffu, dz, j), bq = __shfl_sync(0xffffffffu, qq, j);
+                const double q = pw[j][3 * TMAX];
 #pragma unroll
-                for (int k = 0; k < NS; k++)
-                    if (lane + 32 * k < nc) acc[k] += bq * mono(bx, by, bz, ma[k], mb[k], mc[k]);
+                for (int k = 0; k < NS; k++) acc[k] += q * (pw[j][ia[k]] * pw[j][ib[k]] * pw[j][ic[k]]);
             }
+            __syncwarp();
         }
 #pragma unroll
         for (int k = 0; k < NS; k++) {
             const int m = lane + 32 * k;
-            if (m < nc) M[(int64_t)c * nc + m] = acc[k] * w[k];
+            if (m < nc) M[(int64_t)c * nc + m] = acc[k];
         }
     }
 }
@@ -209,18 +211,18 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
     const int nc = ncoef(p);
     const int32_t total = host_level_off[nlev];
     if (total > 0) {
-        const int g = grid_for((int64_t)total * 32, 128, 148 * 16);
+        const int g = grid_for(total, kP2MWarps, 148 * 16);
         const int ns = (nc + 31) / 32;
         if (ns <= 1)
-            p2m_kernel<1><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+            p2m_kernel<1><<<g, kP2MWarps * 32, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
         else if (ns <= 2)
-            p2m_kernel<2><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+            p2m_kernel<2><<<g, kP2MWarps * 32, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
         else if (ns <= 4)
-            p2m_kernel<4><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+            p2m_kernel<4><<<g, kP2MWarps * 32, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
         else if (ns <= 8)
-            p2m_kernel<8><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
+            p2m_kernel<8><<<g, kP2MWarps * 32, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M);
         else
-            p2m_kernel<kMaxSlots><<<g, 128, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs,
+            p2m_kernel<kMaxSlots><<<g, kP2MWarps * 32, 0, s>>>(p, cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs,
                                                    M);
         fmm::note_launch();
     }
