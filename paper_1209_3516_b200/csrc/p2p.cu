@@ -478,8 +478,11 @@ constexpr int p2p_f32_pool_bytes() {
     return (!SAFE && !ANCHOR ? kP2PWarps * kWStages * kChunk : kP2PWarps * kStages * 32) * (int)sizeof(float4);
 }
 
+#ifndef FMM_P2P_MINB
+#define FMM_P2P_MINB 4  // resident CTAs per SM the register budget is cut for
+#endif
 template <bool SAFE, bool ANCHOR>
-__global__ void __launch_bounds__(kP2PWarps * 32, 4) p2p_f32_kernel(
+__global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
     int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
     const float4 *__restrict__ b, const float4 *__restrict__ blo, double *phi, double *fx, double *fy,
