@@ -382,6 +382,8 @@ def run_ours(args):
     line = {
         "metric": "FMM particles/s (Laplace, P=%d)" % solver["p"], "value": value, "unit": "particles/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "step_ms": {"min": 1e3 * float(np.min(times)), "median": 1e3 * float(np.median(times)),
+                    "max": 1e3 * float(np.max(times))},
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32 P2P / f64 tree+far field" if args.precision == "fp32" else "f64",
         "data": "synthetic", "config": config_block(args, n, solver, {"precision": args.precision,
