@@ -78,110 +78,79 @@ __global__ void __launch_bounds__(kP2MWarps * 32) p2m_kernel(
     }
 }
 
-// ---- M2M / L2L: warp per cell of the level, lanes over coefficients -----
-// The source expansion (a child's multipoles, or the parent's locals) and
-// the shift's scaled powers t^a / a! sit in the warp's shared slab, the
-// multi-index table in the block's, so every term is shared-memory loads
-// and FP64 math.  The terms, their products and their order are those of
-// the running-product loops they replace (results unchanged bit for bit).
-constexpr int kVertWarps = 4;
-
-struct VertSmem {
-    int16_t idx3[TMAX][TMAX][TMAX];
-    double src[kVertWarps][NMI];
-    double tp[kVertWarps][3][TMAX + 1];
-};
-
-__device__ __forceinline__ void vert_load_idx3(VertSmem &sm) {
-    for (int i = threadIdx.x; i < TMAX * TMAX * TMAX; i += blockDim.x)
-        (&sm.idx3[0][0][0])[i] = (int16_t)d_tab.idx3[i / (TMAX * TMAX)][(i / TMAX) % TMAX][i % TMAX];
-    __syncthreads();
-}
-
-// tp[axis][a] = t^a / a! for a < p, built by the same running products
-__device__ __forceinline__ void vert_powers(double (*tp)[TMAX + 1], int p, double tx, double ty, double tz, int lane) {
-    if (lane < 3) {
-        const double t = lane == 0 ? tx : lane == 1 ? ty : tz;
-        double f = 1.0;
-        for (int a = 0; a < p; a++) {
-            tp[lane][a] = f;
-            f = f * t * d_tab.rcp[a + 1];
-        }
-    }
-}
-
+// ---- M2M: thread per (internal cell of this level, coefficient m) --------
 // Mdst[m] += sum_child sum_{k<=m} Msrc[k] t^{m-k}/(m-k)!, t = c_child - c_parent
-// (src/_taylor.py:146-166)
-__global__ void __launch_bounds__(kVertWarps * 32) m2m_level(int p, const int32_t *__restrict__ cells, int32_t count,
-                                                            const uint8_t *__restrict__ leaf,
-                                                            const int32_t *__restrict__ children,
-                                                            const double *__restrict__ ctr, double *M) {
-    __shared__ VertSmem sm;
-    vert_load_idx3(sm);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// (src/_taylor.py:146-166); the powers t^a/a! are carried as running
+// products inside the loops, so nothing spills to local memory.
+__global__ void m2m_level(int p, const int32_t *__restrict__ cells, int32_t count,
+                          const uint8_t *__restrict__ leaf, const int32_t *__restrict__ children,
+                          const double *__restrict__ ctr, double *M) {
     const int nc = ncoef(p);
-    double *ms = sm.src[w];
-    double (*tp)[TMAX + 1] = sm.tp[w];
-    for (int32_t ci = blockIdx.x * kVertWarps + w; ci < count; ci += gridDim.x * kVertWarps) {
-        const int32_t c = cells[ci];
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < (int64_t)count * nc;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = cells[it / nc];
+        const int m = (int)(it % nc);
         if (leaf[c]) continue;
-        const double px = ctr[c * 3], py = ctr[c * 3 + 1], pz = ctr[c * 3 + 2];
-        for (int m0 = 0; m0 < nc; m0 += 32) {
-            const int m = m0 + lane;
-            const int mx = m < nc ? d_tab.mi[m][0] : -1, my = m < nc ? d_tab.mi[m][1] : 0,
-                      mz = m < nc ? d_tab.mi[m][2] : 0;
-            double total = 0.0;
-            for (int o = 0; o < 8; o++) {
-                const int32_t ch = children[c * 8 + o];
-                if (ch < 0) continue;
-                __syncwarp();  // the previous child's slab is consumed
-                for (int k = lane; k < nc; k += 32) ms[k] = M[(int64_t)ch * nc + k];
-                vert_powers(tp, p, ctr[ch * 3] - px, ctr[ch * 3 + 1] - py, ctr[ch * 3 + 2] - pz, lane);
-                __syncwarp();
-                double acc = 0.0;
-                for (int a = 0; a <= mx; a++)          // a = mx - kx
-                    for (int b = 0; b <= my; b++)      // b = my - ky
-                        for (int g = 0; g <= mz; g++)  // g = mz - kz
-                            acc += ms[sm.idx3[mx - a][my - b][mz - g]] * (tp[0][a] * tp[1][b] * tp[2][g]);
-                total += acc;
+        const int mx = d_tab.mi[m][0], my = d_tab.mi[m][1], mz = d_tab.mi[m][2];
+        double total = 0.0;
+        for (int o = 0; o < 8; o++) {
+            const int32_t ch = children[c * 8 + o];
+            if (ch < 0) continue;
+            const double tx = ctr[ch * 3] - ctr[c * 3], ty = ctr[ch * 3 + 1] - ctr[c * 3 + 1],
+                         tz = ctr[ch * 3 + 2] - ctr[c * 3 + 2];
+            const double *Ms = M + (int64_t)ch * nc;
+            double acc = 0.0, fx = 1.0;
+            for (int a = 0; a <= mx; a++) {          // a = mx - kx
+                double fy = 1.0;
+                for (int b = 0; b <= my; b++) {      // b = my - ky
+                    double fz = 1.0;
+                    for (int g = 0; g <= mz; g++) {  // g = mz - kz
+                        acc += Ms[d_tab.idx3[mx - a][my - b][mz - g]] * (fx * fy * fz);
+                        fz = fz * tz * d_tab.rcp[g + 1];
+                    }
+                    fy = fy * ty * d_tab.rcp[b + 1];
+                }
+                fx = fx * tx * d_tab.rcp[a + 1];
             }
-            if (m < nc) M[(int64_t)c * nc + m] += total;
+            total += acc;
         }
+        M[(int64_t)c * nc + m] += total;
     }
 }
 
+// ---- L2L: thread per (cell of this level, coefficient k), pull from parent
 // Ldst[k] += (1/k!) sum_{n>=k} Lsrc[n] n! t^{n-k}/(n-k)!,  t = c_child - c_parent
-// (src/_taylor.py:220-240), pull from the parent.
-__global__ void __launch_bounds__(kVertWarps * 32) l2l_level(int p, const int32_t *__restrict__ cells, int32_t count,
-                                                            const int32_t *__restrict__ parent,
-                                                            const double *__restrict__ ctr, double *L) {
-    __shared__ VertSmem sm;
-    vert_load_idx3(sm);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// (src/_taylor.py:220-240), running products as in M2M.
+__global__ void l2l_level(int p, const int32_t *__restrict__ cells, int32_t count,
+                          const int32_t *__restrict__ parent, const double *__restrict__ ctr,
+                          double *L) {
     const int nc = ncoef(p);
-    double *ls = sm.src[w];
-    double (*tp)[TMAX + 1] = sm.tp[w];
-    for (int32_t ci = blockIdx.x * kVertWarps + w; ci < count; ci += gridDim.x * kVertWarps) {
-        const int32_t c = cells[ci];
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < (int64_t)count * nc;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = cells[it / nc];
+        const int k = (int)(it % nc);
         const int32_t pa = parent[c];
         if (pa < 0) continue;
-        __syncwarp();  // the previous cell's slab is consumed
-        for (int k = lane; k < nc; k += 32) ls[k] = L[(int64_t)pa * nc + k];
-        vert_powers(tp, p, ctr[c * 3] - ctr[pa * 3], ctr[c * 3 + 1] - ctr[pa * 3 + 1], ctr[c * 3 + 2] - ctr[pa * 3 + 2],
-                    lane);
-        __syncwarp();
-        for (int k = lane; k < nc; k += 32) {
-            const int kx = d_tab.mi[k][0], ky = d_tab.mi[k][1], kz = d_tab.mi[k][2];
-            const int rem = p - 1 - (kx + ky + kz);  // max degree of n-k
-            double acc = 0.0;
-            for (int ax = 0; ax <= rem; ax++)
-                for (int ay = 0; ay <= rem - ax; ay++)
-                    for (int az = 0; az <= rem - ax - ay; az++) {
-                        const int n = sm.idx3[kx + ax][ky + ay][kz + az];
-                        acc += ls[n] * d_tab.mfact[n] * (tp[0][ax] * tp[1][ay] * tp[2][az]);
-                    }
-            L[(int64_t)c * nc + k] += acc * (d_tab.ifact[kx] * d_tab.ifact[ky] * d_tab.ifact[kz]);
+        const int kx = d_tab.mi[k][0], ky = d_tab.mi[k][1], kz = d_tab.mi[k][2];
+        const int rem = p - 1 - (kx + ky + kz);  // max degree of n-k
+        const double tx = ctr[c * 3] - ctr[pa * 3], ty = ctr[c * 3 + 1] - ctr[pa * 3 + 1],
+                     tz = ctr[c * 3 + 2] - ctr[pa * 3 + 2];
+        const double *Ls = L + (int64_t)pa * nc;
+        double acc = 0.0, fx = 1.0;
+        for (int ax = 0; ax <= rem; ax++) {
+            double fy = 1.0;
+            for (int ay = 0; ay <= rem - ax; ay++) {
+                double fz = 1.0;
+                for (int az = 0; az <= rem - ax - ay; az++) {
+                    const int n = d_tab.idx3[kx + ax][ky + ay][kz + az];
+                    acc += Ls[n] * d_tab.mfact[n] * (fx * fy * fz);
+                    fz = fz * tz * d_tab.rcp[az + 1];
+                }
+                fy = fy * ty * d_tab.rcp[ay + 1];
+            }
+            fx = fx * tx * d_tab.rcp[ax + 1];
         }
+        L[(int64_t)c * nc + k] += acc * (d_tab.ifact[kx] * d_tab.ifact[ky] * d_tab.ifact[kz]);
     }
 }
 
@@ -260,8 +229,8 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
     for (int L = nlev - 2; L >= 0; L--) {
         int32_t off = host_level_off[L], cnt = host_level_off[L + 1] - off;
         if (cnt <= 0) continue;
-        m2m_level<<<grid_for(cnt, kVertWarps, 148 * 8), kVertWarps * 32, 0, s>>>(p, cells_by_level + off, cnt, leaf,
-                                                                               children, ctr, M); fmm::note_launch();
+        m2m_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, leaf,
+                                                                  children, ctr, M); fmm::note_launch();
     }
     FMM_CUDA_CHECK("fmm_upward");
     return FMM_OK;
@@ -277,8 +246,8 @@ int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *le
     for (int Lv = 1; Lv < nlev; Lv++) {
         int32_t off = host_level_off[Lv], cnt = host_level_off[Lv + 1] - off;
         if (cnt <= 0) continue;
-        l2l_level<<<grid_for(cnt, kVertWarps, 148 * 8), kVertWarps * 32, 0, s>>>(p, cells_by_level + off, cnt, parent,
-                                                                               ctr, L); fmm::note_launch();
+        l2l_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, parent,
+                                                                  ctr, L); fmm::note_launch();
     }
     if (body_hi > body_lo)
         l2p_kernel<<<grid_for(body_hi - body_lo, 128), 128, 0, s>>>(p, body_lo, body_hi, body_leaf, ctr, xs, ys,
