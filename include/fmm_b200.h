@@ -313,9 +313,12 @@ FMM_API int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_
  * _m2p, src/_taylor.py:272-307): for every target leaf row t of the CSR M2P
  * list and every body j of t, phi[j] += sum (-1)^|m| M_m D_m(x_j - c_s) and
  * f[j] -= the gradient terms (f = -grad phi); bodies at a cell center are
- * skipped.  Accumulates (+=) into phi/fx/fy/fz; float64; 1 <= p <= 12. */
-FMM_API int fmm_m2p_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const int32_t *start,
-                const int32_t *end, const double *ctr, const double *M, const double *x, const double *y,
+ * skipped.  Accumulates (+=) into phi/fx/fy/fz; 1 <= p <= 12.  precision
+ * FMM_PREC_FP64 is the reference's arithmetic; FMM_PREC_FP32 (p <= 6; higher
+ * orders stay float64) forms D, the moments and each source's contribution in
+ * float32 and accumulates them in float64. */
+FMM_API int fmm_m2p_csr(int p, int precision, int32_t ncells, const int64_t *rows, const int32_t *src,
+                const int32_t *start, const int32_t *end, const double *ctr, const double *M, const double *x, const double *y,
                 const double *z, double *phi, double *fx, double *fy, double *fz, void *stream);
 
 /* Near field over the P2P plan.  precision FMM_PREC_FP32 reads the float4

@@ -59,7 +59,7 @@ SIGNATURES = {
                      P],
     "fmm_sort_rows": [I32, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P, P],
-    "fmm_m2p_csr": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "fmm_m2p_csr": [INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p_coincident": [I32, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_unpermute": [P, I64, P, P, P, P, P, P, P, P, P],

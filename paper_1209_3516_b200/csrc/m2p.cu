@@ -6,7 +6,10 @@
 //   f_i(y) -= sum_{|m| < p} (-1)^|m| M_m D_{m+e_i}(y - c)      (f = -grad phi)
 //
 // with D_k = d^k (1/|r|) for |k| <= p from the reference's recurrence.  A
-// body exactly at the cell center is skipped, as in the reference.  Float64.
+// body exactly at the cell center is skipped, as in the reference.  Float64,
+// or (precision="fp32", p <= 6) float32 D, moments and per-source sums: the
+// shift is formed in float64 and rounded once, the running sums stay
+// float64.
 //
 // One warp per target row, one LANE per body (rows of more than 32 bodies
 // take several passes); the warp walks the row's source cells together, so
@@ -19,7 +22,7 @@
 
 namespace fmm {
 
-template <int P>
+template <int P, typename T = double>
 __global__ void __launch_bounds__(128) m2p_reg(int32_t ncells, const int64_t *__restrict__ rows,
                                                const int32_t *__restrict__ src,
                                                const int32_t *__restrict__ start,
@@ -40,27 +43,46 @@ __global__ void __launch_bounds__(128) m2p_reg(int32_t ncells, const int64_t *__
             const bool valid = i < end[t];
             const double bx = valid ? x[i] : 0.0, by = valid ? y[i] : 0.0, bz = valid ? z[i] : 0.0;
             double ap = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
-            for (int64_t k = k0; k < k1; k++) {
-                const int32_t s = src[k];
-                const double rx = bx - ctr[s * 3], ry = by - ctr[s * 3 + 1], rz = bz - ctr[s * 3 + 2];
-                if (!valid || rx * rx + ry * ry + rz * rz == 0.0) continue;
-                double D[ND];
-                d_tensors_reg<P + 1>(rx, ry, rz, D);
+            // one source's contribution (zero for a body at its center)
+            auto term = [&](int32_t s, double cx, double cy, double cz, T &pot, T &gx, T &gy, T &gz) {
+                pot = gx = gy = gz = T(0);
+                const double rx = bx - cx, ry = by - cy, rz = bz - cz;
+                if (!valid || rx * rx + ry * ry + rz * rz == 0.0) return false;
+                T D[ND];
+                d_tensors_reg<P + 1, T>(T(rx), T(ry), T(rz), D);
                 const double *Ms = M + (int64_t)s * NC;
-                double pot = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
                 static_for<0, NC>([&](auto Im) {
                     constexpr int m = decltype(Im)::value;
                     constexpr int mx = kTab.mi[m][0], my = kTab.mi[m][1], mz = kTab.mi[m][2];
-                    const double mm = (kTab.deg[m] & 1) ? -__ldg(&Ms[m]) : __ldg(&Ms[m]);
+                    const T mm = T((kTab.deg[m] & 1) ? -__ldg(&Ms[m]) : __ldg(&Ms[m]));
                     pot += mm * D[m];
                     gx += mm * D[IX(mx + 1, my, mz)];
                     gy += mm * D[IX(mx, my + 1, mz)];
                     gz += mm * D[IX(mx, my, mz + 1)];
                 });
-                ap += pot;
-                ax -= gx;
-                ay -= gy;
-                az -= gz;
+                return true;
+            };
+            auto add = [&](T pot, T gx, T gy, T gz) {
+                ap += (double)pot;
+                ax -= (double)gx;
+                ay -= (double)gy;
+                az -= (double)gz;
+            };
+            // the next source's id and center are fetched one iteration
+            // ahead, off the dependent chain of the current one
+            int32_t sn = src[k0];
+            double cxn = ctr[sn * 3], cyn = ctr[sn * 3 + 1], czn = ctr[sn * 3 + 2];
+            for (int64_t k = k0; k < k1; k++) {
+                const int32_t s = sn;
+                const double cx = cxn, cy = cyn, cz = czn;
+                if (k + 1 < k1) {
+                    sn = src[k + 1];
+                    cxn = ctr[sn * 3];
+                    cyn = ctr[sn * 3 + 1];
+                    czn = ctr[sn * 3 + 2];
+                }
+                T p0, x0, y0, z0;
+                if (term(s, cx, cy, cz, p0, x0, y0, z0)) add(p0, x0, y0, z0);
             }
             if (valid) {
                 phi[i] += ap;
@@ -159,7 +181,7 @@ __global__ void __launch_bounds__(128) m2p_gen(int p, int32_t ncells, const int6
 
 using namespace fmm;
 
-extern "C" int fmm_m2p_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const int32_t *start,
+extern "C" int fmm_m2p_csr(int p, int precision, int32_t ncells, const int64_t *rows, const int32_t *src, const int32_t *start,
                            const int32_t *end, const double *ctr, const double *M, const double *x,
                            const double *y, const double *z, double *phi, double *fx, double *fy, double *fz,
                            void *stream) {
@@ -170,9 +192,13 @@ extern "C" int fmm_m2p_csr(int p, int32_t ncells, const int64_t *rows, const int
     if (ncells <= 0) return FMM_OK;
     cudaStream_t s = as_stream(stream);
     const int grid = grid_for((int64_t)ncells * 32, 128, 148 * 16);
-#define M2P_REG(PP)                                                                                        \
-    case PP:                                                                                               \
-        m2p_reg<PP><<<grid, 128, 0, s>>>(ncells, rows, src, start, end, ctr, M, x, y, z, phi, fx, fy, fz); \
+#define M2P_REG(PP)                                                                                           \
+    case PP:                                                                                                  \
+        if (precision == FMM_PREC_FP32)                                                                       \
+            m2p_reg<PP, float><<<grid, 128, 0, s>>>(ncells, rows, src, start, end, ctr, M, x, y, z, phi, fx, fy, \
+                                                    fz);                                                      \
+        else                                                                                                  \
+            m2p_reg<PP><<<grid, 128, 0, s>>>(ncells, rows, src, start, end, ctr, M, x, y, z, phi, fx, fy, fz); \
         break;
     switch (p) {
         M2P_REG(1)

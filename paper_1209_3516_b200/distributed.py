@@ -218,7 +218,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     with torch.cuda.stream(side):
         ev[3].record(side)
         if treecode:
-            run_m2p(tree, lists, cfg.p, tuple(far))
+            run_m2p(tree, lists, cfg.p, tuple(far), precision=cfg.precision)
         else:
             run_m2l(tree, lists, cfg.p)
         ev[4].record(side)

@@ -568,12 +568,15 @@ def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
                  **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
-def run_m2p(tree: Tree, lists: Lists, p: int, out, src: Tree | None = None) -> None:
+def run_m2p(tree: Tree, lists: Lists, p: int, out, src: Tree | None = None, precision: str = "fp64") -> None:
     """Treecode far field into ``out`` = (phi, fx, fy, fz) (accumulated);
-    the accepted cells (centres, multipoles) are ``src``'s when given."""
+    the accepted cells (centres, multipoles) are ``src``'s when given.
+    ``precision="fp32"`` evaluates each (body, cell) term in float32 for
+    p <= 6 (float64 running sums); higher orders stay float64."""
     P = _lib.ptr
     sb = tree if src is None else src
-    _lib.call("fmm_m2p_csr", p, tree.ncells, P(lists.m2p_rows), P(lists.m2p_src), P(tree.d_start),
+    prec = _lib.PREC_FP32 if precision == "fp32" else _lib.PREC_FP64
+    _lib.call("fmm_m2p_csr", p, prec, tree.ncells, P(lists.m2p_rows), P(lists.m2p_src), P(tree.d_start),
               P(tree.d_end), P(sb.d_ctr), P(sb._M), P(tree.d_x), P(tree.d_y), P(tree.d_z), *(P(a) for a in out),
               _lib.stream_handle())
 
@@ -845,7 +848,7 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         side.wait_event(m2p_ready)
         with torch.cuda.stream(side):
             e_m0.record(side)
-            run_m2p(tree, lists, p, tuple(far), src)
+            run_m2p(tree, lists, p, tuple(far), src, cfg.precision)
             e_m1.record(side)
         e_p0.record(main)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)

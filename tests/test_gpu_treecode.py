@@ -58,6 +58,24 @@ def test_m2p_fp64_only(case):
             assert abs(np.linalg.norm(g) - want) <= FP64_TOL * max(want, 1e-300)
 
 
+def test_m2p_fp32(case):
+    """precision="fp32" M2P (float32 terms for p <= 6, float64 above) against
+    the reference's _exec_m2p: float32 rounding of D and the moments, far
+    below the expansion's truncation error."""
+    if not case.has("m2p_phi"):
+        pytest.skip("no stored M2P-only sums for this case")
+    t = build(case)
+    fb.upward_pass(t, case.p)
+    from paper_1209_3516_b200.traversal import run_m2p
+    lists = fb.treecode_lists(t, fb.MacConfig("fmm", case.theta))
+    out = torch.zeros((4, t.n), dtype=torch.float64, device="cuda")
+    run_m2p(t, lists, case.p, tuple(out), precision="fp32")
+    got = out.cpu().numpy()
+    tol = 2e-5 if case.p <= 6 else FP64_TOL
+    for k, g in zip(("phi", "fx", "fy", "fz"), got):
+        assert rel_l2(g, case["m2p_" + k]) <= tol, k
+
+
 def test_treecode_fp64_matches_reference(case):
     t = build(case)
     cfg = fb.EvalConfig(strategy="treecode", mac=fb.MacConfig("fmm", case.theta), p=case.p)
