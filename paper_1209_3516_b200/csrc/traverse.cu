@@ -93,15 +93,20 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
     const int64_t nround = (nfront + stride - 1) / stride;
     for (int64_t r = 0; r < nround; r++) {
         const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        // children in their octant slots (absent ones flagged, not
+        // compacted: a runtime slot index would turn every register array
+        // access into a select chain)
         int32_t ca[8], cb[8];
+        bool ok[8];
         int fate[8];
-        int n = 0;
+#pragma unroll
+        for (int o = 0; o < 8; o++) ok[o] = false;
         if (k < nfront) {
             const int32_t a = fa[k], b = fb[k];
             if (classify_self) {
                 ca[0] = a;
                 cb[0] = b;
-                n = 1;
+                ok[0] = true;
             } else {
                 const bool la = A.leaf[a], lb = B.leaf[b];
                 const bool open_a = la ? false : (lb ? true : (A.rmax[a] >= B.rmax[b]));
@@ -109,11 +114,9 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
 #pragma unroll
                 for (int o = 0; o < 8; o++) {
                     const int32_t ch = kids[o];
-                    if (ch >= 0) {
-                        ca[n] = open_a ? ch : a;
-                        cb[n] = open_a ? b : ch;
-                        n++;
-                    }
+                    ok[o] = ch >= 0;
+                    ca[o] = open_a ? ch : a;
+                    cb[o] = open_a ? b : ch;
                 }
             }
         }
@@ -121,7 +124,7 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             fate[q] = 0;
-            if (q < n) {
+            if (ok[q]) {
                 // multi-GPU: only targets whose body range meets [blo, bhi)
                 if (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi) continue;
                 fate[q] = pair_fate(ca[q], cb[q], A, B, kind_mac, th2);
