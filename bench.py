@@ -111,8 +111,12 @@ class Clocks:
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
+            q = os.environ.get("FMM_BENCH_CLOCK_Q", self.Q)
+            if q == "none":
+                raise RuntimeError("sampler disabled")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms",
+                                          os.environ.get("FMM_BENCH_CLOCK_MS", "50")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -275,7 +279,12 @@ def run_ours(args):
 
     clocks = Clocks(local)
     clocks.start()  # sampled through warm-up and the timed region (both under load)
-    for _ in range(max(3, args.warmup)):
+    # at least W warm-up steps, and at least 5: the caching allocator settles
+    # its block layout over the first four evaluations (two trees alive while
+    # a step builds the next); a fifth keeps its last cudaMalloc (C2 32 MB,
+    # C3 128 MB) out of the first timed step (tools/alloc_probe.py)
+    warm = max(5, args.warmup)
+    for _ in range(warm):
         tree, rep = step()
     torch.cuda.synchronize()
     if world > 1:
@@ -329,7 +338,7 @@ def run_ours(args):
             fb.evaluate_on_tree(tr, cfg)
             return tr.results_in_input_order()
 
-        for _ in range(2):
+        for _ in range(4):
             e2e_step()
         torch.cuda.synchronize()
         et = []
@@ -381,9 +390,9 @@ def run_ours(args):
     kernel_ms = {k: 1e3 * v for k, v in rep.stats.times.items()}
     line = {
         "metric": "FMM particles/s (Laplace, P=%d)" % solver["p"], "value": value, "unit": "particles/s",
-        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": ms,
         "step_ms": {"min": 1e3 * float(np.min(times)), "median": 1e3 * float(np.median(times)),
-                    "max": 1e3 * float(np.max(times))},
+                    "max": 1e3 * float(np.max(times)), "all": [round(1e3 * t, 3) for t in times]},
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32 P2P / f64 tree+far field" if args.precision == "fp32" else "f64",
         "data": "synthetic", "config": config_block(args, n, solver, {"precision": args.precision,

@@ -20,10 +20,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--nogc", action="store_true")
 ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--strategy", default="dualtree")
+ap.add_argument("--mutual", action="store_true")
+ap.add_argument("--all", action="store_true", help="print every step time")
+ap.add_argument("--warmup", type=int, default=4)
 args = ap.parse_args()
 gen, n, solver = workloads.CONFIGS[args.config]
 pos, q = gen(n, 0)
-cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"], precision="fp32")
+cfg = fb.EvalConfig(strategy=args.strategy, mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"], precision="fp32",
+                    mutual=args.mutual)
 dpos = torch.as_tensor(pos, device="cuda")
 ps = fb.ParticleSet(dpos[:, 0].contiguous(), dpos[:, 1].contiguous(), dpos[:, 2].contiguous(),
                     torch.as_tensor(q, device="cuda"))
@@ -37,7 +42,7 @@ def step():
 
 
 tree = None
-for _ in range(4):
+for _ in range(args.warmup):
     tree = step()
 torch.cuda.synchronize()
 if args.nogc:
@@ -53,14 +58,18 @@ for _ in range(args.steps):
     e1.record()
     e1.synchronize()
     ts.append(e0.elapsed_time(e1))
-    ev0, pev, eend = fb.traversal.last_events
-    pre.append(e0.elapsed_time(pev[0][0]))
-    p2p.append(pev[0][0].elapsed_time(pev[-1][1]))
-    post.append(pev[-1][1].elapsed_time(e1))
+    if args.strategy == "dualtree":
+        ev0, pev, eend = fb.traversal.last_events
+        pre.append(e0.elapsed_time(pev[0][0]))
+        p2p.append(pev[0][0].elapsed_time(pev[-1][1]))
+        post.append(pev[-1][1].elapsed_time(e1))
 s1 = torch.cuda.memory_stats()
 d = {k: s1[k] - s0.get(k, 0) for k in ("segment.all.allocated", "num_alloc_retries", "num_device_alloc")
      if k in s1}
 print(f"{args.config} nogc={args.nogc} ms/step median {np.median(ts):.3f} mean {np.mean(ts):.3f} "
       f"min {np.min(ts):.3f} allocator deltas {d}")
-print(f"  step start -> P2P start {np.median(pre):.3f} ms, P2P {np.median(p2p):.3f} ms, P2P end -> step end "
+if args.all:
+    print("  steps:", " ".join(f"{t:.2f}" for t in ts))
+if pre:
+  print(f"  step start -> P2P start {np.median(pre):.3f} ms, P2P {np.median(p2p):.3f} ms, P2P end -> step end "
       f"{np.median(post):.3f} ms")
