@@ -32,6 +32,7 @@ oracle, all threads) on rank 0 only.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -278,6 +279,12 @@ def run_ours(args):
         return tree, rep
 
     clocks = Clocks(local)
+    # the interpreter's cyclic GC stays out of the timed steps (as in
+    # timeit): a full collection over torch's object graph is a ~15 ms host
+    # pause that leaves the GPU idle (seen as one slow step in ten)
+    gc.collect()
+    gc.freeze()
+    gc.disable()
     clocks.start()  # sampled through warm-up and the timed region (both under load)
     # at least W warm-up steps, and at least 5: the caching allocator settles
     # its block layout over the first four evaluations (two trees alive while
@@ -362,6 +369,7 @@ def run_ours(args):
                        "step, median of the max over ranks"}
         del res
 
+    gc.enable()
     # accuracy of the last timed step: relative L2 error against direct
     # summation on the reference's 1000-body sample (tree order, seed 0)
     acc = None
