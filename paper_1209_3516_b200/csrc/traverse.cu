@@ -89,6 +89,8 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
     // buffer capacity were never written
     int64_t nfront = nfront_dev ? (int64_t)*nfront_dev : nfront_host;
     if (nfront > cap_front) nfront = cap_front;
+    // a range that covers the root's bodies filters nothing: skip the loads
+    const bool ranged = blo > cstart[0] || bhi < cend[0];
     // iterate in warp-uniform trip counts so the shuffles see full warps
     const int64_t nround = (nfront + stride - 1) / stride;
     for (int64_t r = 0; r < nround; r++) {
@@ -126,7 +128,7 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
             fate[q] = 0;
             if (ok[q]) {
                 // multi-GPU: only targets whose body range meets [blo, bhi)
-                if (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi) continue;
+                if (ranged && (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi)) continue;
                 fate[q] = pair_fate(ca[q], cb[q], A, B, kind_mac, th2);
                 // chunked single-GPU runs: an M2L pair belongs to the chunk
                 // holding its target's first body (no pair is emitted twice)
