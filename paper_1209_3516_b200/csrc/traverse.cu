@@ -103,6 +103,10 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
         int fate[8];
 #pragma unroll
         for (int o = 0; o < 8; o++) ok[o] = false;
+        // the side of the pair that is not opened is the same for all its
+        // children: its leaf flag, centre and radius are read once
+        bool open_a = false, lfix = false;
+        double fx = 0.0, fy = 0.0, fz = 0.0, fbm = 0.0, frm = 0.0;
         if (k < nfront) {
             const int32_t a = fa[k], b = fb[k];
             if (classify_self) {
@@ -111,7 +115,15 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                 ok[0] = true;
             } else {
                 const bool la = A.leaf[a], lb = B.leaf[b];
-                const bool open_a = la ? false : (lb ? true : (A.rmax[a] >= B.rmax[b]));
+                open_a = la ? false : (lb ? true : (A.rmax[a] >= B.rmax[b]));
+                const Cells &F = open_a ? B : A;
+                const int32_t f = open_a ? b : a;
+                lfix = open_a ? lb : la;
+                fx = F.ctr[f * 3];
+                fy = F.ctr[f * 3 + 1];
+                fz = F.ctr[f * 3 + 2];
+                fbm = F.bmax[f];
+                frm = F.rmax[f];
                 const int32_t *kids = open_a ? A.children + a * 8 : B.children + b * 8;
 #pragma unroll
                 for (int o = 0; o < 8; o++) {
@@ -122,6 +134,24 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                 }
             }
         }
+        // pair_fate with the fixed side's values (same operations and order)
+        auto fate_of = [&](int32_t a, int32_t b) {
+            if (classify_self) return pair_fate(a, b, A, B, kind_mac, th2);
+            const Cells &O = open_a ? A : B;
+            const int32_t c = open_a ? a : b;  // the opened side's child
+            if (lfix && O.leaf[c]) return 1;
+            const double ax = open_a ? O.ctr[c * 3] : fx, ay = open_a ? O.ctr[c * 3 + 1] : fy,
+                         az = open_a ? O.ctr[c * 3 + 2] : fz;
+            const double bx = open_a ? fx : O.ctr[c * 3], by = open_a ? fy : O.ctr[c * 3 + 1],
+                         bz = open_a ? fz : O.ctr[c * 3 + 2];
+            const double dx = ax - bx, dy = ay - by, dz = az - bz;
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 == 0.0) return 3;
+            const double bma = open_a ? O.bmax[c] : fbm, bmb = open_a ? fbm : O.bmax[c];
+            const double rmb = open_a ? frm : O.rmax[c];
+            const double sz = kind_mac == 2 ? bma + bmb : (kind_mac == 1 ? bmb : 2.0 * rmb);
+            return sz * sz < th2 * r2 ? 2 : 3;
+        };
         int np = 0, nm = 0, nn = 0;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
@@ -129,7 +159,7 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
             if (ok[q]) {
                 // multi-GPU: only targets whose body range meets [blo, bhi)
                 if (ranged && (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi)) continue;
-                fate[q] = pair_fate(ca[q], cb[q], A, B, kind_mac, th2);
+                fate[q] = fate_of(ca[q], cb[q]);
                 // chunked single-GPU runs: an M2L pair belongs to the chunk
                 // holding its target's first body (no pair is emitted twice)
                 if (fate[q] == 2 && m2l_owner && (cstart[ca[q]] < blo || cstart[ca[q]] >= bhi)) fate[q] = 0;
