@@ -34,10 +34,9 @@ namespace fmm {
 // the target leaf itself, and only between bodies with equal depth-21 keys
 // -- with the sorted keys given, leaves without two equal adjacent keys
 // skip the O(|t|^2) scan.
-constexpr int kPlanWarps = 8;
+constexpr int kPlanWarps = 4;
 constexpr int kPlanSegWords = 1024;  // 32768 ordinals per bitmap pass
-constexpr int kWideWarps = 4;       // plan_rows_wide_kernel: warps per block
-constexpr int kWideMax = 1024;      // longest row it takes (ordinals staged in shared memory)
+constexpr int kWideMax = 1024;      // longest row staged in shared memory (longer ones gather per pass)
 
 // A row's coincident-pair scan, counters and run range (one warp).
 __device__ __forceinline__ void plan_row_finish(int32_t r, int32_t t, int64_t k0, int64_t nrun, long long blocks,
@@ -161,86 +160,22 @@ __device__ __forceinline__ uint32_t plan_pass(uint32_t *bm, uint32_t seg, uint32
     return top;
 }
 
-__global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
-    const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows,
-    const int32_t *__restrict__ src, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-    const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
-    const int32_t *__restrict__ s_bend, int cross, int32_t soff, const double *__restrict__ xs,
-    const double *__restrict__ ys, const double *__restrict__ zs, const uint64_t *__restrict__ keys,
-    int64_t *run_rng, int4 *runs, unsigned long long *stats, unsigned long long *nruns_total, int32_t *wide,
-    unsigned long long *nwide) {
-    __shared__ uint32_t bm_all[kPlanWarps][kPlanSegWords + 2];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t *bm = bm_all[wid] + 1;  // bm[-1] and bm[kPlanSegWords] stay 0: neighbour words of the edges
-    for (int x = lane; x < kPlanSegWords + 2; x += 32) bm_all[wid][x] = 0u;
-    __syncwarp();
-    const int32_t nrows = *nrows_dev;
-    for (int32_t r = blockIdx.x * kPlanWarps + wid; r < nrows; r += gridDim.x * kPlanWarps) {
-        const int32_t t = leaf_rows[r];
-        const int64_t k0 = rows[t], k1 = rows[t + 1];
-        const int32_t ts = start[t], te = end[t];
-        const int64_t nt = te - ts;
-        const int32_t ot = cross ? -1 : t_ord[t];  // the self leaf's ordinal
-        uint32_t lo = 0xffffffffu, hi = 0u;
-        for (int64_t k = k0 + lane; k < k1; k += 32) {
-            const uint32_t v = (uint32_t)s_ord[src[k]];
-            lo = min(lo, v);
-            hi = max(hi, v);
-        }
-        lo = __reduce_min_sync(0xffffffffu, lo);
-        hi = __reduce_max_sync(0xffffffffu, hi);
-        if (k1 - k0 <= kWideMax && (hi >> 15) != (lo >> 15)) {  // several bitmap windows: plan_rows_wide_kernel
-            if (lane == 0) wide[atomicAdd(nwide, 1ull)] = r;
-            continue;
-        }
-        long long blocks = 0;
-        bool self = false;
-        int64_t nrun = 0;        // runs so far in this row (warp-uniform)
-        uint32_t prev_top = 0u;  // bit 31 of the word before the current pass
-        for (uint32_t seg = lo >> 15; k1 > k0 && seg <= (hi >> 15); seg++) {
-            const uint32_t sbase = seg << 15;
-            bool next_first = false;  // is ordinal sbase + 32768 (next pass) set?
-            for (int64_t k = k0 + lane; k < k1; k += 32) {
-                const uint32_t v = (uint32_t)s_ord[src[k]];
-                if ((v >> 15) == seg) atomicOr(&bm[(v >> 5) & (kPlanSegWords - 1)], 1u << (v & 31u));
-                next_first |= v == sbase + 32768u;
-            }
-            next_first = __any_sync(0xffffffffu, next_first);
-            __syncwarp();
-            const uint32_t wa = (seg == (lo >> 15)) ? ((lo >> 5) & (kPlanSegWords - 1)) : 0u;
-            const uint32_t wb = (seg == (hi >> 15)) ? ((hi >> 5) & (kPlanSegWords - 1)) : kPlanSegWords - 1;
-            prev_top = plan_pass(bm, seg, wa, wb, prev_top, next_first, ot, k0, nt, nrun, blocks, self, s_bstart,
-                                 s_bend, soff, runs, lane);
-        }
-        plan_row_finish(r, t, k0, nrun, blocks, self, ts, te, xs, ys, zs, keys, run_rng, stats, nruns_total, lane);
-    }
-}
-
-// Rows whose ordinals span several bitmap windows (and hold <= 1024
-// sources): the ordinals are staged once in the warp's shared-memory slab
-// and the passes visit only the windows that hold some -- a row of leaf
-// neighbours in an adaptive tree clusters into a few dense groups of
-// ordinals far apart -- each pass scanning only the words between its
-// smallest and largest ordinal.
-__device__ __forceinline__ void plan_row_wide(int32_t r, int32_t t, int64_t k0, int64_t len, uint32_t *bm,
-                                              uint32_t *ent, const int32_t *__restrict__ src,
-                                              const int32_t *__restrict__ start, const int32_t *__restrict__ end,
-                                              const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord,
-                                              const int32_t *__restrict__ s_bstart, const int32_t *__restrict__ s_bend,
-                                              int cross, int32_t soff, const double *__restrict__ xs,
-                                              const double *__restrict__ ys, const double *__restrict__ zs,
-                                              const uint64_t *__restrict__ keys, int64_t *run_rng, int4 *runs,
-                                              unsigned long long *stats, unsigned long long *nruns_total, int lane) {
+// Rows of up to kWideMax sources: the ordinals were staged in the warp's
+// shared slab `ent` while their range was found, and the passes visit only
+// the bitmap windows that hold some -- a row of leaf neighbours in an
+// adaptive tree clusters into a few dense groups of ordinals far apart --
+// each pass scanning only the words between its smallest and largest
+// ordinal, with no second gather of the row.
+__device__ __forceinline__ void plan_row_staged(int32_t r, int32_t t, int64_t k0, int n, uint32_t seg, uint32_t *bm,
+                                                const uint32_t *ent, const int32_t *__restrict__ start,
+                                                const int32_t *__restrict__ end, const int32_t *__restrict__ t_ord,
+                                                const int32_t *__restrict__ s_bstart,
+                                                const int32_t *__restrict__ s_bend, int cross, int32_t soff,
+                                                const double *__restrict__ xs, const double *__restrict__ ys,
+                                                const double *__restrict__ zs, const uint64_t *__restrict__ keys,
+                                                int64_t *run_rng, int4 *runs, unsigned long long *stats,
+                                                unsigned long long *nruns_total, int lane) {
     constexpr uint32_t kNone = 0xffffffffu;
-    const int n = (int)len;
-    uint32_t seg = kNone;
-    for (int e = lane; e < n; e += 32) {
-        const uint32_t v = (uint32_t)s_ord[src[k0 + e]];
-        ent[e] = v;
-        seg = min(seg, v >> 15);
-    }
-    seg = __reduce_min_sync(0xffffffffu, seg);
-    __syncwarp();
     const int32_t ts = start[t], te = end[t];
     const int64_t nt = te - ts;
     const int32_t ot = cross ? -1 : t_ord[t];
@@ -248,7 +183,7 @@ __device__ __forceinline__ void plan_row_wide(int32_t r, int32_t t, int64_t k0, 
     bool self = false;
     int64_t nrun = 0;
     uint32_t prev_seg = kNone, prev_top = 0u;
-    while (seg != kNone) {
+    while (n > 0 && seg != kNone) {
         const uint32_t sbase = seg << 15;
         uint32_t wa = kNone, wb = 0u, nseg = kNone;
         bool next_first = false;
@@ -279,26 +214,63 @@ __device__ __forceinline__ void plan_row_wide(int32_t r, int32_t t, int64_t k0, 
     __syncwarp();  // ent is rewritten by the warp's next row
 }
 
-__global__ void __launch_bounds__(kWideWarps * 32) plan_rows_wide_kernel(
-    const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows, const int32_t *__restrict__ src,
-    const int32_t *__restrict__ start, const int32_t *__restrict__ end, const int32_t *__restrict__ t_ord,
-    const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart, const int32_t *__restrict__ s_bend,
-    int cross, int32_t soff, const double *__restrict__ xs, const double *__restrict__ ys,
-    const double *__restrict__ zs, const uint64_t *__restrict__ keys, int64_t *run_rng, int4 *runs,
-    unsigned long long *stats, unsigned long long *nruns_total, const int32_t *__restrict__ wide,
-    const unsigned long long *__restrict__ nwide) {
-    __shared__ uint32_t bm_all[kWideWarps][kPlanSegWords + 2];
-    __shared__ uint32_t ent_all[kWideWarps][kWideMax];
+__global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
+    const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows,
+    const int32_t *__restrict__ src, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+    const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
+    const int32_t *__restrict__ s_bend, int cross, int32_t soff, const double *__restrict__ xs,
+    const double *__restrict__ ys, const double *__restrict__ zs, const uint64_t *__restrict__ keys,
+    int64_t *run_rng, int4 *runs, unsigned long long *stats, unsigned long long *nruns_total) {
+    __shared__ uint32_t bm_all[kPlanWarps][kPlanSegWords + 2];
+    __shared__ uint32_t ent_all[kPlanWarps][kWideMax];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t *bm = bm_all[wid] + 1;  // bm[-1] and bm[kPlanSegWords] stay 0
+    uint32_t *ent = ent_all[wid];
+    uint32_t *bm = bm_all[wid] + 1;  // bm[-1] and bm[kPlanSegWords] stay 0: neighbour words of the edges
     for (int x = lane; x < kPlanSegWords + 2; x += 32) bm_all[wid][x] = 0u;
     __syncwarp();
-    const int64_t n = (int64_t)*nwide;
-    for (int64_t q = (int64_t)blockIdx.x * kWideWarps + wid; q < n; q += (int64_t)gridDim.x * kWideWarps) {
-        const int32_t r = wide[q], t = leaf_rows[r];
-        const int64_t k0 = rows[t], len = rows[t + 1] - k0;
-        plan_row_wide(r, t, k0, len, bm, ent_all[wid], src, start, end, t_ord, s_ord, s_bstart, s_bend, cross, soff,
-                      xs, ys, zs, keys, run_rng, runs, stats, nruns_total, lane);
+    const int32_t nrows = *nrows_dev;
+    for (int32_t r = blockIdx.x * kPlanWarps + wid; r < nrows; r += gridDim.x * kPlanWarps) {
+        const int32_t t = leaf_rows[r];
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        const int32_t ts = start[t], te = end[t];
+        const int64_t nt = te - ts;
+        const int32_t ot = cross ? -1 : t_ord[t];  // the self leaf's ordinal
+        const bool staged = k1 - k0 <= kWideMax;
+        uint32_t lo = 0xffffffffu, hi = 0u;
+        for (int64_t k = k0 + lane; k < k1; k += 32) {
+            const uint32_t v = (uint32_t)s_ord[src[k]];
+            if (staged) ent[k - k0] = v;
+            lo = min(lo, v);
+            hi = max(hi, v);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (staged) {  // one gather of the row, non-empty windows only
+            __syncwarp();
+            plan_row_staged(r, t, k0, (int)(k1 - k0), lo >> 15, bm, ent, start, end, t_ord, s_bstart, s_bend, cross,
+                            soff, xs, ys, zs, keys, run_rng, runs, stats, nruns_total, lane);
+            continue;
+        }
+        long long blocks = 0;
+        bool self = false;
+        int64_t nrun = 0;        // runs so far in this row (warp-uniform)
+        uint32_t prev_top = 0u;  // bit 31 of the word before the current pass
+        for (uint32_t seg = lo >> 15; k1 > k0 && seg <= (hi >> 15); seg++) {
+            const uint32_t sbase = seg << 15;
+            bool next_first = false;  // is ordinal sbase + 32768 (next pass) set?
+            for (int64_t k = k0 + lane; k < k1; k += 32) {
+                const uint32_t v = (uint32_t)s_ord[src[k]];
+                if ((v >> 15) == seg) atomicOr(&bm[(v >> 5) & (kPlanSegWords - 1)], 1u << (v & 31u));
+                next_first |= v == sbase + 32768u;
+            }
+            next_first = __any_sync(0xffffffffu, next_first);
+            __syncwarp();
+            const uint32_t wa = (seg == (lo >> 15)) ? ((lo >> 5) & (kPlanSegWords - 1)) : 0u;
+            const uint32_t wb = (seg == (hi >> 15)) ? ((hi >> 5) & (kPlanSegWords - 1)) : kPlanSegWords - 1;
+            prev_top = plan_pass(bm, seg, wa, wb, prev_top, next_first, ot, k0, nt, nrun, blocks, self, s_bstart,
+                                 s_bend, soff, runs, lane);
+        }
+        plan_row_finish(r, t, k0, nrun, blocks, self, ts, te, xs, ys, zs, keys, run_rng, stats, nruns_total, lane);
     }
 }
 
@@ -356,8 +328,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     }
     Arena ar(ws, ws_bytes);
     int32_t *nsel_ws = ar.take<int32_t>(1);
-    unsigned long long *st3 = ar.take<unsigned long long>(4);  // {pairs, skipped, runs, wide rows}
-    int32_t *wide = ar.take<int32_t>((size_t)ncells);
+    unsigned long long *st3 = ar.take<unsigned long long>(4);  // {pairs, skipped, runs, -}
     uint8_t *flag = ar.take<uint8_t>((size_t)ncells);
     int32_t *t_ord = ar.take<int32_t>((size_t)ncells);
     int32_t *t_bs = ar.take<int32_t>((size_t)ncells);
@@ -365,7 +336,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     int32_t *s_ord = cross ? ar.take<int32_t>((size_t)src_ncells) : t_ord;
     int32_t *s_bs = cross ? ar.take<int32_t>((size_t)src_ncells) : t_bs;
     int32_t *s_be = cross ? ar.take<int32_t>((size_t)src_ncells) : t_be;
-    if (!nsel_ws || !st3 || !wide || !flag || !t_ord || !t_bs || !t_be || !s_ord || !s_bs || !s_be) {
+    if (!nsel_ws || !st3 || !flag || !t_ord || !t_bs || !t_be || !s_ord || !s_bs || !s_be) {
         set_error("workspace too small");
         return FMM_ERR_INVALID;
     }
@@ -386,10 +357,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     // leaf_rows is sized ncells: the kernel reads the row count on the device
     plan_rows_kernel<<<grid_for(ncells, kPlanWarps, 148 * 8), kPlanWarps * 32, 0, s>>>(
         nsel, leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross, cross ? src_offset : 0, xs, ys, zs,
-        keys, run_rng, (int4 *)runs, stats, st3 + 2, wide, st3 + 3); fmm::note_launch();
-    plan_rows_wide_kernel<<<148 * 6, kWideWarps * 32, 0, s>>>(leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross,
-                                                  cross ? src_offset : 0, xs, ys, zs, keys, run_rng, (int4 *)runs,
-                                                  stats, st3 + 2, wide, st3 + 3); fmm::note_launch();
+        keys, run_rng, (int4 *)runs, stats, st3 + 2); fmm::note_launch();
     if (host_nleaf_rows || host_nruns) {  // optional host view (synchronises)
         int32_t nrows = 0;
         unsigned long long total = 0;
