@@ -322,7 +322,9 @@ FMM_API int fmm_m2p_csr(int p, int precision, int32_t ncells, const int64_t *row
                 const double *z, double *phi, double *fx, double *fy, double *fz, void *stream);
 
 /* Near field over the P2P plan.  precision FMM_PREC_FP32 reads the float4
- * body copy b32; FMM_PREC_FP64 reads the float64 SoA.  Results are STORED
+ * body copy b32; FMM_PREC_FP64 reads, when b32 is given, the double4 body
+ * copy written by fmm_pack_bodies_f64 (streamed rows, rsqrt.approx.f64 +
+ * Newton), else the float64 SoA.  Results are STORED
  * (not accumulated) into phi/fx/fy/fz for every body of a planned leaf row.
  * use_rsqrt (FP64 only) mirrors src/_taylor.py:318-323.
  * nrows bounds the grid; when dev_nrows is given the kernels stop at the
@@ -337,6 +339,11 @@ FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_t n
             const int32_t *start, const int32_t *end, const int64_t *run_rng, const void *runs,
             const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
             const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);
+
+/* Pack the float64 SoA bodies into the double4 (x, y, z, q) copy the
+ * streamed FP64 P2P reads (32 B per body). */
+FMM_API int fmm_pack_bodies_f64(int64_t n, const double *xs, const double *ys, const double *zs, const double *qs,
+                                void *out, void *stream);
 
 /* Coincident (target, source) pairs of a cross-tree P2P plan (r2 == 0.0 in
  * float64, which the reference skips and counts as p2p_skipped,

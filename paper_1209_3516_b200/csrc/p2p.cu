@@ -364,11 +364,13 @@ struct RunCursor {
 
 // Copy sequence positions [p0, p0 + need) into `dst` (lane 0 only): walk
 // the cursor forward to p0, then one bulk copy per run segment.
-__device__ __forceinline__ void chunk_produce(float4 *dst, uint64_t *bar, int32_t p0, int32_t need, RunCursor &c,
-                                              const int2 *srun, const float4 *__restrict__ b) {
+template <typename T>
+__device__ __forceinline__ void chunk_produce(T *dst, uint64_t *bar, int32_t p0, int32_t need, RunCursor &c,
+                                              const int2 *srun, const T *__restrict__ b) {
     // (no proxy fence: every LDS of this stage has returned -- its values were
-    // consumed by the FP32 math -- before the __syncwarp that precedes us)
-    mbar_expect_tx(bar, (uint32_t)need * 16u);
+    // consumed by the math -- before the __syncwarp that precedes us)
+    constexpr uint32_t kBytes = sizeof(T);
+    mbar_expect_tx(bar, (uint32_t)need * kBytes);
     int2 run = srun[c.r];
     while (c.rpos + (run.y - run.x) <= p0) {
         c.rpos += run.y - run.x;
@@ -377,7 +379,7 @@ __device__ __forceinline__ void chunk_produce(float4 *dst, uint64_t *bar, int32_
     int32_t off = p0 - c.rpos;
     while (need > 0) {
         const int32_t take = min(run.y - run.x - off, need);
-        if (take > 0) bulk_g2s(dst, b + run.x + off, (uint32_t)take * 16u, bar);
+        if (take > 0) bulk_g2s(dst, b + run.x + off, (uint32_t)take * kBytes, bar);
         dst += take;
         need -= take;
         if (need > 0) {
@@ -610,7 +612,269 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
     }
 }
 
-// ---- FP64 variant (parity mode) ------------------------------------------
+// ---- FP64 streamed variant (parity mode, and the promoted near field of
+// precision="fp32" at the high-order corner) -------------------------------
+//
+// Same decomposition as the FP32 streamed rows: one CTA per target leaf row,
+// 4 warps, every target block's source line (self leaf guarded, then the
+// row's non-self run sequence) split over the warps by weight, the run
+// sequence streamed per warp through a 2-stage ring of double4 chunks filled
+// by cp.async.bulk on mbarriers.  Targets are register-blocked 4 per lane.
+// 1/sqrt(r2) is MUFU.RSQ64H (rsqrt.approx.f64, ~2^-23 relative) refined by
+// one third-order step, y + y e (1/2 + 3/8 e) with e = 1 - r2 y^2 (error
+// O(e^3), below float64 rounding), instead of IEEE div + sqrt: 5 FP64 ops
+// against 2 Newton steps' 8.  Each lane's sums are float64 throughout.
+constexpr int kK64 = 4;                 // targets per lane
+constexpr int kSPL64 = 4;               // sources per lane per chunk
+constexpr int kChunk64 = 32 * kSPL64;   // sources per chunk
+constexpr int kMaxUnits64 = 128;        // 4 parts x 32 blocks (ncrit <= 128 folds)
+
+__device__ __forceinline__ double rsqrt_f64(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-(x * y), y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
+template <bool GUARD>
+__device__ __forceinline__ void p2p_f64_pairs(const double4 &s, int32_t rel, const double (&tx)[kK64],
+                                              const double (&ty)[kK64], const double (&tz)[kK64], double (&ap)[kK64],
+                                              double (&ax)[kK64], double (&ay)[kK64], double (&az)[kK64]) {
+#pragma unroll
+    for (int u = 0; u < kK64; u++) {
+        const double dx = tx[u] - s.x, dy = ty[u] - s.y, dz = tz[u] - s.z;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double rinv = rsqrt_f64(r2);
+        if (GUARD) rinv = (r2 > 0.0 && rel != u) ? rinv : 0.0;
+        const double qr = s.w * rinv;
+        const double qr3 = qr * rinv * rinv;
+        ap[u] += qr;
+        ax[u] = fma(qr3, dx, ax[u]);
+        ay[u] = fma(qr3, dy, ay[u]);
+        az[u] = fma(qr3, dz, az[u]);
+    }
+}
+
+// warp_fold for the 16 float64 sums of a 4-target block: lane l ends holding
+// value index l mod 16 = quantity (l mod 16) / 4 of target l mod 4.
+__device__ __forceinline__ double warp_fold_f64(const double (&ap)[kK64], const double (&ax)[kK64],
+                                                const double (&ay)[kK64], const double (&az)[kK64], int lane) {
+    constexpr int N = 4 * kK64;
+    double v[N];
+#pragma unroll
+    for (int u = 0; u < kK64; u++) {
+        v[u] = ap[u];
+        v[kK64 + u] = ax[u];
+        v[2 * kK64 + u] = ay[u];
+        v[3 * kK64 + u] = az[u];
+    }
+#pragma unroll
+    for (int n = N; n > 1; n >>= 1) {
+        const int o = n >> 1;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < n / 2; k++) {
+            const double keep = up ? v[k + n / 2] : v[k];
+            const double send = up ? v[k] : v[k + n / 2];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+#pragma unroll
+    for (int o = N; o < 32; o <<= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    return v[0];
+}
+
+// One unit of a streamed FP64 row (see p2p_f32_stream_unit).  GUARD_ALL
+// (cross-tree rows) guards every source against r2 == 0.
+template <bool GUARD_ALL>
+__device__ __forceinline__ double p2p_f64_stream_unit(int32_t i0, int32_t ilast, int32_t ts, int32_t cnt, int32_t s0,
+                                                      int32_t s1, int lane, const double4 *__restrict__ b,
+                                                      double4 *ring, uint64_t *bars, uint32_t &phase,
+                                                      const int2 *srun) {
+    double tx[kK64], ty[kK64], tz[kK64], ap[kK64], ax[kK64], ay[kK64], az[kK64];
+    const int32_t lo = max(s0, cnt) - cnt, hi = max(s1, cnt) - cnt;
+    const int nk = (hi - lo + kChunk64 - 1) / kChunk64;
+    RunCursor cur{0, 0};
+    if (lane == 0)
+        for (int k = 0; k < min(nk, kWStages); k++) {
+            const int32_t p0 = lo + k * kChunk64;
+            chunk_produce(ring + k * kChunk64, &bars[k], p0, min(kChunk64, hi - p0), cur, srun, b);
+        }
+#pragma unroll
+    for (int u = 0; u < kK64; u++) {
+        const double4 t = b[min(i0 + u, ilast)];
+        tx[u] = t.x;
+        ty[u] = t.y;
+        tz[u] = t.z;
+        ap[u] = ax[u] = ay[u] = az[u] = 0.0;
+    }
+    for (int32_t j = ts + s0 + lane; j < ts + min(s1, cnt); j += 32)
+        p2p_f64_pairs<true>(b[j], j - i0, tx, ty, tz, ap, ax, ay, az);
+    int st = 0;
+    for (int k = 0; k < nk; k++) {
+        if (k > 0 && lane == 0 && k - 1 + kWStages < nk) {
+            const int sp = st == 0 ? kWStages - 1 : st - 1;
+            const int32_t p0 = lo + (k - 1 + kWStages) * kChunk64;
+            chunk_produce(ring + sp * kChunk64, &bars[sp], p0, min(kChunk64, hi - p0), cur, srun, b);
+        }
+        __syncwarp();
+        mbar_wait(&bars[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const double4 *src = ring + st * kChunk64 + lane;
+        const int32_t valid = hi - (lo + k * kChunk64);
+        if (valid >= kChunk64) {
+            double4 s = src[0];
+#pragma unroll
+            for (int q = 0; q < kSPL64; q++) {
+                const double4 nxt = src[((q + 1) % kSPL64) * 32];
+                p2p_f64_pairs<GUARD_ALL>(s, -1, tx, ty, tz, ap, ax, ay, az);
+                s = nxt;
+            }
+        } else {
+#pragma unroll 1
+            for (int q = 0; q < kSPL64; q++)
+                if (q * 32 + lane < valid) p2p_f64_pairs<GUARD_ALL>(src[q * 32], -1, tx, ty, tz, ap, ax, ay, az);
+        }
+        __syncwarp();
+        if (++st == kWStages) st = 0;
+    }
+    return warp_fold_f64(ap, ax, ay, az, lane);
+}
+
+// One unit of a row that does not stream (more than kMaxRuns runs): block tb
+// against every run, part `part` of P lane-interleaved parts, from global.
+__device__ __forceinline__ double p2p_f64_runs_unit(int32_t i0, int32_t ilast, int64_t r0, int64_t r1, int part,
+                                                    int P, int lane, bool guard_all, const int4 *__restrict__ runs,
+                                                    const double4 *__restrict__ b) {
+    double tx[kK64], ty[kK64], tz[kK64], ap[kK64], ax[kK64], ay[kK64], az[kK64];
+#pragma unroll
+    for (int u = 0; u < kK64; u++) {
+        const double4 t = b[min(i0 + u, ilast)];
+        tx[u] = t.x;
+        ty[u] = t.y;
+        tz[u] = t.z;
+        ap[u] = ax[u] = ay[u] = az[u] = 0.0;
+    }
+    const int step = 32 * P;
+    for (int64_t r = r0; r < r1; r++) {
+        const int4 run = __ldg(&runs[r]);
+        if (run.z || guard_all) {
+            for (int32_t j = run.x + part * 32 + lane; j < run.y; j += step)
+                p2p_f64_pairs<true>(b[j], j - i0, tx, ty, tz, ap, ax, ay, az);
+        } else {
+            for (int32_t j = run.x + part * 32 + lane; j < run.y; j += step)
+                p2p_f64_pairs<false>(b[j], -1, tx, ty, tz, ap, ax, ay, az);
+        }
+    }
+    return warp_fold_f64(ap, ax, ay, az, lane);
+}
+
+template <bool CROSS>
+__global__ void __launch_bounds__(kP2PWarps * 32, 3) p2p_f64s_kernel(
+    int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
+    const int32_t *__restrict__ start, const int32_t *__restrict__ end, const int64_t *__restrict__ run_off,
+    const int4 *__restrict__ runs, const double4 *__restrict__ b, double *phi, double *fx, double *fy, double *fz) {
+    extern __shared__ __align__(128) double4 pool64[];  // kP2PWarps * kWStages * kChunk64
+    __shared__ double red[kMaxUnits64][4][kK64];
+    __shared__ int2 srun[kMaxRuns];
+    __shared__ int32_t stotal;
+    __shared__ uint64_t wbars[kP2PWarps][kWStages];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        for (int k = 0; k < kWStages; k++) mbar_init(&wbars[w][k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double4 *wring = pool64 + w * kWStages * kChunk64;
+    uint32_t phase = 0;
+    const int32_t nrows = nrows_dev ? *nrows_dev : nrows_host;
+    for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const int32_t t = leaf_rows[row];
+        const int32_t ts = start[t], cnt = end[t] - ts;
+        const int nblk = (cnt + kK64 - 1) / kK64;
+        const int64_t r0 = run_off[2 * (int64_t)row], r1 = run_off[2 * (int64_t)row + 1];
+        const int nr = (int)(r1 - r0);
+        const bool fold = nblk * kP2PWarps <= kMaxUnits64;
+        const bool streamed = fold && nr <= kMaxRuns;
+        if (streamed) {
+            if (threadIdx.x == 0) stotal = 0;
+            __syncthreads();
+            int32_t len = 0;
+            for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+                const int4 rr = __ldg(&runs[r0 + k]);
+                const int2 v = rr.z ? make_int2(rr.x, rr.x) : make_int2(rr.x, rr.y);  // self run: swept apart
+                srun[k] = v;
+                len += v.y - v.x;
+            }
+            for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
+            if (lane == 0) atomicAdd(&stotal, len);
+        }
+        if (fold)
+            for (int k = threadIdx.x; k < nblk * kP2PWarps * 4 * kK64; k += blockDim.x) (&red[0][0][0])[k] = 0.0;
+        __syncthreads();
+        // lane l holds quantity (l >> 2) & 3 of target l & 3
+        auto emit = [&](int u, int tb, double val) {
+            const int q = (lane >> 2) & 3, uu = lane & 3;
+            if (lane >= 16) return;
+            if (fold) {
+                red[u][q][uu] = val;
+            } else if (tb * kK64 + uu < cnt) {
+                double *out = q == 0 ? phi : q == 1 ? fx : q == 2 ? fy : fz;
+                out[ts + tb * kK64 + uu] = val;
+            }
+        };
+        if (streamed) {
+            const int32_t scnt = CROSS ? 0 : cnt;
+            const int64_t L = (int64_t)scnt + stotal;
+            const int64_t Wl = L * nblk;
+            const int64_t A = Wl * w / kP2PWarps, B = Wl * (w + 1) / kP2PWarps;
+            for (int tb = (int)(L > 0 ? A / L : nblk); tb < nblk && L * tb < B; tb++) {
+                const int64_t Sb = L * tb;
+                const int32_t s0 = (int32_t)(max(A, Sb) - Sb), s1 = (int32_t)(min(B, Sb + L) - Sb);
+                if (s1 <= s0) continue;
+                const double val = p2p_f64_stream_unit<CROSS>(ts + tb * kK64, ts + cnt - 1, ts, scnt, s0, s1, lane,
+                                                             b, wring, wbars[w], phase, srun);
+                emit(tb * kP2PWarps + w, tb, val);
+            }
+        } else {
+            const int P = fold ? kP2PWarps : 1;
+            for (int u = w; u < nblk * P; u += kP2PWarps) {
+                const int tb = u / P, part = u % P;
+                const double val =
+                    p2p_f64_runs_unit(ts + tb * kK64, ts + cnt - 1, r0, r1, part, P, lane, CROSS, runs, b);
+                emit(tb * kP2PWarps + part, tb, val);
+            }
+        }
+        __syncthreads();
+        if (fold) {
+            for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+                const int tb = k / kK64, l = k % kK64;
+                double p_ = 0.0, x_ = 0.0, y_ = 0.0, z_ = 0.0;
+                for (int q = 0; q < kP2PWarps; q++) {  // fixed order: deterministic
+                    const int uu = tb * kP2PWarps + q;
+                    p_ += red[uu][0][l];
+                    x_ += red[uu][1][l];
+                    y_ += red[uu][2][l];
+                    z_ += red[uu][3][l];
+                }
+                const int32_t i = ts + k;
+                phi[i] = p_;
+                fx[i] = x_;
+                fy[i] = y_;
+                fz[i] = z_;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void pack_b64_kernel(int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
+                                const double *__restrict__ zs, const double *__restrict__ qs, double4 *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = make_double4(xs[i], ys[i], zs[i], qs[i]);
+}
+
+// ---- FP64 variant (use_rsqrt: the reference's float32 1/sqrt, FP64 sums) --
 template <int K>
 __global__ void __launch_bounds__(kP2PWarps * 32) p2p_f64_kernel(
     int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
@@ -770,6 +1034,13 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_
         kern<<<grid, kP2PWarps * 32, pool, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
                                              (const float4 *)b32, (const float4 *)b32lo, phi, fx, fy, fz,
                                              dev_flag, cross); fmm::note_launch();
+    } else if (precision == FMM_PREC_FP64 && b32 && !use_rsqrt) {
+        // streamed rows over the double4 body copy (fmm_pack_bodies_f64)
+        auto kern = cross ? p2p_f64s_kernel<true> : p2p_f64s_kernel<false>;
+        const int pool = kP2PWarps * kWStages * kChunk64 * (int)sizeof(double4);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pool);
+        kern<<<grid, kP2PWarps * 32, pool, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs,
+                                                (const double4 *)b32, phi, fx, fy, fz); fmm::note_launch();
     } else if (precision == FMM_PREC_FP64) {
         p2p_f64_kernel<4><<<grid, kP2PWarps * 32, 0, s>>>(nrows, dev_nrows, leaf_rows, start, end, run_off,
                                                           (const int4 *)runs, xs, ys, zs, qs, use_rsqrt, phi,
@@ -790,5 +1061,14 @@ extern "C" int fmm_p2p_coincident(int32_t nrows, const int32_t *dev_nrows, const
     p2p_coincident_kernel<<<grid_for(nrows, 1, 148 * 8), 256, 0, as_stream(stream)>>>(
         nrows, dev_nrows, leaf_rows, start, end, run_off, (const int4 *)runs, xs, ys, zs, count); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_p2p_coincident");
+    return FMM_OK;
+}
+
+extern "C" int fmm_pack_bodies_f64(int64_t n, const double *xs, const double *ys, const double *zs, const double *qs,
+                                   void *out, void *stream) {
+    if (n <= 0) return FMM_OK;
+    pack_b64_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, xs, ys, zs, qs, (double4 *)out);
+    fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_pack_bodies_f64");
     return FMM_OK;
 }

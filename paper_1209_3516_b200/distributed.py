@@ -164,14 +164,15 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import (EvalReport, interaction_lists, listfmm_lists, mutual_lists, run_m2l, run_m2p, run_p2p,
-                            treecode_lists)
+    from .traversal import (EvalReport, interaction_lists, listfmm_lists, mutual_lists, near_field_precision,
+                            run_m2l, run_m2p, run_p2p, treecode_lists)
     from .tree import downward_pass
 
     if world == 1:
         from .traversal import evaluate_on_tree
         return evaluate_on_tree(tree, cfg)
     treecode = cfg.strategy == "treecode"
+    nf = near_field_precision(cfg)
     plan = getattr(tree, "_dist_plan", None)
     if plan is None or len(plan.cuts) != world + 1 or plan.rank != rank:
         plan = _Plan(tree, world, rank)
@@ -218,7 +219,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     with torch.cuda.stream(side):
         ev[3].record(side)
         if treecode:
-            run_m2p(tree, lists, cfg.p, tuple(far), precision=cfg.precision)
+            run_m2p(tree, lists, cfg.p, tuple(far), precision=nf)
         else:
             run_m2l(tree, lists, cfg.p)
         ev[4].record(side)
@@ -226,9 +227,9 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
             downward_pass(tree, None, sync=False, body_range=(lo, hi), out=tuple(far))
         ev[5].record(side)
     ev[6].record(main)
-    run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
-    if cfg.precision == "fp32" and int(flag.item()) != 0:
-        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+    run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag)
+    if nf == "fp32" and int(flag.item()) != 0:
+        run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag)
     ev[7].record(main)
     main.wait_event(ev[5])
     P = _lib.ptr

@@ -445,21 +445,65 @@ class CrossBodies:
         self.fp32_exact = tree.fp32_exact and src.fp32_exact
 
 
+# precision="fp32" keeps the near field in float32 only while float32
+# rounding stays well under the expansion's truncation error.  The FP32
+# near-field floor is ~3-6e-7 relative (mixed-sign charges, tens of
+# thousands of sources per target; profiles/r01_c4_sweep.json), while the
+# reference's own error scales as ~1.6e-3 * theta^p (potential, C4 grid).
+# Below theta^p = FP32_GUARD_THETA_P the truncation error would drop under
+# the float32 floor (the C4 corner p=10/theta<=0.4, p=8/theta=0.3), so the
+# near field is evaluated in float64 there and the result stays within 2x
+# the reference's error, the north-star bar for FP32 mode.
+FP32_GUARD_THETA_P = 5e-4
+# listfmm ignores theta: its V-list pairs same-level cells at least one cell
+# apart, an opening ratio of (2 * sqrt(3)/2 * s) / (2 s) = sqrt(3)/2
+LISTFMM_THETA_EQ = 3 ** 0.5 / 2
+
+
+def near_field_precision(cfg: "EvalConfig") -> str:
+    """Arithmetic of the near field for ``cfg``: "fp64" for precision="fp64";
+    for precision="fp32", "fp32" unless theta^p < FP32_GUARD_THETA_P (then
+    "fp64", see above; FMM_B200_FP32_STRICT=1 disables the promotion)."""
+    if cfg.precision == "fp64":
+        return "fp64"
+    if os.environ.get("FMM_B200_FP32_STRICT", "0") == "1":
+        return "fp32"
+    theta = LISTFMM_THETA_EQ if cfg.strategy == "listfmm" else cfg.mac.theta
+    return "fp64" if theta ** cfg.p < FP32_GUARD_THETA_P else "fp32"
+
+
+def _packed_f64(b) -> torch.Tensor:
+    """The double4 (x, y, z, q) body copy the streamed FP64 P2P reads,
+    packed once per body set (32 B per body)."""
+    t = b.__dict__.get("d_b64")
+    if t is None:
+        t = torch.empty((b.d_x.numel(), 4), dtype=torch.float64, device=b.d_x.device)
+        P = _lib.ptr
+        _lib.call("fmm_pack_bodies_f64", b.d_x.numel(), P(b.d_x), P(b.d_y), P(b.d_z), P(b.d_q), P(t),
+                  _lib.stream_handle())
+        b.__dict__["d_b64"] = t
+    return t
+
+
 def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, safe: bool = False,
             flag=None, bodies: CrossBodies | None = None) -> None:
     """P2P over the plan into ``tree``'s accumulators; ``bodies`` holds the
     concatenated body arrays of a cross-tree plan (the target leaf then
-    sweeps only the source runs)."""
+    sweeps only the source runs).  ``precision`` is the near-field
+    arithmetic (``near_field_precision``)."""
     P = _lib.ptr
     b = tree if bodies is None else bodies
     if precision == "fp32":
         # float32 cannot hold these float64 inputs: anchor offsets per row
         prec = _lib.PREC_FP32 if b.fp32_exact else _lib.PREC_FP32_ANCHORED
+        packed, packed_lo = b.d_b32, b.d_b32lo
     else:
         prec = _lib.PREC_FP64
+        # use_rsqrt (the reference's float32 1/sqrt) keeps the SoA kernel
+        packed, packed_lo = (None if use_rsqrt else _packed_f64(b)), None
     _lib.call("fmm_p2p", prec, int(safe), int(use_rsqrt), int(bodies is not None), lists.nrows,
               P(lists.dev_nrows), P(lists.leaf_rows), P(tree.d_start), P(tree.d_end), P(lists.run_off),
-              P(lists.runs), P(b.d_x), P(b.d_y), P(b.d_z), P(b.d_q), P(b.d_b32), P(b.d_b32lo), P(tree.d_phi),
+              P(lists.runs), P(b.d_x), P(b.d_y), P(b.d_z), P(b.d_q), P(packed), P(packed_lo), P(tree.d_phi),
               P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag), _lib.stream_handle())
 
 
@@ -667,6 +711,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
+    nf = near_field_precision(cfg)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -738,7 +783,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             with torch.cuda.stream(pst):
                 ea, eb = E(), E()
                 ea.record(pst)
-                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag, bodies)
+                run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag, bodies)
                 eb.record(pst)
                 p2p_ev.append((ea, eb))
         e_l1.record(lst)
@@ -749,13 +794,13 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             e_down1.record(side)
         e_pend.record(pst)
         main.wait_event(e_pend)
-        redo = cfg.precision == "fp32" and int(flag.item()) != 0
+        redo = nf == "fp32" and int(flag.item()) != 0
         if redo:
             # two distinct bodies collided in FP32 outside a self run: redo guarded
             for lists in parts:
-                run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag, bodies)
+                run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag, bodies)
         # cross-tree: float64-coincident pairs (none unless FP32 saw one)
-        coinc = [count_coincident(tree, x, bodies) for x in parts] if cross and (redo or cfg.precision == "fp64") \
+        coinc = [count_coincident(tree, x, bodies) for x in parts] if cross and (redo or nf == "fp64") \
             else []
         main.wait_event(e_down1)
         P = _lib.ptr
@@ -824,6 +869,7 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
+    nf = near_field_precision(cfg)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -848,17 +894,17 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         side.wait_event(m2p_ready)
         with torch.cuda.stream(side):
             e_m0.record(side)
-            run_m2p(tree, lists, p, tuple(far), src, cfg.precision)
+            run_m2p(tree, lists, p, tuple(far), src, nf)
             e_m1.record(side)
         e_p0.record(main)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag, bodies)
+        run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag, bodies)
         e_p1.record(main)
-        redo = cfg.precision == "fp32" and int(flag.item()) != 0
+        redo = nf == "fp32" and int(flag.item()) != 0
         if redo:
-            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag, bodies)
+            run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag, bodies)
             e_p1.record(main)
-        coinc = count_coincident(tree, lists, bodies) if cross and (redo or cfg.precision == "fp64") else None
+        coinc = count_coincident(tree, lists, bodies) if cross and (redo or nf == "fp64") else None
         main.wait_event(e_m1)
         P = _lib.ptr
         _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
@@ -909,6 +955,7 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
+    nf = near_field_precision(cfg)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -940,10 +987,10 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
             e_d1.record(side)
         e_p0.record(main)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, False, flag)
+        run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag)
         e_p1.record(main)
-        if cfg.precision == "fp32" and int(flag.item()) != 0:
-            run_p2p(tree, lists, cfg.precision, cfg.use_rsqrt, True, flag)
+        if nf == "fp32" and int(flag.item()) != 0:
+            run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag)
             e_p1.record(main)
         main.wait_event(e_d1)
         P = _lib.ptr

@@ -12,7 +12,7 @@ import torch
 
 import paper_1209_3516_b200 as fb
 from paper_1209_3516_b200 import workloads
-from goldens import CASES, Case, canon_pairs, rel_l2, sha
+from goldens import FP32_BAR_FLOOR, CASES, Case, canon_pairs, rel_l2, sha
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -138,8 +138,8 @@ def test_fp32_within_twice_reference_error(case):
     ferr = float(np.sqrt(((fgot - fref) ** 2).sum() / (fref ** 2).sum()))
     perr = rel_l2(b.phi[idx], case["direct_phi"])
     # FP32 rounding floor (~1e-6) matters only where the reference is near-exact
-    assert ferr <= 2.0 * case.meta["force_err"] + 2e-6, (ferr, case.meta["force_err"])
-    assert perr <= 2.0 * case.meta["pot_err"] + 2e-6, (perr, case.meta["pot_err"])
+    assert ferr <= 2.0 * case.meta["force_err"] + FP32_BAR_FLOOR, (ferr, case.meta["force_err"])
+    assert perr <= 2.0 * case.meta["pot_err"] + FP32_BAR_FLOOR, (perr, case.meta["pot_err"])
 
 
 def test_device_direct_matches_oracle():

@@ -208,3 +208,15 @@ def test_integration_binding_matches_header():
     for name, args in found:
         n = len([a for a in args.split(",") if a.strip()])
         assert decls[name] == n, (name, decls[name], n)
+
+
+def test_fp32_promotion_rule():
+    """precision="fp32" keeps FP32 near fields except where the expansion is
+    more accurate than float32 rounding (theta^p < 5e-4): on the C4 grid
+    exactly the three points whose reference error is under ~3.5e-7."""
+    import paper_1209_3516_b200 as fb
+    from paper_1209_3516_b200.traversal import near_field_precision
+    nf = {(p, t): near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", t), p=p, precision="fp32"))
+          for p in (3, 4, 6, 8, 10) for t in (0.3, 0.4, 0.5, 0.6)}
+    assert sorted(k for k, v in nf.items() if v == "fp64") == [(8, 0.3), (10, 0.3), (10, 0.4)]
+    assert near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", 0.3), p=10, precision="fp64")) == "fp64"
