@@ -285,7 +285,11 @@ FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs,
  * synchronises unless host_nruns / host_nleaf_rows are given; the row
  * count is written to dev_nrows for fmm_p2p.
  * Also computes the reference's pair counters (p2p_pairs, p2p_skipped)
- * into dev_stats[2] (src/_taylor.py:366-407 accounting).  keys (the sorted
+ * into dev_stats[0..1] (src/_taylor.py:366-407 accounting); dev_stats[2]
+ * is 0, or -- when a row's runs would pass cap_runs (rows are then left
+ * empty) -- the runs capacity required.  With host_nruns the call then
+ * returns FMM_ERR_CAPACITY and *host_nruns holds that capacity
+ * (grow-and-retry); async callers read dev_stats[2].  keys (the sorted
  * body keys, optional) let leaves without two equal keys skip the
  * coincident-pair scan (coincident bodies share a key); NULL scans all.
  * Cross-tree plans (src_start given, with src_leaf, src_end, src_ncells):

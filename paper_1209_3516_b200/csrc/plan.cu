@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
     const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
     const int32_t *__restrict__ s_bend, int cross, int32_t soff, const double *__restrict__ xs,
     const double *__restrict__ ys, const double *__restrict__ zs, const uint64_t *__restrict__ keys,
-    int64_t *run_rng, int4 *runs, unsigned long long *stats, unsigned long long *nruns_total) {
+    int64_t *run_rng, int4 *runs, int64_t cap_runs, unsigned long long *stats, unsigned long long *nruns_total,
+    unsigned long long *runs_needed) {
     __shared__ uint32_t bm_all[kPlanWarps][kPlanSegWords + 2];
     __shared__ uint32_t ent_all[kPlanWarps][kWideMax];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -235,6 +236,13 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
         const int32_t ts = start[t], te = end[t];
         const int64_t nt = te - ts;
         const int32_t ot = cross ? -1 : t_ord[t];  // the self leaf's ordinal
+        if (k1 > cap_runs) {  // runs are row-local (k0 + run < k1): the buffer is short
+            if (lane == 0) {
+                run_rng[2 * (int64_t)r] = run_rng[2 * (int64_t)r + 1] = k0;
+                atomicMax(runs_needed, (unsigned long long)k1);
+            }
+            continue;
+        }
         const bool staged = k1 - k0 <= kWideMax;
         uint32_t lo = 0xffffffffu, hi = 0u;
         for (int64_t k = k0 + lane; k < k1; k += 32) {
@@ -346,6 +354,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     // the row count and the counters go straight to the caller's buffers
     int32_t *nsel = dev_nrows ? dev_nrows : nsel_ws;
     unsigned long long *stats = dev_stats ? dev_stats : st3;
+    unsigned long long *runs_need = dev_stats ? dev_stats + 2 : st3 + 3;  // 0, or the runs capacity required
     leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag); fmm::note_launch();
     size_t need = 0;
     cub::CountingInputIterator<int32_t> it(0);
@@ -353,21 +362,27 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     if (need > ar.left()) { set_error("select workspace"); return FMM_ERR_INVALID; }
     cub::DeviceSelect::Flagged(ar.rest(), need, it, flag, leaf_rows, nsel, ncells, s);
     cudaMemsetAsync(st3, 0, 4 * sizeof(unsigned long long), s);
-    if (dev_stats) cudaMemsetAsync(dev_stats, 0, 2 * sizeof(unsigned long long), s);
+    if (dev_stats) cudaMemsetAsync(dev_stats, 0, 3 * sizeof(unsigned long long), s);
     // leaf_rows is sized ncells: the kernel reads the row count on the device
     plan_rows_kernel<<<grid_for(ncells, kPlanWarps, 148 * 8), kPlanWarps * 32, 0, s>>>(
         nsel, leaf_rows, rows, src, start, end, t_ord, s_ord, s_bs, s_be, cross, cross ? src_offset : 0, xs, ys, zs,
-        keys, run_rng, (int4 *)runs, stats, st3 + 2); fmm::note_launch();
+        keys, run_rng, (int4 *)runs, cap_runs, stats, st3 + 2, runs_need); fmm::note_launch();
     if (host_nleaf_rows || host_nruns) {  // optional host view (synchronises)
         int32_t nrows = 0;
-        unsigned long long total = 0;
+        unsigned long long total = 0, needed = 0;
         cudaMemcpyAsync(&nrows, nsel, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(&total, st3 + 2, sizeof(total), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&needed, runs_need, sizeof(needed), cudaMemcpyDeviceToHost, s);
         if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status("fmm_p2p_plan sync");
         if (host_nleaf_rows) *host_nleaf_rows = nrows;
+        if (needed) {  // grow-and-retry: the exact capacity comes back in *host_nruns
+            if (host_nruns) *host_nruns = (int64_t)needed;
+            set_error("P2P runs buffer too small: %lld entries needed, cap_runs %lld", (long long)needed,
+                      (long long)cap_runs);
+            return FMM_ERR_CAPACITY;
+        }
         if (host_nruns) *host_nruns = (int64_t)total;
     }
-    (void)cap_runs;
     FMM_CUDA_CHECK("fmm_p2p_plan");
     return FMM_OK;
 }

@@ -35,8 +35,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-__all__ = ["body_cuts", "cell_chunks", "shared_cells", "allgather_rows", "TorchDistComm",
-           "evaluate_partitioned"]
+__all__ = ["body_cuts", "cell_chunks", "shared_cells", "allgather_rows", "gather_rows", "TorchDistComm",
+           "evaluate_partitioned", "RESULTS"]
 
 
 def body_cuts(leaf_start: np.ndarray, leaf_end: np.ndarray, n: int, world: int) -> np.ndarray:
@@ -69,23 +69,58 @@ def shared_cells(cell_start: np.ndarray, cell_end: np.ndarray, cuts: np.ndarray)
     return m
 
 
-def allgather_rows(full: torch.Tensor, chunks, rank: int, world: int, group=None) -> None:
-    """Replace ``full[chunks[r]:chunks[r+1]]`` with rank r's rows, for every r
-    (one padded all-gather; works with NCCL on GPU and gloo on CPU)."""
+def _device_collectives(t: torch.Tensor, group=None) -> bool:
+    """True when the group's backend moves CUDA tensors itself (NCCL over
+    NVLink); gloo moves host tensors, so device rows are staged through the
+    host."""
+    return t.is_cuda and dist.get_backend(group) == "nccl"
+
+
+def _padded_rows(full: torch.Tensor, chunks, rank: int, world: int):
     sizes = [int(chunks[r + 1] - chunks[r]) for r in range(world)]
     width = int(np.prod(full.shape[1:])) if full.dim() > 1 else 1
     rows = max(max(sizes), 1)
     send = torch.zeros((rows, width), dtype=full.dtype, device=full.device)
     mine = full[int(chunks[rank]):int(chunks[rank + 1])].reshape(-1, width)
     send[:mine.shape[0]].copy_(mine)
-    recv = torch.empty((world * rows, width), dtype=full.dtype, device=full.device)
-    if hasattr(dist, "all_gather_into_tensor") and full.is_cuda:
+    return sizes, width, rows, send
+
+
+def allgather_rows(full: torch.Tensor, chunks, rank: int, world: int, group=None) -> None:
+    """Replace ``full[chunks[r]:chunks[r+1]]`` with rank r's rows, for every r:
+    one padded all-gather (``all_gather_into_tensor`` on device tensors under
+    NCCL; host-staged ``all_gather`` under gloo)."""
+    sizes, width, rows, send = _padded_rows(full, chunks, rank, world)
+    if _device_collectives(full, group):
+        recv = torch.empty((world * rows, width), dtype=full.dtype, device=full.device)
         dist.all_gather_into_tensor(recv, send, group=group)
     else:
-        parts = list(recv.split(rows))
-        dist.all_gather(parts, send, group=group)
+        send = send.cpu()
+        recv = torch.empty((world * rows, width), dtype=full.dtype)
+        dist.all_gather(list(recv.split(rows)), send, group=group)
+    recv = recv.to(full.device, non_blocking=True)
     for r in range(world):
         if sizes[r]:
+            full[int(chunks[r]):int(chunks[r + 1])].reshape(-1, width).copy_(recv[r * rows:r * rows + sizes[r]])
+
+
+def gather_rows(full: torch.Tensor, chunks, rank: int, world: int, root: int = 0, group=None) -> None:
+    """Like ``allgather_rows`` but only ``root`` receives the other ranks'
+    rows (one padded gather: (world - 1) / world of the all-gather's
+    traffic stays off the other ranks)."""
+    sizes, width, rows, send = _padded_rows(full, chunks, rank, world)
+    dev = _device_collectives(full, group)
+    if not dev:
+        send = send.cpu()
+    recv = None
+    if rank == root:
+        recv = torch.empty((world * rows, width), dtype=full.dtype, device=send.device)
+    dist.gather(send, list(recv.split(rows)) if recv is not None else None, dst=root, group=group)
+    if rank != root:
+        return
+    recv = recv.to(full.device, non_blocking=True)
+    for r in range(world):
+        if sizes[r] and r != rank:
             full[int(chunks[r]):int(chunks[r + 1])].reshape(-1, width).copy_(recv[r * rows:r * rows + sizes[r]])
 
 
@@ -145,7 +180,8 @@ def _upward_cells(tree, p, cells, off, M):
 
 
 class TorchDistComm:
-    """Exchange through ``torch.distributed`` (NCCL over NVLink on the box)."""
+    """Exchange through ``torch.distributed`` (NCCL over NVLink on the box,
+    gloo with host staging elsewhere)."""
 
     def __init__(self, group=None):
         self.group = group
@@ -153,19 +189,30 @@ class TorchDistComm:
     def allgather_rows(self, full, chunks, rank, world):
         allgather_rows(full, chunks, rank, world, self.group)
 
+    def gather_rows(self, full, chunks, rank, world, root=0):
+        gather_rows(full, chunks, rank, world, root, self.group)
 
-def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None):
+
+RESULTS = ("all", "root", "local")
+
+
+def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None, results: str = "all"):
     """Evaluate ``tree`` with targets Morton-partitioned over ``world`` ranks.
 
-    Every rank returns the same full results in ``tree`` (after the final
-    all-gather) and an ``EvalReport`` whose counters cover its own rows.
-    ``comm`` defaults to :class:`TorchDistComm`; tests pass an in-process
-    exchange to emulate ranks on one device."""
+    ``results`` picks where the (phi, f) rows end up: "all" (one all-gather:
+    every rank holds the full result), "root" (one gather to rank 0; the
+    other ranks keep their own rows) or "local" (no exchange: each rank's
+    tree is valid on its own bodies ``tree.owned_range`` only).  The
+    ``EvalReport`` counters cover the rank's own rows.  ``comm`` defaults to
+    :class:`TorchDistComm`; tests pass an in-process exchange to emulate
+    ranks on one device."""
+    if results not in RESULTS:
+        raise ValueError(f"results must be one of {RESULTS}, got {results!r}")
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import (EvalReport, interaction_lists, listfmm_lists, mutual_lists, near_field_precision,
-                            run_m2l, run_m2p, run_p2p, treecode_lists)
+    from .traversal import (EvalReport, critical_path, interaction_lists, listfmm_lists, mutual_lists,
+                            near_field_precision, run_m2l, run_m2p, run_p2p, treecode_lists)
     from .tree import downward_pass
 
     if world == 1:
@@ -235,10 +282,17 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     P = _lib.ptr
     _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
               P(tree.d_fz), _lib.stream_handle())
-    res = torch.stack([tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz], 1)
-    comm.allgather_rows(res, plan.cuts, rank, world)
-    for k, a in enumerate((tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz)):
-        a.copy_(res[:, k])
+    tree.owned_range = (lo, hi)
+    if results != "local":
+        res = torch.stack([tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz], 1)
+        if results == "all":
+            comm.allgather_rows(res, plan.cuts, rank, world)
+        else:
+            comm.gather_rows(res, plan.cuts, rank, world, 0)
+        if results == "all" or rank == 0:
+            tree.owned_range = (0, tree.n)
+            for k, a in enumerate((tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz)):
+                a.copy_(res[:, k])
     ev[8].record(main)
     ev[8].synchronize()
     pairs, skipped = lists.dev_stats.tolist()
@@ -251,8 +305,13 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     stats.add_time("allgather", ev[7].elapsed_time(ev[8]) * 1e-3)
     tree._results_changed()
     del _lib
+    ms = lambda a, b: ev[a].elapsed_time(ev[b]) * 1e-3  # noqa: E731
+    up, trav, down = critical_path(ms(0, 7), ms(0, 1), ms(0, 4), ms(0, 8))
+    if treecode:
+        trav, down = trav + down, 0.0
+    spans = {"lists": ms(0, 2), "upward_allgather": ms(0, 1), "m2p" if treecode else "m2l": ms(3, 4),
+             "downward": ms(4, 5), "p2p": ms(6, 7), "result_allgather": ms(7, 8), "wall": ms(0, 8)}
     return EvalReport(strategy=cfg.strategy, n=tree.n, n_sources=tree.n, p=cfg.p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=cfg.mutual, threads=world, task_grain=cfg.task_grain, stats=stats,
-                      build_time=tree.build_time, upward_time=ev[0].elapsed_time(ev[1]) * 1e-3,
-                      traversal_time=ev[0].elapsed_time(ev[7]) * 1e-3,
-                      downward_time=0.0 if treecode else ev[4].elapsed_time(ev[5]) * 1e-3)
+                      build_time=tree.build_time, upward_time=up, traversal_time=trav, downward_time=down,
+                      spans=spans, near_field=nf)

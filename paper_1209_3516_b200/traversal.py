@@ -105,6 +105,10 @@ class EvalReport:
     downward_time: float
     achieved_error: float | None = None
     trace: list | None = None
+    # raw per-stream spans (seconds) of the overlapped evaluation; the phase
+    # times above are their critical-path split (``critical_path``)
+    spans: dict = field(default_factory=dict)
+    near_field: str = "fp64"
 
     @property
     def total_time(self) -> float:
@@ -125,10 +129,39 @@ class EvalReport:
                          "total": int(round(self.total_time * 1e3))},
             "kernel_times_ms": {k: int(round(v * 1e3)) for k, v in sorted(self.stats.times.items())},
             "achieved_error": self.achieved_error,
+            # additive keys (not in the reference's schema)
+            "stream_spans_ms": {k: round(v * 1e3, 3) for k, v in sorted(self.spans.items())},
+            "near_field_precision": self.near_field,
         }
 
     def to_json(self, indent: int = 2) -> str:
         return json.dumps(self.to_dict(), indent=indent)
+
+
+def critical_path(t_near: float, t_up: float, t_far: float, wall: float) -> tuple[float, float, float]:
+    """Split one overlapped evaluation's wall time into the reference's
+    sequential phases (src/traversal.py:104-106, :875-931), so that
+    upward + traversal + downward == wall (times from the evaluation start):
+
+    * traversal: until the near field (lists + P2P) ends, plus any far-field
+      interaction (M2L / M2P) still running after it and after the upward
+      pass -- the reference's traversal phase runs M2L and P2P;
+    * upward: the part of the upward pass that outlasts the near field;
+    * downward: the remainder (L2L/L2P tail and the final combine).
+
+    ``t_near``/``t_up``/``t_far`` are the end times of the near field, the
+    upward pass and the far-field interactions."""
+    up = max(0.0, t_up - t_near)
+    trav = t_near + max(0.0, t_far - max(t_near, t_up))
+    return up, trav, max(0.0, wall - up - trav)
+
+
+def _setup_gap(tree: Tree, e0) -> float:
+    """Seconds between the end of ``tree``'s build and this evaluation's
+    first event, once per build: host set-up the reference bills to its
+    upward phase (src/traversal.py:875-879)."""
+    ev = tree.__dict__.pop("_ev_built", None)
+    return ev.elapsed_time(e0) * 1e-3 if ev is not None else 0.0
 
 
 # ---------------------------------------------------------------------------
@@ -175,6 +208,7 @@ class Lists:
         peak = max(fronts)
         self.__dict__.update(n_p2p=n_p2p, n_m2l=n_m2l, peak_frontier=peak, _deferred=None)
         ok = n_p2p <= caps[0] and n_m2l <= caps[1] and peak <= caps[2] and fronts[-1] == 0
+        ok = ok and int(self.__dict__["dev_runs_needed"][0]) == 0  # (runs are sized like pairs)
         if ok:
             _hint[key] = (max(caps[0], int(n_p2p * 1.02) + 4096), max(caps[1], int(n_m2l * 1.02) + 4096),
                           max(caps[2], int(peak * 1.05) + 4096))
@@ -406,7 +440,7 @@ def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
     dev, P, i32, ncells = tree.device, _lib.ptr, torch.int32, tree.ncells
     leaf_rows = torch.empty(ncells, dtype=i32, device=dev)
     run_off = torch.empty(2 * ncells, dtype=torch.int64, device=dev)  # (first, end) run per row
-    dev_stats = torch.empty(2, dtype=torch.int64, device=dev)
+    stats3 = torch.empty(3, dtype=torch.int64, device=dev)  # pairs, skipped, runs capacity needed (0: fit)
     dev_nrows = torch.empty(1, dtype=i32, device=dev)
     cap_runs = max(n_p2p, 1)
     runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)  # row-local: runs <= pairs per row
@@ -415,9 +449,9 @@ def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
     _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
               P(p2p_grp), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), sleaf,
               src.ncells if cross else 0, sstart, send, tree.n if cross else 0, P(leaf_rows), P(run_off), P(runs), cap_runs,
-              None, None, P(dev_nrows), P(dev_stats), wsp, wsb, st)
+              None, None, P(dev_nrows), P(stats3), wsp, wsb, st)
     return dict(p2p_grp=p2p_grp, leaf_rows=leaf_rows, nrows=tree.nleaves, dev_nrows=dev_nrows, run_off=run_off,
-                runs=runs, dev_stats=dev_stats)
+                runs=runs, dev_stats=stats3[:2], dev_runs_needed=stats3[2:])
 
 
 def run_m2l(tree: Tree, lists: Lists, p: int, src: Tree | None = None) -> None:
@@ -631,12 +665,15 @@ last_events = None
 
 def _side_stream(dev, which: int = 0) -> torch.cuda.Stream:
     """Persistent auxiliary streams per device: 0 = far field, 1 = P2P,
-    2 = list construction (highest priority: its short kernels take SM slots
-    as far-field blocks retire instead of queueing behind them), 3 = the
-    upward pass."""
+    2 = list construction, 3 = the upward pass.  All but P2P run at high
+    priority: their short kernels take SM slots as P2P blocks retire instead
+    of queueing behind the whole P2P grid, so the far field finishes early
+    (its spans are then its kernel times) and the step is unchanged (P2P
+    absorbs the same SM time either way)."""
     key = (torch.device(dev).index or 0, which)
     if key not in _side:
-        prio = torch.cuda.Stream.priority_range()[1] if which == 2 else 0
+        hi = os.environ.get("FMM_B200_FAR_PRIORITY", "1") == "1" or which == 2
+        prio = torch.cuda.Stream.priority_range()[1] if which != 1 and hi else 0
         _side[key] = torch.cuda.Stream(device=dev, priority=prio)
     return _side[key]
 
@@ -839,14 +876,19 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
-    # phases overlap (far field on the side stream, near field on the P2P
-    # stream): upward and downward are their own stream's spans, traversal
-    # is the span from the start to the last P2P chunk
+    # phases overlap (far field on the side streams, near field on the P2P
+    # stream): the report splits the wall time along the critical path; the
+    # raw stream spans stay in ``spans``
+    ms = lambda a, b: a.elapsed_time(b) * 1e-3  # noqa: E731
+    wall = ms(e0, e_end)
+    up, trav, down = critical_path(ms(e0, e_pend), ms(e0, e_up1), max(ms(e0, b) for _, b in m2l_ev), wall)
+    up += _setup_gap(tree, e0)
+    spans = {"lists": ms(e0, e_l1), "upward": ms(e_up0, e_up1), "m2l": sum(ms(a, b) for a, b in m2l_ev),
+             "p2p": sum(ms(a, b) for a, b in p2p_ev), "downward": ms(e_down0, e_down1), "wall": wall}
     return EvalReport(strategy="dualtree", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain, stats=stats,
-                      build_time=_build_time(tree, src), upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
-                      traversal_time=e0.elapsed_time(e_pend) * 1e-3,
-                      downward_time=e_down0.elapsed_time(e_down1) * 1e-3, trace=events)
+                      build_time=_build_time(tree, src), upward_time=up, traversal_time=trav, downward_time=down,
+                      trace=events, spans=spans, near_field=nf)
 
 
 def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
@@ -931,10 +973,17 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         events += [("m2p", int(a), int(b)) for a, b in zip(mt, ms)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
+    ms = lambda a, b: a.elapsed_time(b) * 1e-3  # noqa: E731
+    wall = ms(e0, e_end)
+    up, trav, down = critical_path(ms(e0, e_p1), ms(e0, e_up1), ms(e0, e_m1), wall)
+    up += _setup_gap(tree, e0)
+    trav, down = trav + down, 0.0  # the treecode has no downward phase (src/traversal.py:1002-1046)
+    spans = {"lists": ms(e0, e_l1), "upward": ms(e_up0, e_up1), "m2p": ms(e_m0, e_m1), "p2p": ms(e_p0, e_p1),
+             "wall": wall}
     return EvalReport(strategy="treecode", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain,
-                      stats=stats, build_time=_build_time(tree, src), upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
-                      traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=0.0, trace=events)
+                      stats=stats, build_time=_build_time(tree, src), upward_time=up, traversal_time=trav,
+                      downward_time=down, trace=events, spans=spans, near_field=nf)
 
 
 def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
@@ -1014,11 +1063,16 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
+    ms = lambda a, b: a.elapsed_time(b) * 1e-3  # noqa: E731
+    wall = ms(e0, e_end)
+    up, trav, down = critical_path(ms(e0, e_p1), ms(e0, e_up1), ms(e0, e_m1), wall)
+    up += _setup_gap(tree, e0)
+    spans = {"lists": ms(e0, e_l1), "upward": ms(e_up0, e_up1), "m2l": ms(e_m0, e_m1), "p2p": ms(e_p0, e_p1),
+             "downward": ms(e_m1, e_d1), "wall": wall}
     return EvalReport(strategy="listfmm", n=tree.n, n_sources=tree.n, p=p, mac_kind=cfg.mac.kind,
                       theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain,
-                      stats=stats, build_time=tree.build_time, upward_time=e_up0.elapsed_time(e_up1) * 1e-3,
-                      traversal_time=e0.elapsed_time(e_p1) * 1e-3, downward_time=e_m1.elapsed_time(e_d1) * 1e-3,
-                      trace=events)
+                      stats=stats, build_time=tree.build_time, upward_time=up, traversal_time=trav,
+                      downward_time=down, trace=events, spans=spans, near_field=nf)
 
 
 def _same_device(tree: Tree, src: Tree) -> None:

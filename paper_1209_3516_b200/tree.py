@@ -383,6 +383,9 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
     tree._fp32_exact = int(inexact_host.value) == 0
     tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
     tree.build_time = time.perf_counter() - t0
+    with torch.cuda.device(dev):  # the evaluation bills the host gap after the build to its first phase
+        tree._ev_built = torch.cuda.Event(enable_timing=True)
+        tree._ev_built.record()
     return tree
 
 

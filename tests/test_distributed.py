@@ -94,8 +94,11 @@ def _worker(rank, world, port, out):
         full = torch.full((ncells, nc), -1.0, dtype=torch.float64)
         lo, hi = int(chunks[rank]), int(chunks[rank + 1])
         full[lo:hi] = torch.arange(lo * nc, hi * nc, dtype=torch.float64).reshape(-1, nc)
+        mine = full.clone()
         fd.allgather_rows(full, chunks, rank, world)
         out[rank] = full.numpy().tolist()
+        fd.gather_rows(mine, chunks, rank, world, root=0)
+        out[(rank, "gather")] = mine.numpy().tolist()
     finally:
         dist.destroy_process_group()
 
@@ -109,3 +112,6 @@ def test_allgather_rows_gloo(world):
     want = np.arange(37 * 5, dtype=np.float64).reshape(37, 5)
     for r in range(world):
         assert np.array_equal(np.array(out[r]), want)
+    assert np.array_equal(np.array(out[(0, "gather")]), want)  # only the root receives
+    for r in range(1, world):
+        assert (np.array(out[(r, "gather")]) == -1.0).sum() > 0

@@ -132,3 +132,46 @@ def test_plan_with_wide_rows_matches_oracle_p2p():
     assert np.linalg.norm(got - phi) <= 1e-12 * np.linalg.norm(phi)
     pairs, skipped = lists.dev_stats.tolist()
     assert (pairs, skipped) == (int(st[0]), int(st[1]))
+
+
+def test_plan_short_runs_buffer_reports_capacity():
+    """fmm_p2p_plan honours cap_runs: a short runs buffer leaves the
+    overflowing rows empty, flags the required capacity in dev_stats[2] and
+    (when the host asks for the run count) returns FMM_ERR_CAPACITY with the
+    exact size -- the reference's grow-and-retry contract."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1209_3516_b200 import _lib
+    c = Case("c1")
+    t = _tree(c)
+    lists = fb.interaction_lists(t, fb.MacConfig("fmm", c.theta), defer=False)
+    P, dev = _lib.ptr, t.device
+    wsp, wsb = _lib.workspace(max(lists.n_p2p, t.n, t.ncells + 1), dev)
+
+    def plan(cap):
+        leaf_rows = torch.empty(t.ncells, dtype=torch.int32, device=dev)
+        run_off = torch.empty(2 * t.ncells, dtype=torch.int64, device=dev)
+        runs = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=dev)
+        stats = torch.empty(3, dtype=torch.int64, device=dev)
+        nruns, nrows = C.c_int64(0), C.c_int32(0)
+        _lib.call("fmm_p2p_plan", t.ncells, P(t.d_leaf), P(t.d_start), P(t.d_end), 0, t.n, P(lists.p2p_rows),
+                  P(lists.p2p_grp), P(t.d_x), P(t.d_y), P(t.d_z), P(t.d_keys), None, 0, None, None, 0, P(leaf_rows),
+                  P(run_off), P(runs), cap, C.byref(nruns), C.byref(nrows), None, P(stats), wsp, wsb,
+                  _lib.stream_handle())
+        return nruns.value, stats.tolist()
+
+    n_ok, st_ok = plan(lists.n_p2p)
+    assert st_ok[2] == 0 and st_ok[0] == c.meta["stats"]["p2p_pairs"] and 0 < n_ok <= lists.n_p2p
+    short = lists.n_p2p // 3
+    with pytest.raises(_lib.CapacityError):
+        plan(short)
+    # the exact requirement is the CSR end of the last row that did not fit
+    rows = lists.p2p_rows.cpu().numpy()
+    need = int(rows[1:][rows[1:] > short].max())
+    nruns = C.c_int64(0)
+    try:
+        plan(short)
+    except _lib.CapacityError as e:
+        assert "needed" in str(e) and str(need) in str(e)

@@ -33,6 +33,17 @@ class ThreadComm:
         torch.cuda.current_stream().synchronize()
         self.barrier.wait()
 
+    def gather_rows(self, full, chunks, rank, world, root=0):
+        torch.cuda.current_stream().synchronize()
+        self.bufs[rank] = full[int(chunks[rank]):int(chunks[rank + 1])].clone()
+        torch.cuda.current_stream().synchronize()
+        self.barrier.wait()
+        if rank == root:
+            for r in range(world):
+                full[int(chunks[r]):int(chunks[r + 1])].copy_(self.bufs[r])
+            torch.cuda.current_stream().synchronize()
+        self.barrier.wait()
+
 
 def _ps(c):
     pos = np.asarray(c.pos, np.float64)
