@@ -175,13 +175,18 @@ FMM_API int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfro
  * cap_front each).  dev_log (nsteps + 3 entries) receives {n_p2p, n_m2l,
  * frontier size entering step 0, 1, ..., nsteps}; the caller reads it once:
  * a non-zero last entry means nsteps was too small, and any count above its
- * capacity means buffers must grow (the lists are then incomplete; rerun). */
+ * capacity means buffers must grow (the lists are then incomplete; rerun).
+ * tmask (optional, one byte per target cell) keeps only pairs whose target
+ * cell is flagged: a sampled evaluation flags the cells holding the sample
+ * bodies (leaves and their ancestors), and every kept target's row is the
+ * same as in the full lists. */
 FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
                  int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
                  const double *ctr, const double *bmax, const double *rmax, const int32_t *children_b,
                  const uint8_t *leaf_b, const double *ctr_b, const double *bmax_b, const double *rmax_b,
                  const int32_t *start,
-                 const int32_t *end, int32_t body_lo, int32_t body_hi, int m2l_owner_only, int kind,
+                 const int32_t *end, int32_t body_lo, int32_t body_hi, const uint8_t *tmask, int m2l_owner_only,
+                 int kind,
                  double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s,
                  int64_t cap_m2l, unsigned long long *dev_log, void *stream);
 
@@ -295,9 +300,10 @@ FMM_API int fmm_pairs_to_csr(const int32_t *t, const int32_t *s, int64_t npairs,
  * Cross-tree plans (src_start given, with src_leaf, src_end, src_ncells):
  * the sources are the source tree's leaves, their body runs shifted by
  * src_offset (where the source bodies sit in the P2P body arrays); no self
- * leaf, no coincident scan (see fmm_p2p_coincident). */
+ * leaf, no coincident scan (see fmm_p2p_coincident).  tmask (optional)
+ * plans only the flagged target leaves (as fmm_traverse). */
 FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
-                 int32_t body_lo, int32_t body_hi, const int64_t *rows, const int32_t *src,
+                 int32_t body_lo, int32_t body_hi, const uint8_t *tmask, const int64_t *rows, const int32_t *src,
                  const double *xs, const double *ys, const double *zs,
                  const uint64_t *keys, const uint8_t *src_leaf, int32_t src_ncells, const int32_t *src_start,
                  const int32_t *src_end, int32_t src_offset, int32_t *leaf_rows, int64_t *run_rng, void *runs,

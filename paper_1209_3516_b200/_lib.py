@@ -45,8 +45,8 @@ SIGNATURES = {
     "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],
     "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64,
                           P, P, I64, P, P, I64, P, P],
-    "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64, P,
-                     P, I64, P, P],
+    "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, INT, INT, DBL, P, P, I64,
+                     P, P, I64, P, P],
     "fmm_pairs_to_rows": [P, P, P, I64, I32, I32, INT, P, P, P, SZ, P],
     "fmm_partition_owner": [I32, P, P, P, P, I64, P, P],
     "fmm_traverse_mutual": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64,
@@ -55,8 +55,8 @@ SIGNATURES = {
                               I64, P, P, I64, P, P, SZ, P],
     "fmm_listfmm_lists": [I32, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, I64, P, P, I64, P, P, SZ, P],
     "fmm_pairs_to_csr": [P, P, I64, I32, P, P, P, SZ, P],
-    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, I32, P, P, I32, P, P, P, I64, P, P, P, P, P, SZ,
-                     P],
+    "fmm_p2p_plan": [I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, I32, P, P, I32, P, P, P, I64, P, P, P, P, P,
+                     SZ, P],
     "fmm_sort_rows": [I32, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P, P],
     "fmm_m2p_csr": [INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],

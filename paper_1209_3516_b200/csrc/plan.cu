@@ -310,9 +310,9 @@ static int leaf_ordinals(int32_t ncells, const uint8_t *leaf, const int32_t *sta
 }
 
 __global__ void leaf_in_range(int32_t ncells, const uint8_t *leaf, const int32_t *start, int32_t lo, int32_t hi,
-                              uint8_t *flag) {
+                              const uint8_t *tmask, uint8_t *flag) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x)
-        flag[c] = leaf[c] && start[c] >= lo && start[c] < hi;
+        flag[c] = leaf[c] && start[c] >= lo && start[c] < hi && (!tmask || tmask[c]);
 }
 
 }  // namespace fmm
@@ -321,7 +321,8 @@ using namespace fmm;
 
 
 extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *start, const int32_t *end,
-                            int32_t body_lo, int32_t body_hi, const int64_t *rows, const int32_t *src,
+                            int32_t body_lo, int32_t body_hi, const uint8_t *tmask, const int64_t *rows,
+                            const int32_t *src,
                             const double *xs, const double *ys, const double *zs,
                             const uint64_t *keys, const uint8_t *src_leaf, int32_t src_ncells,
                             const int32_t *src_start, const int32_t *src_end, int32_t src_offset, int32_t *leaf_rows,
@@ -355,7 +356,7 @@ extern "C" int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *
     int32_t *nsel = dev_nrows ? dev_nrows : nsel_ws;
     unsigned long long *stats = dev_stats ? dev_stats : st3;
     unsigned long long *runs_need = dev_stats ? dev_stats + 2 : st3 + 3;  // 0, or the runs capacity required
-    leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, flag); fmm::note_launch();
+    leaf_in_range<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, leaf, start, body_lo, body_hi, tmask, flag); fmm::note_launch();
     size_t need = 0;
     cub::CountingInputIterator<int32_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, need, it, flag, leaf_rows, nsel, ncells, s);

@@ -76,8 +76,8 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
                                      int64_t nfront_host, const unsigned long long *__restrict__ nfront_dev,
                                      int64_t cap_front, int classify_self, Cells A, Cells B,
                                      const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend,
-                                     int32_t blo, int32_t bhi, int m2l_owner, int kind_mac, double th2,
-                                     int32_t *p2p_t,
+                                     int32_t blo, int32_t bhi, const uint8_t *__restrict__ tmask, int m2l_owner,
+                                     int kind_mac, double th2, int32_t *p2p_t,
                                      int32_t *p2p_s, int64_t cap_p2p,
                                      int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l, int32_t *na,
                                      int32_t *nb, int64_t cap_next, unsigned long long *cnt_p2p,
@@ -159,6 +159,8 @@ __global__ void traverse_step_kernel(const int32_t *__restrict__ fa, const int32
             if (ok[q]) {
                 // multi-GPU: only targets whose body range meets [blo, bhi)
                 if (ranged && (cend[ca[q]] <= blo || cstart[ca[q]] >= bhi)) continue;
+                // target subset (sampled evaluations): only flagged target cells
+                if (tmask && !tmask[ca[q]]) continue;
                 fate[q] = fate_of(ca[q], cb[q]);
                 // chunked single-GPU runs: an M2L pair belongs to the chunk
                 // holding its target's first body (no pair is emitted twice)
@@ -857,7 +859,7 @@ int fmm_traverse_step(const int32_t *fa, const int32_t *fb, int64_t nfront, int 
     const Cells B = source_cells(A, children_b, leaf_b, ctr_b, bmax_b, rmax_b);
     traverse_step_kernel<<<grid_for(nfront, 256, 148 * 16), 256, 0, as_stream(stream)>>>(
         fa, fb, nfront, nullptr, nfront, classify_self, A, B, start, end, body_lo,
-        body_hi, m2l_owner_only, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
+        body_hi, nullptr, m2l_owner_only, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
         na, nb, cap_next, dev_counts, dev_counts + 1, dev_counts + 2); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_traverse_step");
     return FMM_OK;
@@ -867,8 +869,8 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
                  int nsteps, const int32_t *children, const uint8_t *leaf, const double *ctr,
                  const double *bmax, const double *rmax, const int32_t *children_b, const uint8_t *leaf_b,
                  const double *ctr_b, const double *bmax_b, const double *rmax_b, const int32_t *start, const int32_t *end,
-                 int32_t body_lo, int32_t body_hi, int m2l_owner_only, int kind, double th2, int32_t *p2p_t,
-                 int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
+                 int32_t body_lo, int32_t body_hi, const uint8_t *tmask, int m2l_owner_only, int kind, double th2,
+                 int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l,
                  unsigned long long *dev_log, void *stream) {
     cudaStream_t st = as_stream(stream);
     const Cells A = cells_of(children, leaf, ctr, bmax, rmax);
@@ -880,7 +882,7 @@ int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_
         const bool even = (sidx & 1) == 0;
         traverse_step_kernel<<<grid, 256, 0, st>>>(
             even ? front_a0 : front_a1, even ? front_b0 : front_b1, 0, dev_log + 2 + sidx, cap_front, sidx == 0,
-            A, B, start, end, body_lo, body_hi, m2l_owner_only, kind, th2, p2p_t,
+            A, B, start, end, body_lo, body_hi, tmask, m2l_owner_only, kind, th2, p2p_t,
             p2p_s, cap_p2p,
             m2l_t, m2l_s, cap_m2l, even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front,
             dev_log, dev_log + 1, dev_log + 3 + sidx); fmm::note_launch();

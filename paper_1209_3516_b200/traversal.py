@@ -230,7 +230,8 @@ _hint = {}
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
                       m2l_ready: torch.cuda.Event | None = None,
                       side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False,
-                      src: Tree | None = None, defer: bool = True) -> Lists:
+                      src: Tree | None = None, defer: bool = True,
+                      target_mask: torch.Tensor | None = None) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
@@ -239,7 +240,9 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     ``src`` is a separate source tree (cross-tree lists: sources index its
     cells, the P2P plan points at its bodies appended after the targets).
     With ``defer`` and a capacity hint for this shape the host does not wait
-    for the traversal's counters (``Lists.settle``)."""
+    for the traversal's counters (``Lists.settle``).  ``target_mask`` (uint8
+    per target cell) keeps only the flagged targets' rows (sampled
+    evaluations: ``tuner.ErrorProbe``)."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev = tree.device
     P = _lib.ptr
@@ -248,7 +251,8 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     th2 = mac.theta * mac.theta
     cross = src is not None and src is not tree
     sb = src if cross else tree
-    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, m2l_owner_only, sb.ncells if cross else 0)
+    tm = _lib.ptr(target_mask)
+    key = (tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, m2l_owner_only, sb.ncells if cross else 0, tm)
     # every step opens one side of a pair: at most depth_A + depth_B + 1 steps
     nsteps = tree.depth + sb.depth + 2
     bcells = _source_cells(tree, src)
@@ -262,7 +266,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         p2p_t, p2p_s, m2l_t, m2l_s, *fr = torch.split(pool, [cap_p2p, cap_p2p, cap_m2l, cap_m2l] + [cap_next] * 4)
         _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
                   P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), *bcells, P(tree.d_start),
-                  P(tree.d_end), blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p,
+                  P(tree.d_end), blo, bhi, tm, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p,
                   P(m2l_t), P(m2l_s), cap_m2l, P(log), st)
         del fr
         ncells = tree.ncells
@@ -275,7 +279,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         del p2p_t, p2p_s, m2l_t, m2l_s
         return Lists(m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_rows=p2p_rows,
                      _deferred=(log, (cap_p2p, cap_m2l, cap_next), key),
-                     **_p2p_plan(tree, p2p_grp, p2p_rows, cap_p2p, blo, bhi, wsp, wsb, st, src=src))
+                     **_p2p_plan(tree, p2p_grp, p2p_rows, cap_p2p, blo, bhi, wsp, wsb, st, src=src, tmask=target_mask))
     cap_p2p, cap_m2l, cap_next = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
                                                  max(4096, tree.ncells * 8)))
     while True:
@@ -286,8 +290,8 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         fr = [torch.empty(cap_next, dtype=i32, device=dev) for _ in range(4)]
         _lib.call("fmm_traverse", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps, P(tree.d_children),
                   P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), *bcells, P(tree.d_start),
-                  P(tree.d_end), blo, bhi, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t), P(m2l_s),
-                  cap_m2l, P(log), st)
+                  P(tree.d_end), blo, bhi, tm, int(m2l_owner_only), mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t),
+                  P(m2l_s), cap_m2l, P(log), st)
         hl = log.tolist()  # the one synchronisation of the traversal
         done_p2p, done_m2l, fronts = hl[0], hl[1], hl[2:]
         peak = max(fronts)
@@ -308,7 +312,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     del p2p_t, p2p_s, m2l_t, m2l_s
     return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
                  p2p_rows=p2p_rows, peak_frontier=peak,
-                 **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src))
+                 **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st, src=src, tmask=target_mask))
 
 
 def _source_cells(tree: Tree, src: Tree | None) -> tuple:
@@ -432,7 +436,7 @@ def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0
 
 
 def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st,
-              src: Tree | None = None) -> dict:
+              src: Tree | None = None, tmask: torch.Tensor | None = None) -> dict:
     """P2P run plan + the reference's pair counters (no host round trip:
     runs <= pairs, and the row count stays on the device).  With a separate
     source tree the runs address its bodies at offset ``tree.n`` of the
@@ -446,7 +450,7 @@ def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
     runs = torch.empty((cap_runs, 4), dtype=i32, device=dev)  # row-local: runs <= pairs per row
     cross = src is not None and src is not tree
     sleaf, sstart, send = (P(src.d_leaf), P(src.d_start), P(src.d_end)) if cross else (None, None, None)
-    _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(p2p_rows),
+    _lib.call("fmm_p2p_plan", ncells, P(tree.d_leaf), P(tree.d_start), P(tree.d_end), blo, bhi, P(tmask), P(p2p_rows),
               P(p2p_grp), P(tree.d_x), P(tree.d_y), P(tree.d_z), P(tree.d_keys), sleaf,
               src.ncells if cross else 0, sstart, send, tree.n if cross else 0, P(leaf_rows), P(run_off), P(runs), cap_runs,
               None, None, P(dev_nrows), P(stats3), wsp, wsb, st)
@@ -719,7 +723,7 @@ class ChunkedLists:
 
 
 def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
-                       trace: bool = False) -> EvalReport:
+                       trace: bool = False, target_mask: torch.Tensor | None = None) -> EvalReport:
     """Simultaneous traversal of the tree against itself, on the GPU.
 
     Three streams.  The targets may be cut into Morton chunks on leaf
@@ -737,11 +741,18 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     pass runs on the source tree, the traversal pairs target cells with
     source cells, and P2P sweeps the source bodies (``CrossBodies``);
     coincident target/source bodies are skipped and counted as the
-    reference does."""
+    reference does.
+
+    ``target_mask`` (uint8 per cell, additive) evaluates only the flagged
+    target cells: results are exact on the bodies of flagged leaves whose
+    ancestors are all flagged (``tuner.ErrorProbe.mask``), the counters
+    cover the kept rows."""
     src = tree if source_tree is None else source_tree
     cross = src is not tree
     if cfg.mutual and cross:
         raise ValueError("mutual traversal needs target and source to share one tree")
+    if target_mask is not None and cfg.mutual:
+        raise ValueError("a target mask needs the directed traversal (mutual=False)")
     if threads < 1:
         raise ValueError(f"threads must be >= 1, got {threads}")
     _same_device(tree, src)
@@ -804,7 +815,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                     lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side)
                 else:
                     lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
-                                              m2l_owner_only=nch > 1, src=src)
+                                              m2l_owner_only=nch > 1, src=src, target_mask=target_mask)
             parts.append(lists)
             if k == 0:
                 launch_upward()
@@ -847,7 +858,8 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         e_end.synchronize()
         if not all([x.settle() for x in parts]):
             # a hinted list outgrew its buffer: redo with exact counts
-            return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace)
+            return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace,
+                                      target_mask=target_mask)
         pairs = skipped = 0
         for lists in parts:
             a, b = lists.dev_stats.tolist()

@@ -10,7 +10,7 @@ from paper_1209_3516_b200 import cli
 
 
 def _opts(argv):
-    return cli.Options(cli._parser().parse_args(argv))
+    return cli.settings(cli.parser().parse_args(argv))
 
 
 def test_precedence_flag_over_file_over_default(tmp_path):
@@ -41,8 +41,19 @@ def test_usage_errors_exit_2(capsys):
 
 
 def test_list_parsing():
-    assert cli._split("1e3, 2000,", int, "n") == [1000, 2000]
+    assert cli.split_list("1e3, 2000,", int, "n") == [1000, 2000]
     with pytest.raises(cli.CliError):
-        cli._split("a,b", float, "target")
+        cli.split_list("a,b", float, "target")
     with pytest.raises(cli.CliError):
-        cli._split(" , ", int, "n")
+        cli.split_list(" , ", int, "n")
+
+
+def test_option_table_drives_parser_and_config():
+    """Every option of the table is a flag of exactly the commands that
+    take it, and a config-file key of the same name."""
+    ap = cli.parser()
+    sub = next(a for a in ap._actions if isinstance(a, argparse._SubParsersAction))
+    for cmd, sp in sub.choices.items():
+        flags = {a.dest for a in sp._actions if a.option_strings} - {"help", "config"}
+        assert flags == {o.key for o in cli.OPTIONS if cmd in o.commands}, cmd
+    assert set(cli.BY_KEY) == {o.key for o in cli.OPTIONS}

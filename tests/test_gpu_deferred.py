@@ -156,7 +156,7 @@ def test_plan_short_runs_buffer_reports_capacity():
         runs = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=dev)
         stats = torch.empty(3, dtype=torch.int64, device=dev)
         nruns, nrows = C.c_int64(0), C.c_int32(0)
-        _lib.call("fmm_p2p_plan", t.ncells, P(t.d_leaf), P(t.d_start), P(t.d_end), 0, t.n, P(lists.p2p_rows),
+        _lib.call("fmm_p2p_plan", t.ncells, P(t.d_leaf), P(t.d_start), P(t.d_end), 0, t.n, None, P(lists.p2p_rows),
                   P(lists.p2p_grp), P(t.d_x), P(t.d_y), P(t.d_z), P(t.d_keys), None, 0, None, None, 0, P(leaf_rows),
                   P(run_off), P(runs), cap, C.byref(nruns), C.byref(nrows), None, P(stats), wsp, wsb,
                   _lib.stream_handle())

@@ -57,3 +57,33 @@ def test_select_p_theta_consistent(tree):
     assert res.best.traversal_time == min(e.traversal_time for e in res.entries)
     with pytest.raises(ValueError, match="unreachable"):
         fb.select_p_theta(tree, 1e-20, p_candidates=(2,), reps=1)
+
+
+@pytest.mark.parametrize("name,precision", [("c2_32k", "fp64"), ("plummer_32k", "fp32"), ("c1", "fp64")])
+def test_sampled_evaluation_is_exact_at_the_sample(name, precision):
+    """A sampled evaluation (target mask = the cells holding the sample
+    bodies) gives the full evaluation's values at the sample bodies,
+    bit for bit, with a small fraction of the P2P work."""
+    from goldens import Case
+    from paper_1209_3516_b200.tuner import ErrorProbe
+    c = Case(name)
+    pos = np.asarray(c.pos, np.float64)
+    t = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], c.q), ncrit=c.ncrit)
+    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", c.theta), p=c.p, precision=precision)
+    full = fb.evaluate_on_tree(t, cfg)
+    probe = ErrorProbe(t, 200, 3)
+    b = t.bodies
+    want = np.stack([b.phi[probe.idx], b.fx[probe.idx], b.fy[probe.idx], b.fz[probe.idx]])
+    ferr = probe.force_error()
+    t._results_changed()
+    for a in (t.d_phi, t.d_fx, t.d_fy, t.d_fz):
+        a.fill_(float("nan"))
+    part = probe.evaluate(cfg)
+    t._results_changed()
+    b = t.bodies
+    got = np.stack([b.phi[probe.idx], b.fx[probe.idx], b.fy[probe.idx], b.fz[probe.idx]])
+    assert np.array_equal(got, want)
+    assert probe.force_error() == ferr
+    assert 0 < part.stats.p2p_pairs < full.stats.p2p_pairs
+    if t.nleaves > 1000:
+        assert part.stats.p2p_pairs < 0.5 * full.stats.p2p_pairs
