@@ -473,7 +473,15 @@ __device__ __forceinline__ int gcd_small(int a, int b) {
 // Partial sums of the parts are folded through shared memory in a fixed
 // order (deterministic).  Leaves too large for the fold buffer (oversized
 // leaves) fall back to P = 1 with direct stores.
-constexpr int kMaxUnits = 64;
+// FMM_P2P_BLK = 8 (default): blocks of 8 targets per lane, the last block
+// of a leaf 4 or 8; = 4: every block 4 targets (fewer registers, more
+// resident warps: an occupancy experiment)
+#ifndef FMM_P2P_BLK
+#define FMM_P2P_BLK 8
+#endif
+constexpr int kBlk = FMM_P2P_BLK;
+constexpr bool kK4Only = kBlk == 4;
+constexpr int kMaxUnits = kK4Only ? 128 : 64;
 
 template <bool SAFE, bool ANCHOR>
 constexpr int p2p_f32_pool_bytes() {
@@ -493,7 +501,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
     // the tile ring (streamed rows) and the lane rings (run-by-run rows) share
     // one pool: a row uses one or the other
     extern __shared__ __align__(128) float4 pool[];  // p2p_f32_pool_bytes<SAFE, ANCHOR>()
-    __shared__ float red[kMaxUnits][4][8];
+    __shared__ float red[kMaxUnits][4][kBlk];
     __shared__ int2 srun[kMaxRuns];
     __shared__ int32_t stotal;
     __shared__ uint64_t wbars[kP2PWarps][kWStages];
@@ -510,9 +518,9 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
         const int32_t t = leaf_rows[row];
         const int32_t ts = start[t], cnt = end[t] - ts;
-        const int rem = cnt & 7;
-        const int nblk = (cnt >> 3) + (rem ? 1 : 0);
-        const bool small_last = rem != 0 && rem <= 4;
+        const int rem = cnt & (kBlk - 1);
+        const int nblk = cnt / kBlk + (rem ? 1 : 0);
+        const bool small_last = !kK4Only && rem != 0 && rem <= 4;
         const int64_t r0 = run_off[2 * (int64_t)row], r1 = run_off[2 * (int64_t)row + 1];
         const int nr = (int)(r1 - r0);
         // streamed rows split every block's source line over the warps by
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
         }
         if (streamed) {
             if (threadIdx.x == 0) stotal = 0;
-            for (int k = threadIdx.x; k < nunits * 32; k += blockDim.x) (&red[0][0][0])[k] = 0.f;
+            for (int k = threadIdx.x; k < nunits * 4 * kBlk; k += blockDim.x) (&red[0][0][0])[k] = 0.f;
             __syncthreads();
             int32_t len = 0;
             for (int k = threadIdx.x; k < nr; k += blockDim.x) {
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
             const int uu = k4 ? lane & 3 : lane & 7;
             if (fold) {
                 if (lane < (k4 ? 16 : 32)) red[u][q][uu] = val;
-            } else if (lane < (k4 ? 16 : 32) && tb * 8 + uu < cnt) {
+            } else if (lane < (k4 ? 16 : 32) && tb * kBlk + uu < cnt) {
                 double *out = q == 0 ? phi : q == 1 ? fx : q == 2 ? fy : fz;
                 out[i0 + uu] = (double)val;
                 if (!isfinite(val)) atomicOr(flag, 1);
@@ -560,15 +568,16 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
             // w-th quarter of the concatenated weighted lines
             const int32_t scnt = cross ? 0 : cnt;  // cross-tree rows have no self leaf
             const int64_t L = (int64_t)scnt + stotal;
-            const int64_t Wl = L * (2 * nblk - (small_last ? 1 : 0));
+            constexpr int64_t bw = kK4Only ? 1 : 2;  // weight per source of a full block
+            const int64_t Wl = L * (bw * nblk - (small_last ? 1 : 0));
             const int64_t A = Wl * w / kP2PWarps, B = Wl * (w + 1) / kP2PWarps;
-            for (int tb = (int)(A / (2 * L)); tb < nblk && 2 * L * tb < B; tb++) {
-                const bool k4 = tb == nblk - 1 && small_last;
-                const int64_t Sb = 2 * L * tb, sc = k4 ? 1 : 2;
+            for (int tb = (int)(A / (bw * L)); tb < nblk && bw * L * tb < B; tb++) {
+                const bool k4 = kK4Only || (tb == nblk - 1 && small_last);
+                const int64_t Sb = bw * L * tb, sc = k4 ? 1 : 2;
                 const int32_t s0 = (int32_t)((max(A, Sb) - Sb) / sc);
                 const int32_t s1 = (int32_t)((min(B, Sb + sc * L) - Sb) / sc);
                 if (s1 <= s0) continue;
-                const int32_t i0 = ts + tb * 8;
+                const int32_t i0 = ts + tb * kBlk;
                 const float val =
                     k4 ? p2p_f32_stream_unit<4>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w], phase,
                                                 srun)
@@ -579,8 +588,8 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
         } else {
             for (int u = w; u < nunits; u += kP2PWarps) {
                 const int tb = u / P, part = u % P;
-                const int32_t i0 = ts + tb * 8;
-                const bool k4 = tb == nblk - 1 && small_last;
+                const int32_t i0 = ts + tb * kBlk;
+                const bool k4 = kK4Only || (tb == nblk - 1 && small_last);
                 const float val =
                     k4 ? p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring)
                        : p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an,
@@ -591,7 +600,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
         __syncthreads();  // partial sums complete; srun / pool may be rewritten after this
         if (fold) {
             for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
-                const int tb = k >> 3, l = k & 7;
+                const int tb = k / kBlk, l = k % kBlk;
                 float p_ = 0.f, x_ = 0.f, y_ = 0.f, z_ = 0.f;
                 for (int q = 0; q < P; q++) {  // fixed order: deterministic
                     const int uu = tb * P + q;

@@ -159,9 +159,17 @@ def critical_path(t_near: float, t_up: float, t_far: float, wall: float) -> tupl
 def _setup_gap(tree: Tree, e0) -> float:
     """Seconds between the end of ``tree``'s build and this evaluation's
     first event, once per build: host set-up the reference bills to its
-    upward phase (src/traversal.py:875-879)."""
+    upward phase (src/traversal.py:875-879).  The first evaluation after a
+    build also replaces the build's host-timed ``build_time`` by its span
+    on the device timeline (the evaluation has synchronised by now), so
+    build + upward + traversal + downward tiles the device time."""
     ev = tree.__dict__.pop("_ev_built", None)
-    return ev.elapsed_time(e0) * 1e-3 if ev is not None else 0.0
+    ev0 = tree.__dict__.pop("_ev_build_start", None)
+    if ev is None:
+        return 0.0
+    if ev0 is not None:
+        tree.build_time = ev0.elapsed_time(ev) * 1e-3
+    return ev.elapsed_time(e0) * 1e-3
 
 
 # ---------------------------------------------------------------------------

@@ -302,6 +302,8 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         dev = torch.device(device)
     n = ps.n
     with torch.cuda.device(dev):
+        ev_start = torch.cuda.Event(enable_timing=True)  # the build's span on the device timeline
+        ev_start.record()
         st = _lib.stream_handle()
         f64, i32 = torch.float64, torch.int32
         if ps.on_device:
@@ -386,6 +388,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
     with torch.cuda.device(dev):  # the evaluation bills the host gap after the build to its first phase
         tree._ev_built = torch.cuda.Event(enable_timing=True)
         tree._ev_built.record()
+    tree._ev_build_start = ev_start
     return tree
 
 

@@ -1,0 +1,41 @@
+#!/bin/bash
+# One measurement pass on a gpurun box (outputs under gpurun_out/, copy the
+# ones to keep into profiles/rNN_*):
+#   bash tools/measure.sh bench     bench lines: C2 (driver default), C2 fp64, C1/C3/C5, strategies, reference arm
+#   bash tools/measure.sh launches  ncu launch list of one C2 and one C3 bench step (gpu__time_duration per launch)
+#   bash tools/measure.sh p2p       ncu --set full of the C2 P2P kernel (tools/p2p_bench.py)
+#   bash tools/measure.sh c4        the C4 accuracy/speed sweep, fp32 and fp64 (tools/c4_sweep.py)
+# Each ncu pass runs only after the same command exited 0 without ncu.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+case "$1" in
+bench)
+  python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+  python bench.py --precision fp64 --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_fp64.json 2> gpurun_out/bench_c2_fp64.err
+  for c in C1 C3 C5; do
+    python bench.py --config $c --steps 5 --warmup 5 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+  done
+  for s in treecode listfmm; do
+    python bench.py --strategy $s --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_$s.json 2> gpurun_out/bench_$s.err
+  done
+  python bench.py --mutual --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_mutual.json 2> gpurun_out/bench_mu.err
+  python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+  ;;
+launches)
+  for c in C2 C3; do
+    CMD="python bench.py --config $c --steps 1 --warmup 5 --no-cpu-baseline --no-e2e --no-accuracy"
+    $CMD > gpurun_out/plain_$c.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_$c.csv $CMD > gpurun_out/ncu_launches_$c.log 2>&1; echo "launches $c rc=$?"
+  done
+  ;;
+p2p)
+  CMD="python tools/p2p_bench.py --reps 3"
+  $CMD > gpurun_out/plain_p2p.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:p2p_f32 \
+    -s 2 -c 1 -o gpurun_out/p2p_prof -f $CMD > gpurun_out/ncu_p2p.log 2>&1; echo "p2p rc=$?"
+  ;;
+c4)
+  python tools/c4_sweep.py fp32 > gpurun_out/c4_fp32.log 2>&1
+  python tools/c4_sweep.py fp64 > gpurun_out/c4_fp64.log 2>&1
+  ;;
+*) echo "usage: $0 bench|launches|p2p|c4"; exit 2;;
+esac
