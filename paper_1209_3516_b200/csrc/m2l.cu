@@ -118,16 +118,29 @@ __device__ inline DRecipe make_recipe(int idx) {
     return r;
 }
 
-template <int P>
-__global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *__restrict__ rows,
+#ifndef FMM_M2L_WARPS
+#define FMM_M2L_WARPS 8
+#endif
+#ifndef FMM_M2L_ACC
+#define FMM_M2L_ACC 1
+#endif
+constexpr int kM2LAcc = FMM_M2L_ACC;  // independent FMA chains per output
+// warps per row CTA: FMM_M2L_WARPS while three NC-double slices per warp fit
+// the 48 KB of static shared memory, else 4
+__host__ __device__ constexpr int m2l_warps(int P) {
+    return ncoef(P) * 3 * 8 * FMM_M2L_WARPS <= 44000 ? FMM_M2L_WARPS : 4;
+}
+
+template <int P, int kM2LWarps = m2l_warps(P)>
+__global__ void __launch_bounds__(kM2LWarps * 32) m2l_lanes(int32_t ncells, const int64_t *__restrict__ rows,
                                                  const int32_t *__restrict__ src, const double *__restrict__ ctr,
                                                  const double *__restrict__ cs, const double *__restrict__ M,
                                                  double *L) {
     constexpr int NC = ncoef(P);
     constexpr int NS = (NC + 31) / 32;
-    __shared__ double sM[4][NC];
-    __shared__ double sD[4][NC];
-    __shared__ double red[4][NC];
+    __shared__ double sM[kM2LWarps][NC];
+    __shared__ double sD[kM2LWarps][NC];
+    __shared__ double red[kM2LWarps][NC];
     __shared__ DRecipe rec[NC];
     __shared__ double sgn[NC];
     for (int i = threadIdx.x; i < NC; i += blockDim.x) {
@@ -144,7 +157,7 @@ __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *
         double acc[NS];
 #pragma unroll
         for (int i = 0; i < NS; i++) acc[i] = 0.0;
-        for (int64_t k = k0 + w; k < k1; k += 4) {
+        for (int64_t k = k0 + w; k < k1; k += kM2LWarps) {
             const int32_t s = src[k];
             for (int m = lane; m < NC; m += 32) Ms[m] = sgn[m] * __ldg(&M[(int64_t)s * NC + m]);
             const double r[3] = {cx - cs[s * 3], cy - cs[s * 3 + 1], cz - cs[s * 3 + 2]};
@@ -176,7 +189,9 @@ __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *
                 const DRecipe qn = rec[nn];
                 const int nx = qn.k[0], nz = qn.k[2];
                 const int dn = valid ? qn.k[0] + qn.k[1] + qn.k[2] : P;
-                double a = 0.0;
+                double a[kM2LAcc];
+#pragma unroll
+                for (int c = 0; c < kM2LAcc; c++) a[c] = 0.0;
                 static_for<0, P>([&](auto Idm) {
                     constexpr int dm = decltype(Idm)::value;
                     if (dn + dm <= P - 1) {
@@ -186,11 +201,18 @@ __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *
                             constexpr int bm = ncoef(dm) + tri(dm - mx), len = dm - mx + 1;
                             const int bd = dv * (dv + 1) * (dv + 2) / 6 + tri(dv - nx - mx) + nz;
 #pragma unroll
-                            for (int u = 0; u < len; u++) a = fma(Ms[bm + u], D[bd + u], a);
+                            for (int u = 0; u < len; u++) {
+                                constexpr int c0 = (tri(dm) + mx) % kM2LAcc;  // rows rotate over the chains
+                                double &ac = a[(c0 + u) % kM2LAcc];
+                                ac = fma(Ms[bm + u], D[bd + u], ac);
+                            }
                         });
                     }
                 });
-                acc[i] += a;
+                double sum = a[0];
+#pragma unroll
+                for (int c = 1; c < kM2LAcc; c++) sum += a[c];
+                acc[i] += sum;
             }
             __syncwarp();  // the warp's slices are rewritten by its next pair
         }
@@ -198,8 +220,12 @@ __global__ void __launch_bounds__(128) m2l_lanes(int32_t ncells, const int64_t *
         for (int i = 0; i < NS; i++)
             if (32 * i + lane < NC) red[w][32 * i + lane] = acc[i];
         __syncthreads();
-        for (int n = threadIdx.x; n < NC; n += blockDim.x)
-            L[(int64_t)t * NC + n] += (((red[0][n] + red[1][n]) + red[2][n]) + red[3][n]) / d_tab.mfact[n];
+        for (int n = threadIdx.x; n < NC; n += blockDim.x) {
+            double v = red[0][n];
+#pragma unroll
+            for (int q = 1; q < kM2LWarps; q++) v += red[q][n];  // fixed order: deterministic
+            L[(int64_t)t * NC + n] += v / d_tab.mfact[n];
+        }
         __syncthreads();  // red is rewritten by the next row
     }
 }
@@ -222,7 +248,7 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
         case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
 #define M2L_LANES(PP)                                                                                 \
     case PP:                                                                                          \
-        m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); \
+        m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), m2l_warps(PP) * 32, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); \
         fmm::note_launch();                                                                           \
         break;
         M2L_LANES(6)
