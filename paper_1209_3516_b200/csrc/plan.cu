@@ -35,8 +35,19 @@ namespace fmm {
 // -- with the sorted keys given, leaves without two equal adjacent keys
 // skip the O(|t|^2) scan.
 constexpr int kPlanWarps = 4;
-constexpr int kPlanSegWords = 1024;  // 32768 ordinals per bitmap pass
-constexpr int kWideMax = 1024;      // longest row staged in shared memory (longer ones gather per pass)
+#ifndef FMM_PLAN_SEG_SHIFT
+#define FMM_PLAN_SEG_SHIFT 14
+#endif
+#ifndef FMM_PLAN_WIDE
+#define FMM_PLAN_WIDE 512
+#endif
+#ifndef FMM_PLAN_MINB
+#define FMM_PLAN_MINB 8
+#endif
+constexpr int kSegShift = FMM_PLAN_SEG_SHIFT;             // log2(ordinals per bitmap pass)
+constexpr uint32_t kSegOrd = 1u << kSegShift;             // 16384 ordinals per bitmap pass
+constexpr int kPlanSegWords = 1 << (kSegShift - 5);       // 512 words (2 KB per warp)
+constexpr int kWideMax = FMM_PLAN_WIDE;  // longest row staged in shared memory (longer ones gather per pass)
 
 // A row's coincident-pair scan, counters and run range (one warp).
 __device__ __forceinline__ void plan_row_finish(int32_t r, int32_t t, int64_t k0, int64_t nrun, long long blocks,
@@ -76,9 +87,9 @@ __device__ __forceinline__ void plan_row_finish(int32_t r, int32_t t, int64_t k0
 }
 
 // Runs of one bitmap pass.  bm (the warp's window, bm[-1] and
-// bm[kPlanSegWords] zero) holds the row's ordinals in [seg << 15, (seg + 1)
+// bm[kPlanSegWords] zero) holds the row's ordinals in [seg << kSegShift, (seg + 1)
 // << 15); words [wa, wb] are the touched ones.  prev_top: is ordinal
-// (seg << 15) - 1 in the row; next_first: is (seg + 1) << 15.  Appends the
+// (seg << kSegShift) - 1 in the row; next_first: is (seg + 1) << 15.  Appends the
 // pass's runs after the row's first nrun, updates the counters, clears the
 // window and returns bit 31 of the pass's last word (the next pass's
 // prev_top when that pass is seg + 1).
@@ -86,13 +97,13 @@ __device__ __forceinline__ uint32_t plan_pass(uint32_t *bm, uint32_t seg, uint32
                                               bool next_first, int32_t ot, int64_t k0, int64_t nt, int64_t &nrun,
                                               long long &blocks, bool &self, const int32_t *__restrict__ s_bstart,
                                               const int32_t *__restrict__ s_bend, int32_t soff, int4 *runs, int lane) {
-    const uint32_t sbase = seg << 15;
+    const uint32_t sbase = seg << kSegShift;
     // the pass's word window, split into contiguous per-lane blocks
     const uint32_t nw = wb - wa + 1, per = (nw + 31) / 32;
     const uint32_t w0 = wa + min(lane * per, nw), w1 = wa + min(lane * per + per, nw);
-    const int32_t self_word = (ot >= 0 && ((uint32_t)ot >> 15) == seg) ? (int32_t)(((uint32_t)ot >> 5) & 1023u) : -2;
+    const int32_t self_word = (ot >= 0 && ((uint32_t)ot >> kSegShift) == seg) ? (int32_t)(((uint32_t)ot >> 5) & (kPlanSegWords - 1)) : -2;
     const int32_t prev_self = (ot >= 0 && (uint32_t)ot + 1u == sbase) ? 1 : 0;  // self just before this pass
-    const int32_t next_self = (ot >= 0 && (uint32_t)ot == sbase + 32768u) ? 1 : 0;
+    const int32_t next_self = (ot >= 0 && (uint32_t)ot == sbase + kSegOrd) ? 1 : 0;
     // masks of run starts / ends in word x
     auto masks = [&](uint32_t x, uint32_t &st, uint32_t &en) {
         const uint32_t W = bm[x];
@@ -184,11 +195,11 @@ __device__ __forceinline__ void plan_row_staged(int32_t r, int32_t t, int64_t k0
     int64_t nrun = 0;
     uint32_t prev_seg = kNone, prev_top = 0u;
     while (n > 0 && seg != kNone) {
-        const uint32_t sbase = seg << 15;
+        const uint32_t sbase = seg << kSegShift;
         uint32_t wa = kNone, wb = 0u, nseg = kNone;
         bool next_first = false;
         for (int e = lane; e < n; e += 32) {
-            const uint32_t v = ent[e], g = v >> 15;
+            const uint32_t v = ent[e], g = v >> kSegShift;
             if (g == seg) {
                 const uint32_t wd = (v >> 5) & (kPlanSegWords - 1);
                 atomicOr(&bm[wd], 1u << (v & 31u));
@@ -197,7 +208,7 @@ __device__ __forceinline__ void plan_row_staged(int32_t r, int32_t t, int64_t k0
             } else if (g > seg) {
                 nseg = min(nseg, g);
             }
-            next_first |= v == sbase + 32768u;
+            next_first |= v == sbase + kSegOrd;
         }
         wa = __reduce_min_sync(0xffffffffu, wa);
         wb = __reduce_max_sync(0xffffffffu, wb);
@@ -214,7 +225,7 @@ __device__ __forceinline__ void plan_row_staged(int32_t r, int32_t t, int64_t k0
     __syncwarp();  // ent is rewritten by the warp's next row
 }
 
-__global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
+__global__ void __launch_bounds__(kPlanWarps * 32, FMM_PLAN_MINB) plan_rows_kernel(
     const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int64_t *__restrict__ rows,
     const int32_t *__restrict__ src, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
     const int32_t *__restrict__ t_ord, const int32_t *__restrict__ s_ord, const int32_t *__restrict__ s_bstart,
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
         hi = __reduce_max_sync(0xffffffffu, hi);
         if (staged) {  // one gather of the row, non-empty windows only
             __syncwarp();
-            plan_row_staged(r, t, k0, (int)(k1 - k0), lo >> 15, bm, ent, start, end, t_ord, s_bstart, s_bend, cross,
+            plan_row_staged(r, t, k0, (int)(k1 - k0), lo >> kSegShift, bm, ent, start, end, t_ord, s_bstart, s_bend, cross,
                             soff, xs, ys, zs, keys, run_rng, runs, stats, nruns_total, lane);
             continue;
         }
@@ -263,18 +274,18 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_rows_kernel(
         bool self = false;
         int64_t nrun = 0;        // runs so far in this row (warp-uniform)
         uint32_t prev_top = 0u;  // bit 31 of the word before the current pass
-        for (uint32_t seg = lo >> 15; k1 > k0 && seg <= (hi >> 15); seg++) {
-            const uint32_t sbase = seg << 15;
+        for (uint32_t seg = lo >> kSegShift; k1 > k0 && seg <= (hi >> kSegShift); seg++) {
+            const uint32_t sbase = seg << kSegShift;
             bool next_first = false;  // is ordinal sbase + 32768 (next pass) set?
             for (int64_t k = k0 + lane; k < k1; k += 32) {
                 const uint32_t v = (uint32_t)s_ord[src[k]];
-                if ((v >> 15) == seg) atomicOr(&bm[(v >> 5) & (kPlanSegWords - 1)], 1u << (v & 31u));
-                next_first |= v == sbase + 32768u;
+                if ((v >> kSegShift) == seg) atomicOr(&bm[(v >> 5) & (kPlanSegWords - 1)], 1u << (v & 31u));
+                next_first |= v == sbase + kSegOrd;
             }
             next_first = __any_sync(0xffffffffu, next_first);
             __syncwarp();
-            const uint32_t wa = (seg == (lo >> 15)) ? ((lo >> 5) & (kPlanSegWords - 1)) : 0u;
-            const uint32_t wb = (seg == (hi >> 15)) ? ((hi >> 5) & (kPlanSegWords - 1)) : kPlanSegWords - 1;
+            const uint32_t wa = (seg == (lo >> kSegShift)) ? ((lo >> 5) & (kPlanSegWords - 1)) : 0u;
+            const uint32_t wb = (seg == (hi >> kSegShift)) ? ((hi >> 5) & (kPlanSegWords - 1)) : kPlanSegWords - 1;
             prev_top = plan_pass(bm, seg, wa, wb, prev_top, next_first, ot, k0, nt, nrun, blocks, self, s_bstart,
                                  s_bend, soff, runs, lane);
         }

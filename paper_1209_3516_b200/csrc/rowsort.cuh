@@ -12,7 +12,11 @@
 
 namespace fmm {
 
-constexpr int kSortSegWords = 1024;  // 32768 ids per pass
+#ifndef FMM_SORT_SHIFT
+#define FMM_SORT_SHIFT 14
+#endif
+constexpr int kSortShift = FMM_SORT_SHIFT;              // log2(ids per bitmap pass)
+constexpr int kSortSegWords = 1 << (kSortShift - 5);    // 512 words: 16384 ids per pass
 
 // Sorts in[k0..k1) (distinct ids) into out[k0..k1).
 __device__ __forceinline__ void warp_bitmap_sort(const int32_t *__restrict__ in, int32_t *out, int64_t k0, int64_t k1,
@@ -71,7 +75,7 @@ __device__ __forceinline__ void warp_bitmap_sort_sparse(const int32_t *__restric
     for (int e = lane; e < n; e += 32) {
         const uint32_t v = (uint32_t)in[k0 + e];
         ent[e] = v;
-        seg = min(seg, v >> 15);
+        seg = min(seg, v >> kSortShift);
     }
     seg = __reduce_min_sync(0xffffffffu, seg);
     __syncwarp();
@@ -79,7 +83,7 @@ __device__ __forceinline__ void warp_bitmap_sort_sparse(const int32_t *__restric
     while (seg != kNone) {
         uint32_t wa = kNone, wb = 0u, nseg = kNone;
         for (int e = lane; e < n; e += 32) {
-            const uint32_t v = ent[e], g = v >> 15;
+            const uint32_t v = ent[e], g = v >> kSortShift;
             if (g == seg) {
                 const uint32_t wd = (v >> 5) & (kSortSegWords - 1);
                 atomicOr(&bm[wd], 1u << (v & 31u));
@@ -106,7 +110,7 @@ __device__ __forceinline__ void warp_bitmap_sort_sparse(const int32_t *__restric
         int64_t at = pos + incl - cnt;
         for (uint32_t x = w0; x < w1; x++) {
             for (uint32_t bits = bm[x]; bits; bits &= bits - 1u)
-                out[at++] = (int32_t)((seg << 15) + (x << 5) + (uint32_t)(__ffs(bits) - 1));
+                out[at++] = (int32_t)((seg << kSortShift) + (x << 5) + (uint32_t)(__ffs(bits) - 1));
             bm[x] = 0u;
         }
         pos += __shfl_sync(0xffffffffu, incl, 31);

@@ -300,6 +300,9 @@ __global__ void __launch_bounds__(kRowLargeThreads) row_sort_large_kernel(
 // Bitmap sort (rowsort.cuh): one warp per row.
 constexpr int kRowBitmapWarps = 8;
 constexpr int kRowSparseWarps = 4;
+#ifndef FMM_SORT_MINB
+#define FMM_SORT_MINB 8
+#endif
 
 // Rows whose ids fit one bitmap pass (or are too long to stage) are sorted
 // here; wide rows of up to kSparseMax ids are queued for the sparse kernel,
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(kRowBitmapWarps * 32) row_sort_bitmap_kernel(
     }
 }
 
-__global__ void __launch_bounds__(kRowSparseWarps * 32) row_sort_sparse_kernel(const int64_t *__restrict__ rows,
+__global__ void __launch_bounds__(kRowSparseWarps * 32, FMM_SORT_MINB) row_sort_sparse_kernel(const int64_t *__restrict__ rows,
                                                                              const int32_t *__restrict__ in,
                                                                              int32_t *out,
                                                                              const int32_t *__restrict__ wide_rows,
@@ -342,7 +345,7 @@ static int sort_rows_launch(int32_t ncells, const int64_t *rows, const int32_t *
     cudaMemsetAsync(nwide, 0, sizeof(unsigned long long), st);
     row_sort_bitmap_kernel<<<grid_for(ncells, kRowBitmapWarps, 148 * 8), kRowBitmapWarps * 32, 0, st>>>(
         ncells, rows, in, out, wide_rows, nwide); fmm::note_launch();
-    row_sort_sparse_kernel<<<148 * 6, kRowSparseWarps * 32, 0, st>>>(rows, in, out, wide_rows, nwide); fmm::note_launch();
+    row_sort_sparse_kernel<<<148 * (FMM_SORT_MINB > 6 ? FMM_SORT_MINB : 6), kRowSparseWarps * 32, 0, st>>>(rows, in, out, wide_rows, nwide); fmm::note_launch();
     return FMM_OK;
 }
 
