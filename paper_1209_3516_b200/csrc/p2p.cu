@@ -778,8 +778,11 @@ __device__ __forceinline__ double p2p_f64_runs_unit(int32_t i0, int32_t ilast, i
     return warp_fold_f64(ap, ax, ay, az, lane);
 }
 
+#ifndef FMM_P2P64_MINB
+#define FMM_P2P64_MINB 4
+#endif
 template <bool CROSS>
-__global__ void __launch_bounds__(kP2PWarps * 32, 3) p2p_f64s_kernel(
+__global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P64_MINB) p2p_f64s_kernel(
     int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows,
     const int32_t *__restrict__ start, const int32_t *__restrict__ end, const int64_t *__restrict__ run_off,
     const int4 *__restrict__ runs, const double4 *__restrict__ b, double *phi, double *fx, double *fy, double *fz) {

@@ -4,6 +4,7 @@
 #   bash tools/measure.sh bench     bench lines: C2 (driver default), C2 fp64, C1/C3/C5, strategies, reference arm
 #   bash tools/measure.sh launches  ncu launch list of one C2 and one C3 bench step (gpu__time_duration per launch)
 #   bash tools/measure.sh p2p       ncu --set full of the C2 P2P kernel (tools/p2p_bench.py)
+#   bash tools/measure.sh p2p64     ncu --set full of the C2 FP64 P2P kernel (tools/p2p64_check.py)
 #   bash tools/measure.sh c4        the C4 accuracy/speed sweep, fp32 and fp64 (tools/c4_sweep.py)
 # Each ncu pass runs only after the same command exited 0 without ncu.
 cd "$(dirname "$0")/.."
@@ -33,9 +34,14 @@ p2p)
   $CMD > gpurun_out/plain_p2p.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:p2p_f32 \
     -s 2 -c 1 -o gpurun_out/p2p_prof -f $CMD > gpurun_out/ncu_p2p.log 2>&1; echo "p2p rc=$?"
   ;;
+p2p64)
+  CMD="python tools/p2p64_check.py --reps 2"
+  $CMD > gpurun_out/plain_p2p64.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:p2p_f64s \
+    -s 1 -c 1 -o gpurun_out/p2p64_prof -f $CMD > gpurun_out/ncu_p2p64.log 2>&1; echo "p2p64 rc=$?"
+  ;;
 c4)
   python tools/c4_sweep.py fp32 > gpurun_out/c4_fp32.log 2>&1
   python tools/c4_sweep.py fp64 > gpurun_out/c4_fp64.log 2>&1
   ;;
-*) echo "usage: $0 bench|launches|p2p|c4"; exit 2;;
+*) echo "usage: $0 bench|launches|p2p|p2p64|c4"; exit 2;;
 esac
