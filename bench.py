@@ -255,9 +255,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FMM_BENCH_BACKEND / FMM_BENCH_SAME_DEVICE exist for testing the
+    # multi-rank code path on a one-GPU box (gloo, every rank on cuda:0);
+    # the driver's runs use NCCL with one GPU per rank
+    if os.environ.get("FMM_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("FMM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     pos, q, n, solver = workload(args)
     cfg = fb.EvalConfig(strategy=args.strategy, mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"],
                         precision=args.precision, mutual=args.mutual, task_grain=args.task_grain)
@@ -273,7 +282,7 @@ def run_ours(args):
     def step():
         tree = fb.build_tree(ps_dev, ncrit=solver["ncrit"])
         if world > 1:
-            rep = fdist.evaluate_partitioned(tree, cfg, rank, world)
+            rep = fdist.evaluate_partitioned(tree, cfg, rank, world, results="root")
         else:
             rep = fb.evaluate_on_tree(tree, cfg)
         return tree, rep
@@ -316,11 +325,14 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    total = float(np.sum(times))
-    if world > 1:
-        t = torch.tensor([total], dtype=torch.float64, device=dev)
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total = float(t.item())
+        return float(t.item())
+
+    total = max_over_ranks(float(np.sum(times)))
     ms = 1e3 * total / args.steps
     value = n * args.steps / total
     rep = reps[-1]
@@ -340,7 +352,7 @@ def run_ours(args):
             ps = fb.ParticleSet(hx, hy, hz, hq)
             tr = fb.build_tree(ps, ncrit=solver["ncrit"])
             if world > 1:
-                fdist.evaluate_partitioned(tr, cfg, rank, world)
+                fdist.evaluate_partitioned(tr, cfg, rank, world, results="root")
                 return tr.results_in_input_order() if rank == 0 else None
             fb.evaluate_on_tree(tr, cfg)
             return tr.results_in_input_order()
@@ -356,16 +368,12 @@ def run_ours(args):
                 dist.barrier()
             t0 = time.perf_counter()
             res = e2e_step()
-            dt = time.perf_counter() - t0
-            if world > 1:
-                tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                dt = float(tt.item())
-            et.append(dt)
+            et.append(max_over_ranks(time.perf_counter() - t0))
         e2e = {"value": n / float(np.median(et)), "unit": "particles/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 4 * 8 * n,
                "note": "ParticleSet(host numpy) -> build_tree -> evaluate_on_tree (evaluate_partitioned over the "
-                       "ranks) -> results_in_input_order() (phi, f back in input order as float64); wall clock per "
+                       "ranks, results gathered to rank 0) -> results_in_input_order() (phi, f back in input "
+                       "order as float64); wall clock per "
                        "step, median of the max over ranks"}
         del res
 
