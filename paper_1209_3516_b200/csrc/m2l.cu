@@ -17,6 +17,10 @@
 //    (|m|, m_x) term rows -- see below.
 #include "taylor.cuh"
 
+#ifndef FMM_M2L_VEC
+#define FMM_M2L_VEC 1
+#endif
+
 namespace fmm {
 
 // ---- register kernel, compile-time multi-indices (taylor.cuh) -----------
@@ -26,9 +30,22 @@ namespace fmm {
 template <int P>
 __device__ __forceinline__ void m2l_contract_mouter(const double *__restrict__ Mrow, const double (&D)[ncoef(P)],
                                                     double (&acc)[ncoef(P)]) {
+#if FMM_M2L_VEC
+    // 16 B loads from the row's 16 B-aligned window (an odd-length row starts
+    // 8 B into it for odd cells): element m is window element m + odd
+    const bool odd = (reinterpret_cast<uintptr_t>(Mrow) & 15u) != 0;
+    const double2 *win = reinterpret_cast<const double2 *>(Mrow - (odd ? 1 : 0));
+#endif
     static_for<0, ncoef(P)>([&](auto Im) {
         constexpr int m = decltype(Im)::value;
+#if FMM_M2L_VEC
+        const double2 we = __ldg(&win[m >> 1]), wo = __ldg(&win[(m + 1) >> 1]);
+        const double me = (m & 1) ? we.y : we.x, mo = ((m + 1) & 1) ? wo.y : wo.x;
+        const double raw = odd ? mo : me;
+        const double mm = (kTab.deg[m] & 1) ? -raw : raw;
+#else
         const double mm = (kTab.deg[m] & 1) ? -__ldg(&Mrow[m]) : __ldg(&Mrow[m]);
+#endif
         static_for<0, ncoef(P - kTab.deg[m])>([&](auto In) {
             constexpr int n = decltype(In)::value;
             constexpr int j = kTab.idx3[kTab.mi[n][0] + kTab.mi[m][0]][kTab.mi[n][1] + kTab.mi[m][1]]
@@ -43,8 +60,23 @@ __device__ __forceinline__ void m2l_contract_nouter(const double *__restrict__ M
                                                     double (&acc)[ncoef(P)]) {
     constexpr int NC = ncoef(P);
     double Ms[NC];
+#if FMM_M2L_VEC
+    if constexpr (NC % 2 == 0) {  // rows of an even count are 16 B aligned: LDG.128
+        const double2 *r2 = reinterpret_cast<const double2 *>(Mrow);
+#pragma unroll
+        for (int q = 0; q < NC / 2; q++) {
+            const double2 v = __ldg(&r2[q]);
+            Ms[2 * q] = v.x;
+            Ms[2 * q + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < NC; m++) Ms[m] = __ldg(&Mrow[m]);
+    }
+#else
 #pragma unroll
     for (int m = 0; m < NC; m++) Ms[m] = __ldg(&Mrow[m]);
+#endif
     static_for<0, NC>([&](auto In) {
         constexpr int n = decltype(In)::value;
         double a = 0.0;
@@ -59,15 +91,19 @@ __device__ __forceinline__ void m2l_contract_nouter(const double *__restrict__ M
     });
 }
 
-// P = 5 streams the moments (moments-outer order: 168 registers instead of
-// 254, 3 CTAs per SM, C3 M2L 2.78 -> 2.57 ms); P <= 4 keeps the row of
-// moments in registers (moments-outer was 13 % slower there)
+// P = 5 streams the moments (moments-outer order: ~170 registers instead of
+// 254); P <= 4 keeps the row of moments in registers (moments-outer was 13 %
+// slower there).  Every lane reads its own source's row, so the L1 sees 32
+// cache lines per load instruction (90 % L1 throughput at C3,
+// profiles/r02_m2l5_ncu_c3.json): the rows are read as 16 B pairs from their
+// 16 B-aligned window (odd-length rows of odd cells start 8 B into it), which
+// halves the load instructions -- C2 p=4 0.346 -> 0.291 ms, C3 p=5 2.56 ->
+// 2.41 ms (FMM_M2L_VEC=0 keeps 8 B loads).
 template <int P>
-__global__ void __launch_bounds__(128) m2l_reg(int32_t ncells, const int64_t *__restrict__ rows,
-                                               const int32_t *__restrict__ src,
-                                               const double *__restrict__ ctr,
-                                               const double *__restrict__ cs,
-                                               const double *__restrict__ M, double *L) {
+__device__ __forceinline__ void m2l_reg_body(int32_t ncells, const int64_t *__restrict__ rows,
+                                             const int32_t *__restrict__ src, const double *__restrict__ ctr,
+                                             const double *__restrict__ cs, const double *__restrict__ M,
+                                             double *L) {
     constexpr int NC = ncoef(P);
     const int lane = threadIdx.x & 31;
     for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ncells;
@@ -100,6 +136,25 @@ __global__ void __launch_bounds__(128) m2l_reg(int32_t ncells, const int64_t *__
             });
         }
     }
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) m2l_reg(int32_t ncells, const int64_t *__restrict__ rows,
+                                               const int32_t *__restrict__ src, const double *__restrict__ ctr,
+                                               const double *__restrict__ cs, const double *__restrict__ M,
+                                               double *L) {
+    m2l_reg_body<P>(ncells, rows, src, ctr, cs, M, L);
+}
+
+#ifndef FMM_M2L_REG5_MINB
+#define FMM_M2L_REG5_MINB 1
+#endif
+__global__ void __launch_bounds__(128, FMM_M2L_REG5_MINB) m2l_reg5(int32_t ncells, const int64_t *__restrict__ rows,
+                                                                  const int32_t *__restrict__ src,
+                                                                  const double *__restrict__ ctr,
+                                                                  const double *__restrict__ cs,
+                                                                  const double *__restrict__ M, double *L) {
+    m2l_reg_body<5>(ncells, rows, src, ctr, cs, M, L);
 }
 
 // ---- high orders (P >= 6): lanes own outputs ------------------------------
@@ -274,7 +329,7 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
         case 2: m2l_reg<2><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
         case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
         case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
-        case 5: m2l_reg<5><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        case 5: m2l_reg5<<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
 #define M2L_LANES(PP)                                                                                 \
     case PP:                                                                                          \
         m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), m2l_warps(PP) * 32, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); \
