@@ -4,8 +4,10 @@
 // cells, gather/pull form, so no atomics), L2P per body.
 //
 // Float64 throughout (these passes are <1% of the flops; they keep the
-// reference's 1e-12 agreement).  Expansion order p is a runtime value
-// (1..12); a thread owns one (cell, coefficient) so every write is private.
+// reference's 1e-12 agreement).  For p <= 5 (the BASELINE orders) M2M, L2L
+// and L2P are compiled per order with every multi-index a constant and a
+// thread owning a whole cell or body; for higher orders a thread owns one
+// (cell, coefficient) with runtime term loops.  Every write is private.
 #include "taylor.cuh"
 
 namespace fmm {
@@ -287,6 +289,50 @@ __global__ void l2p_kernel(int p, int64_t b0, int64_t n, const int32_t *__restri
     }
 }
 
+// L2P for p <= 5 with compile-time multi-indices: the body's powers
+// u_d^a and their derivatives a u_d^(a-1) are built once, every term of
+// phi = sum L_k u^k and of its gradient is an FMA with constant indices.
+template <int P>
+__global__ void __launch_bounds__(128) l2p_body_kernel(int64_t b0, int64_t n, const int32_t *__restrict__ body_leaf,
+                                                       const double *__restrict__ ctr, const double *__restrict__ xs,
+                                                       const double *__restrict__ ys, const double *__restrict__ zs,
+                                                       const double *__restrict__ L, double *phi, double *fx,
+                                                       double *fy, double *fz) {
+    constexpr int NC = ncoef(P);
+    for (int64_t i = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = body_leaf[i];
+        const double u[3] = {xs[i] - ctr[c * 3], ys[i] - ctr[c * 3 + 1], zs[i] - ctr[c * 3 + 2]};
+        double pw[3][P], dp[3][P];  // u_d^a, a u_d^(a-1)
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            pw[d][0] = 1.0;
+            dp[d][0] = 0.0;
+#pragma unroll
+            for (int a = 1; a < P; a++) {
+                dp[d][a] = dp[d][a - 1] * u[d] + pw[d][a - 1];
+                pw[d][a] = pw[d][a - 1] * u[d];
+            }
+        }
+        const double *Lc = L + (int64_t)c * NC;
+        double pot = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+        static_for<0, NC>([&](auto Ik) {
+            constexpr int k = decltype(Ik)::value;
+            constexpr int a = kTab.mi[k][0], b = kTab.mi[k][1], g = kTab.mi[k][2];
+            const double lk = Lc[k];
+            const double yz = pw[1][b] * pw[2][g];
+            pot = fma(lk, pw[0][a] * yz, pot);
+            gx = fma(lk, dp[0][a] * yz, gx);
+            gy = fma(lk, pw[0][a] * (dp[1][b] * pw[2][g]), gy);
+            gz = fma(lk, pw[0][a] * (pw[1][b] * dp[2][g]), gz);
+        });
+        phi[i] += pot;
+        fx[i] -= gx;
+        fy[i] -= gy;
+        fz[i] -= gz;
+    }
+}
+
 }  // namespace fmm
 
 using namespace fmm;
@@ -360,9 +406,20 @@ int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *le
         }
         fmm::note_launch();
     }
-    if (body_hi > body_lo)
-        l2p_kernel<<<grid_for(body_hi - body_lo, 128), 128, 0, s>>>(p, body_lo, body_hi, body_leaf, ctr, xs, ys,
-                                                                    zs, L, phi, fx, fy, fz); fmm::note_launch();
+    if (body_hi > body_lo) {
+        const int g = grid_for(body_hi - body_lo, 128);
+        switch (p) {
+#define L2P_BODY(PP)                                                                                         \
+    case PP:                                                                                                 \
+        l2p_body_kernel<PP><<<g, 128, 0, s>>>(body_lo, body_hi, body_leaf, ctr, xs, ys, zs, L, phi, fx, fy, fz); \
+        break;
+            L2P_BODY(1) L2P_BODY(2) L2P_BODY(3) L2P_BODY(4) L2P_BODY(5)
+#undef L2P_BODY
+            default:
+                l2p_kernel<<<g, 128, 0, s>>>(p, body_lo, body_hi, body_leaf, ctr, xs, ys, zs, L, phi, fx, fy, fz);
+        }
+        fmm::note_launch();
+    }
     FMM_CUDA_CHECK("fmm_downward");
     return FMM_OK;
 }
