@@ -677,15 +677,24 @@ last_events = None
 
 def _side_stream(dev, which: int = 0) -> torch.cuda.Stream:
     """Persistent auxiliary streams per device: 0 = far field, 1 = P2P,
-    2 = list construction, 3 = the upward pass.  All but P2P run at high
-    priority: their short kernels take SM slots as P2P blocks retire instead
-    of queueing behind the whole P2P grid, so the far field finishes early
-    (its spans are then its kernel times) and the step is unchanged (P2P
-    absorbs the same SM time either way)."""
+    2 = list construction, 3 = the upward pass.  Three priority levels:
+    the lists (they gate P2P) highest, the far field and the upward pass
+    above P2P -- their short kernels take SM slots as P2P blocks retire
+    instead of queueing behind the whole P2P grid, so the far field finishes
+    early (its spans are then its kernel times) -- and P2P lowest.  The far
+    field sits below the lists so that the M2L row sort does not compete
+    with the P2P plan (FMM_B200_FAR_PRIORITY: "mid" (default), "high", or
+    "low" = P2P's)."""
     key = (torch.device(dev).index or 0, which)
     if key not in _side:
-        hi = os.environ.get("FMM_B200_FAR_PRIORITY", "1") == "1" or which == 2
-        prio = torch.cuda.Stream.priority_range()[1] if which != 1 and hi else 0
+        least, greatest = torch.cuda.Stream.priority_range()
+        mode = os.environ.get("FMM_B200_FAR_PRIORITY", "mid")
+        if which == 2:
+            prio = greatest
+        elif which == 1:
+            prio = least
+        else:
+            prio = {"high": greatest, "low": least}.get(mode, (least + greatest) // 2)
         _side[key] = torch.cuda.Stream(device=dev, priority=prio)
     return _side[key]
 
