@@ -7,11 +7,12 @@
 // degree recurrence (no stored translation operators).  Float64.
 //
 // Two kernels:
-//  * m2l_reg<P> (P <= 5): one warp per target row, one LANE per (t, s) pair;
-//    D, M_s and the per-lane L partial sums live in registers, every
-//    multi-index resolves at compile time; the 32 partial sums are folded
-//    with shuffles at row end and added once to L_t.
-//  * m2l_lanes<P> (6 <= P <= 12): one block per target row, one WARP per
+//  * m2l_reg<P> (P <= 7): one warp per target row, one LANE per (t, s) pair;
+//    D and the per-lane L partial sums live in registers (for P >= 5 the
+//    source moments stream through, P <= 4 keeps them in registers too),
+//    every multi-index resolves at compile time; the 32 partial sums are
+//    folded with shuffles at row end and added once to L_t.
+//  * m2l_lanes<P> (8 <= P <= 12): one block per target row, one WARP per
 //    pair; lanes split each degree of the D recurrence (a shared-memory
 //    recipe per entry), then own output coefficients and walk contiguous
 //    (|m|, m_x) term rows -- see below.
@@ -20,6 +21,7 @@
 #ifndef FMM_M2L_VEC
 #define FMM_M2L_VEC 1
 #endif
+
 
 namespace fmm {
 
@@ -330,13 +332,18 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
         case 3: m2l_reg<3><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
         case 4: m2l_reg<4><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
         case 5: m2l_reg5<<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        // p = 6, 7: the register kernel too (moments streamed; D and the sums
+        // fill the 255 registers, a few spill to L1): C4 p = 6, theta = 0.3
+        // M2L 19.3 -> 1.6 ms, p = 7 13.3 -> 1.9 ms at C2 against m2l_lanes.
+        // From p = 8 the register arrays spill wholesale (tens of KB of local
+        // memory per thread) and m2l_lanes is 4-6x faster.
+        case 6: m2l_reg<6><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
+        case 7: m2l_reg<7><<<grid, 128, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); fmm::note_launch(); break;
 #define M2L_LANES(PP)                                                                                 \
     case PP:                                                                                          \
         m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), m2l_warps(PP) * 32, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); \
         fmm::note_launch();                                                                           \
         break;
-        M2L_LANES(6)
-        M2L_LANES(7)
         M2L_LANES(8)
         M2L_LANES(9)
         M2L_LANES(10)

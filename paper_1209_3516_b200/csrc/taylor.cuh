@@ -5,6 +5,7 @@
 #pragma once
 
 #include <type_traits>
+#include <utility>
 
 #include "fmm_common.cuh"
 
@@ -12,12 +13,14 @@ namespace fmm {
 
 // static_for hands each iteration its index as a type, so every table
 // lookup below is a constant expression and D / M / L stay in registers.
+template <int B, class F, int... I>
+__device__ __forceinline__ void static_for_seq(F &&f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, B + I>{}), ...);  // a fold: no recursion depth limit
+}
+
 template <int B, int E, class F>
 __device__ __forceinline__ void static_for(F &&f) {
-    if constexpr (B < E) {
-        f(std::integral_constant<int, B>{});
-        static_for<B + 1, E>(f);
-    }
+    if constexpr (B < E) static_for_seq<B>(f, std::make_integer_sequence<int, E - B>{});
 }
 
 #define IX(a, b, c) (std::integral_constant<int, kTab.idx3[a][b][c]>::value)
