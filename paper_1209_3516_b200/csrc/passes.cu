@@ -289,6 +289,45 @@ __global__ void l2p_kernel(int p, int64_t b0, int64_t n, const int32_t *__restri
     }
 }
 
+// P2M for p <= 5: a thread per leaf walks its bodies; per body the scaled
+// powers u_d^a / a! once, then every moment an FMA with constant indices.
+template <int P>
+__global__ void __launch_bounds__(128) p2m_leaf_kernel(const int32_t *__restrict__ cells, int32_t ncells,
+                                                       const uint8_t *__restrict__ leaf,
+                                                       const int32_t *__restrict__ start,
+                                                       const int32_t *__restrict__ end, const double *__restrict__ ctr,
+                                                       const double *__restrict__ xs, const double *__restrict__ ys,
+                                                       const double *__restrict__ zs, const double *__restrict__ qs,
+                                                       double *M) {
+    constexpr int NC = ncoef(P);
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ncells; i += gridDim.x * blockDim.x) {
+        const int32_t c = cells[i];
+        if (!leaf[c]) continue;
+        const double cc[3] = {ctr[c * 3], ctr[c * 3 + 1], ctr[c * 3 + 2]};
+        double acc[NC];
+#pragma unroll
+        for (int m = 0; m < NC; m++) acc[m] = 0.0;
+        for (int32_t j = start[c]; j < end[c]; j++) {
+            const double u[3] = {xs[j] - cc[0], ys[j] - cc[1], zs[j] - cc[2]};
+            const double q = qs[j];
+            double pw[3][P];
+#pragma unroll
+            for (int d = 0; d < 3; d++) {
+                pw[d][0] = 1.0;
+#pragma unroll
+                for (int a = 1; a < P; a++) pw[d][a] = pw[d][a - 1] * u[d] * (1.0 / a);
+            }
+            static_for<0, NC>([&](auto Im) {
+                constexpr int m = decltype(Im)::value;
+                constexpr int a = kTab.mi[m][0], b = kTab.mi[m][1], g = kTab.mi[m][2];
+                acc[m] = fma(q, pw[0][a] * (pw[1][b] * pw[2][g]), acc[m]);
+            });
+        }
+#pragma unroll
+        for (int m = 0; m < NC; m++) M[(int64_t)c * NC + m] = acc[m];
+    }
+}
+
 // L2P for p <= 5 with compile-time multi-indices: the body's powers
 // u_d^a and their derivatives a u_d^(a-1) are built once, every term of
 // phi = sum L_k u^k and of its gradient is an FMA with constant indices.
@@ -347,7 +386,18 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
     cudaStream_t s = as_stream(stream);
     const int nc = ncoef(p);
     const int32_t total = host_level_off[nlev];
-    if (total > 0) {
+    if (total > 0 && p <= 5) {
+        const int g = grid_for(total, 128);
+        switch (p) {
+#define P2M_LEAF(PP)                                                                                                \
+    case PP:                                                                                                        \
+        p2m_leaf_kernel<PP><<<g, 128, 0, s>>>(cells_by_level, total, leaf, start, end, ctr, xs, ys, zs, qs, M); \
+        break;
+            P2M_LEAF(1) P2M_LEAF(2) P2M_LEAF(3) P2M_LEAF(4) P2M_LEAF(5)
+#undef P2M_LEAF
+        }
+        fmm::note_launch();
+    } else if (total > 0) {
         const int g = grid_for(total, kP2MWarps, 148 * 16);
         const int ns = (nc + 31) / 32;
         if (ns <= 1)

@@ -1,8 +1,10 @@
-"""Rows whose ids span several 32768-id bitmap windows (the adaptive C3
-trees): the sparse row sort (csrc/rowsort.cuh ``warp_bitmap_sort_sparse``,
-M2L/M2P CSR and ``Lists.p2p_src``) and the wide P2P plan rows
-(csrc/plan.cu ``plan_rows_wide_kernel``) against independent torch / numpy
-computations.  The golden cases are too small to reach these paths."""
+"""Rows whose ids span several bitmap windows (16384 ids per pass; the
+adaptive C3 trees) and rows longer than the plan's 512-source staging (the
+per-pass gather path; theta = 0.3 at C4 density): the sparse row sort
+(csrc/rowsort.cuh ``warp_bitmap_sort_sparse``, M2L/M2P CSR and
+``Lists.p2p_src``) and the P2P plan rows (csrc/plan.cu ``plan_rows_kernel``:
+``plan_row_staged`` and the gather passes) against independent torch /
+numpy computations.  The golden cases are too small to reach these paths."""
 import numpy as np
 import pytest
 import torch
@@ -42,19 +44,29 @@ def test_sparse_row_sort_matches_torch():
     assert torch.equal(rows[1:] - rows[:-1], counts)
 
 
-@pytest.fixture(scope="module")
-def plummer_tree():
-    gen, _, solver = workloads.CONFIGS["C3"]
-    pos, q = gen(1 << 21, 0)
+@pytest.fixture(scope="module", params=["plummer_2e21", "uniform_2e18_theta0.3"])
+def plummer_tree(request):
+    if request.param == "plummer_2e21":
+        gen, _, solver = workloads.CONFIGS["C3"]
+        pos, q = gen(1 << 21, 0)
+        theta = solver["theta"]
+    else:
+        gen, _, solver = workloads.CONFIGS["C4"]
+        pos, q = gen(1 << 18, 0)
+        theta = 0.3
     d = torch.as_tensor(pos, device="cuda")
     ps = fb.ParticleSet(d[:, 0].contiguous(), d[:, 1].contiguous(), d[:, 2].contiguous(),
                         torch.as_tensor(q, device="cuda"))
     tree = fb.build_tree(ps, ncrit=solver["ncrit"])
-    return tree, fb.interaction_lists(tree, fb.MacConfig("fmm", solver["theta"]))
+    return request.param, tree, fb.interaction_lists(tree, fb.MacConfig("fmm", theta))
+
+
+def cnt_max(rows):
+    return (rows[1:] - rows[:-1]).max()
 
 
 def test_wide_plan_rows_match_numpy(plummer_tree):
-    tree, lists = plummer_tree
+    name, tree, lists = plummer_tree
     lists.settle()
     leaf = tree.d_leaf.cpu().numpy().astype(bool)
     start, end = tree.d_start.cpu().numpy(), tree.d_end.cpu().numpy()
@@ -64,8 +76,10 @@ def test_wide_plan_rows_match_numpy(plummer_tree):
     src = lists.p2p_src[:rows[-1]].cpu().numpy()
     spans = [(ordinal[src[rows[c]:rows[c + 1]]].max() - ordinal[src[rows[c]:rows[c + 1]]].min())
              for c in np.nonzero(rows[1:] > rows[:-1])[0]]
-    if max(spans) < 32768:
-        pytest.skip("no row spans several bitmap windows at this size")
+    if name.startswith("plummer"):
+        assert max(spans) >= 16384  # rows spanning several bitmap windows
+    else:
+        assert int(cnt_max(rows)) > 512  # rows past the staged size
     # expected runs, vectorised: an entry opens a run at a row start, at the
     # self leaf, right after it, or where the ordinals stop being consecutive
     cnt = rows[1:] - rows[:-1]
