@@ -43,6 +43,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import os
+import threading
 from dataclasses import dataclass, field
 
 import torch
@@ -739,6 +740,27 @@ class ChunkedLists:
         return np.concatenate(tt), np.concatenate(ss)
 
 
+class _EventPool:
+    """Timing events of one evaluation, reused across evaluations of the
+    calling thread (an evaluation synchronises before it returns, so its
+    events are free again): creating ~10-20 CUDA events per step costs host
+    time while the GPU waits for the first launch."""
+
+    _pools = threading.local()
+
+    def __init__(self, dev):
+        key = torch.device(dev).index or 0
+        pools = self._pools.__dict__.setdefault("by_dev", {})
+        self.events = pools.setdefault(key, [])
+        self.i = 0
+
+    def __call__(self) -> torch.cuda.Event:
+        if self.i == len(self.events):
+            self.events.append(torch.cuda.Event(enable_timing=True))
+        self.i += 1
+        return self.events[self.i - 1]
+
+
 def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
                        trace: bool = False, target_mask: torch.Tensor | None = None) -> EvalReport:
     """Simultaneous traversal of the tree against itself, on the GPU.
@@ -781,25 +803,30 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
         pst = _side_stream(dev, 1)
-        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-        e0, e_up0, e_up1, e_down0, e_down1, e_l1, e_pend, e_end = (E() for _ in range(8))
+        ust = _side_stream(dev, 3)  # the upward pass: launched after the first lists
+        E = _EventPool(dev)
+        e0, e_alloc, e_up0, e_up1, e_down0, e_down1, e_l1, e_pend, e_end = (E() for _ in range(9))
         need_up = src._M is None or src.p != p
         nc = ncoef(p)
-        # every buffer the other streams touch is allocated here, on main;
-        # the expansions and the flag share one fill: [M (if rebuilt) | L | flag]
-        nm = src.ncells * nc if need_up else 0
-        nl = tree.ncells * nc
-        buf = torch.zeros(nm + nl + 1, dtype=torch.float64, device=dev)
-        M = buf[:nm].view(src.ncells, nc) if need_up else src._M
-        L = buf[nm:nm + nl].view(tree.ncells, nc)
-        flag = buf[-1:].view(torch.int32)[:1]
-        far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
-        bodies = CrossBodies(tree, src) if cross else None
+        # the traversal starts first (it needs no buffers); the far-field and
+        # accumulator buffers are allocated on main while it runs, and the
+        # other streams wait for them (e_alloc)
         e0.record(main)
-        side.wait_event(e0)
-        pst.wait_event(e0)
-        ust = _side_stream(dev, 3)  # the upward pass: launched after the first lists
-        ust.wait_event(e0)
+
+        def allocate():
+            # the expansions and the flag share one fill: [M (if rebuilt) | L | flag]
+            nm = src.ncells * nc if need_up else 0
+            nl = tree.ncells * nc
+            buf = torch.zeros(nm + nl + 1, dtype=torch.float64, device=dev)
+            M = buf[:nm].view(src.ncells, nc) if need_up else src._M
+            L = buf[nm:nm + nl].view(tree.ncells, nc)
+            flag = buf[-1:].view(torch.int32)[:1]
+            far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
+            bodies = CrossBodies(tree, src) if cross else None
+            e_alloc.record(main)
+            for st_ in (side, pst, ust):
+                st_.wait_event(e_alloc)
+            return M, L, flag, far, bodies
 
         def launch_upward():
             # after the traversal's launches, so its host cost is off the
@@ -813,8 +840,6 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             _attach_locals(tree, p, L)
             side.wait_event(e_up1)
 
-        src._M, src.p = (M, p) if need_up else (src._M, src.p)
-        _attach_locals(tree, p, L)
         cuts = _chunk_cuts(tree, 1 if cfg.mutual else _nchunks(tree))
         nch = len(cuts) - 1
         # the lists gate P2P, so they build on a high-priority stream: the
@@ -835,6 +860,9 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                                               m2l_owner_only=nch > 1, src=src, target_mask=target_mask)
             parts.append(lists)
             if k == 0:
+                M, L, flag, far, bodies = allocate()
+                src._M, src.p = (M, p) if need_up else (src._M, src.p)
+                _attach_locals(tree, p, L)
                 launch_upward()
             with torch.cuda.stream(side):  # M2L rows of this chunk: after upward and its sorted list
                 ea, eb = E(), E()
