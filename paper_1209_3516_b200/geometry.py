@@ -143,11 +143,15 @@ class ParticleSet:
 
     @property
     def n(self) -> int:
+        # (a host float32 cloud must not be read through self.x here: that
+        # materialises its float64 view, ~1 ms of conversions at 2^20 bodies)
+        if "_n" in self.__dict__:
+            return self.__dict__["_n"]
         return int(self.x.shape[0])
 
     @property
     def on_device(self) -> bool:
-        return _is_torch(self.x)
+        return self._raw is None and self._f64 is None
 
     def positions(self) -> np.ndarray:
         return np.column_stack([_np(self.x), _np(self.y), _np(self.z)])
