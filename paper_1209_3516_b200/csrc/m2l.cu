@@ -12,7 +12,9 @@
 //    source moments stream through, P <= 4 keeps them in registers too),
 //    every multi-index resolves at compile time; the 32 partial sums are
 //    folded with shuffles at row end and added once to L_t.
-//  * m2l_lanes<P> (8 <= P <= 12): one block per target row, one WARP per
+//  * m2l_smem<8>: lane per pair with D in a thread-private shared-memory
+//    row and the outputs in two register passes (below).
+//  * m2l_lanes<P> (9 <= P <= 12): one block per target row, one WARP per
 //    pair; lanes split each degree of the D recurrence (a shared-memory
 //    recipe per entry), then own output coefficients and walk contiguous
 //    (|m|, m_x) term rows -- see below.
@@ -21,6 +23,7 @@
 #ifndef FMM_M2L_VEC
 #define FMM_M2L_VEC 1
 #endif
+
 
 
 namespace fmm {
@@ -157,6 +160,76 @@ __global__ void __launch_bounds__(128, FMM_M2L_REG5_MINB) m2l_reg5(int32_t ncell
                                                                   const double *__restrict__ cs,
                                                                   const double *__restrict__ M, double *L) {
     m2l_reg_body<5>(ncells, rows, src, ctr, cs, M, L);
+}
+
+// ---- p >= 8: lane per pair, D in shared memory, outputs in G passes -------
+// The register kernel's per-lane state (D and every output's sum) outgrows
+// the register file from p = 8.  Here each lane keeps its pair's D in a
+// thread-private shared-memory row (odd stride: conflict-free) and the
+// target row is swept G times, each pass owning one slice of the outputs
+// in registers and recomputing D per pair (the recurrence is ~1/5 of the
+// contraction's work at p = 10).
+__host__ __device__ constexpr int m2l_smem_groups(int P) { return (ncoef(P) + 59) / 60; }  // 60 outputs per pass
+__host__ __device__ constexpr int m2l_smem_stride(int P) { return ncoef(P) | 1; }
+constexpr int kM2LSmemThreads = 64;
+
+template <int P, int N0, int N1, int M>
+__host__ __device__ constexpr bool m2l_group_uses(void) {
+    for (int n = N0; n < N1; n++)
+        if (kTab.deg[n] + kTab.deg[M] <= P - 1) return true;
+    return false;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kM2LSmemThreads) m2l_smem(int32_t ncells, const int64_t *__restrict__ rows,
+                                                            const int32_t *__restrict__ src,
+                                                            const double *__restrict__ ctr,
+                                                            const double *__restrict__ cs,
+                                                            const double *__restrict__ M, double *L) {
+    constexpr int NC = ncoef(P), S = m2l_smem_stride(P), G = m2l_smem_groups(P);
+    extern __shared__ double dsm[];
+    double *D = dsm + threadIdx.x * S;
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ncells; t += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t k0 = rows[t], k1 = rows[t + 1];
+        if (k0 == k1) continue;
+        const double cx = ctr[t * 3], cy = ctr[t * 3 + 1], cz = ctr[t * 3 + 2];
+        static_for<0, G>([&](auto Ig) {
+            constexpr int g = decltype(Ig)::value;
+            constexpr int n0 = g * NC / G, n1 = (g + 1) * NC / G;
+            double acc[n1 - n0];
+#pragma unroll
+            for (int i = 0; i < n1 - n0; i++) acc[i] = 0.0;
+            for (int64_t k = k0 + lane; k < k1; k += 32) {
+                const int32_t s = src[k];
+                d_tensors_ptr<P>(cx - cs[s * 3], cy - cs[s * 3 + 1], cz - cs[s * 3 + 2], D);
+                const double *Mrow = M + (int64_t)s * NC;
+                static_for<0, NC>([&](auto Im) {
+                    constexpr int m = decltype(Im)::value;
+                    if constexpr (m2l_group_uses<P, n0, n1, m>()) {
+                        const double mm = (kTab.deg[m] & 1) ? -__ldg(&Mrow[m]) : __ldg(&Mrow[m]);
+                        static_for<n0, n1>([&](auto In) {
+                            constexpr int n = decltype(In)::value;
+                            if constexpr (kTab.deg[n] + kTab.deg[m] <= P - 1) {
+                                constexpr int j = kTab.idx3[kTab.mi[n][0] + kTab.mi[m][0]]
+                                                           [kTab.mi[n][1] + kTab.mi[m][1]]
+                                                           [kTab.mi[n][2] + kTab.mi[m][2]];
+                                acc[n - n0] = fma(mm, D[j], acc[n - n0]);
+                            }
+                        });
+                    }
+                });
+            }
+            static_for<n0, n1>([&](auto In) {
+                constexpr int n = decltype(In)::value;
+                double v = acc[n - n0];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                constexpr double inv = 1.0 / kTab.mfact[n];
+                if (lane == 0) L[(int64_t)t * NC + n] += v * inv;
+            });
+        });
+    }
 }
 
 // ---- high orders (P >= 6): lanes own outputs ------------------------------
@@ -344,7 +417,18 @@ extern "C" int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int
         m2l_lanes<PP><<<grid_for(ncells, 1, 148 * 8), m2l_warps(PP) * 32, 0, s>>>(ncells, rows, src, ctr, ctr_src, M, L); \
         fmm::note_launch();                                                                           \
         break;
-        M2L_LANES(8)
+        // p = 8: lane per pair with D in shared memory, two output passes
+        // (C4 theta = 0.4: 18.4 -> 7.9 ms against m2l_lanes); at p = 10 the
+        // per-pass D recurrences cost more than they save (36.6 -> 60-91 ms
+        // for 4-9 passes), so p >= 9 stays on m2l_lanes
+        case 8: {
+            const int shm = kM2LSmemThreads * m2l_smem_stride(8) * (int)sizeof(double);
+            cudaFuncSetAttribute(m2l_smem<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm);
+            m2l_smem<8><<<grid_for((int64_t)ncells * 32, kM2LSmemThreads, 148 * 16), kM2LSmemThreads, shm, s>>>(
+                ncells, rows, src, ctr, ctr_src, M, L);
+            fmm::note_launch();
+            break;
+        }
         M2L_LANES(9)
         M2L_LANES(10)
         M2L_LANES(11)

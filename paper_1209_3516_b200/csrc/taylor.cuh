@@ -60,4 +60,41 @@ __device__ __forceinline__ void d_tensors_reg(T rx, T ry, T rz, T (&D)[ncoef(P)]
     });
 }
 
+// The same recurrence into a thread-private array in shared memory (orders
+// whose D does not fit the register file).
+template <int P>
+__device__ __forceinline__ void d_tensors_ptr(double rx, double ry, double rz, double *D) {
+    const double r2 = rx * rx + ry * ry + rz * rz;
+    const double inv_r2 = 1.0 / r2;
+    D[0] = sqrt(inv_r2);
+    static_for<1, ncoef(P)>([&](auto I) {
+        constexpr int idx = decltype(I)::value;
+        constexpr int kx = kTab.mi[idx][0], ky = kTab.mi[idx][1], kz = kTab.mi[idx][2];
+        double acc = 0.0;
+        if constexpr (kx > 0) {
+            acc -= (2.0 * kx - 1.0) * rx * D[IX(kx - 1, ky, kz)];
+            if constexpr (kx > 1) acc -= ((kx - 1.0) * (kx - 1.0)) * D[IX(kx - 2, ky, kz)];
+            if constexpr (ky > 0) {
+                acc -= (2.0 * ky) * ry * D[IX(kx, ky - 1, kz)];
+                if constexpr (ky > 1) acc -= (ky * (ky - 1.0)) * D[IX(kx, ky - 2, kz)];
+            }
+            if constexpr (kz > 0) {
+                acc -= (2.0 * kz) * rz * D[IX(kx, ky, kz - 1)];
+                if constexpr (kz > 1) acc -= (kz * (kz - 1.0)) * D[IX(kx, ky, kz - 2)];
+            }
+        } else if constexpr (ky > 0) {
+            acc -= (2.0 * ky - 1.0) * ry * D[IX(kx, ky - 1, kz)];
+            if constexpr (ky > 1) acc -= ((ky - 1.0) * (ky - 1.0)) * D[IX(kx, ky - 2, kz)];
+            if constexpr (kz > 0) {
+                acc -= (2.0 * kz) * rz * D[IX(kx, ky, kz - 1)];
+                if constexpr (kz > 1) acc -= (kz * (kz - 1.0)) * D[IX(kx, ky, kz - 2)];
+            }
+        } else {
+            acc -= (2.0 * kz - 1.0) * rz * D[IX(kx, ky, kz - 1)];
+            if constexpr (kz > 1) acc -= ((kz - 1.0) * (kz - 1.0)) * D[IX(kx, ky, kz - 2)];
+        }
+        D[idx] = acc * inv_r2;
+    });
+}
+
 }  // namespace fmm
