@@ -24,6 +24,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--precision", default="fp32")
+ap.add_argument("--dump", default="", help="save the P2P outputs (torch.save) for a bitwise A/B")
 args = ap.parse_args()
 gen, n, solver = workloads.CONFIGS[args.config]
 n = args.n or n
@@ -50,6 +51,8 @@ for _ in range(args.reps):
     e1.synchronize()
     times.append(e0.elapsed_time(e1) * 1e-3)
 got = [tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz]
+if args.dump:
+    torch.save([g.cpu() for g in got], args.dump)
 rel = [float(torch.linalg.norm(g - r) / torch.linalg.norm(r)) for g, r in zip(got, ref)]
 t = float(np.median(times))
 print(json.dumps({"config": args.config, "n": n, "precision": args.precision, "p2p_pairs": pairs,
