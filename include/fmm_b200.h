@@ -319,6 +319,21 @@ FMM_API int fmm_p2p_plan(int32_t ncells, const uint8_t *leaf, const int32_t *sta
 FMM_API int fmm_m2l_csr(int p, int32_t ncells, const int64_t *rows, const int32_t *src, const double *ctr,
                 const double *ctr_src, const double *M, double *L, void *stream);
 
+/* The same M2L (same tree, cubic cells, geometric centres), evaluated by
+ * offset group on the FP64 tensor pipe: pairs sharing (level_t, level_s,
+ * lattice offset) share one D tensor, targets are batched 8 per CTA, and
+ * each group is one block-triangular matrix product (mma.m8n8k4.f64) over
+ * the batch's source moments.  rows/src: the M2L CSR (any order within a
+ * row; rows[ncells] is the pair count, read on the device), cap_pairs >=
+ * that count (the src buffer's size); level/cell_key: the tree's cell
+ * arrays; root: the device root record (root[3] = root size).  Results are
+ * deterministic (a radix sort fixes the order) and equal fmm_m2l_csr's to
+ * float64 rounding.  6 <= p <= 10.  ws: fmm_m2l_grouped_bytes. */
+FMM_API int fmm_m2l_grouped_bytes(int p, int32_t ncells, int64_t cap_pairs, size_t *host_bytes);
+FMM_API int fmm_m2l_grouped(int p, int32_t ncells, const int64_t *rows, const int32_t *src, int64_t cap_pairs,
+                    const int8_t *level, const uint64_t *cell_key, const double *ctr, const double *root,
+                    const double *M, double *L, void *ws, size_t ws_bytes, void *stream);
+
 /* Treecode far field (replaces _exec_m2p, src/traversal.py:520-528 ->
  * _m2p, src/_taylor.py:272-307): for every target leaf row t of the CSR M2P
  * list and every body j of t, phi[j] += sum (-1)^|m| M_m D_m(x_j - c_s) and

@@ -59,6 +59,8 @@ SIGNATURES = {
                      SZ, P],
     "fmm_sort_rows": [I32, P, P, P, P, SZ, P],
     "fmm_m2l_csr": [INT, I32, P, P, P, P, P, P, P],
+    "fmm_m2l_grouped_bytes": [INT, I32, I64, P],
+    "fmm_m2l_grouped": [INT, I32, P, P, I64, P, P, P, P, P, P, P, SZ, P],
     "fmm_m2p_csr": [INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_pack_bodies_f64": [I64, P, P, P, P, P, P],

@@ -17,6 +17,7 @@
 // (q*rinv), FADD (phi), 2 FMUL (q*rinv^3), 3 FFMA (force) = 13 FP32-pipe
 // instructions + 1 SFU; 20 flops under the reference's cost model.  The
 // guarded variant (i != j, r2 > 0) is used only for the self run.
+#include "bulk.cuh"
 #include "fmm_common.cuh"
 
 namespace fmm {
@@ -328,33 +329,6 @@ constexpr int kMaxRuns = 512;
 constexpr int kSPL = FMM_P2P_SPL;          // sources per lane per chunk
 constexpr int kWStages = FMM_P2P_WSTAGES;  // chunks in flight per warp
 constexpr int kChunk = 32 * kSPL;          // sources per chunk
-
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
 
 // Lane 0's cursor into the run table: run r starts at sequence position rpos.
 struct RunCursor {

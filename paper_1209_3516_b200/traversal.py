@@ -467,12 +467,36 @@ def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp
                 runs=runs, dev_stats=stats3[:2], dev_runs_needed=stats3[2:])
 
 
+# Orders from which M2L runs offset-grouped on the FP64 tensor pipe
+# (fmm_m2l_grouped: one D per (level_t, level_s, lattice offset), 8 targets
+# per CTA, mma.m8n8k4.f64); it needs lattice centres (cubic, geometric) and
+# one tree.  FMM_B200_M2L_GROUPED_MIN_P=99 keeps the per-pair kernels.
+M2L_GROUPED_MIN_P = int(os.environ.get("FMM_B200_M2L_GROUPED_MIN_P", "8"))
+M2L_GROUPED_MAX_P = 10
+
+
+def m2l_grouped(tree: Tree, p: int, src: Tree | None = None) -> bool:
+    """Whether ``run_m2l`` takes the offset-grouped tensor-pipe kernel."""
+    cross = src is not None and src is not tree
+    return (not cross and tree.shape == "cubic" and tree.center_mode == "geometric"
+            and M2L_GROUPED_MIN_P <= p <= M2L_GROUPED_MAX_P)
+
+
 def run_m2l(tree: Tree, lists: Lists, p: int, src: Tree | None = None) -> None:
     """M2L over the target CSR into ``tree``'s locals; the multipoles and
     centres are ``src``'s when it is a separate source tree
     (src/traversal.py:500-517 with ``MA``/``ctrB`` of the source)."""
     P = _lib.ptr
     cross = src is not None and src is not tree
+    if m2l_grouped(tree, p, src):
+        cap = lists.m2l_src.numel()
+        need = C.c_size_t(0)
+        _lib.call("fmm_m2l_grouped_bytes", p, tree.ncells, cap, C.byref(need))
+        ws = torch.empty(int(need.value), dtype=torch.uint8, device=tree.device)  # on the current (M2L) stream
+        _lib.call("fmm_m2l_grouped", p, tree.ncells, P(lists.m2l_rows), P(lists.m2l_src), cap, P(tree.d_level),
+                  P(tree.d_key), P(tree.d_ctr), P(tree.d_root), P(tree._M), P(tree._L), P(ws), ws.numel(),
+                  _lib.stream_handle())
+        return
     _lib.call("fmm_m2l_csr", p, tree.ncells, P(lists.m2l_rows), P(lists.m2l_src), P(tree.d_ctr),
               P(src.d_ctr) if cross else None, P(src._M if cross else tree._M), P(tree._L), _lib.stream_handle())
 

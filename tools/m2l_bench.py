@@ -23,6 +23,7 @@ ap.add_argument("--config", default="C3")
 ap.add_argument("--p", type=int, default=0)
 ap.add_argument("--theta", type=float, default=0.0)
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--mode", default="both", choices=["both", "pairs", "grouped"])
 args = ap.parse_args()
 gen, n, solver = workloads.CONFIGS[args.config]
 p = args.p or solver["p"]
@@ -37,26 +38,33 @@ lists = fb.interaction_lists(tree, fb.MacConfig("fmm", theta))
 nm2l = lists.n_m2l
 tree._L = torch.zeros((tree.ncells, ncoef(p)), dtype=torch.float64, device="cuda")
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-ts = []
-for r in range(args.reps + 1):
-    tree._L.zero_()
-    flush.fill_(1.0)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    run_m2l(tree, lists, p)
-    e1.record()
-    e1.synchronize()
-    if r:
-        ts.append(e0.elapsed_time(e1))
-L = tree._L.double().cpu().numpy()
-ref_path = f"/tmp/m2l_ref_{args.config}_{p}_{theta}.npy"
-if os.environ.get("FMM_B200_LIB"):
-    ref = np.load(ref_path) if os.path.exists(ref_path) else None
-else:
-    np.save(ref_path, L)
-    ref = L
-rel = None if ref is None else float(np.linalg.norm(L - ref) / np.linalg.norm(ref))
-ms = float(np.median(ts))
-print(json.dumps({"config": args.config, "p": p, "theta": theta, "m2l_calls": nm2l, "ms": ms,
-                  "calls_per_s": nm2l / ms * 1e3, "rel_l2_vs_default": rel,
+from paper_1209_3516_b200 import traversal as trv  # noqa: E402
+
+
+def timed(min_p):
+    trv.M2L_GROUPED_MIN_P = min_p
+    ts = []
+    for r in range(args.reps + 1):
+        tree._L.zero_()
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_m2l(tree, lists, p)
+        e1.record()
+        e1.synchronize()
+        if r:
+            ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts)), tree._L.double().cpu().numpy()
+
+
+modes = {"pairs": 99, "grouped": 6} if args.mode == "both" else {args.mode: 99 if args.mode == "pairs" else 6}
+out = {}
+base = None
+for name, mp in modes.items():
+    ms, L = timed(mp)
+    if base is None:
+        base = L
+    rel = float(np.linalg.norm(L - base) / np.linalg.norm(base))
+    out[name] = {"ms": ms, "calls_per_s": nm2l / ms * 1e3, "rel_l2_vs_first": rel}
+print(json.dumps({"config": args.config, "p": p, "theta": theta, "m2l_calls": nm2l, **out,
                   "lib": os.environ.get("FMM_B200_LIB", "default")}))
