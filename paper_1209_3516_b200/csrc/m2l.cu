@@ -400,9 +400,9 @@ __global__ void __launch_bounds__(kM2LWarps * 32) m2l_lanes(int32_t ncells, cons
 // (level_t, level_s, o)).  Pairs that share (level_t, level_s, o) share D,
 // so the contraction L_n += sum_m T_nm M_m with T_nm = (-1)^|m| D_{n+m}
 // becomes a matrix product once targets are batched: a CTA owns a BATCH of
-// up to 8 target cells of one level with the same octant at their last two
-// levels (their lists are near-translates: 62 % of the 8 columns filled at
-// C4), walks the union of their groups in key order and, per group, applies
+// up to 8 target cells of one level at the same octant of Morton-consecutive
+// parents (their lists are near-translates: 72 % of the 8 columns filled
+// at C4), walks the union of their groups in key order and, per group, applies
 // the (NC x NC, block-triangular) T to the 8 source moment columns with
 // mma.m8n8k4.f64 (tile (n-tile i, m-tile j) is needed iff deg(8i) + deg(4j)
 // <= p-1: 197 DMMAs per group at p = 10, 79 % of their MACs useful).
@@ -743,9 +743,10 @@ __device__ __forceinline__ uint32_t mg_hash(uint64_t k) {
     return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> (64 - kMgHashBits));
 }
 
-// batch order of the target cells: (level, octant digits of the last two
-// levels, the remaining key) -- cells of one level, one relative position
-// in their grandparent, Morton-near grandparents
+// batch order of the target cells: (level, octant in the parent, the
+// parent's key) -- cells of one level at one relative position in Morton-
+// consecutive parents, whose lists are near-translates (C4 theta = 0.3: 72 %
+// of the batch columns filled; the octant of the last two levels: 62 %)
 __global__ void mg_cell_keys(int32_t ncells, const int64_t *__restrict__ rows, const int8_t *__restrict__ level,
                              const uint64_t *__restrict__ ckey, uint64_t *out, int32_t *iota) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
@@ -756,10 +757,10 @@ __global__ void mg_cell_keys(int32_t ncells, const int64_t *__restrict__ rows, c
         }
         const int l = level[c];
         const uint64_t k = ckey[c];
-        const uint64_t low = k & 63ull, high = k >> 6;
-        const int hb = 3 * l - 6;
-        const uint64_t h52 = hb > 52 ? high >> (hb - 52) : high;
-        out[c] = ((uint64_t)l << 58) | (low << 52) | h52;
+        const uint64_t low = k & 7ull, high = k >> 3;
+        const int hb = 3 * l - 3;
+        const uint64_t h55 = hb > 55 ? high >> (hb - 55) : high;
+        out[c] = ((uint64_t)l << 58) | (low << 55) | h55;
     }
 }
 

@@ -1,4 +1,4 @@
-"""Summarise an ncu --set full report of the P2P kernel into profiles/:
+"""Summarise an ncu --set full report of one kernel into profiles/:
 key throughput metrics, stall breakdown, and DRAM traffic per launch."""
 import csv
 import io
@@ -23,6 +23,11 @@ want = {
     "lts__t_bytes.sum": "l2_bytes",
     "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_active_pct",
+    "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "fp64_pipe_active_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wavefronts_pct",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_ld_bank_conflicts",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum": "smem_ld_wavefronts",
 }
 out = {"kernel": rows[2][h.index("Kernel Name")] if "Kernel Name" in h else ""}
 for i, name in enumerate(h):
