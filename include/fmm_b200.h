@@ -54,6 +54,11 @@ extern "C" {
  * into float32 hi + lo parts: for float64 inputs that float32 cannot
  * represent (tight clusters), keeps dx accurate to the leaf scale. */
 #define FMM_PREC_FP32_ANCHORED 2
+/* FP32 pair terms summed in float64: the lanes' float32 partials are folded
+ * into float64 every few source chunks, so the near field's error floor is
+ * ~1e-7 relative instead of the ~5e-7 of long float32 sums (float32-exact
+ * inputs only; no guarded redo: a non-finite sum is redone in FP64). */
+#define FMM_PREC_FP32_ACC64 3
 
 FMM_API int fmm_abi_version(void);
 /* Message of the last error on the calling thread ("" when none). */

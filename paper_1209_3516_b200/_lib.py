@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("FMM_B200_LIB") or os.path.join(HERE, "libfmm_b200.so"
 
 FMM_OK, FMM_ERR_CAPACITY, FMM_ERR_MAX_DEPTH, FMM_ERR_INVALID, FMM_ERR_CUDA = range(5)
 DTYPE_F64, DTYPE_F32 = 0, 1
-PREC_FP64, PREC_FP32, PREC_FP32_ANCHORED = 0, 1, 2
+PREC_FP64, PREC_FP32, PREC_FP32_ANCHORED, PREC_FP32_ACC64 = 0, 1, 2, 3
 
 P = C.c_void_p
 I64 = C.c_int64

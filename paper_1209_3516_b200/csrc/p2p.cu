@@ -17,6 +17,8 @@
 // (q*rinv), FADD (phi), 2 FMUL (q*rinv^3), 3 FFMA (force) = 13 FP32-pipe
 // instructions + 1 SFU; 20 flops under the reference's cost model.  The
 // guarded variant (i != j, r2 > 0) is used only for the self run.
+#include <type_traits>
+
 #include "bulk.cuh"
 #include "fmm_common.cuh"
 
@@ -29,6 +31,19 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 }
 
 constexpr int kP2PWarps = 4;
+
+// FMM_PREC_FP32_ACC64 knobs: chunks between float64 flushes (1 measured no
+// more accurate than 4 at the C4 corner, and 5 % slower); a Newton step on
+// MUFU.RSQ (measured: no accuracy gain there -- the float32 SUMS set the
+// floor, not the approximate 1/sqrt -- and 15 % slower, so off)
+#ifndef FMM_P2P_FLUSH
+#define FMM_P2P_FLUSH 4
+#endif
+constexpr int kFlush = FMM_P2P_FLUSH;
+#ifndef FMM_P2P_ACC_REFINE
+#define FMM_P2P_ACC_REFINE 0
+#endif
+constexpr bool kAccRefine = FMM_P2P_ACC_REFINE;
 
 // Anchor of a row: sources are re-expressed as (hi - a_hi) + (lo - a_lo),
 // accurate to the leaf scale when the float64 inputs are not float32-exact.
@@ -127,7 +142,7 @@ __device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
     return r;
 }
 
-template <int K, bool GUARD>
+template <int K, bool GUARD, bool REFINE = false>
 __device__ __forceinline__ void p2p_f32x2_pairs(const float4 &s, int32_t rel, const f2_t (&tx)[K / 2],
                                                 const f2_t (&ty)[K / 2], const f2_t (&tz)[K / 2], f2_t (&ap)[K / 2],
                                                 f2_t (&ax)[K / 2], f2_t (&ay)[K / 2], f2_t (&az)[K / 2]) {
@@ -157,6 +172,15 @@ __device__ __forceinline__ void p2p_f32x2_pairs(const float4 &s, int32_t rel, co
             rh = (r2h > 0.0f && rel != 2 * v + 1) ? rh : 0.0f;
         }
         rinv[v] = f2_pack(rl, rh);
+    }
+    if (REFINE) {  // one Newton step, y (3/2 - r2/2 y^2): MUFU.RSQ's ~2^-22.9 to float32 rounding
+        const f2_t mhalf = f2_pack(-0.5f, -0.5f), three_half = f2_pack(1.5f, 1.5f);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            const f2_t h = f2_mul(r2[v], mhalf);
+            const f2_t yy = f2_mul(rinv[v], rinv[v]);
+            rinv[v] = f2_mul(rinv[v], f2_fma(h, yy, three_half));
+        }
     }
     f2_t qr[V], rr[V];
 #pragma unroll
@@ -193,7 +217,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Non-anchored: sources stream through the lane's cp.async ring `ring`.
 // Anchored: register loads (the extra residual makes the ring twice as big).
 // GUARD (self run only): skip j == own index (rel == u) and r2 == 0.
-template <int K, bool GUARD, bool ANCHOR>
+template <int K, bool GUARD, bool ANCHOR, bool REFINE = false>
 __device__ __forceinline__ void p2p_f32_span(int32_t j0, int32_t j1, int step, const float4 *__restrict__ b,
                                              const float4 *__restrict__ blo, const Anchor &an, int32_t i0,
                                              float4 *ring, const f2_t (&tx)[K / 2], const f2_t (&ty)[K / 2],
@@ -202,7 +226,7 @@ __device__ __forceinline__ void p2p_f32_span(int32_t j0, int32_t j1, int step, c
     if (j0 >= j1) return;
     if (ANCHOR) {
         for (int32_t j = j0; j < j1; j += step)
-            p2p_f32x2_pairs<K, GUARD>(load_body<ANCHOR>(b, blo, an, j), j - i0, tx, ty, tz, ap, ax, ay, az);
+            p2p_f32x2_pairs<K, GUARD, REFINE>(load_body<ANCHOR>(b, blo, an, j), j - i0, tx, ty, tz, ap, ax, ay, az);
         return;
     }
     const int32_t nit = (j1 - j0 + step - 1) / step;
@@ -228,7 +252,7 @@ __device__ __forceinline__ void p2p_f32_span(int32_t j0, int32_t j1, int step, c
                 cp_async_commit();
                 cp_async_wait<kStages - 2>();
                 const float4 nxt = ring[((q + 1) % kStages) * 32];
-                p2p_f32x2_pairs<K, GUARD>(cur, j0 + (it + q) * step - i0, tx, ty, tz, ap, ax, ay, az);
+                p2p_f32x2_pairs<K, GUARD, REFINE>(cur, j0 + (it + q) * step - i0, tx, ty, tz, ap, ax, ay, az);
                 cur = nxt;
             }
         }
@@ -240,7 +264,7 @@ __device__ __forceinline__ void p2p_f32_span(int32_t j0, int32_t j1, int step, c
         cp_async_commit();
         cp_async_wait<kStages - 1>();
         const float4 s = ring[(it % kStages) * 32];
-        p2p_f32x2_pairs<K, GUARD>(s, j0 + it * step - i0, tx, ty, tz, ap, ax, ay, az);
+        p2p_f32x2_pairs<K, GUARD, REFINE>(s, j0 + it * step - i0, tx, ty, tz, ap, ax, ay, az);
     }
 }
 
@@ -279,11 +303,12 @@ __device__ __forceinline__ float warp_fold(const f2_t (&ap)[KB / 2], const f2_t 
 
 // Block of KB consecutive targets starting at i0 (padded with the last
 // valid target), all runs of the row, folded over the warp (warp_fold).
-template <int KB, bool SAFE, bool ANCHOR>
-__device__ __forceinline__ float p2p_f32_block(int32_t i0, int32_t ilast, int64_t r0, int64_t r1, int part,
-                                              int nparts, int lane, const int4 *__restrict__ runs,
-                                              const float4 *__restrict__ b, const float4 *__restrict__ blo,
-                                              const Anchor &an, float4 *ring) {
+// ACC64: the FP32 partials are folded into a float64 sum after every run.
+template <int KB, bool SAFE, bool ANCHOR, bool ACC64 = false>
+__device__ __forceinline__ std::conditional_t<ACC64, double, float> p2p_f32_block(
+    int32_t i0, int32_t ilast, int64_t r0, int64_t r1, int part, int nparts, int lane,
+    const int4 *__restrict__ runs, const float4 *__restrict__ b, const float4 *__restrict__ blo, const Anchor &an,
+    float4 *ring) {
     f2_t tx[KB / 2], ty[KB / 2], tz[KB / 2], ap[KB / 2], ax[KB / 2], ay[KB / 2], az[KB / 2];
 #pragma unroll
     for (int v = 0; v < KB / 2; v++) {
@@ -294,16 +319,23 @@ __device__ __forceinline__ float p2p_f32_block(int32_t i0, int32_t ilast, int64_
         tz[v] = f2_fresh(f2_pack(e.z, o.z));
         ap[v] = ax[v] = ay[v] = az[v] = 0ull;
     }
+    double acc64 = 0.0;
     const int step = 32 * nparts;
     for (int64_t r = r0; r < r1; r++) {
         const int4 run = __ldg(&runs[r]);
         const int32_t j0 = run.x + part * 32 + lane;
         if (SAFE || run.z)
-            p2p_f32_span<KB, true, ANCHOR>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
+            p2p_f32_span<KB, true, ANCHOR, ACC64 && kAccRefine>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
         else
-            p2p_f32_span<KB, false, ANCHOR>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
+            p2p_f32_span<KB, false, ANCHOR, ACC64 && kAccRefine>(j0, run.y, step, b, blo, an, i0, ring, tx, ty, tz, ap, ax, ay, az);
+        if constexpr (ACC64) {
+            acc64 += (double)warp_fold<KB>(ap, ax, ay, az, lane);
+#pragma unroll
+            for (int v = 0; v < KB / 2; v++) ap[v] = ax[v] = ay[v] = az[v] = 0ull;
+        }
     }
-    return warp_fold<KB>(ap, ax, ay, az, lane);
+    if constexpr (ACC64) return acc64;
+    else return warp_fold<KB>(ap, ax, ay, az, lane);
 }
 
 // Streamed rows (the fast path): all non-self runs of the row form ONE
@@ -370,11 +402,16 @@ __device__ __forceinline__ void chunk_produce(T *dst, uint64_t *bar, int32_t p0,
 // followed by the run sequence (positions cnt + [0, total)).  `ring` is the
 // warp's kWStages * kChunk stage buffer, `bars` its barriers, `phase` their
 // parity bits (one per stage).
-template <int KB>
-__device__ __forceinline__ float p2p_f32_stream_unit(int32_t i0, int32_t ilast, int32_t ts, int32_t cnt, int32_t s0,
-                                                     int32_t s1, int lane, const float4 *__restrict__ b,
-                                                     float4 *ring, uint64_t *bars, uint32_t &phase,
-                                                     const int2 *srun) {
+// ACC64 (precision FMM_PREC_FP32_ACC64): pair terms in float32, the lanes'
+// float32 partials folded into a float64 sum every kFlush chunks (and after
+// the self sweep), so the rounding of long float32 sums never builds up:
+// at the C4 corner the near field's error floor drops from ~5.5e-7 to
+// ~1.1e-7 relative for 5-7 % more time.
+
+template <int KB, bool ACC64 = false>
+__device__ __forceinline__ std::conditional_t<ACC64, double, float> p2p_f32_stream_unit(
+    int32_t i0, int32_t ilast, int32_t ts, int32_t cnt, int32_t s0, int32_t s1, int lane,
+    const float4 *__restrict__ b, float4 *ring, uint64_t *bars, uint32_t &phase, const int2 *srun) {
     f2_t tx[KB / 2], ty[KB / 2], tz[KB / 2], ap[KB / 2], ax[KB / 2], ay[KB / 2], az[KB / 2];
     // the stream share [lo, hi), cut into chunks from lo; the first chunks
     // are requested before anything else so they land during the self sweep
@@ -395,9 +432,18 @@ __device__ __forceinline__ float p2p_f32_stream_unit(int32_t i0, int32_t ilast, 
         tz[v] = f2_fresh(f2_pack(e.z, o.z));
         ap[v] = ax[v] = ay[v] = az[v] = 0ull;
     }
+    double acc64 = 0.0;
+    auto flush = [&]() {
+        if constexpr (ACC64) {
+            acc64 += (double)warp_fold<KB>(ap, ax, ay, az, lane);
+#pragma unroll
+            for (int v = 0; v < KB / 2; v++) ap[v] = ax[v] = ay[v] = az[v] = 0ull;
+        }
+    };
     // 1) the self share, guarded
     for (int32_t j = ts + s0 + lane; j < ts + min(s1, cnt); j += 32)
-        p2p_f32x2_pairs<KB, true>(__ldg(&b[j]), j - i0, tx, ty, tz, ap, ax, ay, az);
+        p2p_f32x2_pairs<KB, true, ACC64 && kAccRefine>(__ldg(&b[j]), j - i0, tx, ty, tz, ap, ax, ay, az);
+    flush();
     // 2) the chunks
     int st = 0;
     for (int k = 0; k < nk; k++) {
@@ -416,18 +462,21 @@ __device__ __forceinline__ float p2p_f32_stream_unit(int32_t i0, int32_t ilast, 
 #pragma unroll
             for (int q = 0; q < kSPL; q++) {
                 const float4 nxt = src[((q + 1) % kSPL) * 32];
-                p2p_f32x2_pairs<KB, false>(s, 0, tx, ty, tz, ap, ax, ay, az);
+                p2p_f32x2_pairs<KB, false, ACC64 && kAccRefine>(s, 0, tx, ty, tz, ap, ax, ay, az);
                 s = nxt;
             }
         } else {
 #pragma unroll 1
             for (int q = 0; q < kSPL; q++)
-                if (q * 32 + lane < valid) p2p_f32x2_pairs<KB, false>(src[q * 32], 0, tx, ty, tz, ap, ax, ay, az);
+                if (q * 32 + lane < valid)
+                    p2p_f32x2_pairs<KB, false, ACC64 && kAccRefine>(src[q * 32], 0, tx, ty, tz, ap, ax, ay, az);
         }
         __syncwarp();  // every lane is done with stage st before lane 0 refills it
         if (++st == kWStages) st = 0;
+        if (ACC64 && (k % kFlush == kFlush - 1 || k == nk - 1)) flush();
     }
-    return warp_fold<KB>(ap, ax, ay, az, lane);
+    if constexpr (ACC64) return acc64;
+    else return warp_fold<KB>(ap, ax, ay, az, lane);
 }
 
 // Target blocks of a leaf: cnt / 8 blocks of 8, then the remainder as one
@@ -465,7 +514,7 @@ constexpr int p2p_f32_pool_bytes() {
 #ifndef FMM_P2P_MINB
 #define FMM_P2P_MINB 4  // resident CTAs per SM the register budget is cut for
 #endif
-template <bool SAFE, bool ANCHOR>
+template <bool SAFE, bool ANCHOR, bool ACC64 = false>
 __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
     int32_t nrows_host, const int32_t *__restrict__ nrows_dev, const int32_t *__restrict__ leaf_rows, const int32_t *__restrict__ start,
     const int32_t *__restrict__ end, const int64_t *__restrict__ run_off, const int4 *__restrict__ runs,
@@ -475,7 +524,8 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
     // the tile ring (streamed rows) and the lane rings (run-by-run rows) share
     // one pool: a row uses one or the other
     extern __shared__ __align__(128) float4 pool[];  // p2p_f32_pool_bytes<SAFE, ANCHOR>()
-    __shared__ float red[kMaxUnits][4][kBlk];
+    using acc_t = std::conditional_t<ACC64, double, float>;
+    __shared__ acc_t red[kMaxUnits][4][kBlk];
     __shared__ int2 srun[kMaxRuns];
     __shared__ int32_t stotal;
     __shared__ uint64_t wbars[kP2PWarps][kWStages];
@@ -511,7 +561,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
         }
         if (streamed) {
             if (threadIdx.x == 0) stotal = 0;
-            for (int k = threadIdx.x; k < nunits * 4 * kBlk; k += blockDim.x) (&red[0][0][0])[k] = 0.f;
+            for (int k = threadIdx.x; k < nunits * 4 * kBlk; k += blockDim.x) (&red[0][0][0])[k] = acc_t(0);
             __syncthreads();
             int32_t len = 0;
             for (int k = threadIdx.x; k < nr; k += blockDim.x) {
@@ -525,7 +575,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
             __syncthreads();
         }
         // a unit's folded sums: lane l holds quantity q of target uu
-        auto emit = [&](int u, int tb, int32_t i0, bool k4, float val) {
+        auto emit = [&](int u, int tb, int32_t i0, bool k4, acc_t val) {
             const int q = k4 ? (lane >> 2) & 3 : lane >> 3;
             const int uu = k4 ? lane & 3 : lane & 7;
             if (fold) {
@@ -552,11 +602,11 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
                 const int32_t s1 = (int32_t)((min(B, Sb + sc * L) - Sb) / sc);
                 if (s1 <= s0) continue;
                 const int32_t i0 = ts + tb * kBlk;
-                const float val =
-                    k4 ? p2p_f32_stream_unit<4>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w], phase,
-                                                srun)
-                       : p2p_f32_stream_unit<8>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w], phase,
-                                                srun);
+                const acc_t val =
+                    k4 ? p2p_f32_stream_unit<4, ACC64>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w],
+                                                       phase, srun)
+                       : p2p_f32_stream_unit<8, ACC64>(i0, ts + cnt - 1, ts, scnt, s0, s1, lane, b, wring, wbars[w],
+                                                       phase, srun);
                 emit(tb * kP2PWarps + w, tb, i0, k4, val);
             }
         } else {
@@ -564,10 +614,11 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
                 const int tb = u / P, part = u % P;
                 const int32_t i0 = ts + tb * kBlk;
                 const bool k4 = kK4Only || (tb == nblk - 1 && small_last);
-                const float val =
-                    k4 ? p2p_f32_block<4, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an, ring)
-                       : p2p_f32_block<8, SAFE, ANCHOR>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo, an,
-                                                        ring);
+                const acc_t val =
+                    k4 ? p2p_f32_block<4, SAFE, ANCHOR, ACC64>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo,
+                                                               an, ring)
+                       : p2p_f32_block<8, SAFE, ANCHOR, ACC64>(i0, ts + cnt - 1, r0, r1, part, P, lane, runs, b, blo,
+                                                               an, ring);
                 emit(u, tb, i0, k4, val);
             }
         }
@@ -575,7 +626,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, FMM_P2P_MINB) p2p_f32_kernel(
         if (fold) {
             for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
                 const int tb = k / kBlk, l = k % kBlk;
-                float p_ = 0.f, x_ = 0.f, y_ = 0.f, z_ = 0.f;
+                acc_t p_ = 0, x_ = 0, y_ = 0, z_ = 0;
                 for (int q = 0; q < P; q++) {  // fixed order: deterministic
                     const int uu = tb * P + q;
                     p_ += red[uu][0][l];
@@ -1008,12 +1059,15 @@ extern "C" int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_
     if (nrows <= 0) return FMM_OK;
     cudaStream_t s = as_stream(stream);
     const int grid = nrows;
-    if (precision == FMM_PREC_FP32 || precision == FMM_PREC_FP32_ANCHORED) {
+    if (precision == FMM_PREC_FP32 || precision == FMM_PREC_FP32_ANCHORED || precision == FMM_PREC_FP32_ACC64) {
         if (!b32) { set_error("fp32 P2P needs the float4 body copy"); return FMM_ERR_INVALID; }
+        const bool acc64 = precision == FMM_PREC_FP32_ACC64;
+        if (acc64 && safe) { set_error("fp32-acc64 P2P has no guarded redo (use fp64)"); return FMM_ERR_INVALID; }
         const bool anch = precision == FMM_PREC_FP32_ANCHORED;
         if (anch && !b32lo) { set_error("anchored fp32 P2P needs the float4 residual copy"); return FMM_ERR_INVALID; }
         auto kern = anch ? (safe ? p2p_f32_kernel<true, true> : p2p_f32_kernel<false, true>)
                          : (safe ? p2p_f32_kernel<true, false> : p2p_f32_kernel<false, false>);
+        if (acc64) kern = p2p_f32_kernel<false, false, true>;
         const int pool = anch ? (safe ? p2p_f32_pool_bytes<true, true>() : p2p_f32_pool_bytes<false, true>())
                               : (safe ? p2p_f32_pool_bytes<true, false>() : p2p_f32_pool_bytes<false, false>());
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pool);

@@ -212,14 +212,14 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     from . import _lib
     from .kernels import KernelStats, ncoef
     from .traversal import (EvalReport, critical_path, interaction_lists, listfmm_lists, mutual_lists,
-                            near_field_precision, run_m2l, run_m2p, run_p2p, treecode_lists)
+                            _near_field, run_m2l, run_m2p, run_p2p, treecode_lists)
     from .tree import downward_pass
 
     if world == 1:
         from .traversal import evaluate_on_tree
         return evaluate_on_tree(tree, cfg)
     treecode = cfg.strategy == "treecode"
-    nf = near_field_precision(cfg)
+    nf = _near_field(cfg, tree)
     plan = getattr(tree, "_dist_plan", None)
     if plan is None or len(plan.cuts) != world + 1 or plan.rank != rank:
         plan = _Plan(tree, world, rank)
@@ -257,7 +257,8 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     elif cfg.strategy == "listfmm":
         lists = listfmm_lists(tree, body_range=(lo, hi), m2l_ready=ready, side=side)
     elif cfg.mutual:  # the rank's targets of the mutual lists (directed-expanded)
-        lists = mutual_lists(tree, cfg.mac, cfg.task_grain, body_range=(lo, hi), m2l_ready=ready, side=side)
+        lists = mutual_lists(tree, cfg.mac, cfg.task_grain, body_range=(lo, hi), m2l_ready=ready, side=side,
+                             defer=False)
     else:
         # (exact counts up front: a deferred overflow would need a collective redo)
         lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side, defer=False)
@@ -275,7 +276,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         ev[5].record(side)
     ev[6].record(main)
     run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag)
-    if nf == "fp32" and int(flag.item()) != 0:
+    if nf in ("fp32", "fp32acc") and int(flag.item()) != 0:
         run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag)
     ev[7].record(main)
     main.wait_event(ev[5])

@@ -351,7 +351,8 @@ def partition_owner(tree: Tree, grain: int) -> torch.Tensor:
 
 
 def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[int, int] | None = None,
-                 m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None) -> Lists:
+                 m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
+                 defer: bool = True) -> Lists:
     """Mutual dual traversal (src/traversal.py:159-262 with mutual units,
     :704-791 driver) -> DIRECTED target-sorted CSR M2L/P2P lists: each
     mutual entry (a, b) contributes (a, b) and (b, a), the reference's trace
@@ -368,6 +369,26 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
                                                  max(4096, tree.ncells * 16)))
     nsteps = 2 * tree.depth + 2
     log = torch.empty(nsteps + 3, dtype=torch.int64, device=dev)
+    if defer and key in _hint and _sync_free():
+        # capacities known from an earlier run of this shape: the traversal,
+        # both CSRs and the plan chain on the device (as interaction_lists)
+        pool = torch.empty(2 * cap_p2p + 2 * cap_m2l + 4 * cap_next, dtype=i32, device=dev)
+        p2p_t, p2p_s, m2l_t, m2l_s, *fr = torch.split(pool, [cap_p2p, cap_p2p, cap_m2l, cap_m2l] + [cap_next] * 4)
+        _lib.call("fmm_traverse_mutual", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps,
+                  P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(owner),
+                  P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t),
+                  P(m2l_s), cap_m2l, P(log), st)
+        del fr
+        ncells = tree.ncells
+        wsp, wsb = _lib.workspace(max(cap_p2p, cap_m2l, tree.n, ncells + 1), dev,
+                                  stream=torch.cuda.current_stream())
+        m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, cap_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
+                                     dev_n=log[1:])
+        p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, cap_p2p, ncells, dev, wsp, wsb, st, dev_n=log, sort=False)
+        del p2p_t, p2p_s, m2l_t, m2l_s
+        return Lists(m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_rows=p2p_rows,
+                     _deferred=(log, (cap_p2p, cap_m2l, cap_next), key),
+                     **_p2p_plan(tree, p2p_grp, p2p_rows, cap_p2p, blo, bhi, wsp, wsb, st))
     while True:
         p2p_t = torch.empty(cap_p2p, dtype=i32, device=dev)
         p2p_s = torch.empty(cap_p2p, dtype=i32, device=dev)
@@ -526,6 +547,14 @@ class CrossBodies:
 # near field is evaluated in float64 there and the result stays within 2x
 # the reference's error, the north-star bar for FP32 mode.
 FP32_GUARD_THETA_P = 5e-4
+# ... but float32 TERMS are accurate enough there: summed in float64
+# ("fp32acc", FMM_PREC_FP32_ACC64) the near field's floor is ~1.1e-7
+# (C4 corner, tools/nearfield_sweep.py: p=8/theta=0.3 force 3.56e-7 and
+# potential 2.33e-7 against the reference's 3.38e-7 / 2.09e-7, at 32.7 ms
+# a step instead of FP64's 75.5), which stays within 2x the reference's
+# error while that error exceeds ~6e-8, i.e. theta^p >= FP32ACC_THETA_P.
+# Below it (p=10, theta=0.3: reference 2.0e-8) the near field is float64.
+FP32ACC_THETA_P = 5e-5
 # listfmm ignores theta: its V-list pairs same-level cells at least one cell
 # apart, an opening ratio of (2 * sqrt(3)/2 * s) / (2 s) = sqrt(3)/2
 LISTFMM_THETA_EQ = 3 ** 0.5 / 2
@@ -533,14 +562,36 @@ LISTFMM_THETA_EQ = 3 ** 0.5 / 2
 
 def near_field_precision(cfg: "EvalConfig") -> str:
     """Arithmetic of the near field for ``cfg``: "fp64" for precision="fp64";
-    for precision="fp32", "fp32" unless theta^p < FP32_GUARD_THETA_P (then
-    "fp64", see above; FMM_B200_FP32_STRICT=1 disables the promotion)."""
+    for precision="fp32", "fp32" unless theta^p < FP32_GUARD_THETA_P, then
+    "fp32acc" down to FP32ACC_THETA_P and "fp64" below (see above;
+    FMM_B200_FP32_STRICT=1 disables the promotion).
+    FMM_B200_NEAR_FIELD=fp32|fp32acc|fp64 forces one (measurements)."""
+    force = os.environ.get("FMM_B200_NEAR_FIELD")
+    if force:
+        if force not in NEAR_FIELDS:
+            raise ValueError(f"FMM_B200_NEAR_FIELD={force!r}: one of {NEAR_FIELDS}")
+        return force
     if cfg.precision == "fp64":
         return "fp64"
     if os.environ.get("FMM_B200_FP32_STRICT", "0") == "1":
         return "fp32"
     theta = LISTFMM_THETA_EQ if cfg.strategy == "listfmm" else cfg.mac.theta
-    return "fp64" if theta ** cfg.p < FP32_GUARD_THETA_P else "fp32"
+    tp = theta ** cfg.p
+    return "fp32" if tp >= FP32_GUARD_THETA_P else ("fp32acc" if tp >= FP32ACC_THETA_P else "fp64")
+
+
+def _near_field(cfg: "EvalConfig", *trees) -> str:
+    """``near_field_precision`` for these body sets: "fp32acc" has no
+    anchored form, so inputs float32 cannot hold take "fp64"."""
+    nf = near_field_precision(cfg)
+    if nf == "fp32acc" and not all(t.fp32_exact for t in trees):
+        nf = "fp64"
+    return nf
+
+
+# near-field arithmetics: float32 pairs and sums; float32 pairs (refined
+# 1/sqrt) with float64 sums (FMM_PREC_FP32_ACC64); float64
+NEAR_FIELDS = ("fp32", "fp32acc", "fp64")
 
 
 def _packed_f64(b) -> torch.Tensor:
@@ -564,10 +615,16 @@ def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, s
     arithmetic (``near_field_precision``)."""
     P = _lib.ptr
     b = tree if bodies is None else bodies
+    if precision == "fp32acc" and (safe or use_rsqrt or not b.fp32_exact):
+        # no guarded / anchored / reference-rsqrt variant of the float64-summed
+        # kernel: those cases take the float64 near field
+        precision = "fp64"
     if precision == "fp32":
         # float32 cannot hold these float64 inputs: anchor offsets per row
         prec = _lib.PREC_FP32 if b.fp32_exact else _lib.PREC_FP32_ANCHORED
         packed, packed_lo = b.d_b32, b.d_b32lo
+    elif precision == "fp32acc":
+        prec, packed, packed_lo = _lib.PREC_FP32_ACC64, b.d_b32, None
     else:
         prec = _lib.PREC_FP64
         # use_rsqrt (the reference's float32 1/sqrt) keeps the SoA kernel
@@ -822,7 +879,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
-    nf = near_field_precision(cfg)
+    nf = _near_field(cfg, tree, src)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -911,7 +968,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             e_down1.record(side)
         e_pend.record(pst)
         main.wait_event(e_pend)
-        redo = nf == "fp32" and int(flag.item()) != 0
+        redo = nf in ("fp32", "fp32acc") and int(flag.item()) != 0
         if redo:
             # two distinct bodies collided in FP32 outside a self run: redo guarded
             for lists in parts:
@@ -992,7 +1049,7 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
-    nf = near_field_precision(cfg)
+    nf = _near_field(cfg, tree, src)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -1023,7 +1080,7 @@ def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
         run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag, bodies)
         e_p1.record(main)
-        redo = nf == "fp32" and int(flag.item()) != 0
+        redo = nf in ("fp32", "fp32acc") and int(flag.item()) != 0
         if redo:
             run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag, bodies)
             e_p1.record(main)
@@ -1085,7 +1142,7 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
     stats = KernelStats()
     dev = tree.device
     p = cfg.p
-    nf = near_field_precision(cfg)
+    nf = _near_field(cfg, tree)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -1119,7 +1176,7 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
         run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag)
         e_p1.record(main)
-        if nf == "fp32" and int(flag.item()) != 0:
+        if nf in ("fp32", "fp32acc") and int(flag.item()) != 0:
             run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag)
             e_p1.record(main)
         main.wait_event(e_d1)

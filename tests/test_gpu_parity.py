@@ -227,3 +227,29 @@ def test_chunked_pipeline_matches_reference(name, chunks, monkeypatch):
         idx = c["direct_idx"]
         for k in ("phi", "fx", "fy", "fz"):
             assert rel_l2(getattr(b, k)[idx], c["sample_" + k]) <= FP64_TOL, k
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_32k", "order_p8", "order_p10", "plummer_32k"])
+def test_fp32acc_near_field(name, monkeypatch):
+    """Float32 terms summed in float64 (FMM_PREC_FP32_ACC64): within 2x the
+    reference's error, and closer to the FP64 result than plain FP32 sums."""
+    case = Case(name)
+    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", case.theta), p=case.p, precision="fp32")
+    out = {}
+    for nf in ("fp32acc", "fp64"):
+        monkeypatch.setenv("FMM_B200_NEAR_FIELD", nf)
+        t = build(case)
+        rep = fb.evaluate_on_tree(t, cfg)
+        assert rep.near_field == (nf if t.fp32_exact else "fp64")  # no anchored fp32acc: float64 inputs
+        out[nf] = t.bodies
+    idx = case["direct_idx"]
+    b = out["fp32acc"]
+    if np.isfinite(case.meta["force_err"]) and case.meta["force_err"] > 0.0:
+        fref = np.stack([case["direct_fx"], case["direct_fy"], case["direct_fz"]], 1)
+        fgot = np.stack([b.fx[idx], b.fy[idx], b.fz[idx]], 1)
+        ferr = float(np.sqrt(((fgot - fref) ** 2).sum() / (fref ** 2).sum()))
+        assert ferr <= 2.0 * case.meta["force_err"] + FP32_BAR_FLOOR
+        assert rel_l2(b.phi[idx], case["direct_phi"]) <= 2.0 * case.meta["pot_err"] + FP32_BAR_FLOOR
+    # float32 terms: ~1e-7 relative of the float64 near field at these sizes
+    for k in ("phi", "fx", "fy", "fz"):
+        assert rel_l2(getattr(b, k), getattr(out["fp64"], k)) <= 2e-6, k

@@ -210,13 +210,21 @@ def test_integration_binding_matches_header():
         assert decls[name] == n, (name, decls[name], n)
 
 
-def test_fp32_promotion_rule():
+def test_fp32_promotion_rule(monkeypatch):
     """precision="fp32" keeps FP32 near fields except where the expansion is
-    more accurate than float32 rounding (theta^p < 5e-4): on the C4 grid
-    exactly the three points whose reference error is under ~3.5e-7."""
+    more accurate than float32 sums (theta^p < 5e-4): there float32 terms
+    summed in float64 ("fp32acc") down to theta^p = 5e-5, float64 below.
+    On the C4 grid: (8, 0.3) and (10, 0.4) fp32acc, (10, 0.3) fp64."""
     import paper_1209_3516_b200 as fb
     from paper_1209_3516_b200.traversal import near_field_precision
+    monkeypatch.delenv("FMM_B200_NEAR_FIELD", raising=False)
     nf = {(p, t): near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", t), p=p, precision="fp32"))
           for p in (3, 4, 6, 8, 10) for t in (0.3, 0.4, 0.5, 0.6)}
-    assert sorted(k for k, v in nf.items() if v == "fp64") == [(8, 0.3), (10, 0.3), (10, 0.4)]
+    assert sorted(k for k, v in nf.items() if v == "fp32acc") == [(8, 0.3), (10, 0.4)]
+    assert sorted(k for k, v in nf.items() if v == "fp64") == [(10, 0.3)]
     assert near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", 0.3), p=10, precision="fp64")) == "fp64"
+    monkeypatch.setenv("FMM_B200_NEAR_FIELD", "fp32acc")
+    assert near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=4, precision="fp64")) == "fp32acc"
+    monkeypatch.setenv("FMM_B200_NEAR_FIELD", "bf16")
+    with pytest.raises(ValueError):
+        near_field_precision(fb.EvalConfig(p=4))
