@@ -39,6 +39,33 @@ __global__ void dmma_probe(int iters, const double *in, double *sink) {
     if (s == 12345.678) sink[blockIdx.x] = s;
 }
 
+// DFMA and DMMA interleaved: do the two pipes overlap?
+template <int CH>
+__global__ void mixed_probe(int iters, const double *in, double *sink) {
+    const double m = in[0], cc = in[1];
+    double a = in[0] + threadIdx.x * 1e-9, b = in[1] - threadIdx.x * 1e-9;
+    double c[CH][2], f[16];
+#pragma unroll
+    for (int k = 0; k < CH; k++) c[k][0] = c[k][1] = k;
+#pragma unroll
+    for (int k = 0; k < 16; k++) f[k] = threadIdx.x * 1e-3 + k;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < CH; k++)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c[k][0]), "+d"(c[k][1])
+                         : "d"(a), "d"(b));
+#pragma unroll
+        for (int k = 0; k < 16; k++) f[k] = fma(f[k], m, cc);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < CH; k++) s += c[k][0] + c[k][1];
+#pragma unroll
+    for (int k = 0; k < 16; k++) s += f[k];
+    if (s == 12345.678) sink[blockIdx.x] = s;
+}
+
 template <class K>
 float timeit(K kern, int blocks, int threads, int iters, const double *in, double *sink) {
     cudaEvent_t e0, e1;
@@ -69,5 +96,14 @@ int main() {
     printf("DMMA8 %.2f TFLOP/s\n", 2.0 * 256 * 8 * it * blocks * 8.0 / (ms * 1e-3) / 1e12);
     ms = timeit(dmma_probe<2>, blocks, 256, it, in, sink);
     printf("DMMA2 %.2f TFLOP/s\n", 2.0 * 256 * 2 * it * blocks * 8.0 / (ms * 1e-3) / 1e12);
+    // per iteration: CH DMMAs (CH * 512 flops per warp) and 16 DFMAs per thread (32 flops)
+    ms = timeit(mixed_probe<2>, blocks, 256, it, in, sink);
+    printf("mixed(2 DMMA + 16 DFMA per thread-iter): total %.2f TFLOP/s (dmma part %.2f, dfma part %.2f)\n",
+           (2.0 * 256 * 2 * 8 + 2.0 * 16 * 256) * it * blocks / (ms * 1e-3) / 1e12,
+           2.0 * 256 * 2 * 8 * it * blocks / (ms * 1e-3) / 1e12, 2.0 * 16 * 256 * it * blocks / (ms * 1e-3) / 1e12);
+    ms = timeit(mixed_probe<4>, blocks, 256, it, in, sink);
+    printf("mixed(4 DMMA + 16 DFMA per thread-iter): total %.2f TFLOP/s (dmma part %.2f, dfma part %.2f)\n",
+           (2.0 * 256 * 4 * 8 + 2.0 * 16 * 256) * it * blocks / (ms * 1e-3) / 1e12,
+           2.0 * 256 * 4 * 8 * it * blocks / (ms * 1e-3) / 1e12, 2.0 * 16 * 256 * it * blocks / (ms * 1e-3) / 1e12);
     return 0;
 }
