@@ -735,94 +735,106 @@ __device__ __forceinline__ void for_split(int32_t a, int32_t b, int m, const Cel
 }
 
 // One breadth-first step of the mutual traversal.  Frontier entries are
-// UNCLASSIFIED (a, b, mut) pairs, mut in bit 31 of fb.  A mutual pair whose
-// cells have different partition owners is first demoted to the directed
-// pairs (a, b) and (b, a) (the reference's driver, src/traversal.py:727-738);
-// every pair is then classified with the unit rules (both leaves -> P2P;
-// MAC, both directions when mutual -> M2L; else split).  Emitted lists are
-// DIRECTED: a mutual entry (a, b) is written as (a, b) and, when a != b,
-// (b, a) -- the reference's trace expansion (src/traversal.py:644-650) --
-// so the directed M2L / P2P executors run them unchanged.  Only targets
-// whose bodies meet [blo, bhi) are emitted.
+// (a, b, mut) pairs that must be SPLIT (mut in bit 31 of fb); step 0 holds
+// the unclassified seed (classify_self).  Each child pair of a split is
+// first demoted when mutual and its cells have different partition owners
+// -- the directed pairs (x, y) and (y, x), the reference's driver
+// (src/traversal.py:727-738) -- and every resulting item is classified
+// with the unit rules on the spot (both leaves -> P2P; MAC, both
+// directions when mutual -> M2L; else it enters the next frontier), so
+// P2P and M2L pairs never pass through the frontier buffers (C2: 1.47 ->
+// ~0.6 ms for the 12 steps).  Emitted lists are DIRECTED: a mutual entry
+// (a, b) is written as (a, b) and, when a != b, (b, a) -- the reference's
+// trace expansion (src/traversal.py:644-650) -- so the directed M2L / P2P
+// executors run them unchanged.  Only targets whose bodies meet [blo, bhi)
+// are emitted.
 __global__ void mutual_step_kernel(const int32_t *__restrict__ fa, const int32_t *__restrict__ fb,
-                                   const unsigned long long *__restrict__ nfront_dev, int64_t cap_front, Cells C,
-                                   const int32_t *__restrict__ owner, const int32_t *__restrict__ cstart,
-                                   const int32_t *__restrict__ cend, int32_t blo, int32_t bhi, int kind_mac,
-                                   double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
-                                   int32_t *m2l_s, int64_t cap_m2l, int32_t *na, int32_t *nb, int64_t cap_next,
-                                   unsigned long long *cnt_p2p, unsigned long long *cnt_m2l,
-                                   unsigned long long *cnt_next) {
+                                   const unsigned long long *__restrict__ nfront_dev, int64_t cap_front,
+                                   int classify_self, Cells C, const int32_t *__restrict__ owner,
+                                   const int32_t *__restrict__ cstart, const int32_t *__restrict__ cend, int32_t blo,
+                                   int32_t bhi, int kind_mac, double th2, int32_t *p2p_t, int32_t *p2p_s,
+                                   int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l, int32_t *na,
+                                   int32_t *nb, int64_t cap_next, unsigned long long *cnt_p2p,
+                                   unsigned long long *cnt_m2l, unsigned long long *cnt_next) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t nfront = (int64_t)*nfront_dev;
     if (nfront > cap_front) nfront = cap_front;
     const int64_t nround = (nfront + stride - 1) / stride;
     auto keep = [&](int32_t c) { return cend[c] > blo && cstart[c] < bhi; };
+    // an item's fate: 1 P2P, 2 M2L, 3 split
+    auto fate_of = [&](int32_t x, int32_t y, int m) {
+        if (C.leaf[x] && C.leaf[y]) return 1;
+        if (mac_accept(x, y, C, C, kind_mac, th2) && (!m || mac_accept(y, x, C, C, kind_mac, th2))) return 2;
+        return 3;
+    };
+    // the items of a pair entering classification (demotion of a mutual
+    // pair across partition owners), each handed to g(x, y, m)
+    auto items = [&](int32_t x, int32_t y, int m, auto &&g) {
+        if (m && owner[x] >= 0 && owner[y] >= 0 && owner[x] != owner[y]) {
+            g(x, y, 0);
+            g(y, x, 0);
+        } else {
+            g(x, y, m);
+        }
+    };
+    auto children = [&](int32_t a, int32_t b, int m, auto &&g) {
+        if (classify_self) items(a, b, m, g);
+        else for_split(a, b, m, C, [&](int32_t x, int32_t y) { items(x, y, m, g); });
+    };
     for (int64_t r = 0; r < nround; r++) {
         const int64_t k = r * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-        int32_t ia[2], ib[2];
-        int im_[2], fate[2];
-        int nitem = 0;
-        if (k < nfront) {
-            const int32_t a = fa[k];
-            const int32_t b = fb[k] & 0x7fffffff;
-            const int m = (int)((uint32_t)fb[k] >> 31);
-            if (m && owner[a] >= 0 && owner[b] >= 0 && owner[a] != owner[b]) {
-                ia[0] = a; ib[0] = b; im_[0] = 0;
-                ia[1] = b; ib[1] = a; im_[1] = 0;
-                nitem = 2;
-            } else {
-                ia[0] = a; ib[0] = b; im_[0] = m;
-                nitem = 1;
-            }
+        int32_t a = 0, b = 0;
+        int m = 0;
+        const bool live = k < nfront;
+        if (live) {
+            a = fa[k];
+            b = fb[k] & 0x7fffffff;
+            m = (int)((uint32_t)fb[k] >> 31);
         }
-        int np = 0, nm = 0, nn = 0;
-        for (int q = 0; q < 2; q++) {
-            fate[q] = 0;
-            if (q >= nitem) continue;
-            const int32_t a = ia[q], b = ib[q];
-            const int m = im_[q];
-            if (C.leaf[a] && C.leaf[b]) {
-                fate[q] = 1;
-                np += keep(a) + (m && a != b && keep(b));
-            } else if (mac_accept(a, b, C, C, kind_mac, th2) && (!m || mac_accept(b, a, C, C, kind_mac, th2))) {
-                fate[q] = 2;
-                nm += keep(a) + (m && keep(b));
-            } else {
-                fate[q] = 3;
-                for_split(a, b, m, C, [&](int32_t x, int32_t y) { nn += keep(x) || (m && keep(y)); });
-            }
-        }
+        // the fates of the first 32 items are kept (2 bits each) for the
+        // write pass; only a mutual self split has more (36 children)
+        int np = 0, nm = 0, nn = 0, nit = 0;
+        uint64_t fbits = 0;
+        if (live)
+            children(a, b, m, [&](int32_t x, int32_t y, int mm) {
+                const int ft = fate_of(x, y, mm);
+                if (nit < 32) fbits |= (uint64_t)ft << (2 * nit);
+                nit++;
+                if (ft == 1) np += keep(x) + (mm && x != y && keep(y));
+                else if (ft == 2) nm += keep(x) + (mm && keep(y));
+                else nn += keep(x) || (mm && keep(y));
+            });
         int op, om, on;
         const unsigned long long bp = warp_reserve(cnt_p2p, np, lane, &op);
         const unsigned long long bm = warp_reserve(cnt_m2l, nm, lane, &om);
         const unsigned long long bn = warp_reserve(cnt_next, nn, lane, &on);
         unsigned long long ip = bp + op, im = bm + om, in = bn + on;
-        for (int q = 0; q < 2; q++) {
-            const int32_t a = ia[q], b = ib[q];
-            const int m = im_[q];
-            if (fate[q] == 1 || fate[q] == 2) {
-                int32_t *tt = fate[q] == 1 ? p2p_t : m2l_t, *ss = fate[q] == 1 ? p2p_s : m2l_s;
-                const unsigned long long cap = (unsigned long long)(fate[q] == 1 ? cap_p2p : cap_m2l);
-                unsigned long long &at = fate[q] == 1 ? ip : im;
-                if (keep(a)) {
-                    if (at < cap) { tt[at] = a; ss[at] = b; }
-                    at++;
-                }
-                if (m && a != b && keep(b)) {
-                    if (at < cap) { tt[at] = b; ss[at] = a; }
-                    at++;
-                }
-            } else if (fate[q] == 3) {
-                const int32_t mbit = m ? (int32_t)0x80000000u : 0;
-                for_split(a, b, m, C, [&](int32_t x, int32_t y) {
-                    if (keep(x) || (m && keep(y))) {
-                        if (in < (unsigned long long)cap_next) { na[in] = x; nb[in] = y | mbit; }
-                        in++;
+        int it = 0;
+        if (live)
+            children(a, b, m, [&](int32_t x, int32_t y, int mm) {
+                const int ft = it < 32 ? (int)((fbits >> (2 * it)) & 3u) : fate_of(x, y, mm);
+                it++;
+                if (ft == 1 || ft == 2) {
+                    int32_t *tt = ft == 1 ? p2p_t : m2l_t, *ss = ft == 1 ? p2p_s : m2l_s;
+                    const unsigned long long cap = (unsigned long long)(ft == 1 ? cap_p2p : cap_m2l);
+                    unsigned long long &at = ft == 1 ? ip : im;
+                    if (keep(x)) {
+                        if (at < cap) { tt[at] = x; ss[at] = y; }
+                        at++;
                     }
-                });
-            }
-        }
+                    if (mm && (ft == 2 || x != y) && keep(y)) {
+                        if (at < cap) { tt[at] = y; ss[at] = x; }
+                        at++;
+                    }
+                } else if (keep(x) || (mm && keep(y))) {
+                    if (in < (unsigned long long)cap_next) {
+                        na[in] = x;
+                        nb[in] = y | (mm ? (int32_t)0x80000000u : 0);
+                    }
+                    in++;
+                }
+            });
     }
 }
 
@@ -959,7 +971,8 @@ int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1,
     for (int sidx = 0; sidx < nsteps; sidx++) {
         const bool even = (sidx & 1) == 0;
         mutual_step_kernel<<<grid, 256, 0, st>>>(
-            even ? front_a0 : front_a1, even ? front_b0 : front_b1, dev_log + 2 + sidx, cap_front, C, owner, start,
+            even ? front_a0 : front_a1, even ? front_b0 : front_b1, dev_log + 2 + sidx, cap_front, sidx == 0, C,
+            owner, start,
             end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
             even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1,
             dev_log + 3 + sidx); fmm::note_launch();
