@@ -436,13 +436,28 @@ struct MG {
     static constexpr int STAGES = P >= 9 ? 3 : 4;
 };
 
-// Tile schedule of one order, evaluated once: J[i] m-tiles pair with n-tile
-// i (a prefix, deg(4j) grows with j), n-tiles go to the consumer warps by
-// LPT over J, slot[i][j] is tile (i, j)'s place in its owner's index array.
+// Tile schedule of one order, evaluated once.  The NW consumer warps form
+// an NG x KG grid: n-tiles go to the NG row groups (LPT over J[i], the
+// number of m-tiles paired with n-tile i -- a prefix, deg(4j) grows with
+// j), and within a row group the m-tiles go to its KG warps (LPT over the
+// tiles they carry).  Each B fragment (moment column j) is then loaded by
+// NG warps instead of all NW, and the KG warps of a row group sum their
+// accumulators once per batch.  slot[i][j] is tile (i, j)'s place in its
+// owner's per-lane index array.
+// KG = 2 from p = 9 (C4: p = 9 3.44 -> 3.28 ms, p = 10 8.29 -> 8.18), 1 at
+// p = 8 (4.82 against 5.28 ms); KG = 4 doubles the accumulators and drops
+// to 2 CTAs per SM (p = 10 14.2 ms).  FMM_MG_KG overrides (experiments).
+#ifdef FMM_MG_KG
+constexpr int mg_kg(int) { return FMM_MG_KG; }
+#else
+constexpr int mg_kg(int p) { return p >= 9 ? 2 : 1; }
+#endif
 template <int P>
 struct MGSched {
+    static constexpr int KG = mg_kg(P), NG = MG<P>::NW / KG;
     int J[MG<P>::NT];
-    int owner[MG<P>::NT];
+    int ng[MG<P>::NT];
+    int owner[MG<P>::NT][MG<P>::MT];
     int slot[MG<P>::NT][MG<P>::MT];
     int count[MG<P>::NW];
     bool col_used[MG<P>::NW][MG<P>::MT];
@@ -452,6 +467,7 @@ struct MGSched {
 template <int P>
 constexpr MGSched<P> make_mg_sched() {
     using G = MG<P>;
+    using S = MGSched<P>;
     MGSched<P> s{};
     for (int i = 0; i < G::NT; i++) {
         s.J[i] = 0;
@@ -459,26 +475,41 @@ constexpr MGSched<P> make_mg_sched() {
         for (int j = 0; j < G::MT; j++)
             if (dn + kTab.deg[4 * j] <= P - 1) s.J[i]++;
     }
-    int load[G::NW] = {};
+    int gload[S::NG] = {};
     for (int i = 0; i < G::NT; i++) {
-        int w = 0;
-        for (int q = 1; q < G::NW; q++)
-            if (load[q] < load[w]) w = q;
-        load[w] += s.J[i];
-        s.owner[i] = w;
+        int g = 0;
+        for (int q = 1; q < S::NG; q++)
+            if (gload[q] < gload[g]) g = q;
+        gload[g] += s.J[i];
+        s.ng[i] = g;
+    }
+    for (int i = 0; i < G::NT; i++)
+        for (int j = 0; j < G::MT; j++) s.owner[i][j] = s.slot[i][j] = -1;
+    for (int g = 0; g < S::NG; g++) {
+        int kload[S::KG] = {};
+        for (int j = 0; j < G::MT; j++) {
+            int c = 0;
+            for (int i = 0; i < G::NT; i++)
+                if (s.ng[i] == g && j < s.J[i]) c++;
+            if (!c) continue;
+            int k = 0;
+            for (int q = 1; q < S::KG; q++)
+                if (kload[q] < kload[k]) k = q;
+            kload[k] += c;
+            for (int i = 0; i < G::NT; i++)
+                if (s.ng[i] == g && j < s.J[i]) s.owner[i][j] = g * S::KG + k;
+        }
     }
     for (int w = 0; w < G::NW; w++) {
         s.count[w] = 0;
         for (int j = 0; j < G::MT; j++) s.col_used[w][j] = false;
     }
     for (int i = 0; i < G::NT; i++)
-        for (int j = 0; j < G::MT; j++) {
-            s.slot[i][j] = -1;
-            if (j < s.J[i]) {
-                s.slot[i][j] = s.count[s.owner[i]]++;
-                s.col_used[s.owner[i]][j] = true;
+        for (int j = 0; j < G::MT; j++)
+            if (s.owner[i][j] >= 0) {
+                s.slot[i][j] = s.count[s.owner[i][j]]++;
+                s.col_used[s.owner[i][j]][j] = true;
             }
-        }
     s.maxcount = 1;
     for (int w = 0; w < G::NW; w++) s.maxcount = s.count[w] > s.maxcount ? s.count[w] : s.maxcount;
     return s;
@@ -568,7 +599,7 @@ __device__ __forceinline__ void mg_consume(const double *__restrict__ sD, const 
             const double b = brow[4 * j];
             static_for<0, G::NT>([&](auto Ii) {
                 constexpr int i = decltype(Ii)::value;
-                if constexpr (kMGS<P>.owner[i] == W && j < kMGS<P>.J[i]) {
+                if constexpr (kMGS<P>.owner[i][j] == W) {
                     constexpr int sl = kMGS<P>.slot[i][j];
                     dmma884(acc[i], sD[tix[sl]], b);
                 }
@@ -579,8 +610,12 @@ __device__ __forceinline__ void mg_consume(const double *__restrict__ sD, const 
 
 template <int P>
 struct MGSmem {
+    static constexpr int KG = MGSched<P>::KG;
     double D[MG<P>::STAGES][MG<P>::DS];
-    double M[MG<P>::STAGES][8 * MG<P>::RS];
+    union {
+        double M[MG<P>::STAGES][8 * MG<P>::RS];
+        double red[KG > 1 ? KG - 1 : 1][MG<P>::NT][64];  // the batch-end sum of a row group's KG warps
+    };
     double zero[MG<P>::NCP];
     uint64_t full[MG<P>::STAGES], empty[MG<P>::STAGES];
     int rowoff[MG<P>::STAGES][8];
@@ -592,17 +627,19 @@ struct MGSmem {
 template <int P, int W>
 __device__ __forceinline__ void mg_consumer(int32_t e0, int32_t e1, MGSmem<P> &sm, double *L) {
     using G = MG<P>;
+    using S = MGSched<P>;
+    constexpr int g = W / S::KG, kq = W % S::KG;
     const int lane = threadIdx.x & 31;
     int tix[kMGS<P>.maxcount];
     static_for<0, G::NT>([&](auto Ii) {
         constexpr int i = decltype(Ii)::value;
-        if constexpr (kMGS<P>.owner[i] == W) {
-            static_for<0, kMGS<P>.J[i]>([&](auto Ij) {
-                constexpr int j = decltype(Ij)::value;
+        static_for<0, G::MT>([&](auto Ij) {
+            constexpr int j = decltype(Ij)::value;
+            if constexpr (kMGS<P>.owner[i][j] == W) {
                 constexpr int sl = kMGS<P>.slot[i][j];
                 tix[sl] = mg_tile_index<P>(i, j, lane);
-            });
-        }
+            }
+        });
     });
     double acc[G::NT][2];
 #pragma unroll
@@ -616,10 +653,35 @@ __device__ __forceinline__ void mg_consumer(int32_t e0, int32_t e1, MGSmem<P> &s
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[st]);
     }
+    if constexpr (S::KG > 1) {
+        // every group is consumed (all bulk copies landed): the stage ring
+        // is free for the row groups' fold, in a fixed order (deterministic)
+        asm volatile("bar.sync 1, %0;" ::"n"(G::NW * 32) : "memory");
+        if constexpr (kq > 0)
+            static_for<0, G::NT>([&](auto Ii) {
+                constexpr int i = decltype(Ii)::value;
+                if constexpr (kMGS<P>.ng[i] == g) {
+                    sm.red[kq - 1][i][2 * lane] = acc[i][0];
+                    sm.red[kq - 1][i][2 * lane + 1] = acc[i][1];
+                }
+            });
+        asm volatile("bar.sync 1, %0;" ::"n"(G::NW * 32) : "memory");
+        if constexpr (kq > 0) return;
+        static_for<0, G::NT>([&](auto Ii) {
+            constexpr int i = decltype(Ii)::value;
+            if constexpr (kMGS<P>.ng[i] == g) {
+#pragma unroll
+                for (int q = 0; q < S::KG - 1; q++) {
+                    acc[i][0] += sm.red[q][i][2 * lane];
+                    acc[i][1] += sm.red[q][i][2 * lane + 1];
+                }
+            }
+        });
+    }
     // C fragment: row n = 8 i + lane/4, columns (target slots) 2 (lane%4) + {0, 1}
     static_for<0, G::NT>([&](auto Ii) {
         constexpr int i = decltype(Ii)::value;
-        if constexpr (kMGS<P>.owner[i] == W) {
+        if constexpr (kMGS<P>.ng[i] == g) {
             const int n = 8 * i + (lane >> 2);
             if (n < G::NC) {
                 const double inv = 1.0 / d_tab.mfact[n];
