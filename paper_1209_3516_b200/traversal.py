@@ -205,19 +205,30 @@ class Lists:
             return self.__dict__[name]
         raise AttributeError(name)
 
-    def settle(self) -> bool:
+    def device_counters(self) -> list:
+        """The device tensors ``settle`` and the pair counters read (int64),
+        for one batched copy to the host (``EndReadback``)."""
+        out = [self.dev_stats.long(), self.dev_runs_needed.long()]
+        d = self.__dict__.get("_deferred")
+        if d is not None:
+            out.append(d[0].long())
+        return out
+
+    def settle(self, host=None) -> bool:
         """Read deferred traversal counters; False if a list overflowed (the
-        lists are then incomplete and the evaluation must be redone)."""
+        lists are then incomplete and the evaluation must be redone).
+        ``host`` holds ``device_counters()`` already copied to the host."""
         d = self.__dict__.get("_deferred")
         if d is None:
             return True
         log, caps, key = d
-        hl = log.tolist()
+        hl = host[2].tolist() if host is not None else log.tolist()
+        runs_needed = int(host[1][0]) if host is not None else int(self.__dict__["dev_runs_needed"][0])
         n_p2p, n_m2l, fronts = hl[0], hl[1], hl[2:]
         peak = max(fronts)
         self.__dict__.update(n_p2p=n_p2p, n_m2l=n_m2l, peak_frontier=peak, _deferred=None)
         ok = n_p2p <= caps[0] and n_m2l <= caps[1] and peak <= caps[2] and fronts[-1] == 0
-        ok = ok and int(self.__dict__["dev_runs_needed"][0]) == 0  # (runs are sized like pairs)
+        ok = ok and runs_needed == 0  # (runs are sized like pairs)
         if ok:
             _hint[key] = (max(caps[0], int(n_p2p * 1.02) + 4096), max(caps[1], int(n_m2l * 1.02) + 4096),
                           max(caps[2], int(peak * 1.05) + 4096))
@@ -821,6 +832,35 @@ class ChunkedLists:
         return np.concatenate(tt), np.concatenate(ss)
 
 
+class EndReadback:
+    """Every small counter an evaluation needs on the host, copied in ONE
+    device-to-host transfer into pinned memory that is enqueued right after
+    the last kernel: the evaluation then synchronises once (on its end
+    event) instead of once per counter, and the combine kernel no longer
+    waits for a host round trip on the FP32 flag."""
+
+    _pinned = threading.local()
+
+    def __init__(self, tensors):
+        self.sizes = [t.numel() for t in tensors]
+        dev = torch.cat([t.reshape(-1).long() for t in tensors])
+        key = (dev.device.index or 0, dev.numel())
+        pool = self._pinned.__dict__.setdefault("bufs", {})
+        host = pool.get(key)
+        if host is None:
+            host = pool[key] = torch.empty(dev.numel(), dtype=torch.int64, pin_memory=True)
+        host.copy_(dev, non_blocking=True)
+        self.host = host
+
+    def parts(self):
+        """The tensors' host copies (valid after the end event)."""
+        out, o = [], 0
+        for n in self.sizes:
+            out.append(self.host[o:o + n])
+            o += n
+        return out
+
+
 class _EventPool:
     """Timing events of one evaluation, reused across evaluations of the
     calling thread (an evaluation synchronises before it returns, so its
@@ -968,33 +1008,47 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             e_down1.record(side)
         e_pend.record(pst)
         main.wait_event(e_pend)
-        redo = nf in ("fp32", "fp32acc") and int(flag.item()) != 0
-        if redo:
-            # two distinct bodies collided in FP32 outside a self run: redo guarded
-            for lists in parts:
-                run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag, bodies)
-        # cross-tree: float64-coincident pairs (none unless FP32 saw one)
-        coinc = [count_coincident(tree, x, bodies) for x in parts] if cross and (redo or nf == "fp64") \
-            else []
+        # cross-tree, float64 near field: float64-coincident pairs
+        coinc = [count_coincident(tree, x, bodies) for x in parts] if cross and nf == "fp64" else []
         main.wait_event(e_down1)
         P = _lib.ptr
-        _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
-                  P(tree.d_fz), _lib.stream_handle())
+        combine = lambda: _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi),  # noqa: E731
+                                    P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), _lib.stream_handle())
+        combine()
+        rb = EndReadback([flag] + [t for x in parts for t in x.device_counters()] + coinc)
         e_end.record(main)
         e_end.synchronize()
-        if not all([x.settle() for x in parts]):
+        host = rb.parts()
+        redo = nf in ("fp32", "fp32acc") and int(host[0][0]) != 0
+        if redo:
+            # two distinct bodies collided in FP32 outside a self run: redo guarded (the
+            # near field is rewritten, so the far field is added again)
+            for lists in parts:
+                run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag, bodies)
+            combine()
+            if cross:  # (float64-coincident pairs are FP32 collisions too)
+                coinc = [count_coincident(tree, x, bodies) for x in parts]
+            e_end.record(main)
+            e_end.synchronize()
+        k = 1
+        hparts = []
+        for lists in parts:
+            n = 3 if lists.__dict__.get("_deferred") is not None else 2
+            hparts.append(host[k:k + n])
+            k += n
+        if not all([x.settle(h) for x, h in zip(parts, hparts)]):
             # a hinted list outgrew its buffer: redo with exact counts
             return evaluate_dual_tree(tree, cfg, source_tree=source_tree, threads=threads, trace=trace,
                                       target_mask=target_mask)
         pairs = skipped = 0
-        for lists in parts:
-            a, b = lists.dev_stats.tolist()
+        for h in hparts:
+            a, b = h[0].tolist()
             pairs += a
             skipped += b
-        for c in coinc:
-            k = int(c.item())
-            pairs -= k
-            skipped += k
+        for c in (coinc if redo else host[k:]):
+            k_ = int(c.item() if isinstance(c, torch.Tensor) and c.is_cuda else c[0])
+            pairs -= k_
+            skipped += k_
     lists = parts[0] if nch == 1 else ChunkedLists(parts)
     tree.list_cache = lists
     global last_events  # (start, P2P chunk (begin, end) events, end): tools/step_probe.py
