@@ -99,3 +99,26 @@ def test_grouped_only_for_lattice_trees():
     t = _tree(pos, q)
     assert trv.m2l_grouped(t, 10, src=_tree(pos[:100], q[:100])) is False
     assert trv.m2l_grouped(t, 5) is False
+
+
+@pytest.mark.parametrize("strategy,mutual", [("dualtree", False), ("dualtree", True), ("listfmm", False)])
+@pytest.mark.parametrize("p", [8, 10])
+def test_grouped_inside_evaluations(strategy, mutual, p):
+    """Whole evaluations (dual tree, mutual dual tree, listfmm V-lists) with
+    the grouped M2L against the same evaluations on the per-pair kernels."""
+    pos, q = workloads.config4(1 << 15, 7)
+    cfg = fb.EvalConfig(strategy=strategy, mac=fb.MacConfig("fmm", 0.5), p=p, mutual=mutual)
+    out = {}
+    for grouped in (False, True):
+        old = trv.M2L_GROUPED_MIN_P
+        trv.M2L_GROUPED_MIN_P = 6 if grouped else 99
+        try:
+            t = _tree(pos, q)
+            rep = fb.evaluate_on_tree(t, cfg)
+        finally:
+            trv.M2L_GROUPED_MIN_P = old
+        out[grouped] = (t.bodies, rep.stats)
+    (a, sa), (b, sb) = out[False], out[True]
+    assert sa.m2l_calls == sb.m2l_calls and sa.p2p_pairs == sb.p2p_pairs
+    for k in ("phi", "fx", "fy", "fz"):
+        assert rel_l2(getattr(b, k), getattr(a, k)) <= 1e-12, k

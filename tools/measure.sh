@@ -18,7 +18,7 @@ bench)
     python bench.py --config $c --steps 5 --warmup 5 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   done
   for s in treecode listfmm; do
-    python bench.py --strategy $s --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_$s.json 2> gpurun_out/bench_$s.err
+    python bench.py --strategy $s --steps 10 --warmup 10 --no-cpu-baseline > gpurun_out/bench_c2_$s.json 2> gpurun_out/bench_$s.err
   done
   python bench.py --mutual --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_mutual.json 2> gpurun_out/bench_mu.err
   python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
