@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode", "listfmm"],
                     help="evaluation strategy (the headline is the dual-tree FMM)")
     ap.add_argument("--mutual", action="store_true", help="mutual dual traversal (EvalConfig.mutual)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N>1: each rank gets only its block of the input and keeps only its own bodies plus "
+                         "the near-field halo (paper_1209_3516_b200.sharded) instead of the replicated cloud")
     ap.add_argument("--task-grain", type=int, default=5000, help="EvalConfig.task_grain (mutual partition)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -279,7 +282,18 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
+    sharded = args.sharded and world > 1
+    if sharded:
+        from paper_1209_3516_b200 import sharded as fsh
+        blk = slice(rank * n // world, (rank + 1) * n // world)  # this rank's block of the input
+        shard_dev = [dpos[blk, 0].contiguous(), dpos[blk, 1].contiguous(), dpos[blk, 2].contiguous(),
+                     torch.as_tensor(q[blk], device=dev).to(dt)]
+
     def step():
+        if sharded:
+            tree = fsh.build_tree_sharded(*shard_dev, solver["ncrit"], rank, world, device=dev)
+            rep, _ = fsh.evaluate_sharded(tree, cfg, results="local")
+            return tree, rep
         tree = fb.build_tree(ps_dev, ncrit=solver["ncrit"])
         if world > 1:
             rep = fdist.evaluate_partitioned(tree, cfg, rank, world, results="root")
@@ -349,6 +363,11 @@ def run_ours(args):
         h2d = sum(a.nbytes for a in (hx, hy, hz, hq))
 
         def e2e_step():
+            if sharded:  # the rank's block in, its block's (phi, f) back
+                b = slice(rank * n // world, (rank + 1) * n // world)
+                tr = fsh.build_tree_sharded(hx[b], hy[b], hz[b], hq[b], solver["ncrit"], rank, world, device=dev)
+                _, res = fsh.evaluate_sharded(tr, cfg, results="input")
+                return [r.cpu().numpy() for r in res]
             ps = fb.ParticleSet(hx, hy, hz, hq)
             tr = fb.build_tree(ps, ncrit=solver["ncrit"])
             if world > 1:
@@ -370,7 +389,7 @@ def run_ours(args):
             res = e2e_step()
             et.append(max_over_ranks(time.perf_counter() - t0))
         e2e = {"value": n / float(np.median(et)), "unit": "particles/s",
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 4 * 8 * n,
+               "h2d_bytes_per_step": h2d if sharded else h2d * world, "d2h_bytes_per_step": 4 * 8 * n,
                "note": "ParticleSet(host numpy) -> build_tree -> evaluate_on_tree (evaluate_partitioned over the "
                        "ranks, results gathered to rank 0) -> results_in_input_order() (phi, f back in input "
                        "order as float64); wall clock per "
@@ -381,7 +400,7 @@ def run_ours(args):
     # accuracy of the last timed step: relative L2 error against direct
     # summation on the reference's 1000-body sample (tree order, seed 0)
     acc = None
-    if rank == 0 and not args.no_accuracy:
+    if rank == 0 and not args.no_accuracy and not sharded:  # (sharded: rank 0 holds only its rows)
         from paper_1209_3516_b200.tuner import potential_sample, sampled_force_error, sampled_potential_error
         idx, fref, pref = potential_sample(tree, 1000, 0)
         acc = {"force_err": sampled_force_error(tree, idx, fref), "pot_err": sampled_potential_error(tree, idx, pref),
@@ -415,7 +434,8 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32 P2P / f64 tree+far field" if args.precision == "fp32" else "f64",
         "data": "synthetic", "config": config_block(args, n, solver, {"precision": args.precision,
-                                                                      "parallelism": f"morton-partition x{world}"}),
+                                                                      "parallelism": f"morton-partition x{world}"
+                                                                      + (" sharded+halo" if sharded else "")}),
         "p2p_ginteractions_per_s": rep.stats.p2p_pairs / p2p_s / 1e9,
         "p2p_pairs": rep.stats.p2p_pairs, "m2l_calls": rep.stats.m2l_calls, "m2p_calls": rep.stats.m2p_calls,
         "phase_ms": {"build": 1e3 * rep.build_time, "upward": 1e3 * rep.upward_time,

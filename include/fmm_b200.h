@@ -127,6 +127,14 @@ FMM_API int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_
                       const double *qs, int rect, int com, const double *root, double *lo, double *hi,
                       double *ctr, double *bmax, double *rmax, void *ws, size_t ws_bytes, void *stream);
 
+/* bmax over the bodies in [body_lo, body_hi) only (0 for cells without
+ * any): a rank of a sharded build holds just its own bodies, and the
+ * ranks' values are combined with a MAX all-reduce -- max and sqrt
+ * commute, so the result equals fmm_cell_geometry's bit for bit. */
+FMM_API int fmm_cell_bmax_range(int32_t ncells, const int32_t *start, const int32_t *end, const double *ctr,
+                        const double *xs, const double *ys, const double *zs, int32_t body_lo, int32_t body_hi,
+                        double *bmax, void *ws, size_t ws_bytes, void *stream);
+
 /* ---- vertical passes (src/tree.py:163-189, src/_taylor.py:102-269) ------ */
 
 /* P2M at every listed leaf, then M2M bottom-up level by level over the

@@ -41,6 +41,7 @@ SIGNATURES = {
     "fmm_carve_count": [P, I64, I32, INT, P, P, P, P, P, P, P, SZ, P],
     "fmm_carve_emit": [P, I64, P, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_cell_geometry": [I32, P, P, P, P, P, P, P, P, INT, INT, P, P, P, P, P, P, P, SZ, P],
+    "fmm_cell_bmax_range": [I32, P, P, P, P, P, P, I32, I32, P, P, SZ, P],
     "fmm_upward": [INT, I32, P, P, P, P, P, P, P, P, P, P, P, INT, P, P],
     "fmm_downward": [INT, I32, P, P, P, P, P, INT, I64, I64, P, P, P, P, P, P, P, P, P, P],
     "fmm_traverse_step": [P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, INT, DBL, P, P, I64,

@@ -408,11 +408,21 @@ __device__ inline int upper_bound_i32(const int32_t *a, int n, int32_t v) {
     return lo;
 }
 
+// bmax accumulators and chunk counts alone (fmm_cell_bmax_range)
+__global__ void bmax_chunks(int32_t ncells, const int32_t *__restrict__ start, const int32_t *__restrict__ end,
+                            unsigned long long *b2, int32_t *nchunk) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+        b2[c] = 0ull;
+        nchunk[c] = (end[c] - start[c] + kChunk - 1) / kChunk;
+    }
+}
+
 __global__ void geometry_bmax(int32_t ncells, const int32_t *__restrict__ choff,
                               const int32_t *__restrict__ nchunk, const int32_t *__restrict__ start,
                               const int32_t *__restrict__ end, const double *__restrict__ ctr,
                               const double *__restrict__ xs, const double *__restrict__ ys,
-                              const double *__restrict__ zs, unsigned long long *b2) {
+                              const double *__restrict__ zs, unsigned long long *b2, int32_t body_lo = 0,
+                              int32_t body_hi = 0x7fffffff) {
     const int lane = threadIdx.x & 31;
     const int total = choff[ncells - 1] + nchunk[ncells - 1];
     for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total;
@@ -421,6 +431,8 @@ __global__ void geometry_bmax(int32_t ncells, const int32_t *__restrict__ choff,
         int k = it - choff[c];
         int32_t s = start[c] + k * kChunk;
         int32_t e = min(end[c], s + kChunk);
+        s = max(s, body_lo);  // only the resident bodies (a rank's share, fmm_cell_bmax_range)
+        e = min(e, body_hi);
         const double cx = ctr[c * 3], cy = ctr[c * 3 + 1], cz = ctr[c * 3 + 2];
         double best = 0.0;
         for (int32_t j = s + lane; j < e; j += 32) {
@@ -640,6 +652,29 @@ int fmm_cell_geometry(int32_t ncells, const int8_t *level, const uint64_t *key, 
     geometry_bmax<<<148 * 8, 256, 0, s>>>(ncells, choff, nchunk, start, end, ctr, xs, ys, zs, b2); fmm::note_launch();
     geometry_finish<<<g, 256, 0, s>>>(ncells, b2, bmax); fmm::note_launch();
     FMM_CUDA_CHECK("fmm_cell_geometry");
+    return FMM_OK;
+}
+
+
+int fmm_cell_bmax_range(int32_t ncells, const int32_t *start, const int32_t *end, const double *ctr,
+                        const double *xs, const double *ys, const double *zs, int32_t body_lo, int32_t body_hi,
+                        double *bmax, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    Arena ar(ws, ws_bytes);
+    unsigned long long *b2 = ar.take<unsigned long long>(ncells);
+    int32_t *nchunk = ar.take<int32_t>(ncells);
+    int32_t *choff = ar.take<int32_t>(ncells);
+    if (!b2 || !nchunk || !choff) { set_error("workspace too small"); return FMM_ERR_INVALID; }
+    int g = grid_for(ncells, 256);
+    bmax_chunks<<<g, 256, 0, s>>>(ncells, start, end, b2, nchunk); fmm::note_launch();
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, nchunk, choff, ncells, s);
+    if (need > ar.left()) { set_error("scan workspace"); return FMM_ERR_INVALID; }
+    cub::DeviceScan::ExclusiveSum(ar.rest(), need, nchunk, choff, ncells, s);
+    geometry_bmax<<<148 * 8, 256, 0, s>>>(ncells, choff, nchunk, start, end, ctr, xs, ys, zs, b2, body_lo, body_hi);
+    fmm::note_launch();
+    geometry_finish<<<g, 256, 0, s>>>(ncells, b2, bmax); fmm::note_launch();
+    FMM_CUDA_CHECK("fmm_cell_bmax_range");
     return FMM_OK;
 }
 

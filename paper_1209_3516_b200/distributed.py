@@ -196,7 +196,8 @@ class TorchDistComm:
 RESULTS = ("all", "root", "local")
 
 
-def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None, results: str = "all"):
+def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None, results: str = "all",
+                         before_p2p=None):
     """Evaluate ``tree`` with targets Morton-partitioned over ``world`` ranks.
 
     ``results`` picks where the (phi, f) rows end up: "all" (one all-gather:
@@ -205,7 +206,8 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     tree is valid on its own bodies ``tree.owned_range`` only).  The
     ``EvalReport`` counters cover the rank's own rows.  ``comm`` defaults to
     :class:`TorchDistComm`; tests pass an in-process exchange to emulate
-    ranks on one device."""
+    ranks on one device.  ``before_p2p(lists)`` runs once the rank's lists
+    exist, before its near field (``sharded`` fetches its halo there)."""
     if results not in RESULTS:
         raise ValueError(f"results must be one of {RESULTS}, got {results!r}")
     comm = comm or TorchDistComm(group)
@@ -274,6 +276,8 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         if not treecode:
             downward_pass(tree, None, sync=False, body_range=(lo, hi), out=tuple(far))
         ev[5].record(side)
+    if before_p2p is not None:  # the sharded path's halo exchange (sharded.py)
+        before_p2p(lists)
     ev[6].record(main)
     run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag)
     if nf in ("fp32", "fp32acc") and int(flag.item()) != 0:

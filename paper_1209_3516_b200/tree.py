@@ -331,46 +331,64 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         _lib.call("fmm_permute_bodies", P(perm), P(x64), P(y64), P(z64), P(q64), n, P(xs), P(ys), P(zs),
                   P(qs), P(b32), P(b32lo), P(inexact), st)
         del x64, y64, z64, q64, keys, iota
+        tree = _carve_tree(dev, st, wsp, wsb, n, ncrit, shape, center_mode, allow_oversized_leaves, skeys, perm, root,
+                           (xs, ys, zs, qs, b32, b32lo), inexact)
+    tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
+    tree.build_time = time.perf_counter() - t0
+    with torch.cuda.device(dev):  # the evaluation bills the host gap after the build to its first phase
+        tree._ev_built = torch.cuda.Event(enable_timing=True)
+        tree._ev_built.record()
+    tree._ev_build_start = ev_start
+    return tree
 
-        # single-pass carve: per-body leaf level, cells numbered in pre-order
-        # by one scan (csrc/tree_build.cu), one host synchronisation
-        cbase = torch.empty(n, dtype=i32, device=dev)
-        leaf_level = torch.empty(n, dtype=torch.int8, device=dev)
-        hist = (C.c_int32 * 23)()
-        nc_host = C.c_int32(0)
-        inexact_host = C.c_int32(0)  # read with the counts: no separate sync later
-        _lib.call("fmm_carve_count", P(skeys), n, int(ncrit), int(bool(allow_oversized_leaves)), P(cbase),
-                  P(leaf_level), hist, C.byref(nc_host), P(inexact), C.byref(inexact_host), wsp, wsb, st)
-        ncells = int(nc_host.value)
-        nleaves = int(hist[22])
-        depth = max(L for L in range(22) if hist[L] > 0)
-        off = [0]
-        for L in range(22):
-            off.append(off[-1] + int(hist[L]))
-        level_off = off[:depth + 2]
-        off23 = (C.c_int32 * 23)(*off[:23])
-        cc = dict(children=torch.empty((ncells, 8), dtype=i32, device=dev),
-                  parent=torch.empty(ncells, dtype=i32, device=dev),
-                  level=torch.empty(ncells, dtype=torch.int8, device=dev),
-                  key=torch.empty(ncells, dtype=torch.int64, device=dev),
-                  start=torch.empty(ncells, dtype=i32, device=dev),
-                  end=torch.empty(ncells, dtype=i32, device=dev),
-                  sub_end=torch.empty(ncells, dtype=i32, device=dev),
-                  leaf=torch.empty(ncells, dtype=torch.uint8, device=dev))
-        cells_by_level = torch.empty(ncells, dtype=i32, device=dev)
-        body_leaf = torch.empty(n, dtype=i32, device=dev)
-        _lib.call("fmm_carve_emit", P(skeys), n, P(cbase), P(leaf_level), ncells, off23, P(cc["children"]),
-                  P(cc["parent"]), P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]), P(cc["sub_end"]),
-                  P(cc["leaf"]), P(cells_by_level), P(body_leaf), wsp, wsb, st)
-        del cbase, leaf_level
-        lo = torch.empty((ncells, 3), dtype=f64, device=dev)
-        hi, ctr = torch.empty_like(lo), torch.empty_like(lo)
-        bmax = torch.empty(ncells, dtype=f64, device=dev)
-        rmax = torch.empty_like(bmax)
-        _lib.call("fmm_cell_geometry", ncells, P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
-                  P(xs), P(ys), P(zs), P(qs), int(shape == "rect"), int(center_mode == "com"), P(root), P(lo),
-                  P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
-        zeros = torch.zeros((4, n), dtype=f64, device=dev).unbind(0)  # one fill
+
+def _carve_tree(dev, st, wsp, wsb, n: int, ncrit: int, shape: str, center_mode: str, allow_oversized_leaves: bool,
+                skeys, perm, root, bodies, inexact) -> Tree:
+    """Cells from the sorted keys (single-pass carve: per-body leaf level,
+    cells numbered in pre-order by one scan, csrc/tree_build.cu; one host
+    synchronisation) and their geometry, around Morton-ordered ``bodies`` =
+    (xs, ys, zs, qs, b32, b32lo).  Shared by ``build_tree`` and the sharded
+    multi-GPU build (``sharded.build_tree_sharded``)."""
+    P = _lib.ptr
+    f64, i32 = torch.float64, torch.int32
+    xs, ys, zs, qs, b32, b32lo = bodies
+    cbase = torch.empty(n, dtype=i32, device=dev)
+    leaf_level = torch.empty(n, dtype=torch.int8, device=dev)
+    hist = (C.c_int32 * 23)()
+    nc_host = C.c_int32(0)
+    inexact_host = C.c_int32(0)  # read with the counts: no separate sync later
+    _lib.call("fmm_carve_count", P(skeys), n, int(ncrit), int(bool(allow_oversized_leaves)), P(cbase),
+              P(leaf_level), hist, C.byref(nc_host), P(inexact), C.byref(inexact_host), wsp, wsb, st)
+    ncells = int(nc_host.value)
+    nleaves = int(hist[22])
+    depth = max(L for L in range(22) if hist[L] > 0)
+    off = [0]
+    for L in range(22):
+        off.append(off[-1] + int(hist[L]))
+    level_off = off[:depth + 2]
+    off23 = (C.c_int32 * 23)(*off[:23])
+    cc = dict(children=torch.empty((ncells, 8), dtype=i32, device=dev),
+              parent=torch.empty(ncells, dtype=i32, device=dev),
+              level=torch.empty(ncells, dtype=torch.int8, device=dev),
+              key=torch.empty(ncells, dtype=torch.int64, device=dev),
+              start=torch.empty(ncells, dtype=i32, device=dev),
+              end=torch.empty(ncells, dtype=i32, device=dev),
+              sub_end=torch.empty(ncells, dtype=i32, device=dev),
+              leaf=torch.empty(ncells, dtype=torch.uint8, device=dev))
+    cells_by_level = torch.empty(ncells, dtype=i32, device=dev)
+    body_leaf = torch.empty(n, dtype=i32, device=dev)
+    _lib.call("fmm_carve_emit", P(skeys), n, P(cbase), P(leaf_level), ncells, off23, P(cc["children"]),
+              P(cc["parent"]), P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]), P(cc["sub_end"]),
+              P(cc["leaf"]), P(cells_by_level), P(body_leaf), wsp, wsb, st)
+    del cbase, leaf_level
+    lo = torch.empty((ncells, 3), dtype=f64, device=dev)
+    hi, ctr = torch.empty_like(lo), torch.empty_like(lo)
+    bmax = torch.empty(ncells, dtype=f64, device=dev)
+    rmax = torch.empty_like(bmax)
+    _lib.call("fmm_cell_geometry", ncells, P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
+              P(xs), P(ys), P(zs), P(qs), int(shape == "rect"), int(center_mode == "com"), P(root), P(lo),
+              P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
+    zeros = torch.zeros((4, n), dtype=f64, device=dev).unbind(0)  # one fill
     tree = Tree(
         device=dev, n=n, ncrit=ncrit, shape=shape, center_mode=center_mode,
         allow_oversized_leaves=bool(allow_oversized_leaves), _ncells=ncells, _nleaves=nleaves,
@@ -383,12 +401,6 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         d_lo=lo, d_hi=hi, d_ctr=ctr, d_bmax=bmax, d_rmax=rmax,
     )
     tree._fp32_exact = int(inexact_host.value) == 0
-    tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
-    tree.build_time = time.perf_counter() - t0
-    with torch.cuda.device(dev):  # the evaluation bills the host gap after the build to its first phase
-        tree._ev_built = torch.cuda.Event(enable_timing=True)
-        tree._ev_built.record()
-    tree._ev_build_start = ev_start
     return tree
 
 

@@ -115,3 +115,19 @@ def test_allgather_rows_gloo(world):
     assert np.array_equal(np.array(out[(0, "gather")]), want)  # only the root receives
     for r in range(1, world):
         assert (np.array(out[(r, "gather")]) == -1.0).sum() > 0
+
+
+def test_sharded_host_logic():
+    from paper_1209_3516_b200.sharded import halo_ranges, owner_of, shard_offsets
+    assert shard_offsets([3, 0, 5]).tolist() == [0, 3, 3, 8]
+    assert owner_of([0, 2, 3, 7], [0, 3, 3, 8]).tolist() == [0, 0, 2, 2]
+    cuts = [0, 10, 20, 30]
+    # own range [10, 20): runs inside it vanish, the rest merge and split at the cuts
+    out = halo_ranges([12, 5, 8, 18, 25, 28, 0], [15, 9, 12, 24, 27, 29, 0], 10, 20, cuts)
+    assert out[0].tolist() == [[5, 10]]
+    assert out[1].tolist() == []
+    assert out[2].tolist() == [[20, 24], [25, 27], [28, 29]]
+    # a run crossing two foreign ranges is split per owner
+    out = halo_ranges([5], [25], 30, 30, cuts)
+    assert [o.tolist() for o in out] == [[[5, 10]], [[10, 20]], [[20, 25]]]
+    assert all(o.size == 0 for o in halo_ranges([], [], 0, 10, cuts))

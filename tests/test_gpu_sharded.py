@@ -1,0 +1,92 @@
+"""The sharded multi-GPU path (paper_1209_3516_b200/sharded.py) as real
+processes: W = 2 and 4 ranks through ``torch.distributed`` (gloo, host-
+staged collectives) on cuda:0.  Each rank is handed only its contiguous
+block of the input; the build must reproduce the single-GPU tree bit for
+bit (sorted keys, permutation, every cell array including bmax), the own
+rows' near field must need only the own bodies plus a halo, and every
+rank's results for its input block must equal the single-GPU evaluation's
+(results_in_input_order) to 1e-12, with the per-rank P2P pair counts
+summing to the single-GPU count."""
+
+import hashlib
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("c2_32k", "fp32", False), ("plummer_32k", "fp64", False), ("c1", "fp64", False),
+         ("c2_32k", "fp64", True)]
+CELLS = ("children", "parent", "level", "key", "start", "end", "sub_end", "leaf", "ctr", "bmax", "rmax", "lo",
+         "hi")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _digest(t):
+    return {k: hashlib.sha256(getattr(t, "d_" + k).contiguous().cpu().numpy().tobytes()).hexdigest()
+            for k in CELLS + ("keys", "perm")}
+
+
+def _worker(rank, world, port, out):
+    import paper_1209_3516_b200 as fb
+    from goldens import Case
+    from paper_1209_3516_b200 import sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for name, precision, mutual in CASES:
+            c = Case(name)
+            pos = np.asarray(c.pos)
+            qq = np.asarray(c.q)
+            cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", c.theta), p=c.p, precision=precision, mutual=mutual,
+                                task_grain=1500)
+            ref = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], qq), ncrit=c.ncrit)
+            rrep = fb.evaluate_on_tree(ref, cfg)
+            want = ref.results_in_input_order()
+            n = pos.shape[0]
+            a, b = rank * n // world, (rank + 1) * n // world
+            t = sharded.build_tree_sharded(pos[a:b, 0], pos[a:b, 1], pos[a:b, 2], qq[a:b], c.ncrit, rank, world)
+            same_tree = _digest(t) == _digest(ref) and t.fp32_exact == ref.fp32_exact
+            rep, res = sharded.evaluate_sharded(t, cfg)
+            err = max(float(np.linalg.norm(g.cpu().numpy() - np.asarray(getattr(want, k))[a:b]) /
+                            max(np.linalg.norm(np.asarray(getattr(want, k))[a:b]), 1e-300))
+                      for g, k in zip(res, ("phi", "fx", "fy", "fz")))
+            pairs = torch.tensor([rep.stats.p2p_pairs], dtype=torch.int64)
+            dist.all_reduce(pairs)
+            lo, hi = t.shard["own"]
+            out[(rank, name, mutual)] = (same_tree, err, int(pairs.item()), int(rrep.stats.p2p_pairs),
+                                         hi - lo, t.shard["halo_bodies"], n)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_processes_match_single_gpu(world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
+    for name, precision, mutual in CASES:
+        owned = 0
+        for r in range(world):
+            same_tree, err, pairs, ref_pairs, nown, halo, n = out[(r, name, mutual)]
+            assert same_tree, (name, r)
+            assert err <= 1e-12, (name, precision, r, err)
+            assert pairs == ref_pairs, (name, r)
+            assert nown + halo <= n, (name, r)
+            if name == "c2_32k":  # uniform: the halo is a shell, not the rest of the cloud
+                assert nown + halo < n, (name, r)
+            owned += nown
+        assert owned == n
