@@ -798,8 +798,11 @@ __global__ void __launch_bounds__((MG<P>::NW + 1) * 32) m2l_dmma(
 
 // ---- grouping pre-pass ----------------------------------------------------
 constexpr uint64_t kMgNone = ~0ull;
-constexpr int kMgHashBits = 17;  // D-key table: 2^17 slots, <= kMgDCap groups get a D row
-constexpr int kMgDCap = 32768;
+// D-key table: 2^20 slots; up to kMgDCap groups get a D row (C4 at theta =
+// 0.3: 14,128 groups; the adaptive C3 tree: 22,129 at 0.5, 166,647 at 0.3).
+// Groups past the cap keep their batching, and the producer forms their D.
+constexpr int kMgHashBits = 20;
+constexpr int kMgDCap = 131072;
 
 __device__ __forceinline__ uint32_t mg_hash(uint64_t k) {
     return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> (64 - kMgHashBits));
@@ -911,14 +914,14 @@ __global__ void mg_pair_keys(int32_t ncells, const int64_t *__restrict__ rows, c
 // dense ids for the table's D-keys and their signed D rows (thread per slot)
 template <int P>
 __global__ void mg_table_rows(const unsigned long long *__restrict__ htab, const double *__restrict__ root,
-                              int32_t *hid, int32_t *ngroups, double *Dtab) {
+                              int32_t *hid, int32_t *ngroups, double *Dtab, int64_t dcap) {
     const double size = root[3];
     for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < (1 << kMgHashBits); h += gridDim.x * blockDim.x) {
         const unsigned long long dk1 = htab[h];
         if (!dk1) continue;
         const int id = atomicAdd(ngroups, 1);
-        hid[h] = id < kMgDCap ? id : -1;
-        if (id >= kMgDCap) continue;
+        hid[h] = id < dcap ? id : -1;
+        if (id >= dcap) continue;
         const uint64_t dk = dk1 - 1;
         const int lt = (int)(dk >> 35), dl = (int)((dk >> 30) & 31) - 16;
         const int L = dl > 0 ? lt + dl : lt;
@@ -1032,6 +1035,7 @@ struct MgLayout {
     double *Dtab;
     void *tmp;
     size_t tmp_bytes;
+    int64_t dcap;
     int32_t nbmax;
     int end_bit;
 };
@@ -1053,7 +1057,10 @@ size_t mg_layout(int p, int32_t ncells, int64_t cap, void *ws, size_t ws_bytes, 
     int kb = 1;
     while ((1ll << kb) <= l.nbmax) kb++;
     l.end_bit = 40 + kb;
-    const int64_t dcap = cap < kMgDCap ? cap : kMgDCap;
+    int64_t dcap = cap < kMgDCap ? cap : kMgDCap;
+    const int64_t dmem = ((int64_t)512 << 20) / ((2 * ncoef(p) + 2) * 8);  // <= 512 MB of D rows
+    if (dcap > dmem) dcap = dmem;
+    l.dcap = dcap;
     Arena A(ws, ws ? ws_bytes : ~(size_t)0 >> 2);
     l.ckey[0] = A.take<uint64_t>(ncells);
     l.ckey[1] = A.take<uint64_t>(ncells);
@@ -1087,7 +1094,7 @@ size_t mg_layout(int p, int32_t ncells, int64_t cap, void *ws, size_t ws_bytes, 
 template <int P>
 int mg_launch(const MgLayout &l, const double *root, const double *ctr, const double *M, double *L, cudaStream_t s) {
     mg_table_rows<P><<<grid_for((int64_t)1 << kMgHashBits, 128, 148 * 8), 128, 0, s>>>(l.htab, root, l.hid,
-                                                                                       l.ngroups, l.Dtab);
+                                                                                       l.ngroups, l.Dtab, l.dcap);
     fmm::note_launch();
     return 0;
 }
