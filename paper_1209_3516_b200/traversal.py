@@ -453,6 +453,23 @@ def _csr(t, s, n, ncells, dev, wsp, wsb, stream, dev_n=None, nsrc=0, sort=True):
     return src, rows
 
 
+_sync_ring = threading.local()
+
+
+def _sync_event(dev) -> torch.cuda.Event:
+    """A cross-stream ordering event from a per-thread, per-device ring of
+    64: a stream wait captures the event's state when it is issued, so
+    re-recording it later is safe, and no CUDA event is created per call."""
+    ring = _sync_ring.__dict__.setdefault(torch.device(dev).index or 0, [[], 0])
+    evs, i = ring
+    if len(evs) < 64:
+        with torch.cuda.device(dev):
+            evs.append(torch.cuda.Event())
+        return evs[-1]
+    ring[1] = (i + 1) % 64
+    return evs[i]
+
+
 def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0):
     """CSR of a far-field list (M2L or M2P).  Only the far field reads it, so
     with a ``side`` stream it is sorted there, off the P2P critical path,
@@ -464,7 +481,7 @@ def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0
         return out
     if dev_n is None:  # the count, written on this stream before the side stream waits
         dev_n = torch.full((1,), n, dtype=torch.int64, device=dev)
-    traversed = torch.cuda.Event()
+    traversed = _sync_event(dev)
     traversed.record()
     side.wait_event(traversed)
     swp, swb = _lib.workspace(max(n, ncells + 1, 1), dev, slot=1, stream=side)
@@ -972,7 +989,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         parts, m2l_ev, p2p_ev = [], [], []
         for k in range(nch):
             rng = (cuts[k], cuts[k + 1]) if nch > 1 else None
-            ready = torch.cuda.Event()
+            ready = E()
             with torch.cuda.stream(lst):
                 if cfg.mutual:
                     lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side)
@@ -991,7 +1008,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                 run_m2l(tree, lists, p, src)
                 eb.record(side)
                 m2l_ev.append((ea, eb))
-            planned = torch.cuda.Event()
+            planned = E()
             planned.record(lst)
             pst.wait_event(planned)
             with torch.cuda.stream(pst):

@@ -25,6 +25,7 @@ permutation and every cell array; tests/test_gpu_parity.py).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 
@@ -302,7 +303,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         dev = torch.device(device)
     n = ps.n
     with torch.cuda.device(dev):
-        ev_start = torch.cuda.Event(enable_timing=True)  # the build's span on the device timeline
+        ev_start = _build_event(dev)  # the build's span on the device timeline
         ev_start.record()
         st = _lib.stream_handle()
         f64, i32 = torch.float64, torch.int32
@@ -336,10 +337,40 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
     tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
     tree.build_time = time.perf_counter() - t0
     with torch.cuda.device(dev):  # the evaluation bills the host gap after the build to its first phase
-        tree._ev_built = torch.cuda.Event(enable_timing=True)
+        tree._ev_built = _build_event(dev)
         tree._ev_built.record()
     tree._ev_build_start = ev_start
     return tree
+
+
+_cell_hint = {}  # (n, ncrit, allow, device) -> largest cell count built
+
+_build_ring = threading.local()
+
+
+def _build_event(dev) -> torch.cuda.Event:
+    """A timing event for a build's start/end marks, from a per-thread ring
+    of 128 (creating CUDA events costs host time while the GPU waits; a mark
+    is read by the tree's first evaluation, long before the ring wraps)."""
+    ring = _build_ring.__dict__.setdefault("ev", {}).setdefault(torch.device(dev).index or 0, [[], 0])
+    evs, i = ring
+    if len(evs) < 128:
+        with torch.cuda.device(dev):
+            evs.append(torch.cuda.Event(enable_timing=True))
+        ring[1] = len(evs) % 128
+        return evs[-1]
+    ring[1] = (i + 1) % 128
+    return evs[i]
+
+
+def _cell_arrays(cap: int, dev) -> dict:
+    """Every per-cell array of a tree, ``cap`` rows each."""
+    i32, f64 = torch.int32, torch.float64
+    e = lambda *shape, dtype=i32: torch.empty(shape, dtype=dtype, device=dev)  # noqa: E731
+    return dict(children=e(cap, 8), parent=e(cap), level=e(cap, dtype=torch.int8), key=e(cap, dtype=torch.int64),
+                start=e(cap), end=e(cap), sub_end=e(cap), leaf=e(cap, dtype=torch.uint8), by_level=e(cap),
+                lo=e(cap, 3, dtype=f64), hi=e(cap, 3, dtype=f64), ctr=e(cap, 3, dtype=f64), bmax=e(cap, dtype=f64),
+                rmax=e(cap, dtype=f64))
 
 
 def _carve_tree(dev, st, wsp, wsb, n: int, ncrit: int, shape: str, center_mode: str, allow_oversized_leaves: bool,
@@ -354,6 +385,14 @@ def _carve_tree(dev, st, wsp, wsb, n: int, ncrit: int, shape: str, center_mode: 
     xs, ys, zs, qs, b32, b32lo = bodies
     cbase = torch.empty(n, dtype=i32, device=dev)
     leaf_level = torch.empty(n, dtype=torch.int8, device=dev)
+    body_leaf = torch.empty(n, dtype=i32, device=dev)
+    # the cell arrays are allocated BEFORE the carve's one synchronisation
+    # when an earlier build of this size left a capacity (the host would
+    # otherwise allocate them while the GPU idles after the sync), and
+    # sliced to the exact count after it
+    hint_key = (n, int(ncrit), bool(allow_oversized_leaves), dev)
+    cap = _cell_hint.get(hint_key, 0)
+    pre = _cell_arrays(cap, dev) if cap else None
     hist = (C.c_int32 * 23)()
     nc_host = C.c_int32(0)
     inexact_host = C.c_int32(0)  # read with the counts: no separate sync later
@@ -367,24 +406,16 @@ def _carve_tree(dev, st, wsp, wsb, n: int, ncrit: int, shape: str, center_mode: 
         off.append(off[-1] + int(hist[L]))
     level_off = off[:depth + 2]
     off23 = (C.c_int32 * 23)(*off[:23])
-    cc = dict(children=torch.empty((ncells, 8), dtype=i32, device=dev),
-              parent=torch.empty(ncells, dtype=i32, device=dev),
-              level=torch.empty(ncells, dtype=torch.int8, device=dev),
-              key=torch.empty(ncells, dtype=torch.int64, device=dev),
-              start=torch.empty(ncells, dtype=i32, device=dev),
-              end=torch.empty(ncells, dtype=i32, device=dev),
-              sub_end=torch.empty(ncells, dtype=i32, device=dev),
-              leaf=torch.empty(ncells, dtype=torch.uint8, device=dev))
-    cells_by_level = torch.empty(ncells, dtype=i32, device=dev)
-    body_leaf = torch.empty(n, dtype=i32, device=dev)
+    if pre is None or ncells > cap:
+        pre = _cell_arrays(ncells, dev)
+    _cell_hint[hint_key] = max(cap, ncells)
+    cc = {k: v[:ncells] for k, v in pre.items()}
+    cells_by_level = cc.pop("by_level")
     _lib.call("fmm_carve_emit", P(skeys), n, P(cbase), P(leaf_level), ncells, off23, P(cc["children"]),
               P(cc["parent"]), P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]), P(cc["sub_end"]),
               P(cc["leaf"]), P(cells_by_level), P(body_leaf), wsp, wsb, st)
     del cbase, leaf_level
-    lo = torch.empty((ncells, 3), dtype=f64, device=dev)
-    hi, ctr = torch.empty_like(lo), torch.empty_like(lo)
-    bmax = torch.empty(ncells, dtype=f64, device=dev)
-    rmax = torch.empty_like(bmax)
+    lo, hi, ctr, bmax, rmax = (cc.pop(k) for k in ("lo", "hi", "ctr", "bmax", "rmax"))
     _lib.call("fmm_cell_geometry", ncells, P(cc["level"]), P(cc["key"]), P(cc["start"]), P(cc["end"]),
               P(xs), P(ys), P(zs), P(qs), int(shape == "rect"), int(center_mode == "com"), P(root), P(lo),
               P(hi), P(ctr), P(bmax), P(rmax), wsp, wsb, st)
