@@ -24,7 +24,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompi
           "-Xcompiler", "-fvisibility=hidden", "-Xcompiler", "-Wall"]
 # bit-exact units: no a*b+c contraction (the reference never contracts)
 EXACT = {"tree_build.cu", "traverse.cu", "plan.cu"}
-SOURCES = ["tree_build.cu", "passes.cu", "traverse.cu", "plan.cu", "m2l.cu", "m2p.cu", "p2p.cu", "util.cu"]
+SOURCES = ["tree_build.cu", "passes.cu", "traverse.cu", "plan.cu", "m2l.cu", "m2l_grouped.cu", "m2p.cu", "p2p.cu",
+           "util.cu"]
 
 
 def nvcc() -> str:

@@ -97,4 +97,35 @@ __device__ __forceinline__ void d_tensors_ptr(double rx, double ry, double rz, d
     });
 }
 
+// One D-recurrence step (src/_taylor.py:57-95) as data: the entry's
+// multi-index and the indices of the D values it reads (-1 = term absent),
+// pivot first -- D_k = -(1/r^2) [(2k_p - 1) r_p D_{k-e_p} + (k_p - 1)^2
+// D_{k-2e_p} + sum over the later axes a: 2 k_a r_a D_{k-e_a} + k_a (k_a - 1)
+// D_{k-2e_a}].
+struct __align__(16) DRecipe {
+    int16_t i1[3], i2[3];  // per axis: k - e_a, k - 2 e_a (pivot axis and later axes only)
+    int8_t k[3], pivot;
+};
+static_assert(sizeof(DRecipe) == 16, "one LDS.128 per recurrence entry");
+
+__device__ inline DRecipe make_recipe(int idx) {
+    DRecipe r;
+    const int k[3] = {d_tab.mi[idx][0], d_tab.mi[idx][1], d_tab.mi[idx][2]};
+    const int pivot = k[0] > 0 ? 0 : (k[1] > 0 ? 1 : 2);
+    for (int a = 0; a < 3; a++) {
+        r.k[a] = (int8_t)k[a];
+        r.i1[a] = r.i2[a] = -1;
+        if (a < pivot || k[a] == 0) continue;
+        int km[3] = {k[0], k[1], k[2]};
+        km[a] -= 1;
+        r.i1[a] = d_tab.idx3[km[0]][km[1]][km[2]];
+        if (k[a] > 1) {
+            km[a] -= 1;
+            r.i2[a] = d_tab.idx3[km[0]][km[1]][km[2]];
+        }
+    }
+    r.pivot = (int8_t)pivot;
+    return r;
+}
+
 }  // namespace fmm
