@@ -192,6 +192,13 @@ class TorchDistComm:
     def gather_rows(self, full, chunks, rank, world, root=0):
         gather_rows(full, chunks, rank, world, root, self.group)
 
+    def all_true(self, ok: bool, rank: int, world: int) -> bool:
+        """Whether ``ok`` holds on every rank (one MIN all-reduce)."""
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([int(ok)], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
+
 
 RESULTS = ("all", "root", "local")
 
@@ -213,8 +220,8 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import (EvalReport, critical_path, interaction_lists, listfmm_lists, mutual_lists,
-                            _near_field, run_m2l, run_m2p, run_p2p, treecode_lists)
+    from .traversal import (EndReadback, EvalReport, critical_path, interaction_lists, listfmm_lists,
+                            mutual_lists, _near_field, run_m2l, run_m2p, run_p2p, treecode_lists)
     from .tree import downward_pass
 
     if world == 1:
@@ -222,6 +229,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         return evaluate_on_tree(tree, cfg)
     treecode = cfg.strategy == "treecode"
     nf = _near_field(cfg, tree)
+    defer = hasattr(comm, "all_true")  # a collective decision on list overflows is available
     plan = getattr(tree, "_dist_plan", None)
     if plan is None or len(plan.cuts) != world + 1 or plan.rank != rank:
         plan = _Plan(tree, world, rank)
@@ -260,10 +268,11 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         lists = listfmm_lists(tree, body_range=(lo, hi), m2l_ready=ready, side=side)
     elif cfg.mutual:  # the rank's targets of the mutual lists (directed-expanded)
         lists = mutual_lists(tree, cfg.mac, cfg.task_grain, body_range=(lo, hi), m2l_ready=ready, side=side,
-                             defer=False)
+                             defer=defer)
     else:
-        # (exact counts up front: a deferred overflow would need a collective redo)
-        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side, defer=False)
+        # hinted lists do not wait for their counters; an overflow on any rank
+        # is caught at the end and every rank redoes the step (comm.all_true)
+        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side, defer=defer)
     ev[2].record(main)
     side.wait_event(ready)
     with torch.cuda.stream(side):
@@ -280,13 +289,27 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         before_p2p(lists)
     ev[6].record(main)
     run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag)
-    if nf in ("fp32", "fp32acc") and int(flag.item()) != 0:
-        run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag)
     ev[7].record(main)
     main.wait_event(ev[5])
     P = _lib.ptr
-    _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi), P(tree.d_fx), P(tree.d_fy),
-              P(tree.d_fz), _lib.stream_handle())
+    combine = lambda: _lib.call("fmm_combine", tree.n, *(P(a) for a in far), P(tree.d_phi),  # noqa: E731
+                                P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), _lib.stream_handle())
+    combine()
+    # one read-back of the FP32 flag and the list / pair counters
+    rb = EndReadback([flag] + lists.device_counters())
+    done = torch.cuda.Event()
+    done.record(main)
+    done.synchronize()
+    host = rb.parts()
+    ok = lists.settle(host[1:])
+    if defer and not comm.all_true(ok, rank, world):
+        # a hinted list outgrew its buffer on some rank: every rank redoes the
+        # step (the overflowing rank's hint is gone, so it counts exactly)
+        return evaluate_partitioned(tree, cfg, rank, world, group=group, comm=comm, results=results,
+                                    before_p2p=before_p2p)
+    if nf in ("fp32", "fp32acc") and int(host[0][0]) != 0:
+        run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag)  # rewrites the near field: add the far field again
+        combine()
     tree.owned_range = (lo, hi)
     if results != "local":
         res = torch.stack([tree.d_phi, tree.d_fx, tree.d_fy, tree.d_fz], 1)
@@ -300,7 +323,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
                 a.copy_(res[:, k])
     ev[8].record(main)
     ev[8].synchronize()
-    pairs, skipped = lists.dev_stats.tolist()
+    pairs, skipped = host[1].tolist()
     stats.p2p_pairs, stats.p2p_skipped, stats.p2p_flops = int(pairs), int(skipped), 20 * int(pairs)
     stats.m2l_calls = lists.n_m2l
     stats.m2p_calls = getattr(lists, "n_m2p", 0)

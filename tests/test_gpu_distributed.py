@@ -33,6 +33,13 @@ class ThreadComm:
         torch.cuda.current_stream().synchronize()
         self.barrier.wait()
 
+    def all_true(self, ok, rank, world):
+        self.bufs[rank] = bool(ok)
+        self.barrier.wait()
+        res = all(self.bufs[r] for r in range(world))
+        self.barrier.wait()
+        return res
+
     def gather_rows(self, full, chunks, rank, world, root=0):
         torch.cuda.current_stream().synchronize()
         self.bufs[rank] = full[int(chunks[rank]):int(chunks[rank + 1])].clone()
@@ -93,6 +100,61 @@ def test_partitioned_equals_single(name, world, precision, strategy):
         for g, w in zip(got, want):
             rel = float(torch.linalg.norm(g - w) / torch.linalg.norm(w))
             assert rel <= 1e-12, (r, rel)
+
+
+def _run_ranks(cfg, trees, comm, world):
+    reps, errs = [None] * world, []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                reps[r] = fd.evaluate_partitioned(trees[r], cfg, r, world, comm=comm)
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            comm.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    return reps
+
+
+@pytest.mark.parametrize("mutual", [False, True])
+def test_partitioned_redo_when_one_rank_overflows(mutual):
+    """Hinted (deferred) lists: when one rank's lists outgrow its capacity
+    hint, every rank redoes the step (comm.all_true) and the result is
+    exact."""
+    from paper_1209_3516_b200 import traversal as trv
+    c = Case("c2_32k")
+    world = 3
+    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", c.theta), p=c.p, precision="fp64", mutual=mutual, task_grain=1500)
+    ref_tree = fb.build_tree(_ps(c), ncrit=c.ncrit)
+    ref = fb.evaluate_on_tree(ref_tree, cfg)
+    want = [a.clone() for a in (ref_tree.d_phi, ref_tree.d_fx, ref_tree.d_fy, ref_tree.d_fz)]
+    comm = ThreadComm(world)
+    trees = [fb.build_tree(_ps(c), ncrit=c.ncrit) for _ in range(world)]
+    _run_ranks(cfg, trees, comm, world)  # leaves capacity hints behind
+    lo1, hi1 = (int(x) for x in trees[1]._dist_plan.cuts[1:3])
+    shrunk = 0
+    for k in list(trv._hint):
+        # rank 1's keys carry its body range (lo, hi): shrink only those
+        rng = k[5:7] if k[0] == "mutual" else k[4:6]
+        if tuple(rng) == (lo1, hi1):
+            trv._hint[k] = (64, 64, 64)
+            shrunk += 1
+    assert shrunk
+    trees = [fb.build_tree(_ps(c), ncrit=c.ncrit) for _ in range(world)]
+    reps = _run_ranks(cfg, trees, comm, world)
+    assert sum(rp.stats.p2p_pairs for rp in reps) == ref.stats.p2p_pairs
+    for r in range(world):
+        got = (trees[r].d_phi, trees[r].d_fx, trees[r].d_fy, trees[r].d_fz)
+        for g, w in zip(got, want):
+            assert float(torch.linalg.norm(g - w) / torch.linalg.norm(w)) <= 1e-12
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
