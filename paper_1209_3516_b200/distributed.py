@@ -135,38 +135,40 @@ class _Plan:
     * ``owned``: this rank's cells (body range inside its own), grouped by
       level, ``top``: cells straddling an interior cut, grouped by level --
       both as (device id list, host level offsets) for ``fmm_upward``.
-    Three small device-to-host reads, no host copies of cell arrays."""
+    One small device-to-host read, no host copies of cell arrays."""
 
     def __init__(self, tree, world: int, rank: int):
         n, dev = tree.n, tree.device
-        at = torch.tensor([r * n // world for r in range(1, world)], dtype=torch.int64, device=dev)
-        inner = tree.d_start[tree.d_body_leaf[at].long()].tolist() if world > 1 else []
-        cuts = [0]
-        for c in inner:
-            cuts.append(max(int(c), cuts[-1]))
-        cuts.append(n)
-        self.cuts = np.asarray(cuts, np.int64)
+        i64 = torch.int64
         start = tree.d_start.long()
         end = tree.d_end.long()
-        bounds = torch.as_tensor(self.cuts, device=dev)
-        self.chunks = torch.searchsorted(start, bounds, side="left").cpu().numpy().astype(np.int64)
-        shared = torch.zeros(tree.ncells, dtype=torch.bool, device=dev)
-        for c in self.cuts[1:-1]:
-            shared |= (start < int(c)) & (end > int(c))
-        lo, hi = int(self.cuts[rank]), int(self.cuts[rank + 1])
-        own = (start >= lo) & (end <= hi)
+        if world > 1:
+            at = torch.tensor([r * n // world for r in range(1, world)], dtype=i64, device=dev)
+            inner = torch.cummax(start[tree.d_body_leaf[at].long()], 0).values
+        else:
+            inner = torch.zeros(0, dtype=i64, device=dev)
+        cuts = torch.cat([torch.zeros(1, dtype=i64, device=dev), inner, torch.full((1,), n, dtype=i64, device=dev)])
+        chunks = torch.searchsorted(start, cuts, side="left")
+        shared = ((start[:, None] < inner[None, :]) & (end[:, None] > inner[None, :])).any(1)
+        own = (start >= cuts[rank]) & (end <= cuts[rank + 1])
+        # own cells, then shared ones, then the rest: a stable split of the
+        # level-grouped cell list keeps each part level-grouped
         bfs = tree.d_cells_by_level.long()
-        lev = tree.d_level.long()[bfs]
+        group = torch.where(own, 0, torch.where(shared, 1, 2))[bfs]
+        order = torch.argsort(group, stable=True)
+        parts = bfs[order].to(torch.int32)
+        nl = 32
+        counts = torch.bincount(group * nl + tree.d_level.long()[bfs], minlength=3 * nl)
+        # everything the host needs in ONE device-to-host read
+        host = torch.cat([cuts, chunks, counts]).cpu().numpy().astype(np.int64)
+        self.cuts = host[:world + 1]
+        self.chunks = host[world + 1:2 * world + 2]
+        cnt = host[2 * world + 2:].reshape(3, nl)
         depth = len(tree.level_off) - 2
-        counts = []
-        self.lists = []
-        for mask in (own, shared):
-            sel = mask[bfs]
-            self.lists.append(bfs[sel].to(torch.int32))  # level-grouped (bfs is)
-            counts.append(torch.bincount(lev[sel], minlength=depth + 1))
-        both = torch.stack(counts).tolist()
-        self.owned = (self.lists[0], [0] + list(np.cumsum(both[0]).astype(int)))
-        self.top = (self.lists[1], [0] + list(np.cumsum(both[1]).astype(int)))
+        n_own, n_top = int(cnt[0].sum()), int(cnt[1].sum())
+        self.lists = [parts[:n_own], parts[n_own:n_own + n_top]]
+        self.owned = (self.lists[0], [0] + list(np.cumsum(cnt[0][:depth + 1]).astype(int)))
+        self.top = (self.lists[1], [0] + list(np.cumsum(cnt[1][:depth + 1]).astype(int)))
 
 
 def _upward_cells(tree, p, cells, off, M):
