@@ -207,6 +207,21 @@ FMM_API int fmm_traverse(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1
  * _owner_map, src/traversal.py:621-640): owner[c] = the partition root
  * (maximal subtree with < grain bodies, leaves included) holding cell c,
  * -1 above the partition.  grain >= 1 (EvalConfig.task_grain). */
+/* One rank's share of the tree for the Morton-partitioned evaluation
+ * (paper_1209_3516_b200/distributed.py; the reference's target ownership,
+ * src/traversal.py:19-26, :621-639): body cuts on leaf boundaries (cut r =
+ * the start of the leaf holding body r*n/world, made non-decreasing), the
+ * cells whose first body lies in each rank's range (chunks), and the
+ * level-grouped lists of this rank's own cells (body range inside its own)
+ * and of the cells straddling an interior cut, in cells_by_level order.
+ * host_out (2*(world+1) + 96 int64) receives {cuts[world+1], chunks[world+1],
+ * counts[3][32]} (counts by (own, shared, other) x level) in ONE copy; the
+ * call synchronises.  own_cells / shared_cells hold ncells each. */
+FMM_API int fmm_partition_plan(int32_t ncells, int64_t n, int world, int rank, const int32_t *start,
+                       const int32_t *end, const int32_t *body_leaf, const int32_t *cells_by_level,
+                       const int8_t *level, int32_t *own_cells, int32_t *shared_cells, int64_t *host_out,
+                       void *ws, size_t ws_bytes, void *stream);
+
 FMM_API int fmm_partition_owner(int32_t ncells, const int32_t *parent, const uint8_t *leaf, const int32_t *start,
                         const int32_t *end, int64_t grain, int32_t *owner, void *stream);
 

@@ -49,6 +49,7 @@ SIGNATURES = {
     "fmm_traverse": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, INT, INT, DBL, P, P, I64,
                      P, P, I64, P, P],
     "fmm_pairs_to_rows": [P, P, P, I64, I32, I32, INT, P, P, P, SZ, P],
+    "fmm_partition_plan": [I32, I64, INT, INT, P, P, P, P, P, P, P, P, P, SZ, P],
     "fmm_partition_owner": [I32, P, P, P, P, I64, P, P],
     "fmm_traverse_mutual": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64,
                             P, P],

@@ -138,35 +138,22 @@ class _Plan:
     One small device-to-host read, no host copies of cell arrays."""
 
     def __init__(self, tree, world: int, rank: int):
-        n, dev = tree.n, tree.device
-        i64 = torch.int64
-        start = tree.d_start.long()
-        end = tree.d_end.long()
-        if world > 1:
-            at = torch.tensor([r * n // world for r in range(1, world)], dtype=i64, device=dev)
-            inner = torch.cummax(start[tree.d_body_leaf[at].long()], 0).values
-        else:
-            inner = torch.zeros(0, dtype=i64, device=dev)
-        cuts = torch.cat([torch.zeros(1, dtype=i64, device=dev), inner, torch.full((1,), n, dtype=i64, device=dev)])
-        chunks = torch.searchsorted(start, cuts, side="left")
-        shared = ((start[:, None] < inner[None, :]) & (end[:, None] > inner[None, :])).any(1)
-        own = (start >= cuts[rank]) & (end <= cuts[rank + 1])
-        # own cells, then shared ones, then the rest: a stable split of the
-        # level-grouped cell list keeps each part level-grouped
-        bfs = tree.d_cells_by_level.long()
-        group = torch.where(own, 0, torch.where(shared, 1, 2))[bfs]
-        order = torch.argsort(group, stable=True)
-        parts = bfs[order].to(torch.int32)
+        from . import _lib
+        P = _lib.ptr
+        dev, ncells = tree.device, tree.ncells
+        own = torch.empty(ncells, dtype=torch.int32, device=dev)
+        top = torch.empty(ncells, dtype=torch.int32, device=dev)
         nl = 32
-        counts = torch.bincount(group * nl + tree.d_level.long()[bfs], minlength=3 * nl)
-        # everything the host needs in ONE device-to-host read
-        host = torch.cat([cuts, chunks, counts]).cpu().numpy().astype(np.int64)
-        self.cuts = host[:world + 1]
-        self.chunks = host[world + 1:2 * world + 2]
+        host = np.zeros(2 * (world + 1) + 3 * nl, np.int64)
+        wsp, wsb = _lib.workspace(ncells + 1, dev)
+        _lib.call("fmm_partition_plan", ncells, tree.n, world, rank, P(tree.d_start), P(tree.d_end),
+                  P(tree.d_body_leaf), P(tree.d_cells_by_level), P(tree.d_level), P(own), P(top),
+                  host.ctypes.data, wsp, wsb, _lib.stream_handle())
+        self.cuts = host[:world + 1].copy()
+        self.chunks = host[world + 1:2 * world + 2].copy()
         cnt = host[2 * world + 2:].reshape(3, nl)
         depth = len(tree.level_off) - 2
-        n_own, n_top = int(cnt[0].sum()), int(cnt[1].sum())
-        self.lists = [parts[:n_own], parts[n_own:n_own + n_top]]
+        self.lists = [own[:int(cnt[0].sum())], top[:int(cnt[1].sum())]]
         self.owned = (self.lists[0], [0] + list(np.cumsum(cnt[0][:depth + 1]).astype(int)))
         self.top = (self.lists[1], [0] + list(np.cumsum(cnt[1][:depth + 1]).astype(int)))
 

@@ -22,6 +22,9 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--mutual", action="store_true")
+    ap.add_argument("--world", type=int, default=1, help="time rank --rank of a W-rank partitioned evaluation "
+                    "(exchanges as no-ops, tools/rank_probe.py)")
+    ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--gap-us", type=float, default=8.0)
     ap.add_argument("--host", action="store_true", help="interleave host events: every C-ABI call (call:NAME) "
                     "and Python phase (py:NAME) with the device kernels")
@@ -38,7 +41,13 @@ def main():
 
     def step():
         t = fb.build_tree(ps, ncrit=solver["ncrit"])
-        fb.evaluate_on_tree(t, cfg)
+        if args.world > 1:
+            from paper_1209_3516_b200 import distributed as fd
+            sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+            from rank_probe_comm import NoComm
+            fd.evaluate_partitioned(t, cfg, args.rank, args.world, comm=NoComm(), results="root")
+        else:
+            fb.evaluate_on_tree(t, cfg)
 
     for _ in range(4):
         step()
