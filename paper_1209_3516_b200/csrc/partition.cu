@@ -26,20 +26,28 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t n, 
     return lo;
 }
 
-// one thread: cuts (running max of the leaf starts) and chunks
+// one warp: lane r the cut of rank boundary r (a warp max-scan makes them
+// non-decreasing), then lane r the chunk bound of cut r (world <= 31 per
+// pass; more ranks loop)
 __global__ void plan_cuts(int32_t ncells, int64_t n, int world, const int32_t *__restrict__ start,
                           const int32_t *__restrict__ body_leaf, int64_t *cuts, int64_t *chunks) {
-    if (threadIdx.x != 0) return;
-    int64_t run = 0;
-    cuts[0] = 0;
-    for (int r = 1; r < world; r++) {
-        const int64_t at = (int64_t)r * n / world;
-        const int64_t c = start[body_leaf[at]];
-        run = c > run ? c : run;
-        cuts[r] = run;
+    const int lane = threadIdx.x & 31;
+    int64_t carry = 0;
+    for (int r0 = 0; r0 <= world; r0 += 32) {
+        const int r = r0 + lane;
+        int64_t c = 0;
+        if (r >= 1 && r < world) c = start[body_leaf[(int64_t)r * n / world]];
+        if (r == world) c = n;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, c, o);
+            if (lane >= o && v > c) c = v;
+        }
+        if (carry > c) c = carry;
+        if (r <= world) cuts[r] = c;
+        carry = __shfl_sync(0xffffffffu, c, 31);
     }
-    cuts[world] = n;
-    for (int r = 0; r <= world; r++) chunks[r] = lower_bound_i32(start, ncells, cuts[r]);
+    __syncwarp();
+    for (int r = lane; r <= world; r += 32) chunks[r] = lower_bound_i32(start, ncells, cuts[r]);
 }
 
 // per position of cells_by_level: own / shared flags and the per-(group,

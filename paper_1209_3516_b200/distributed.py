@@ -209,7 +209,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     comm = comm or TorchDistComm(group)
     from . import _lib
     from .kernels import KernelStats, ncoef
-    from .traversal import (EndReadback, EvalReport, critical_path, interaction_lists, listfmm_lists,
+    from .traversal import (EndReadback, EvalReport, _EventPool, critical_path, interaction_lists, listfmm_lists,
                             mutual_lists, _near_field, run_m2l, run_m2p, run_p2p, treecode_lists)
     from .tree import downward_pass
 
@@ -230,13 +230,17 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     from .traversal import _side_stream
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
+    E = _EventPool(dev)
+    ev = [E() for _ in range(9)]
     ev[0].record(main)
     nc = ncoef(cfg.p)
-    M = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
-    L = torch.zeros((tree.ncells, nc), dtype=torch.float64, device=dev)
-    far = torch.zeros((4, tree.n), dtype=torch.float64, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    # the expansions, the far-field accumulators and the flag share one fill
+    nm = tree.ncells * nc
+    buf = torch.zeros(2 * nm + 4 * tree.n + 1, dtype=torch.float64, device=dev)
+    M = buf[:nm].view(tree.ncells, nc)
+    L = buf[nm:2 * nm].view(tree.ncells, nc)
+    far = buf[2 * nm:2 * nm + 4 * tree.n].view(4, tree.n)
+    flag = buf[-1:].view(torch.int32)[:1]
     # far field, side stream: owned upward, all-gather, shared top rebuilt
     # redundantly -- beside the main stream's traversal, which needs no moments
     side.wait_event(ev[0])
@@ -250,7 +254,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
             _upward_cells(tree, cfg.p, top, toff, M)
         ev[1].record(side)
     tree._M, tree.p, tree._L = M, cfg.p, L
-    ready = torch.cuda.Event()
+    ready = E()
     if treecode:  # the rank's target leaves walk the whole (replicated) tree
         lists = treecode_lists(tree, cfg.mac, body_range=(lo, hi), m2p_ready=ready, side=side)
     elif cfg.strategy == "listfmm":
@@ -286,7 +290,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     combine()
     # one read-back of the FP32 flag and the list / pair counters
     rb = EndReadback([flag] + lists.device_counters())
-    done = torch.cuda.Event()
+    done = E()
     done.record(main)
     done.synchronize()
     host = rb.parts()
