@@ -1,7 +1,7 @@
 """bench.py -- whole-FMM throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2] [--precision fp32|fp64]
+                    [--config C2] [--precision fp32|fp32acc|fp64]
 
 One step = one full FMM over the configuration's synthetic cloud: tree build
 (keys, sort, carve, geometry) + upward + dual traversal (lists, M2L, P2P) +
@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--n", type=int, default=0, help="override N (testing)")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp32acc", "fp64"])
     ap.add_argument("--p", type=int, default=0, help="override the expansion order (C4 sweep)")
     ap.add_argument("--theta", type=float, default=0.0, help="override theta (C4 sweep)")
     ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode", "listfmm"],
@@ -432,7 +432,8 @@ def run_ours(args):
         "step_ms": {"min": 1e3 * float(np.min(times)), "median": 1e3 * float(np.median(times)),
                     "max": 1e3 * float(np.max(times)), "all": [round(1e3 * t, 3) for t in times]},
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 P2P / f64 tree+far field" if args.precision == "fp32" else "f64",
+        "dtype": {"fp32": "f32 P2P / f64 tree+far field", "fp32acc": "f32 P2P terms, f64 sums / f64 tree+far field",
+                  "fp64": "f64"}[args.precision],
         "data": "synthetic", "config": config_block(args, n, solver, {"precision": args.precision,
                                                                       "parallelism": f"morton-partition x{world}"
                                                                       + (" sharded+halo" if sharded else "")}),

@@ -34,8 +34,9 @@ plan's runs point past the targets.  ``mutual=True``
 runs the mutual traversal (``mutual_lists``): the reference's mutual list
 sets, partition demotion included, written directed so the same M2L / P2P
 executors evaluate them.
-``precision`` is a new knob: "fp64" (default, the reference's arithmetic)
-or "fp32" (FP32 near field; far field stays float64).
+``precision`` is a new knob: "fp64" (default, the reference's arithmetic),
+"fp32" (FP32 near field; far field stays float64) or "fp32acc" (float32
+pair terms summed in float64; ~1e-7 near-field floor for ~5 % more time).
 """
 
 from __future__ import annotations
@@ -54,7 +55,7 @@ from .mac import MacConfig
 from .tree import Tree, downward_pass, upward_pass
 
 STRATEGIES = ("treecode", "listfmm", "dualtree")
-PRECISIONS = ("fp64", "fp32")
+PRECISIONS = ("fp64", "fp32", "fp32acc")
 REPORT_SCHEMA = "fmmkit-report-v1"
 
 __all__ = ["STRATEGIES", "PRECISIONS", "EvalConfig", "EvalReport", "evaluate_dual_tree", "evaluate_list_fmm",
@@ -589,7 +590,8 @@ LISTFMM_THETA_EQ = 3 ** 0.5 / 2
 
 
 def near_field_precision(cfg: "EvalConfig") -> str:
-    """Arithmetic of the near field for ``cfg``: "fp64" for precision="fp64";
+    """Arithmetic of the near field for ``cfg``: "fp64" / "fp32acc" for those
+    precisions;
     for precision="fp32", "fp32" unless theta^p < FP32_GUARD_THETA_P, then
     "fp32acc" down to FP32ACC_THETA_P and "fp64" below (see above;
     FMM_B200_FP32_STRICT=1 disables the promotion).
@@ -599,8 +601,8 @@ def near_field_precision(cfg: "EvalConfig") -> str:
         if force not in NEAR_FIELDS:
             raise ValueError(f"FMM_B200_NEAR_FIELD={force!r}: one of {NEAR_FIELDS}")
         return force
-    if cfg.precision == "fp64":
-        return "fp64"
+    if cfg.precision in ("fp64", "fp32acc"):
+        return cfg.precision
     if os.environ.get("FMM_B200_FP32_STRICT", "0") == "1":
         return "fp32"
     theta = LISTFMM_THETA_EQ if cfg.strategy == "listfmm" else cfg.mac.theta

@@ -223,6 +223,7 @@ def test_fp32_promotion_rule(monkeypatch):
     assert sorted(k for k, v in nf.items() if v == "fp32acc") == [(8, 0.3), (10, 0.4)]
     assert sorted(k for k, v in nf.items() if v == "fp64") == [(10, 0.3)]
     assert near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", 0.3), p=10, precision="fp64")) == "fp64"
+    assert near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", 0.4), p=4, precision="fp32acc")) == "fp32acc"
     monkeypatch.setenv("FMM_B200_NEAR_FIELD", "fp32acc")
     assert near_field_precision(fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=4, precision="fp64")) == "fp32acc"
     monkeypatch.setenv("FMM_B200_NEAR_FIELD", "bf16")

@@ -14,6 +14,7 @@ case "$1" in
 bench)
   python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
   python bench.py --precision fp64 --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_fp64.json 2> gpurun_out/bench_c2_fp64.err
+  python bench.py --precision fp32acc --steps 10 --no-cpu-baseline > gpurun_out/bench_c2_fp32acc.json 2> gpurun_out/bench_c2_fp32acc.err
   for c in C1 C3 C5; do
     python bench.py --config $c --steps 5 --warmup 5 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   done
