@@ -122,3 +122,18 @@ def test_grouped_inside_evaluations(strategy, mutual, p):
     assert sa.m2l_calls == sb.m2l_calls and sa.p2p_pairs == sb.p2p_pairs
     for k in ("phi", "fx", "fy", "fz"):
         assert rel_l2(getattr(b, k), getattr(a, k)) <= 1e-12, k
+
+
+@pytest.mark.parametrize("n,ncrit", [(20, 64), (300, 8)])
+def test_grouped_tiny_trees(n, ncrit):
+    """No M2L pair at all (one leaf) and a few pairs: the grouped path
+    equals the per-pair kernels (zeros when there is nothing to do)."""
+    pos, q = workloads.config4(n, 11)
+    t = _tree(pos, q, ncrit=ncrit)
+    fb.upward_pass(t, 8)
+    lists = fb.interaction_lists(t, fb.MacConfig("fmm", 0.5))
+    a, b = _m2l(t, lists, 8, False), _m2l(t, lists, 8, True)
+    if not np.any(a):
+        assert not np.any(b)
+    else:
+        assert rel_l2(b, a) <= REORDER_TOL
