@@ -6,8 +6,9 @@
 // Float64 throughout (these passes are <1% of the flops; they keep the
 // reference's 1e-12 agreement).  For p <= 5 (the BASELINE orders) M2M, L2L
 // and L2P are compiled per order with every multi-index a constant and a
-// thread owning a whole cell or body; for higher orders a thread owns one
-// (cell, coefficient) with runtime term loops.  Every write is private.
+// thread owning a whole cell or body; for higher orders a warp applies each
+// M2M / L2L shift as three separable 1-D passes (m2m_sep / l2l_sep) and a
+// thread owns a body's L2P.  Every write is private.
 #include "taylor.cuh"
 
 namespace fmm {
@@ -80,44 +81,139 @@ __global__ void __launch_bounds__(kP2MWarps * 32) p2m_kernel(
     }
 }
 
-// ---- M2M: thread per (internal cell of this level, coefficient m) --------
-// Mdst[m] += sum_child sum_{k<=m} Msrc[k] t^{m-k}/(m-k)!, t = c_child - c_parent
-// (src/_taylor.py:146-166); the powers t^a/a! are carried as running
-// products inside the loops, so nothing spills to local memory.
-__global__ void m2m_level(int p, const int32_t *__restrict__ cells, int32_t count,
-                          const uint8_t *__restrict__ leaf, const int32_t *__restrict__ children,
-                          const double *__restrict__ ctr, double *M) {
-    const int nc = ncoef(p);
-    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < (int64_t)count * nc;
-         it += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t c = cells[it / nc];
-        const int m = (int)(it % nc);
+// ---- P >= 6: warp per cell, separable translation passes ----------------
+// The shift operators factor over the axes: t^(m-k)/(m-k)! and the L2L
+// weight C(n,k) t^(n-k) are products of one factor per axis, so a warp
+// applies a translation as three 1-D passes over the expansion (z, then y,
+// then x), each staying inside the |m| < p index set: ~3 x 220 x 3.3 FMAs
+// per child link at p = 10 instead of the 5005 terms x 3 flops of the
+// direct sum the runtime kernels above walk per coefficient.  Same terms,
+// summed in another order (multipoles / locals agree to rounding).
+__host__ __device__ constexpr int sep_idx(int x, int y, int z) {  // graded-lex index of (x, y, z)
+    return (x + y + z) * (x + y + z + 1) * (x + y + z + 2) / 6 + (y + z) * (y + z + 1) / 2 + z;
+}
+constexpr int kSepWarps = 4;
+__constant__ double c_binom[TMAX + 1][TMAX + 1];
+
+__global__ void __launch_bounds__(kSepWarps * 32) m2m_sep(int p, const int32_t *__restrict__ cells, int32_t count,
+                                                         const uint8_t *__restrict__ leaf,
+                                                         const int32_t *__restrict__ children,
+                                                         const double *__restrict__ ctr, double *M) {
+    extern __shared__ double sep_sm[];
+    const int nc = ncoef(p), lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *b0 = sep_sm + w * (2 * nc + 3 * (TMAX + 1)), *b1 = b0 + nc, *pw = b1 + nc;  // pw[3][TMAX+1]
+    constexpr int NS = (ncoef(TMAX) + 31) / 32;
+    for (int32_t wi = blockIdx.x * kSepWarps + w; wi < count; wi += gridDim.x * kSepWarps) {
+        const int32_t c = cells[wi];
         if (leaf[c]) continue;
-        const int mx = d_tab.mi[m][0], my = d_tab.mi[m][1], mz = d_tab.mi[m][2];
-        double total = 0.0;
+        double acc[NS];
+#pragma unroll
+        for (int j = 0; j < NS; j++) acc[j] = 0.0;
         for (int o = 0; o < 8; o++) {
             const int32_t ch = children[c * 8 + o];
             if (ch < 0) continue;
-            const double tx = ctr[ch * 3] - ctr[c * 3], ty = ctr[ch * 3 + 1] - ctr[c * 3 + 1],
-                         tz = ctr[ch * 3 + 2] - ctr[c * 3 + 2];
-            const double *Ms = M + (int64_t)ch * nc;
-            double acc = 0.0, fx = 1.0;
-            for (int a = 0; a <= mx; a++) {          // a = mx - kx
-                double fy = 1.0;
-                for (int b = 0; b <= my; b++) {      // b = my - ky
-                    double fz = 1.0;
-                    for (int g = 0; g <= mz; g++) {  // g = mz - kz
-                        acc += Ms[d_tab.idx3[mx - a][my - b][mz - g]] * (fx * fy * fz);
-                        fz = fz * tz * d_tab.rcp[g + 1];
-                    }
-                    fy = fy * ty * d_tab.rcp[b + 1];
+            for (int q = lane; q < nc; q += 32) b0[q] = M[(int64_t)ch * nc + q];
+            if (lane < 3) {  // t_a^j / j!, as the runtime kernel forms them
+                const double t = ctr[ch * 3 + lane] - ctr[c * 3 + lane];
+                double f = 1.0;
+                for (int j = 0; j < p; j++) {
+                    pw[lane * (TMAX + 1) + j] = f;
+                    f = f * t * d_tab.rcp[j + 1];
                 }
-                fx = fx * tx * d_tab.rcp[a + 1];
             }
-            total += acc;
+            __syncwarp();
+            for (int q = lane; q < nc; q += 32) {  // z: (x, y, kz) -> (x, y, mz)
+                const int x = d_tab.mi[q][0], y = d_tab.mi[q][1], z = d_tab.mi[q][2];
+                double a = 0.0;
+                for (int k = 0; k <= z; k++) a = fma(b0[sep_idx(x, y, k)], pw[2 * (TMAX + 1) + z - k], a);
+                b1[q] = a;
+            }
+            __syncwarp();
+            for (int q = lane; q < nc; q += 32) {  // y
+                const int x = d_tab.mi[q][0], y = d_tab.mi[q][1], z = d_tab.mi[q][2];
+                double a = 0.0;
+                for (int k = 0; k <= y; k++) a = fma(b1[sep_idx(x, k, z)], pw[(TMAX + 1) + y - k], a);
+                b0[q] = a;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < NS; j++) {  // x, into the lane's outputs
+                const int q = lane + 32 * j;
+                if (q < nc) {
+                    const int x = d_tab.mi[q][0], y = d_tab.mi[q][1], z = d_tab.mi[q][2];
+                    double a = acc[j];
+                    for (int k = 0; k <= x; k++) a = fma(b0[sep_idx(k, y, z)], pw[x - k], a);
+                    acc[j] = a;
+                }
+            }
+            __syncwarp();  // b0 / pw are rewritten by the next child
         }
-        M[(int64_t)c * nc + m] += total;
+#pragma unroll
+        for (int j = 0; j < NS; j++) {
+            const int q = lane + 32 * j;
+            if (q < nc) M[(int64_t)c * nc + q] += acc[j];
+        }
     }
+}
+
+__global__ void __launch_bounds__(kSepWarps * 32) l2l_sep(int p, const int32_t *__restrict__ cells, int32_t count,
+                                                         const int32_t *__restrict__ parent,
+                                                         const double *__restrict__ ctr, double *L) {
+    extern __shared__ double sep_sm[];
+    const int nc = ncoef(p), lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *b0 = sep_sm + w * (2 * nc + 3 * (TMAX + 1)), *b1 = b0 + nc, *pw = b1 + nc;
+    for (int32_t wi = blockIdx.x * kSepWarps + w; wi < count; wi += gridDim.x * kSepWarps) {
+        const int32_t c = cells[wi];
+        const int32_t pa = parent[c];
+        if (pa < 0) continue;
+        for (int q = lane; q < nc; q += 32) b0[q] = L[(int64_t)pa * nc + q];
+        if (lane < 3) {  // t_a^j
+            const double t = ctr[c * 3 + lane] - ctr[pa * 3 + lane];
+            double f = 1.0;
+            for (int j = 0; j < p; j++) {
+                pw[lane * (TMAX + 1) + j] = f;
+                f *= t;
+            }
+        }
+        __syncwarp();
+        for (int q = lane; q < nc; q += 32) {  // z: (x, y, nz) -> (x, y, kz), sum over nz >= kz
+            const int x = d_tab.mi[q][0], y = d_tab.mi[q][1], k = d_tab.mi[q][2];
+            double a = 0.0;
+            for (int n = k; n < p - x - y; n++) a = fma(b0[sep_idx(x, y, n)], c_binom[n][k] * pw[2 * (TMAX + 1) + n - k], a);
+            b1[q] = a;
+        }
+        __syncwarp();
+        for (int q = lane; q < nc; q += 32) {  // y
+            const int x = d_tab.mi[q][0], k = d_tab.mi[q][1], z = d_tab.mi[q][2];
+            double a = 0.0;
+            for (int n = k; n < p - x - z; n++) a = fma(b1[sep_idx(x, n, z)], c_binom[n][k] * pw[(TMAX + 1) + n - k], a);
+            b0[q] = a;
+        }
+        __syncwarp();
+        for (int q = lane; q < nc; q += 32) {  // x, added to the child's locals
+            const int k = d_tab.mi[q][0], y = d_tab.mi[q][1], z = d_tab.mi[q][2];
+            double a = 0.0;
+            for (int n = k; n < p - y - z; n++) a = fma(b0[sep_idx(n, y, z)], c_binom[n][k] * pw[n - k], a);
+            L[(int64_t)c * nc + q] += a;
+        }
+        __syncwarp();  // b0 / b1 / pw are rewritten by the next cell
+    }
+}
+
+static int sep_smem(int p) { return kSepWarps * (2 * ncoef(p) + 3 * (TMAX + 1)) * (int)sizeof(double); }
+
+static void sep_tables() {  // binomials up to TMAX, once per device
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return;
+    double b[TMAX + 1][TMAX + 1] = {};
+    for (int n = 0; n <= TMAX; n++) {
+        b[n][0] = 1.0;
+        for (int k = 1; k <= n; k++) b[n][k] = b[n - 1][k - 1] + (k <= n - 1 ? b[n - 1][k] : 0.0);
+    }
+    cudaMemcpyToSymbol(c_binom, b, sizeof(b));
+    if (dev < 64) done[dev] = true;
 }
 
 // ---- P <= 5: thread per cell, every multi-index compile-time -------------
@@ -208,42 +304,6 @@ __global__ void __launch_bounds__(128) l2l_cell_kernel(const int32_t *__restrict
             constexpr double inv = 1.0 / kTab.mfact[k];
             L[(int64_t)c * NC + k] += a * inv;
         });
-    }
-}
-
-// ---- L2L: thread per (cell of this level, coefficient k), pull from parent
-// Ldst[k] += (1/k!) sum_{n>=k} Lsrc[n] n! t^{n-k}/(n-k)!,  t = c_child - c_parent
-// (src/_taylor.py:220-240), running products as in M2M.
-__global__ void l2l_level(int p, const int32_t *__restrict__ cells, int32_t count,
-                          const int32_t *__restrict__ parent, const double *__restrict__ ctr,
-                          double *L) {
-    const int nc = ncoef(p);
-    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < (int64_t)count * nc;
-         it += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t c = cells[it / nc];
-        const int k = (int)(it % nc);
-        const int32_t pa = parent[c];
-        if (pa < 0) continue;
-        const int kx = d_tab.mi[k][0], ky = d_tab.mi[k][1], kz = d_tab.mi[k][2];
-        const int rem = p - 1 - (kx + ky + kz);  // max degree of n-k
-        const double tx = ctr[c * 3] - ctr[pa * 3], ty = ctr[c * 3 + 1] - ctr[pa * 3 + 1],
-                     tz = ctr[c * 3 + 2] - ctr[pa * 3 + 2];
-        const double *Ls = L + (int64_t)pa * nc;
-        double acc = 0.0, fx = 1.0;
-        for (int ax = 0; ax <= rem; ax++) {
-            double fy = 1.0;
-            for (int ay = 0; ay <= rem - ax; ay++) {
-                double fz = 1.0;
-                for (int az = 0; az <= rem - ax - ay; az++) {
-                    const int n = d_tab.idx3[kx + ax][ky + ay][kz + az];
-                    acc += Ls[n] * d_tab.mfact[n] * (fx * fy * fz);
-                    fz = fz * tz * d_tab.rcp[az + 1];
-                }
-                fy = fy * ty * d_tab.rcp[ay + 1];
-            }
-            fx = fx * tx * d_tab.rcp[ax + 1];
-        }
-        L[(int64_t)c * nc + k] += acc * (d_tab.ifact[kx] * d_tab.ifact[ky] * d_tab.ifact[kz]);
     }
 }
 
@@ -424,8 +484,8 @@ int fmm_upward(int p, int32_t ncells, const int32_t *children, const int32_t *st
             M2M_CELL(1) M2M_CELL(2) M2M_CELL(3) M2M_CELL(4) M2M_CELL(5)
 #undef M2M_CELL
             default:
-                m2m_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, leaf,
-                                                                          children, ctr, M);
+                m2m_sep<<<grid_for(cnt, kSepWarps, 148 * 16), kSepWarps * 32, sep_smem(p), s>>>(
+                    p, cells_by_level + off, cnt, leaf, children, ctr, M);
         }
         fmm::note_launch();
     }
@@ -451,8 +511,9 @@ int fmm_downward(int p, int32_t ncells, const int32_t *parent, const uint8_t *le
             L2L_CELL(1) L2L_CELL(2) L2L_CELL(3) L2L_CELL(4) L2L_CELL(5)
 #undef L2L_CELL
             default:
-                l2l_level<<<grid_for((int64_t)cnt * nc, 128), 128, 0, s>>>(p, cells_by_level + off, cnt, parent,
-                                                                          ctr, L);
+                sep_tables();
+                l2l_sep<<<grid_for(cnt, kSepWarps, 148 * 16), kSepWarps * 32, sep_smem(p), s>>>(
+                    p, cells_by_level + off, cnt, parent, ctr, L);
         }
         fmm::note_launch();
     }
