@@ -51,3 +51,12 @@ def test_tune_csv_and_input_file(tmp_path):
 def test_listfmm_on_rect_tree_is_a_usage_error(capsys):
     assert cli.main(["run", "--n", "500", "--strategy", "listfmm", "--shape", "rect", "--reps", "1"]) == 2
     assert "cubic" in capsys.readouterr().err
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp32acc"])
+def test_run_precisions(tmp_path, precision):
+    out = tmp_path / "run.json"
+    assert cli.main(["run", "--n", "4000", "--p", "8", "--theta", "0.4", "--reps", "1", "--precision", precision,
+                     "--output", str(out)]) == 0
+    doc = json.loads(out.read_text())
+    assert doc["precision"] == precision
