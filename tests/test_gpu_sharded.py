@@ -69,6 +69,20 @@ def _worker(rank, world, port, out):
             lo, hi = t.shard["own"]
             out[(rank, name, mutual)] = (same_tree, err, int(pairs.item()), int(rrep.stats.p2p_pairs),
                                          hi - lo, t.shard["halo_bodies"], n)
+        # a cloud smaller than the rank count: empty shards and empty own ranges
+        rng = np.random.default_rng(3)
+        pos = rng.random((3, 3))
+        qq = rng.random(3)
+        cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=4)
+        ref = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], qq), ncrit=2)
+        fb.evaluate_on_tree(ref, cfg)
+        want = ref.results_in_input_order()
+        a, b = rank * 3 // world, (rank + 1) * 3 // world
+        t = sharded.build_tree_sharded(pos[a:b, 0], pos[a:b, 1], pos[a:b, 2], qq[a:b], 2, rank, world)
+        _, res = sharded.evaluate_sharded(t, cfg)
+        ok = all(np.allclose(g.cpu().numpy(), np.asarray(getattr(want, k))[a:b], rtol=1e-12, atol=0)
+                 for g, k in zip(res, ("phi", "fx", "fy", "fz")))
+        out[(rank, "tiny")] = (ok, b - a)
     finally:
         dist.destroy_process_group()
 
@@ -90,3 +104,5 @@ def test_sharded_processes_match_single_gpu(world):
                 assert nown + halo < n, (name, r)
             owned += nown
         assert owned == n
+    assert all(out[(r, "tiny")][0] for r in range(world))
+    assert sum(out[(r, "tiny")][1] for r in range(world)) == 3
