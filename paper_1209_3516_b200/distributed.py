@@ -210,7 +210,7 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
     from . import _lib
     from .kernels import KernelStats, ncoef
     from .traversal import (EndReadback, EvalReport, _EventPool, critical_path, interaction_lists, listfmm_lists,
-                            mutual_lists, _near_field, run_m2l, run_m2p, run_p2p, treecode_lists)
+                            m2l_grouped, mutual_lists, _near_field, run_m2l, run_m2p, run_p2p, treecode_lists)
     from .tree import downward_pass
 
     if world == 1:
@@ -255,17 +255,19 @@ def evaluate_partitioned(tree, cfg, rank: int, world: int, group=None, comm=None
         ev[1].record(side)
     tree._M, tree.p, tree._L = M, cfg.p, L
     ready = E()
+    sort_far = not m2l_grouped(tree, cfg.p)  # (the grouped M2L orders its pairs itself)
     if treecode:  # the rank's target leaves walk the whole (replicated) tree
         lists = treecode_lists(tree, cfg.mac, body_range=(lo, hi), m2p_ready=ready, side=side)
     elif cfg.strategy == "listfmm":
-        lists = listfmm_lists(tree, body_range=(lo, hi), m2l_ready=ready, side=side)
+        lists = listfmm_lists(tree, body_range=(lo, hi), m2l_ready=ready, side=side, sort_far=sort_far)
     elif cfg.mutual:  # the rank's targets of the mutual lists (directed-expanded)
         lists = mutual_lists(tree, cfg.mac, cfg.task_grain, body_range=(lo, hi), m2l_ready=ready, side=side,
-                             defer=defer)
+                             defer=defer, sort_far=sort_far)
     else:
         # hinted lists do not wait for their counters; an overflow on any rank
         # is caught at the end and every rank redoes the step (comm.all_true)
-        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side, defer=defer)
+        lists = interaction_lists(tree, cfg.mac, body_range=(lo, hi), m2l_ready=ready, side=side, defer=defer,
+                                  sort_far=sort_far)
     ev[2].record(main)
     side.wait_event(ready)
     with torch.cuda.stream(side):

@@ -252,7 +252,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
                       m2l_ready: torch.cuda.Event | None = None,
                       side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False,
                       src: Tree | None = None, defer: bool = True,
-                      target_mask: torch.Tensor | None = None) -> Lists:
+                      target_mask: torch.Tensor | None = None, sort_far: bool = True) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
 
@@ -294,7 +294,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
         items = max(cap_p2p, cap_m2l, tree.n, ncells + 1)
         wsp, wsb = _lib.workspace(items, dev, stream=torch.cuda.current_stream())
         m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, cap_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
-                                     dev_n=log[1:], nsrc=sb.ncells)
+                                     dev_n=log[1:], nsrc=sb.ncells, sort=sort_far)
         p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, cap_p2p, ncells, dev, wsp, wsb, st, dev_n=log, nsrc=sb.ncells,
                                  sort=False)
         del p2p_t, p2p_s, m2l_t, m2l_s
@@ -328,7 +328,7 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     ncells = tree.ncells
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n, ncells + 1), dev, stream=torch.cuda.current_stream())
     m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
-                                 nsrc=sb.ncells)
+                                 nsrc=sb.ncells, sort=sort_far)
     p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, nsrc=sb.ncells, sort=False)
     del p2p_t, p2p_s, m2l_t, m2l_s
     return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
@@ -364,7 +364,7 @@ def partition_owner(tree: Tree, grain: int) -> torch.Tensor:
 
 def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[int, int] | None = None,
                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
-                 defer: bool = True) -> Lists:
+                 defer: bool = True, sort_far: bool = True) -> Lists:
     """Mutual dual traversal (src/traversal.py:159-262 with mutual units,
     :704-791 driver) -> DIRECTED target-sorted CSR M2L/P2P lists: each
     mutual entry (a, b) contributes (a, b) and (b, a), the reference's trace
@@ -395,7 +395,7 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
         wsp, wsb = _lib.workspace(max(cap_p2p, cap_m2l, tree.n, ncells + 1), dev,
                                   stream=torch.cuda.current_stream())
         m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, cap_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
-                                     dev_n=log[1:])
+                                     dev_n=log[1:], sort=sort_far)
         p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, cap_p2p, ncells, dev, wsp, wsb, st, dev_n=log, sort=False)
         del p2p_t, p2p_s, m2l_t, m2l_s
         return Lists(m2l_src=m2l_src, m2l_rows=m2l_rows, p2p_rows=p2p_rows,
@@ -425,7 +425,8 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096)
     ncells = tree.ncells
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n, ncells + 1), dev, stream=torch.cuda.current_stream())
-    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready,
+                                 sort=sort_far)
     p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, sort=False)
     del p2p_t, p2p_s, m2l_t, m2l_s
     return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
@@ -471,12 +472,12 @@ def _sync_event(dev) -> torch.cuda.Event:
     return evs[i]
 
 
-def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0):
+def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0, sort=True):
     """CSR of a far-field list (M2L or M2P).  Only the far field reads it, so
     with a ``side`` stream it is sorted there, off the P2P critical path,
     with its own scratch buffer; ``ready`` is recorded once it is final."""
     if side is None:
-        out = _csr(t, s, n, ncells, dev, wsp, wsb, st, dev_n, nsrc)
+        out = _csr(t, s, n, ncells, dev, wsp, wsb, st, dev_n, nsrc, sort=sort)
         if ready is not None:
             ready.record()
         return out
@@ -486,7 +487,7 @@ def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0
     traversed.record()
     side.wait_event(traversed)
     swp, swb = _lib.workspace(max(n, ncells + 1, 1), dev, slot=1, stream=side)
-    out = _csr(t, s, n, ncells, dev, swp, swb, side.cuda_stream, dev_n, nsrc)
+    out = _csr(t, s, n, ncells, dev, swp, swb, side.cuda_stream, dev_n, nsrc, sort=sort)
     for a in (t, s, *out) + ((dev_n,) if dev_n is not None else ()):
         a.record_stream(side)
     if ready is not None:
@@ -733,7 +734,8 @@ def treecode_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | Non
 
 
 def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
-                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None) -> Lists:
+                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
+                  sort_far: bool = True) -> Lists:
     """Level-wise V (M2L) and U (P2P) lists of the cubic tree
     (src/traversal.py:341-497; bit-exact sets with the reference's
     ``_collect_vlist`` / ``_collect_ulist``) -> target-sorted CSR + P2P plan.
@@ -762,7 +764,7 @@ def listfmm_lists(tree: Tree, body_range: tuple[int, int] | None = None,
         cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096)
     wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, tree.n, ncells + 1), dev, stream=torch.cuda.current_stream())
-    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready)
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready, sort=sort_far)
     p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, sort=False)
     del p2p_t, p2p_s, m2l_t, m2l_s
     return Lists(n_m2l=done_m2l, n_p2p=done_p2p, m2l_src=m2l_src, m2l_rows=m2l_rows,
@@ -993,11 +995,14 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             rng = (cuts[k], cuts[k + 1]) if nch > 1 else None
             ready = E()
             with torch.cuda.stream(lst):
+                # the grouped M2L orders its pairs itself: its rows need no sort
+                sort_far = not m2l_grouped(tree, p, src)
                 if cfg.mutual:
-                    lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side)
+                    lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side, sort_far=sort_far)
                 else:
                     lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
-                                              m2l_owner_only=nch > 1, src=src, target_mask=target_mask)
+                                              m2l_owner_only=nch > 1, src=src, target_mask=target_mask,
+                                              sort_far=sort_far)
             parts.append(lists)
             if k == 0:
                 M, L, flag, far, bodies = allocate()
@@ -1235,7 +1240,7 @@ def evaluate_list_fmm(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None =
             e_up1.record(side)
         tree._M, tree.p, tree._L = M, p, L
         m2l_ready = torch.cuda.Event()
-        lists = listfmm_lists(tree, m2l_ready=m2l_ready, side=side)
+        lists = listfmm_lists(tree, m2l_ready=m2l_ready, side=side, sort_far=not m2l_grouped(tree, p))
         tree.list_cache = lists
         e_l1.record(main)
         side.wait_event(m2l_ready)
