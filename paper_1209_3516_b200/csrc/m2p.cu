@@ -18,6 +18,8 @@
 // adds it to its running sums, the reference's per-call `phi[j] += pot`.
 //  * m2p_reg<P> (P <= 6): D and the multi-indices at compile time (taylor.cuh).
 //  * m2p_gen (any p <= 12): the same recurrence from the runtime tables.
+#include <type_traits>
+
 #include "taylor.cuh"
 
 namespace fmm {
@@ -33,7 +35,12 @@ __global__ void __launch_bounds__(128) m2p_reg(int32_t ncells, const int64_t *__
                                                double *fy, double *fz) {
     constexpr int NC = ncoef(P);
     constexpr int ND = ncoef(P + 1);  // D up to degree P
+    constexpr bool kF32 = std::is_same_v<T, float>;
+    // float32 terms: each source's signed moments are converted once per
+    // warp into shared memory (lane m converts moment m), not by every lane
+    __shared__ float msm[kF32 ? 4 : 1][kF32 ? NC : 1];
     const int lane = threadIdx.x & 31;
+    float *mw = msm[kF32 ? (threadIdx.x >> 5) : 0];
     for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ncells;
          t += (gridDim.x * blockDim.x) >> 5) {
         const int64_t k0 = rows[t], k1 = rows[t + 1];
@@ -54,7 +61,10 @@ __global__ void __launch_bounds__(128) m2p_reg(int32_t ncells, const int64_t *__
                 static_for<0, NC>([&](auto Im) {
                     constexpr int m = decltype(Im)::value;
                     constexpr int mx = kTab.mi[m][0], my = kTab.mi[m][1], mz = kTab.mi[m][2];
-                    const T mm = T((kTab.deg[m] & 1) ? -__ldg(&Ms[m]) : __ldg(&Ms[m]));
+                    constexpr bool odd = kTab.deg[m] & 1;
+                    T mm;
+                    if constexpr (kF32) mm = mw[m];
+                    else mm = odd ? -__ldg(&Ms[m]) : __ldg(&Ms[m]);
                     pot += mm * D[m];
                     gx += mm * D[IX(mx + 1, my, mz)];
                     gy += mm * D[IX(mx, my + 1, mz)];
@@ -75,6 +85,14 @@ __global__ void __launch_bounds__(128) m2p_reg(int32_t ncells, const int64_t *__
             for (int64_t k = k0; k < k1; k++) {
                 const int32_t s = sn;
                 const double cx = cxn, cy = cyn, cz = czn;
+                if constexpr (kF32) {
+                    __syncwarp();  // the previous source's moments are consumed
+                    for (int m = lane; m < NC; m += 32) {
+                        const double v = __ldg(&M[(int64_t)s * NC + m]);
+                        mw[m] = (float)((d_tab.deg[m] & 1) ? -v : v);
+                    }
+                    __syncwarp();
+                }
                 if (k + 1 < k1) {
                     sn = src[k + 1];
                     cxn = ctr[sn * 3];

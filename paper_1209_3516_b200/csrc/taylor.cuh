@@ -28,8 +28,16 @@ __device__ __forceinline__ void static_for(F &&f) {
 template <int P, typename T = double>
 __device__ __forceinline__ void d_tensors_reg(T rx, T ry, T rz, T (&D)[ncoef(P)]) {
     const T r2 = rx * rx + ry * ry + rz * rz;
-    const T inv_r2 = T(1) / r2;
-    D[0] = sqrt(inv_r2);
+    T inv_r2;
+    if constexpr (std::is_same_v<T, float>) {  // float32 terms: MUFU.RSQ (~2^-22.9) in place of IEEE div + sqrt
+        float d0;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(r2));
+        D[0] = d0;
+        inv_r2 = d0 * d0;
+    } else {
+        inv_r2 = T(1) / r2;
+        D[0] = sqrt(inv_r2);
+    }
     static_for<1, ncoef(P)>([&](auto I) {
         constexpr int idx = decltype(I)::value;
         constexpr int kx = kTab.mi[idx][0], ky = kTab.mi[idx][1], kz = kTab.mi[idx][2];
