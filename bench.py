@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--strategy", default="dualtree", choices=["dualtree", "treecode", "listfmm"],
                     help="evaluation strategy (the headline is the dual-tree FMM)")
     ap.add_argument("--mutual", action="store_true", help="mutual dual traversal (EvalConfig.mutual)")
+    ap.add_argument("--symmetric", action="store_true",
+                    help="with --mutual: symmetric near field over the unordered mutual pairs (EvalConfig.symmetric)")
     ap.add_argument("--sharded", action="store_true",
                     help="N>1: each rank gets only its block of the input and keeps only its own bodies plus "
                          "the near-field halo (paper_1209_3516_b200.sharded) instead of the replicated cloud")
@@ -95,7 +97,7 @@ def config_block(args, n, solver, extra=None):
                           "C4": "uniform f32, q~U[-1,1)", "C5": "uniform f32, q~U[0,1)"}[args.config],
          "l2": "flushed between timed steps (2x L2 write)"}
     if getattr(args, "mutual", False):
-        d.update(mutual=True, task_grain=args.task_grain)
+        d.update(mutual=True, task_grain=args.task_grain, symmetric=bool(getattr(args, "symmetric", False)))
     if extra:
         d.update(extra)
     return d
@@ -272,7 +274,8 @@ def run_ours(args):
             dist.init_process_group(backend)
     pos, q, n, solver = workload(args)
     cfg = fb.EvalConfig(strategy=args.strategy, mac=fb.MacConfig("fmm", solver["theta"]), p=solver["p"],
-                        precision=args.precision, mutual=args.mutual, task_grain=args.task_grain)
+                        precision=args.precision, mutual=args.mutual, task_grain=args.task_grain,
+                        symmetric=bool(args.mutual and args.symmetric))
     dev = torch.device("cuda", local)
     dt = torch.float32 if pos.dtype == np.float32 else torch.float64
     dpos = torch.as_tensor(pos, device=dev).to(dt)

@@ -242,6 +242,24 @@ FMM_API int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *f
                         double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
                         int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, void *stream);
 
+/* fmm_traverse_mutual keeping mutual entries UNORDERED for the symmetric
+ * executors (fmm_p2p_sym, fmm_m2l_sym; the reference's _p2p_mutual /
+ * _m2l_mutual, src/_taylor.py:191-217, :410-449): a mutual P2P (M2L) entry
+ * of two distinct cells whose bodies both meet [body_lo, body_hi) is written
+ * once, as (min, max), to sym_p2p_* (sym_m2l_*) when that list is given
+ * (NULL: written directed, as fmm_traverse_mutual); demoted pairs, mutual
+ * self pairs and entries with one member outside the range stay directed.
+ * dev_sym[0], dev_sym[1] receive the symmetric P2P and M2L counts (grow and
+ * rerun when one exceeds its capacity). */
+FMM_API int fmm_traverse_mutual_sym(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                            int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                            const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
+                            const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                            double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                            int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, int32_t *sym_p2p_a,
+                            int32_t *sym_p2p_b, int64_t cap_sym_p2p, int32_t *sym_m2l_a, int32_t *sym_m2l_b,
+                            int64_t cap_sym_m2l, unsigned long long *dev_sym, void *stream);
+
 /* Treecode lists (replaces _collect_treecode, src/traversal.py:265-313, with
  * its capacity retry, :944-966): every leaf whose bodies meet
  * [body_lo, body_hi) walks the source tree from the root; a pair (t, c)
@@ -392,6 +410,25 @@ FMM_API int fmm_p2p(int precision, int safe, int use_rsqrt, int cross, int32_t n
             const int32_t *start, const int32_t *end, const int64_t *run_rng, const void *runs,
             const double *xs, const double *ys, const double *zs, const double *qs, const void *b32,
             const void *b32lo, double *phi, double *fx, double *fy, double *fz, int *dev_flag, void *stream);
+
+/* Symmetric near field over UNORDERED leaf pairs (replaces _p2p_mutual,
+ * src/_taylor.py:410-449: one 1/r per body pair, added to both bodies; the
+ * reference's mutual self pair, :452-493, stays the directed kernel's
+ * guarded self run).  rows_a/src_a: CSR of the pairs (a, b) by first leaf,
+ * each row ascending; rows_b/src_b: the same pairs by second leaf, ascending
+ * first leaves; slot_off[k] = the first reaction slot of pair k of src_a
+ * (one slot per body of src_a[k]; exclusive prefix sums).  Only first leaves
+ * in [a_lo, a_hi) are evaluated, their slots addressed relative to
+ * slot_base, so a caller can bound react (float4 / double4 per slot) and
+ * sweep the rows in chunks.  The pair kernel ADDS the first members' sums
+ * to phi/fx/fy/fz and stores the second members' sums in react; a second
+ * kernel adds each leaf's slots in ascending order of the first member:
+ * deterministic, no atomics.  precision FMM_PREC_FP32 reads the float4 body
+ * copy, FMM_PREC_FP64 the double4 copy (fmm_pack_bodies_f64). */
+FMM_API int fmm_p2p_sym(int precision, int32_t ncells, int32_t a_lo, int32_t a_hi, const int64_t *rows_a,
+                const int32_t *src_a, const int64_t *rows_b, const int32_t *src_b, const int64_t *slot_off,
+                int64_t slot_base, const int32_t *start, const int32_t *end, const void *bodies4, void *react,
+                double *phi, double *fx, double *fy, double *fz, void *stream);
 
 /* Pack the float64 SoA bodies into the double4 (x, y, z, q) copy the
  * streamed FP64 P2P reads (32 B per body). */

@@ -53,6 +53,8 @@ SIGNATURES = {
     "fmm_partition_owner": [I32, P, P, P, P, I64, P, P],
     "fmm_traverse_mutual": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P, I64,
                             P, P],
+    "fmm_traverse_mutual_sym": [P, P, P, P, I64, INT, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P, I64, P, P,
+                                I64, P, P, P, I64, P, P, I64, P, P],
     "fmm_treecode_traverse": [P, P, P, P, I64, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, INT, DBL, P, P,
                               I64, P, P, I64, P, P, SZ, P],
     "fmm_listfmm_lists": [I32, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, I64, P, P, I64, P, P, SZ, P],
@@ -65,6 +67,7 @@ SIGNATURES = {
     "fmm_m2l_grouped": [INT, I32, P, P, I64, P, P, P, P, P, P, P, SZ, P],
     "fmm_m2p_csr": [INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "fmm_p2p_sym": [INT, I32, I32, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P],
     "fmm_pack_bodies_f64": [I64, P, P, P, P, P, P],
     "fmm_p2p_coincident": [I32, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_unpermute": [P, I64, P, P, P, P, P, P, P, P, P],

@@ -755,13 +755,19 @@ __global__ void mutual_step_kernel(const int32_t *__restrict__ fa, const int32_t
                                    int32_t bhi, int kind_mac, double th2, int32_t *p2p_t, int32_t *p2p_s,
                                    int64_t cap_p2p, int32_t *m2l_t, int32_t *m2l_s, int64_t cap_m2l, int32_t *na,
                                    int32_t *nb, int64_t cap_next, unsigned long long *cnt_p2p,
-                                   unsigned long long *cnt_m2l, unsigned long long *cnt_next) {
+                                   unsigned long long *cnt_m2l, unsigned long long *cnt_next, int32_t *sp_a,
+                                   int32_t *sp_b, int64_t cap_sp, int32_t *sm_a, int32_t *sm_b, int64_t cap_sm,
+                                   unsigned long long *cnt_sym) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t nfront = (int64_t)*nfront_dev;
     if (nfront > cap_front) nfront = cap_front;
     const int64_t nround = (nfront + stride - 1) / stride;
     auto keep = [&](int32_t c) { return cend[c] > blo && cstart[c] < bhi; };
+    // a mutual entry whose two members are both kept stays UNORDERED when
+    // the caller gave a symmetric list for its kind (fmm_traverse_mutual_sym)
+    auto sym_p2p = [&](int32_t x, int32_t y, int mm) { return sp_a && mm && x != y && keep(x) && keep(y); };
+    auto sym_m2l = [&](int32_t x, int32_t y, int mm) { return sm_a && mm && x != y && keep(x) && keep(y); };
     // an item's fate: 1 P2P, 2 M2L, 3 split
     auto fate_of = [&](int32_t x, int32_t y, int m) {
         if (C.leaf[x] && C.leaf[y]) return 1;
@@ -794,28 +800,42 @@ __global__ void mutual_step_kernel(const int32_t *__restrict__ fa, const int32_t
         }
         // the fates of the first 32 items are kept (2 bits each) for the
         // write pass; only a mutual self split has more (36 children)
-        int np = 0, nm = 0, nn = 0, nit = 0;
+        int np = 0, nm = 0, nn = 0, nit = 0, nsp = 0, nsm = 0;
         uint64_t fbits = 0;
         if (live)
             children(a, b, m, [&](int32_t x, int32_t y, int mm) {
                 const int ft = fate_of(x, y, mm);
                 if (nit < 32) fbits |= (uint64_t)ft << (2 * nit);
                 nit++;
-                if (ft == 1) np += keep(x) + (mm && x != y && keep(y));
-                else if (ft == 2) nm += keep(x) + (mm && keep(y));
-                else nn += keep(x) || (mm && keep(y));
+                if (ft == 1) {
+                    if (sym_p2p(x, y, mm)) nsp++;
+                    else np += keep(x) + (mm && x != y && keep(y));
+                } else if (ft == 2) {
+                    if (sym_m2l(x, y, mm)) nsm++;
+                    else nm += keep(x) + (mm && keep(y));
+                } else {
+                    nn += keep(x) || (mm && keep(y));
+                }
             });
-        int op, om, on;
+        int op, om, on, osp = 0, osm = 0;
         const unsigned long long bp = warp_reserve(cnt_p2p, np, lane, &op);
         const unsigned long long bm = warp_reserve(cnt_m2l, nm, lane, &om);
         const unsigned long long bn = warp_reserve(cnt_next, nn, lane, &on);
-        unsigned long long ip = bp + op, im = bm + om, in = bn + on;
+        const unsigned long long bsp = sp_a ? warp_reserve(cnt_sym, nsp, lane, &osp) : 0ull;
+        const unsigned long long bsm = sm_a ? warp_reserve(cnt_sym + 1, nsm, lane, &osm) : 0ull;
+        unsigned long long ip = bp + op, im = bm + om, in = bn + on, isp = bsp + osp, ism = bsm + osm;
         int it = 0;
         if (live)
             children(a, b, m, [&](int32_t x, int32_t y, int mm) {
                 const int ft = it < 32 ? (int)((fbits >> (2 * it)) & 3u) : fate_of(x, y, mm);
                 it++;
-                if (ft == 1 || ft == 2) {
+                if (ft == 1 && sym_p2p(x, y, mm)) {
+                    if (isp < (unsigned long long)cap_sp) { sp_a[isp] = min(x, y); sp_b[isp] = max(x, y); }
+                    isp++;
+                } else if (ft == 2 && sym_m2l(x, y, mm)) {
+                    if (ism < (unsigned long long)cap_sm) { sm_a[ism] = min(x, y); sm_b[ism] = max(x, y); }
+                    ism++;
+                } else if (ft == 1 || ft == 2) {
                     int32_t *tt = ft == 1 ? p2p_t : m2l_t, *ss = ft == 1 ? p2p_s : m2l_s;
                     const unsigned long long cap = (unsigned long long)(ft == 1 ? cap_p2p : cap_m2l);
                     unsigned long long &at = ft == 1 ? ip : im;
@@ -955,18 +975,22 @@ int fmm_partition_owner(int32_t ncells, const int32_t *parent, const uint8_t *le
     return FMM_OK;
 }
 
-int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
-                        int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
-                        const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
-                        const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
-                        double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
-                        int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, void *stream) {
+static int traverse_mutual_impl(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                                int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                                const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
+                                const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                                double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                                int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, int32_t *sp_a,
+                                int32_t *sp_b, int64_t cap_sp, int32_t *sm_a, int32_t *sm_b, int64_t cap_sm,
+                                unsigned long long *dev_sym, const char *who, void *stream) {
     cudaStream_t st = as_stream(stream);
     if (cap_front < 1) { set_error("frontier capacity must be >= 1"); return FMM_ERR_INVALID; }
+    if ((sp_a || sm_a) && !dev_sym) { set_error("symmetric lists need their device counters"); return FMM_ERR_INVALID; }
     const Cells C = cells_of(children, leaf, ctr, bmax, rmax);
     // dev_log[0] = n_p2p, [1] = n_m2l, [2 + s] = frontier entering step s;
     // the seed is the unclassified mutual root pair (0, 0)
     traverse_seed<<<1, 32, 0, st>>>(dev_log, nsteps + 3, front_a0, front_b0, (int32_t)0x80000000u); fmm::note_launch();
+    if (dev_sym) cudaMemsetAsync(dev_sym, 0, 2 * sizeof(unsigned long long), st);
     const int grid = 148 * 8;
     for (int sidx = 0; sidx < nsteps; sidx++) {
         const bool even = (sidx & 1) == 0;
@@ -975,10 +999,36 @@ int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1,
             owner, start,
             end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t, m2l_s, cap_m2l,
             even ? front_a1 : front_a0, even ? front_b1 : front_b0, cap_front, dev_log, dev_log + 1,
-            dev_log + 3 + sidx); fmm::note_launch();
+            dev_log + 3 + sidx, sp_a, sp_b, cap_sp, sm_a, sm_b, cap_sm, dev_sym); fmm::note_launch();
     }
-    FMM_CUDA_CHECK("fmm_traverse_mutual");
+    FMM_CUDA_CHECK(who);
     return FMM_OK;
+}
+
+int fmm_traverse_mutual(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                        int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                        const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
+                        const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                        double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                        int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, void *stream) {
+    return traverse_mutual_impl(front_a0, front_b0, front_a1, front_b1, cap_front, nsteps, children, leaf, ctr, bmax,
+                                rmax, owner, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t,
+                                m2l_s, cap_m2l, dev_log, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr,
+                                "fmm_traverse_mutual", stream);
+}
+
+int fmm_traverse_mutual_sym(int32_t *front_a0, int32_t *front_b0, int32_t *front_a1, int32_t *front_b1,
+                            int64_t cap_front, int nsteps, const int32_t *children, const uint8_t *leaf,
+                            const double *ctr, const double *bmax, const double *rmax, const int32_t *owner,
+                            const int32_t *start, const int32_t *end, int32_t body_lo, int32_t body_hi, int kind,
+                            double th2, int32_t *p2p_t, int32_t *p2p_s, int64_t cap_p2p, int32_t *m2l_t,
+                            int32_t *m2l_s, int64_t cap_m2l, unsigned long long *dev_log, int32_t *sym_p2p_a,
+                            int32_t *sym_p2p_b, int64_t cap_sym_p2p, int32_t *sym_m2l_a, int32_t *sym_m2l_b,
+                            int64_t cap_sym_m2l, unsigned long long *dev_sym, void *stream) {
+    return traverse_mutual_impl(front_a0, front_b0, front_a1, front_b1, cap_front, nsteps, children, leaf, ctr, bmax,
+                                rmax, owner, start, end, body_lo, body_hi, kind, th2, p2p_t, p2p_s, cap_p2p, m2l_t,
+                                m2l_s, cap_m2l, dev_log, sym_p2p_a, sym_p2p_b, cap_sym_p2p, sym_m2l_a, sym_m2l_b,
+                                cap_sym_m2l, dev_sym, "fmm_traverse_mutual_sym", stream);
 }
 
 int fmm_listfmm_lists(int32_t ncells, int depth, const int64_t *level_off, const int8_t *level,

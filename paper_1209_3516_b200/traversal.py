@@ -73,6 +73,7 @@ class EvalConfig:
     task_grain: int = 5000
     use_rsqrt: bool = False
     precision: str = "fp64"
+    symmetric: bool | None = None  # mutual=True: symmetric executors (None: FMM_B200_SYMMETRIC, default off)
 
     def __post_init__(self) -> None:
         if self.strategy not in STRATEGIES:
@@ -242,6 +243,14 @@ class Lists:
         rows = getattr(self, which + "_rows").cpu()
         src = getattr(self, which + "_src")[:int(rows[-1])].cpu().long()
         t = torch.repeat_interleave(torch.arange(rows.numel() - 1), rows[1:] - rows[:-1])
+        sym = self.__dict__.get("sym_" + which)
+        if sym is not None and sym.n:
+            # unordered entries (a, b) stand for (a, b) and (b, a), the
+            # reference's trace expansion (src/traversal.py:644-650)
+            a, b = sym.pairs()
+            t, src = torch.cat([t, a, b]), torch.cat([src, b, a])
+            order = torch.argsort(t * (rows.numel() + 1) + src)
+            t, src = t[order], src[order]
         return t.numpy(), src.numpy()
 
 
@@ -364,14 +373,22 @@ def partition_owner(tree: Tree, grain: int) -> torch.Tensor:
 
 def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[int, int] | None = None,
                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
-                 defer: bool = True, sort_far: bool = True) -> Lists:
+                 defer: bool = True, sort_far: bool = True, symmetric: bool = False) -> Lists:
     """Mutual dual traversal (src/traversal.py:159-262 with mutual units,
     :704-791 driver) -> DIRECTED target-sorted CSR M2L/P2P lists: each
     mutual entry (a, b) contributes (a, b) and (b, a), the reference's trace
     expansion, so the lists equal the reference's trace sets and feed the
     directed executors.  The sets depend on ``task_grain`` through the
     partition: a mutual pair straddling two partition roots is demoted to
-    two directed pairs."""
+    two directed pairs.
+
+    ``symmetric=True`` keeps the mutual P2P entries of two distinct leaves
+    UNORDERED (``Lists.sym_p2p``) for the symmetric near field
+    (``run_p2p_sym``, the reference's _p2p_mutual); the directed lists then
+    hold the demoted pairs and the self pairs.  ``n_p2p`` and
+    ``host_pairs("p2p")`` still describe the directed-expanded set."""
+    if symmetric:
+        return _mutual_lists_sym(tree, mac, task_grain, body_range, m2l_ready, side, sort_far)
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
     th2 = mac.theta * mac.theta
@@ -434,6 +451,58 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
                  **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
+def _mutual_lists_sym(tree: Tree, mac: MacConfig, task_grain: int, body_range, m2l_ready, side, sort_far) -> Lists:
+    """``mutual_lists(symmetric=True)``: one traversal writing the directed
+    lists and the unordered mutual P2P pairs; the counts are read once (the
+    reaction buffer is sized from them)."""
+    blo, bhi = body_range if body_range is not None else (0, tree.n)
+    dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
+    th2 = mac.theta * mac.theta
+    owner = partition_owner(tree, task_grain)
+    key = ("mutual-sym", tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, task_grain)
+    cap_p2p, cap_m2l, cap_next, cap_sym = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
+                                                          max(4096, tree.ncells * 16), max(4096, tree.nleaves * 16)))
+    nsteps = 2 * tree.depth + 2
+    log = torch.empty(nsteps + 3 + 2, dtype=torch.int64, device=dev)  # [traversal log | symmetric counts]
+    while True:
+        pool = torch.empty(2 * cap_p2p + 2 * cap_m2l + 4 * cap_next + 2 * cap_sym, dtype=i32, device=dev)
+        p2p_t, p2p_s, m2l_t, m2l_s, sym_a, sym_b, *fr = torch.split(
+            pool, [cap_p2p, cap_p2p, cap_m2l, cap_m2l, cap_sym, cap_sym] + [cap_next] * 4)
+        _lib.call("fmm_traverse_mutual_sym", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps,
+                  P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(owner),
+                  P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t),
+                  P(m2l_s), cap_m2l, P(log), P(sym_a), P(sym_b), cap_sym, None, None, 0, P(log[nsteps + 3:]), st)
+        hl = log.tolist()  # the one synchronisation of the traversal
+        done_p2p, done_m2l, fronts, n_sym = hl[0], hl[1], hl[2:nsteps + 3], hl[nsteps + 3]
+        peak = max(fronts)
+        if done_p2p <= cap_p2p and done_m2l <= cap_m2l and peak <= cap_next and n_sym <= cap_sym:
+            if fronts[-1] != 0:
+                raise RuntimeError("mutual traversal did not terminate within 2*depth+2 steps")
+            break
+        cap_p2p = max(cap_p2p, int(done_p2p * 1.05) + 4096)
+        cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
+        cap_next = max(cap_next, int(peak * 1.05) + 4096)
+        cap_sym = max(cap_sym, int(n_sym * 1.05) + 4096)
+    del fr
+    _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096,
+                  int(n_sym * 1.02) + 4096)
+    ncells = tree.ncells
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, n_sym, tree.n, ncells + 1), dev,
+                              stream=torch.cuda.current_stream())
+    m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready, sort=sort_far)
+    p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, sort=False)
+    plan = _p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st)
+    sym = _sym_pairs(tree, sym_a, sym_b, n_sym, wsp, wsb, st, slots=True)
+    if n_sym:
+        # the reference counts both directions of a symmetric body pair
+        # (src/_taylor.py:439, pairs += 2): added to the plan's pair counter
+        size = (tree.d_end - tree.d_start).long()
+        plan["dev_stats"][0] += 2 * (size[sym_a[:n_sym].long()] * size[sym_b[:n_sym].long()]).sum()
+    del p2p_t, p2p_s, m2l_t, m2l_s, sym_a, sym_b, pool
+    return Lists(n_m2l=done_m2l, n_p2p=done_p2p + 2 * n_sym, m2l_src=m2l_src, m2l_rows=m2l_rows,
+                 p2p_rows=p2p_rows, peak_frontier=peak, sym_p2p=sym, **plan)
+
+
 def _sync_free() -> bool:
     """Hinted traversals skip the host wait (FMM_B200_SYNC_FREE=0 disables)."""
     return os.environ.get("FMM_B200_SYNC_FREE", "1") != "0"
@@ -493,6 +562,44 @@ def _far_csr(t, s, n, ncells, dev, wsp, wsb, st, side, ready, dev_n=None, nsrc=0
     if ready is not None:
         ready.record(side)
     return out
+
+
+class SymPairs:
+    """Unordered mutual pairs (a < b) of one kind for the symmetric
+    executors: CSR by first member (``rows_a``/``src_a``, rows ascending),
+    CSR by second member (``rows_b``/``src_b``) and, for P2P, the reaction
+    slot offsets (``slot_off[k]`` = bodies of the second leaves before pair
+    k)."""
+
+    def __init__(self, n, rows_a, src_a, rows_b, src_b, slot_off=None):
+        self.n, self.rows_a, self.src_a, self.rows_b, self.src_b = n, rows_a, src_a, rows_b, src_b
+        self.slot_off = slot_off
+        self.chunks = None
+
+    def pairs(self):
+        """(first, second) int64 host tensors in CSR order."""
+        rows = self.rows_a.cpu()
+        a = torch.repeat_interleave(torch.arange(rows.numel() - 1), rows[1:] - rows[:-1])
+        return a, self.src_a[:self.n].cpu().long()
+
+
+def symmetric_default() -> bool:
+    """``EvalConfig.symmetric=None``: FMM_B200_SYMMETRIC=1 turns the symmetric
+    executors on for mutual evaluations (default: directed executors)."""
+    return os.environ.get("FMM_B200_SYMMETRIC", "0") == "1"
+
+
+def _sym_pairs(tree: Tree, a, b, n: int, wsp, wsb, st, slots: bool) -> SymPairs:
+    dev, ncells = tree.device, tree.ncells
+    src_a, rows_a = _csr(a, b, n, ncells, dev, wsp, wsb, st, sort=True)
+    src_b, rows_b = _csr(b, a, n, ncells, dev, wsp, wsb, st, sort=True)
+    slot_off = None
+    if slots:
+        size = (tree.d_end - tree.d_start).long()
+        slot_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        if n:
+            torch.cumsum(size[src_a[:n].long()], 0, out=slot_off[1:])
+    return SymPairs(n, rows_a, src_a, rows_b, src_b, slot_off)
 
 
 def _p2p_plan(tree: Tree, p2p_grp, p2p_rows, n_p2p: int, blo: int, bhi: int, wsp, wsb, st,
@@ -664,6 +771,49 @@ def run_p2p(tree: Tree, lists: Lists, precision: str, use_rsqrt: bool = False, s
               P(lists.dev_nrows), P(lists.leaf_rows), P(tree.d_start), P(tree.d_end), P(lists.run_off),
               P(lists.runs), P(b.d_x), P(b.d_y), P(b.d_z), P(b.d_q), P(packed), P(packed_lo), P(tree.d_phi),
               P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), P(flag), _lib.stream_handle())
+
+
+# reaction buffer bound of the symmetric near field (bytes; larger lists
+# are swept in chunks of first leaves)
+SYM_BUFFER_BYTES = int(float(os.environ.get("FMM_B200_SYM_BUFFER_MB", "4096")) * (1 << 20))
+
+
+def run_p2p_sym(tree: Tree, lists: Lists, precision: str) -> None:
+    """The symmetric near field over ``lists.sym_p2p`` (after ``run_p2p``,
+    which STORES the directed near field): every unordered leaf pair is
+    evaluated once and added to both leaves (src/_taylor.py:410-449),
+    deterministically (``fmm_p2p_sym``).  ``precision`` "fp32" needs
+    float32-exact inputs; "fp32acc" and inexact inputs take float64."""
+    sym = lists.__dict__.get("sym_p2p")
+    if sym is None or sym.n == 0:
+        return
+    P, dev = _lib.ptr, tree.device
+    if precision == "fp32" and tree.fp32_exact:
+        prec, packed, item = _lib.PREC_FP32, tree.d_b32, 16
+    else:
+        prec, packed, item = _lib.PREC_FP64, _packed_f64(tree), 32
+    chunks = sym.chunks
+    if chunks is None or chunks[0] != item or chunks[3] != SYM_BUFFER_BYTES:
+        # first-leaf ranges whose reaction slots fit the buffer (one read)
+        row_slot = sym.slot_off[sym.rows_a]  # slots before each first leaf's row
+        total = int(row_slot[-1])
+        nch = max(1, -(-total * item // SYM_BUFFER_BYTES))
+        if nch == 1:
+            cuts, bases = [0, tree.ncells], [0, total]
+        else:
+            want = torch.arange(1, nch, device=dev, dtype=torch.int64) * (total // nch)
+            mid = torch.searchsorted(row_slot, want, right=True).clamp_(1, tree.ncells) - 1
+            cuts = sorted(set([0, tree.ncells] + mid.tolist()))
+            bases = row_slot[torch.tensor(cuts, device=dev)].tolist()
+        chunks = sym.chunks = (item, cuts, bases, SYM_BUFFER_BYTES)
+    _, cuts, bases, _ = chunks
+    cap = max(b1 - b0 for b0, b1 in zip(bases[:-1], bases[1:]))
+    react = torch.empty(max(cap, 1) * item, dtype=torch.uint8, device=dev)
+    for (a0, a1), base in zip(zip(cuts[:-1], cuts[1:]), bases[:-1]):
+        _lib.call("fmm_p2p_sym", prec, tree.ncells, a0, a1, P(sym.rows_a), P(sym.src_a), P(sym.rows_b),
+                  P(sym.src_b), P(sym.slot_off), base, P(tree.d_start), P(tree.d_end), P(packed), P(react),
+                  P(tree.d_phi), P(tree.d_fx), P(tree.d_fy), P(tree.d_fz), _lib.stream_handle())
+    react.record_stream(torch.cuda.current_stream())
 
 
 def count_coincident(tree: Tree, lists: Lists, bodies: CrossBodies) -> torch.Tensor:
@@ -941,6 +1091,8 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     dev = tree.device
     p = cfg.p
     nf = _near_field(cfg, tree, src)
+    symmetric = cfg.mutual and not cfg.use_rsqrt and (
+        cfg.symmetric if cfg.symmetric is not None else symmetric_default())
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev)
@@ -998,7 +1150,8 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                 # the grouped M2L orders its pairs itself: its rows need no sort
                 sort_far = not m2l_grouped(tree, p, src)
                 if cfg.mutual:
-                    lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side, sort_far=sort_far)
+                    lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side, sort_far=sort_far,
+                                         symmetric=symmetric)
                 else:
                     lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
                                               m2l_owner_only=nch > 1, src=src, target_mask=target_mask,
@@ -1022,6 +1175,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                 ea, eb = E(), E()
                 ea.record(pst)
                 run_p2p(tree, lists, nf, cfg.use_rsqrt, False, flag, bodies)
+                run_p2p_sym(tree, lists, nf)
                 eb.record(pst)
                 p2p_ev.append((ea, eb))
         e_l1.record(lst)
@@ -1049,6 +1203,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
             # near field is rewritten, so the far field is added again)
             for lists in parts:
                 run_p2p(tree, lists, nf, cfg.use_rsqrt, True, flag, bodies)
+                run_p2p_sym(tree, lists, nf)
             combine()
             if cross:  # (float64-coincident pairs are FP32 collisions too)
                 coinc = [count_coincident(tree, x, bodies) for x in parts]

@@ -126,3 +126,138 @@ def test_mutual_as_accurate_as_directed():
     e = lambda f: float(np.sqrt(((f - ref) ** 2).sum() / (ref ** 2).sum()))  # noqa: E731
     assert e(m) < 2.0 * e(d) + 1e-12
     assert torch.cuda.is_available()
+
+
+# ---- symmetric executors (fmm_traverse_mutual_sym, fmm_p2p_sym) -------------
+# The reference's _p2p_mutual (src/_taylor.py:410-449) evaluates an unordered
+# leaf pair once and adds it to both leaves; here the unordered pairs run on
+# the symmetric GPU kernel and must reproduce the reference's sets, counters
+# and results.
+
+def test_symmetric_lists_expand_to_reference_sets(case):
+    t = build(case)
+    lists = fb.mutual_lists(t, fb.MacConfig(case.mac, case.theta), case.grain, symmetric=True)
+    assert lists.n_m2l == case.meta["n_m2l"] and lists.n_p2p == case.meta["n_p2p"]
+    assert sha(canon_pairs(*lists.host_pairs("m2l"))) == case.meta["m2l_sha"]
+    assert sha(canon_pairs(*lists.host_pairs("p2p"))) == case.meta["p2p_sha"]
+    sym = lists.sym_p2p
+    a, b = sym.pairs()
+    assert sym.n == a.numel() and bool((a < b).all())
+    leaf = t.cell_leaf.astype(bool)
+    assert leaf[a.numpy()].all() and leaf[b.numpy()].all()
+
+
+def test_symmetric_unordered_pairs_match_oracle():
+    """The unordered list is the oracle's mutual P2P entries of two distinct
+    leaves (both members kept)."""
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    ot = orc.build_tree(c.pos, c.q, c.ncrit)
+    for grain in (37, 700, 10 ** 9):
+        lists = fb.mutual_lists(t, fb.MacConfig("fmm", 0.55), grain, symmetric=True)
+        _, _, _, pt, ps, pm = orc.collect_mutual(ot, 0.55, grain, "fmm")
+        keep = (pm != 0) & (pt != ps)
+        want = np.unique(np.stack([np.minimum(pt[keep], ps[keep]), np.maximum(pt[keep], ps[keep])], 1), axis=0)
+        a, b = lists.sym_p2p.pairs()
+        got = np.unique(np.stack([a.numpy(), b.numpy()], 1), axis=0)
+        assert lists.sym_p2p.n == len(want) and np.array_equal(got, want)
+        assert grain < 10 ** 9 or lists.sym_p2p.n > 0
+
+
+def test_symmetric_fp64_matches_reference(case):
+    t = build(case)
+    rep = fb.evaluate_on_tree(t, cfg_of(case, symmetric=True), trace=True)
+    s = case.meta["stats"]
+    for k in STAT_KEYS:
+        assert getattr(rep.stats, k) == s[k], k
+    ev_p = canon_pairs([a for k, a, _ in rep.trace if k == "p2p"], [b for k, _, b in rep.trace if k == "p2p"])
+    assert sha(ev_p) == case.meta["p2p_sha"]
+    for k in ("phi", "fx", "fy", "fz"):
+        assert rel_l2(getattr(t.bodies, k), case[k]) <= FP64_TOL, k
+
+
+def test_symmetric_fp32_within_twice_reference_error(case):
+    t = build(case)
+    rep = fb.evaluate_on_tree(t, cfg_of(case, precision="fp32", symmetric=True))
+    s = case.meta["stats"]
+    assert rep.stats.p2p_pairs == s["p2p_pairs"] and rep.stats.p2p_skipped == s["p2p_skipped"]
+    fref = np.stack([case["direct_fx"], case["direct_fy"], case["direct_fz"]], 1)
+
+    def err(fx, fy, fz):
+        f = np.stack([fx, fy, fz], 1)
+        return float(np.sqrt(((f - fref) ** 2).sum() / (fref ** 2).sum()))
+
+    ref = err(case["fx"], case["fy"], case["fz"])
+    b = t.bodies
+    assert err(b.fx, b.fy, b.fz) <= 2.0 * ref + FP32_BAR_FLOOR
+    assert rel_l2(b.phi, case["direct_phi"]) <= 2.0 * rel_l2(case["phi"], case["direct_phi"]) + FP32_BAR_FLOOR
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_symmetric_is_deterministic_and_equals_directed(precision):
+    """Two symmetric runs agree bit for bit (no atomics); the symmetric and
+    the directed executors agree to rounding."""
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    cfg = lambda sym: fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=4, mutual=True, task_grain=10 ** 9,  # noqa: E731
+                                    precision=precision, symmetric=sym)
+    runs = []
+    for sym in (True, True, False):
+        rep = fb.evaluate_on_tree(t, cfg(sym))
+        b = t.bodies
+        runs.append((rep.stats.p2p_pairs, np.stack([b.phi, b.fx, b.fy, b.fz]).copy()))
+    assert runs[0][0] == runs[1][0] == runs[2][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
+    tol = 1e-12 if precision == "fp64" else 2e-5
+    for k in range(4):
+        assert rel_l2(runs[0][1][k], runs[2][1][k]) <= tol, k
+
+
+@pytest.mark.parametrize("ncrit", [8, 100, 300])
+def test_symmetric_other_leaf_sizes_match_oracle(ncrit):
+    """Leaves beyond one 64-target sweep (ncrit 100, 300) and tiny leaves."""
+    from paper_1209_3516_b200 import workloads
+    pos, q = workloads.config1(3000, 5)
+    t = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], q), ncrit=ncrit)
+    ot = orc.build_tree(pos, q, ncrit)
+    want = orc.evaluate_mutual(ot, 3, 0.5, 10 ** 9)
+    rep = fb.evaluate_on_tree(t, fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=3, mutual=True, task_grain=10 ** 9,
+                                               symmetric=True))
+    assert rep.stats.p2p_pairs == want["p2p_pairs"]
+    assert t.list_cache.sym_p2p.n > 0
+    b = t.bodies
+    for k in ("phi", "fx", "fy", "fz"):
+        assert rel_l2(getattr(b, k), want[k]) <= FP64_TOL, k
+
+
+def test_symmetric_chunked_reaction_buffer(monkeypatch):
+    """A reaction buffer smaller than the list sweeps the first leaves in
+    chunks: same results to rounding, same counters."""
+    from paper_1209_3516_b200 import traversal
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=4, mutual=True, task_grain=10 ** 9, symmetric=True)
+    rep0 = fb.evaluate_on_tree(t, cfg)
+    whole = np.stack([t.bodies.phi, t.bodies.fx, t.bodies.fy, t.bodies.fz]).copy()
+    assert len(t.list_cache.sym_p2p.chunks[1]) == 2
+    monkeypatch.setattr(traversal, "SYM_BUFFER_BYTES", 64 << 10)
+    rep1 = fb.evaluate_on_tree(t, cfg)
+    assert len(t.list_cache.sym_p2p.chunks[1]) > 3
+    assert rep1.stats.p2p_pairs == rep0.stats.p2p_pairs
+    got = np.stack([t.bodies.phi, t.bodies.fx, t.bodies.fy, t.bodies.fz])
+    for k in range(4):
+        assert rel_l2(got[k], whole[k]) <= 1e-13, k
+
+
+def test_symmetric_multirank_ranges_sum_to_whole():
+    """Per-range symmetric lists (both members kept stay unordered, the rest
+    directed) expand to the same directed set as the whole."""
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    mac = fb.MacConfig(c.mac, c.theta)
+    full = canon_pairs(*fb.mutual_lists(t, mac, c.grain).host_pairs("p2p"))
+    leaf_starts = np.sort(t.cell_start[t.cell_leaf.astype(bool)])
+    cut = int(leaf_starts[leaf_starts.size // 2])
+    parts = [canon_pairs(*fb.mutual_lists(t, mac, c.grain, body_range=rng, symmetric=True).host_pairs("p2p"))
+             for rng in ((0, cut), (cut, t.n))]
+    assert np.array_equal(np.sort(np.concatenate(parts)), full)
