@@ -430,6 +430,24 @@ FMM_API int fmm_p2p_sym(int precision, int32_t ncells, int32_t a_lo, int32_t a_h
                 int64_t slot_base, const int32_t *start, const int32_t *end, const void *bodies4, void *react,
                 double *phi, double *fx, double *fy, double *fz, void *stream);
 
+/* Symmetric M2L over UNORDERED cell pairs (replaces _m2l_mutual,
+ * src/_taylor.py:191-217: one derivative tensor D(c_a - c_b) per pair,
+ * contracted in both directions through D_k(-r) = (-1)^|k| D_k(r)).
+ * rows_a/src_a: CSR of the pairs (a, b) by first member, each row ascending;
+ * rows_b/src_b: the same pairs by second member, ascending first members.
+ * Pair k of src_a owns the slot k - slot_base of react (ncoef(p) doubles per
+ * slot); only first members in [a_lo, a_hi) are evaluated, so a caller can
+ * bound react and sweep the rows in chunks (slot_base = rows_a[a_lo]).  The
+ * pair kernel ADDS the first members' sums to L and stores the second
+ * members' finished coefficients in react; a second kernel adds each cell's
+ * slots in ascending order of the first member: deterministic, no atomics.
+ * Orders 1..FMM_M2L_SYM_MAX_P (higher orders: keep the pairs directed, the
+ * offset-grouped fmm_m2l_grouped shares D over whole lattice groups). */
+#define FMM_M2L_SYM_MAX_P 7
+FMM_API int fmm_m2l_sym(int p, int32_t ncells, int32_t a_lo, int32_t a_hi, const int64_t *rows_a,
+                const int32_t *src_a, const int64_t *rows_b, const int32_t *src_b, int64_t slot_base,
+                const double *ctr, const double *M, double *react, double *L, void *stream);
+
 /* Pack the float64 SoA bodies into the double4 (x, y, z, q) copy the
  * streamed FP64 P2P reads (32 B per body). */
 FMM_API int fmm_pack_bodies_f64(int64_t n, const double *xs, const double *ys, const double *zs, const double *qs,

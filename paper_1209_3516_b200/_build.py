@@ -25,7 +25,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompi
 # bit-exact units: no a*b+c contraction (the reference never contracts)
 EXACT = {"tree_build.cu", "traverse.cu", "plan.cu"}
 SOURCES = ["tree_build.cu", "passes.cu", "traverse.cu", "plan.cu", "m2l.cu", "m2l_grouped.cu", "m2p.cu", "p2p.cu",
-           "util.cu", "partition.cu", "p2p_sym.cu"]
+           "util.cu", "partition.cu", "p2p_sym.cu", "m2l_sym.cu"]
 
 
 def nvcc() -> str:

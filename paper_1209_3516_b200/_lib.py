@@ -68,6 +68,7 @@ SIGNATURES = {
     "fmm_m2p_csr": [INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p": [INT, INT, INT, INT, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_p2p_sym": [INT, I32, I32, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P],
+    "fmm_m2l_sym": [INT, I32, I32, I32, P, P, P, P, I64, P, P, P, P, P],
     "fmm_pack_bodies_f64": [I64, P, P, P, P, P, P],
     "fmm_p2p_coincident": [I32, P, P, P, P, P, P, P, P, P, P, P],
     "fmm_unpermute": [P, I64, P, P, P, P, P, P, P, P, P],

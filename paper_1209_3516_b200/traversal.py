@@ -373,7 +373,8 @@ def partition_owner(tree: Tree, grain: int) -> torch.Tensor:
 
 def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[int, int] | None = None,
                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
-                 defer: bool = True, sort_far: bool = True, symmetric: bool = False) -> Lists:
+                 defer: bool = True, sort_far: bool = True, symmetric: bool = False,
+                 symmetric_m2l: bool = False) -> Lists:
     """Mutual dual traversal (src/traversal.py:159-262 with mutual units,
     :704-791 driver) -> DIRECTED target-sorted CSR M2L/P2P lists: each
     mutual entry (a, b) contributes (a, b) and (b, a), the reference's trace
@@ -385,10 +386,12 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
     ``symmetric=True`` keeps the mutual P2P entries of two distinct leaves
     UNORDERED (``Lists.sym_p2p``) for the symmetric near field
     (``run_p2p_sym``, the reference's _p2p_mutual); the directed lists then
-    hold the demoted pairs and the self pairs.  ``n_p2p`` and
-    ``host_pairs("p2p")`` still describe the directed-expanded set."""
+    hold the demoted pairs and the self pairs.  ``symmetric_m2l=True`` keeps
+    the mutual M2L entries unordered too (``Lists.sym_m2l``, ``run_m2l_sym``,
+    the reference's _m2l_mutual).  ``n_p2p`` / ``n_m2l`` and ``host_pairs``
+    still describe the directed-expanded sets."""
     if symmetric:
-        return _mutual_lists_sym(tree, mac, task_grain, body_range, m2l_ready, side, sort_far)
+        return _mutual_lists_sym(tree, mac, task_grain, body_range, m2l_ready, side, sort_far, symmetric_m2l)
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
     th2 = mac.theta * mac.theta
@@ -451,31 +454,35 @@ def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[
                  **_p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st))
 
 
-def _mutual_lists_sym(tree: Tree, mac: MacConfig, task_grain: int, body_range, m2l_ready, side, sort_far) -> Lists:
+def _mutual_lists_sym(tree: Tree, mac: MacConfig, task_grain: int, body_range, m2l_ready, side, sort_far,
+                      sym_m2l: bool = False) -> Lists:
     """``mutual_lists(symmetric=True)``: one traversal writing the directed
-    lists and the unordered mutual P2P pairs; the counts are read once (the
-    reaction buffer is sized from them)."""
+    lists and the unordered mutual P2P (and, ``sym_m2l``, M2L) pairs; the
+    counts are read once (the reaction buffers are sized from them)."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
     dev, P, st, i32 = tree.device, _lib.ptr, _lib.stream_handle(), torch.int32
     th2 = mac.theta * mac.theta
     owner = partition_owner(tree, task_grain)
-    key = ("mutual-sym", tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, task_grain)
-    cap_p2p, cap_m2l, cap_next, cap_sym = _hint.get(key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32),
-                                                          max(4096, tree.ncells * 16), max(4096, tree.nleaves * 16)))
+    key = ("mutual-sym", tree.ncells, tree.nleaves, mac.kind, th2, blo, bhi, task_grain, sym_m2l)
+    cap_p2p, cap_m2l, cap_next, cap_sym, cap_sm = _hint.get(
+        key, (max(4096, tree.nleaves * 64), max(4096, tree.ncells * 32), max(4096, tree.ncells * 16),
+              max(4096, tree.nleaves * 16), max(4096, tree.ncells * 16) if sym_m2l else 0))
     nsteps = 2 * tree.depth + 2
     log = torch.empty(nsteps + 3 + 2, dtype=torch.int64, device=dev)  # [traversal log | symmetric counts]
     while True:
-        pool = torch.empty(2 * cap_p2p + 2 * cap_m2l + 4 * cap_next + 2 * cap_sym, dtype=i32, device=dev)
-        p2p_t, p2p_s, m2l_t, m2l_s, sym_a, sym_b, *fr = torch.split(
-            pool, [cap_p2p, cap_p2p, cap_m2l, cap_m2l, cap_sym, cap_sym] + [cap_next] * 4)
+        pool = torch.empty(2 * cap_p2p + 2 * cap_m2l + 4 * cap_next + 2 * cap_sym + 2 * cap_sm, dtype=i32, device=dev)
+        p2p_t, p2p_s, m2l_t, m2l_s, sym_a, sym_b, sm_a, sm_b, *fr = torch.split(
+            pool, [cap_p2p, cap_p2p, cap_m2l, cap_m2l, cap_sym, cap_sym, cap_sm, cap_sm] + [cap_next] * 4)
         _lib.call("fmm_traverse_mutual_sym", P(fr[0]), P(fr[1]), P(fr[2]), P(fr[3]), cap_next, nsteps,
                   P(tree.d_children), P(tree.d_leaf), P(tree.d_ctr), P(tree.d_bmax), P(tree.d_rmax), P(owner),
                   P(tree.d_start), P(tree.d_end), blo, bhi, mac.code, th2, P(p2p_t), P(p2p_s), cap_p2p, P(m2l_t),
-                  P(m2l_s), cap_m2l, P(log), P(sym_a), P(sym_b), cap_sym, None, None, 0, P(log[nsteps + 3:]), st)
+                  P(m2l_s), cap_m2l, P(log), P(sym_a), P(sym_b), cap_sym, P(sm_a) if sym_m2l else None,
+                  P(sm_b) if sym_m2l else None, cap_sm, P(log[nsteps + 3:]), st)
         hl = log.tolist()  # the one synchronisation of the traversal
-        done_p2p, done_m2l, fronts, n_sym = hl[0], hl[1], hl[2:nsteps + 3], hl[nsteps + 3]
+        done_p2p, done_m2l, fronts, n_sym, n_sm = hl[0], hl[1], hl[2:nsteps + 3], hl[nsteps + 3], hl[nsteps + 4]
         peak = max(fronts)
-        if done_p2p <= cap_p2p and done_m2l <= cap_m2l and peak <= cap_next and n_sym <= cap_sym:
+        if (done_p2p <= cap_p2p and done_m2l <= cap_m2l and peak <= cap_next and n_sym <= cap_sym
+                and n_sm <= cap_sm):
             if fronts[-1] != 0:
                 raise RuntimeError("mutual traversal did not terminate within 2*depth+2 steps")
             break
@@ -483,12 +490,15 @@ def _mutual_lists_sym(tree: Tree, mac: MacConfig, task_grain: int, body_range, m
         cap_m2l = max(cap_m2l, int(done_m2l * 1.05) + 4096)
         cap_next = max(cap_next, int(peak * 1.05) + 4096)
         cap_sym = max(cap_sym, int(n_sym * 1.05) + 4096)
+        cap_sm = max(cap_sm, int(n_sm * 1.05) + 4096) if sym_m2l else 0
     del fr
     _hint[key] = (int(done_p2p * 1.02) + 4096, int(done_m2l * 1.02) + 4096, int(peak * 1.05) + 4096,
-                  int(n_sym * 1.02) + 4096)
+                  int(n_sym * 1.02) + 4096, int(n_sm * 1.02) + 4096 if sym_m2l else 0)
     ncells = tree.ncells
-    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, n_sym, tree.n, ncells + 1), dev,
+    wsp, wsb = _lib.workspace(max(done_m2l, done_p2p, n_sym, n_sm, tree.n, ncells + 1), dev,
                               stream=torch.cuda.current_stream())
+    # (the unordered M2L pairs first: the far-field event is recorded after the directed CSR)
+    sym_far = _sym_pairs(tree, sm_a, sm_b, n_sm, wsp, wsb, st, slots=False) if sym_m2l else None
     m2l_src, m2l_rows = _far_csr(m2l_t, m2l_s, done_m2l, ncells, dev, wsp, wsb, st, side, m2l_ready, sort=sort_far)
     p2p_grp, p2p_rows = _csr(p2p_t, p2p_s, done_p2p, ncells, dev, wsp, wsb, st, sort=False)
     plan = _p2p_plan(tree, p2p_grp, p2p_rows, done_p2p, blo, bhi, wsp, wsb, st)
@@ -498,9 +508,10 @@ def _mutual_lists_sym(tree: Tree, mac: MacConfig, task_grain: int, body_range, m
         # (src/_taylor.py:439, pairs += 2): added to the plan's pair counter
         size = (tree.d_end - tree.d_start).long()
         plan["dev_stats"][0] += 2 * (size[sym_a[:n_sym].long()] * size[sym_b[:n_sym].long()]).sum()
-    del p2p_t, p2p_s, m2l_t, m2l_s, sym_a, sym_b, pool
-    return Lists(n_m2l=done_m2l, n_p2p=done_p2p + 2 * n_sym, m2l_src=m2l_src, m2l_rows=m2l_rows,
-                 p2p_rows=p2p_rows, peak_frontier=peak, sym_p2p=sym, **plan)
+    del p2p_t, p2p_s, m2l_t, m2l_s, sym_a, sym_b, sm_a, sm_b, pool
+    # (m2l_calls counts both directions of a mutual pair, src/traversal.py:500-517)
+    return Lists(n_m2l=done_m2l + 2 * n_sm, n_p2p=done_p2p + 2 * n_sym, m2l_src=m2l_src, m2l_rows=m2l_rows,
+                 p2p_rows=p2p_rows, peak_frontier=peak, sym_p2p=sym, sym_m2l=sym_far, **plan)
 
 
 def _sync_free() -> bool:
@@ -657,6 +668,43 @@ def run_m2l(tree: Tree, lists: Lists, p: int, src: Tree | None = None) -> None:
         return
     _lib.call("fmm_m2l_csr", p, tree.ncells, P(lists.m2l_rows), P(lists.m2l_src), P(tree.d_ctr),
               P(src.d_ctr) if cross else None, P(src._M if cross else tree._M), P(tree._L), _lib.stream_handle())
+
+
+# orders the symmetric M2L kernel covers (include/fmm_b200.h FMM_M2L_SYM_MAX_P)
+M2L_SYM_MAX_P = 7
+
+
+def m2l_symmetric(tree: Tree, p: int) -> bool:
+    """Whether a symmetric mutual evaluation keeps its M2L pairs unordered:
+    orders the register kernel covers, below the offset-grouped tensor
+    kernel's range (that one shares a D over a whole lattice group)."""
+    return p <= M2L_SYM_MAX_P and not m2l_grouped(tree, p)
+
+
+def run_m2l_sym(tree: Tree, lists: Lists, p: int) -> None:
+    """The symmetric M2L over ``lists.sym_m2l`` (after ``run_m2l`` on the
+    same stream): every unordered cell pair gets one derivative tensor,
+    contracted into both cells' locals (src/_taylor.py:191-217),
+    deterministically (``fmm_m2l_sym``)."""
+    sym = lists.__dict__.get("sym_m2l")
+    if sym is None or sym.n == 0:
+        return
+    P, dev, item = _lib.ptr, tree.device, ncoef(p) * 8
+    nch = max(1, -(-sym.n * item // SYM_BUFFER_BYTES))
+    if nch == 1:
+        cuts, bases = [0, tree.ncells], [0, sym.n]
+    else:  # first-member ranges whose slots fit the buffer (one read)
+        want = torch.arange(1, nch, device=dev, dtype=torch.int64) * (sym.n // nch)
+        mid = torch.searchsorted(sym.rows_a, want, right=True).clamp_(1, tree.ncells) - 1
+        cuts = sorted(set([0, tree.ncells] + mid.tolist()))
+        bases = sym.rows_a[torch.tensor(cuts, device=dev)].tolist()
+    cap = max(b1 - b0 for b0, b1 in zip(bases[:-1], bases[1:]))
+    react = torch.empty(max(cap, 1) * ncoef(p), dtype=torch.float64, device=dev)
+    for (a0, a1), base in zip(zip(cuts[:-1], cuts[1:]), bases[:-1]):
+        _lib.call("fmm_m2l_sym", p, tree.ncells, a0, a1, P(sym.rows_a), P(sym.src_a), P(sym.rows_b), P(sym.src_b),
+                  base, P(tree.d_ctr), P(tree._M), P(react), P(tree._L), _lib.stream_handle())
+    for t in (react, sym.rows_a, sym.src_a, sym.rows_b, sym.src_b):
+        t.record_stream(torch.cuda.current_stream())
 
 
 class CrossBodies:
@@ -1151,7 +1199,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                 sort_far = not m2l_grouped(tree, p, src)
                 if cfg.mutual:
                     lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side, sort_far=sort_far,
-                                         symmetric=symmetric)
+                                         symmetric=symmetric, symmetric_m2l=symmetric and m2l_symmetric(tree, p))
                 else:
                     lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
                                               m2l_owner_only=nch > 1, src=src, target_mask=target_mask,
@@ -1166,6 +1214,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                 ea, eb = E(), E()
                 ea.record(side)
                 run_m2l(tree, lists, p, src)
+                run_m2l_sym(tree, lists, p)
                 eb.record(side)
                 m2l_ev.append((ea, eb))
             planned = E()

@@ -261,3 +261,89 @@ def test_symmetric_multirank_ranges_sum_to_whole():
     parts = [canon_pairs(*fb.mutual_lists(t, mac, c.grain, body_range=rng, symmetric=True).host_pairs("p2p"))
              for rng in ((0, cut), (cut, t.n))]
     assert np.array_equal(np.sort(np.concatenate(parts)), full)
+
+
+# ---- symmetric M2L (fmm_m2l_sym, the reference's _m2l_mutual) ---------------
+
+def test_symmetric_m2l_lists_expand_to_reference_sets(case):
+    t = build(case)
+    lists = fb.mutual_lists(t, fb.MacConfig(case.mac, case.theta), case.grain, symmetric=True, symmetric_m2l=True)
+    assert lists.n_m2l == case.meta["n_m2l"] and lists.n_p2p == case.meta["n_p2p"]
+    assert sha(canon_pairs(*lists.host_pairs("m2l"))) == case.meta["m2l_sha"]
+    assert sha(canon_pairs(*lists.host_pairs("p2p"))) == case.meta["p2p_sha"]
+    a, b = lists.sym_m2l.pairs()
+    assert lists.sym_m2l.n == a.numel() and bool((a < b).all())
+
+
+def test_symmetric_m2l_unordered_pairs_match_oracle():
+    """The unordered M2L list is the oracle's mutual M2L entries."""
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    ot = orc.build_tree(c.pos, c.q, c.ncrit)
+    for grain in (37, 700, 10 ** 9):
+        lists = fb.mutual_lists(t, fb.MacConfig("fmm", 0.55), grain, symmetric=True, symmetric_m2l=True)
+        mt, ms, mm, _, _, _ = orc.collect_mutual(ot, 0.55, grain, "fmm")
+        keep = (mm != 0) & (mt != ms)
+        want = np.unique(np.stack([np.minimum(mt[keep], ms[keep]), np.maximum(mt[keep], ms[keep])], 1), axis=0)
+        a, b = lists.sym_m2l.pairs()
+        got = np.unique(np.stack([a.numpy(), b.numpy()], 1), axis=0)
+        assert lists.sym_m2l.n == len(want) and np.array_equal(got, want)
+        assert grain < 10 ** 9 or lists.sym_m2l.n > 0
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_symmetric_m2l_orders_match_oracle(p):
+    """Every order of the symmetric M2L kernel (1..7) against the oracle's
+    _m2l_mutual; p = 8 keeps the M2L pairs directed (grouped tensor kernel)."""
+    from paper_1209_3516_b200 import workloads
+    pos, q = workloads.config1(3000, 9)
+    t = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], q), ncrit=16)
+    ot = orc.build_tree(pos, q, 16)
+    want = orc.evaluate_mutual(ot, p, 0.5, 10 ** 9)
+    rep = fb.evaluate_on_tree(t, fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=p, mutual=True, task_grain=10 ** 9,
+                                               symmetric=True))
+    assert rep.stats.m2l_calls == want["m2l_calls"] and rep.stats.p2p_pairs == want["p2p_pairs"]
+    sym = t.list_cache.__dict__.get("sym_m2l")
+    assert (sym is not None and sym.n > 0) if p <= 7 else sym is None
+    b = t.bodies
+    for k in ("phi", "fx", "fy", "fz"):
+        assert rel_l2(getattr(b, k), want[k]) <= FP64_TOL, k
+
+
+def test_symmetric_m2l_locals_deterministic_and_equal_directed():
+    """The locals after M2L: two symmetric runs agree bit for bit; against
+    the directed M2L of the same pairs they agree to rounding."""
+    from paper_1209_3516_b200.traversal import run_m2l, run_m2l_sym
+    from paper_1209_3516_b200.tree import upward_pass
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    p, mac = 5, fb.MacConfig("fmm", 0.5)
+    upward_pass(t, p)
+    out = []
+    for sym in (True, True, False):
+        lists = fb.mutual_lists(t, mac, 10 ** 9, symmetric=True, symmetric_m2l=sym)
+        t._L = torch.zeros_like(t._M)
+        run_m2l(t, lists, p)
+        run_m2l_sym(t, lists, p)
+        torch.cuda.synchronize()
+        out.append(t._L.cpu().numpy().copy())
+    assert np.array_equal(out[0], out[1])
+    assert np.abs(out[0]).max() > 0
+    assert np.abs(out[0] - out[2]).max() <= 1e-12 * np.abs(out[2]).max()
+
+
+def test_symmetric_m2l_chunked_reaction_buffer(monkeypatch):
+    from paper_1209_3516_b200 import traversal
+    c = MuCase("c1_4k_g700")
+    t = build(c)
+    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", 0.5), p=4, mutual=True, task_grain=10 ** 9, symmetric=True)
+    rep0 = fb.evaluate_on_tree(t, cfg)
+    whole = np.stack([t.bodies.phi, t.bodies.fx, t.bodies.fy, t.bodies.fz]).copy()
+    nsym = t.list_cache.sym_m2l.n
+    assert nsym * 35 * 8 > 8 * (16 << 10)
+    monkeypatch.setattr(traversal, "SYM_BUFFER_BYTES", 16 << 10)
+    rep1 = fb.evaluate_on_tree(t, cfg)
+    assert rep1.stats.m2l_calls == rep0.stats.m2l_calls
+    got = np.stack([t.bodies.phi, t.bodies.fx, t.bodies.fy, t.bodies.fz])
+    for k in range(4):
+        assert rel_l2(got[k], whole[k]) <= 1e-13, k
