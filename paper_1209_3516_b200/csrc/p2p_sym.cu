@@ -13,9 +13,9 @@
 // per-pair slot of a scratch buffer, and a second kernel, one CTA per cell,
 // adds the cell's slots in ascending order of the first member.
 //
-// P2P pair kernel: a CTA per first leaf a, its partners b dealt to 4 warps.
-// A warp keeps 2 targets of a per lane (64 per sweep) and takes b's sources
-// 32 at a time; in step k lane l meets source slot (l + k) mod 32, whose
+// P2P pair kernel: a CTA per first leaf a, its partners' bodies dealt to 4
+// warps as one stream.  A warp keeps up to 2 targets of a per lane (64 per
+// sweep) and takes the stream's sources 32 at a time; in step k lane l meets source slot (l + k) mod 32, whose
 // position comes from the warp's shared-memory copy and whose four reaction
 // sums travel round the warp by one shuffle each per step, so that after 32
 // steps every lane holds the finished sums of its own slot and stores them
@@ -64,9 +64,35 @@ __device__ __forceinline__ void sym_pair(const B &t, const B &s, T (&acc)[4], T 
     rz = fma(t.w, gz, rz);
 }
 
+// One 32-source chunk against the lane's targets: in step k lane l meets
+// source slot (l + k) mod 32; the slot's four reaction sums travel with it.
+template <typename T, typename B, bool TWO>
+__device__ __forceinline__ void sym_chunk(const B *__restrict__ sb, int lane, const B &t0, const B &t1, T (&acc0)[4],
+                                          T (&acc1)[4], T &rp, T &rx, T &ry, T &rz) {
+    const int nxt = (lane + 1) & 31;
+#pragma unroll 4
+    for (int st = 0; st < 32; st++) {
+        const B sv = sb[(lane + st) & 31];
+        sym_pair<T>(t0, sv, acc0, rp, rx, ry, rz);
+        if constexpr (TWO) sym_pair<T>(t1, sv, acc1, rp, rx, ry, rz);
+        rp = __shfl_sync(0xffffffffu, rp, nxt);
+        rx = __shfl_sync(0xffffffffu, rx, nxt);
+        ry = __shfl_sync(0xffffffffu, ry, nxt);
+        rz = __shfl_sync(0xffffffffu, rz, nxt);
+    }
+}
+
 // rowsA/srcA: CSR of the unordered pairs by first leaf (sources ascending);
 // slot_off[k] = first reaction slot of pair k (slots = bodies of srcA[k]).
 // Only first leaves in [a_lo, a_hi) (one chunk of a bounded react buffer).
+//
+// The partners of a first leaf are swept as ONE source stream: the reaction
+// slots of a row are consecutive (slot_off is a prefix sum over the row's
+// partner sizes), so stream position i is slot i, body
+// cstart[srcA[k]] + i - slot_off[k] of the partner k covering it.  The
+// warps take the stream 32 positions at a time, each lane walking its own
+// partner cursor forward; only the row's last chunk is padded.  A sweep
+// whose targets fit one per lane skips the second target's arithmetic.
 template <typename T>
 __global__ void __launch_bounds__(kSymWarps * 32) p2p_sym_kernel(
     int32_t a_lo, int32_t a_hi, const int64_t *__restrict__ rowsA, const int32_t *__restrict__ srcA,
@@ -81,46 +107,38 @@ __global__ void __launch_bounds__(kSymWarps * 32) p2p_sym_kernel(
     if (k0 == k1) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t as = cstart[a], na = cend[a] - as;
+    const int64_t s0 = slot_off[k0], s1 = slot_off[k1];
     __shared__ B sbuf[kSymWarps][32];
     __shared__ T fold[kSymWarps][64][4];
     for (int32_t tb = 0; tb < na; tb += 64) {
+        const bool two = na - tb > 32;
         const int32_t i0 = tb + lane, i1 = tb + 32 + lane;
         B t0 = bodies[as + min(i0, na - 1)], t1 = bodies[as + min(i1, na - 1)];
         if (i0 >= na) t0.w = T(0);
         if (i1 >= na) t1.w = T(0);
         T acc0[4] = {T(0), T(0), T(0), T(0)}, acc1[4] = {T(0), T(0), T(0), T(0)};
-        for (int64_t k = k0 + warp; k < k1; k += kSymWarps) {
-            const int32_t b = srcA[k];
-            const int32_t bs = cstart[b], nb = cend[b] - bs;
-            const int64_t slot = slot_off[k] - slot_base;
-            for (int32_t c = 0; c < nb; c += 32) {
-                const int32_t j = c + lane;
-                B s = bodies[bs + min(j, nb - 1)];
-                if (j >= nb) s.w = T(0);
-                __syncwarp();
-                sbuf[warp][lane] = s;
-                __syncwarp();
-                T rp = T(0), rx = T(0), ry = T(0), rz = T(0);
-                const int nxt = (lane + 1) & 31;
-#pragma unroll 4
-                for (int st = 0; st < 32; st++) {
-                    const B sv = sbuf[warp][(lane + st) & 31];
-                    sym_pair<T>(t0, sv, acc0, rp, rx, ry, rz);
-                    sym_pair<T>(t1, sv, acc1, rp, rx, ry, rz);
-                    rp = __shfl_sync(0xffffffffu, rp, nxt);
-                    rx = __shfl_sync(0xffffffffu, rx, nxt);
-                    ry = __shfl_sync(0xffffffffu, ry, nxt);
-                    rz = __shfl_sync(0xffffffffu, rz, nxt);
+        int64_t kc = k0;  // the lane's partner cursor (stream positions only grow)
+        for (int64_t cb = s0 + warp * 32; cb < s1; cb += kSymWarps * 32) {
+            const int64_t i = cb + lane;
+            const bool valid = i < s1;
+            const int64_t ii = valid ? i : s1 - 1;
+            while (slot_off[kc + 1] <= ii) kc++;
+            B s = bodies[cstart[srcA[kc]] + (int32_t)(ii - slot_off[kc])];
+            if (!valid) s.w = T(0);
+            __syncwarp();
+            sbuf[warp][lane] = s;
+            __syncwarp();
+            T rp = T(0), rx = T(0), ry = T(0), rz = T(0);
+            if (two) sym_chunk<T, B, true>(sbuf[warp], lane, t0, t1, acc0, acc1, rp, rx, ry, rz);
+            else sym_chunk<T, B, false>(sbuf[warp], lane, t0, t1, acc0, acc1, rp, rx, ry, rz);
+            if (valid) {
+                B out;
+                out.x = rp; out.y = -rx; out.z = -ry; out.w = -rz;  // (phi, fx, fy, fz)
+                if (tb > 0) {
+                    const B old = react[i - slot_base];
+                    out.x += old.x; out.y += old.y; out.z += old.z; out.w += old.w;
                 }
-                if (j < nb) {
-                    B out;
-                    out.x = rp; out.y = -rx; out.z = -ry; out.w = -rz;  // (phi, fx, fy, fz)
-                    if (tb > 0) {
-                        const B old = react[slot + j];
-                        out.x += old.x; out.y += old.y; out.z += old.z; out.w += old.w;
-                    }
-                    react[slot + j] = out;
-                }
+                react[i - slot_base] = out;
             }
         }
 #pragma unroll
