@@ -271,9 +271,15 @@ class Tree:
 
 
 def _to_device(a: np.ndarray, dev):
-    """Host array -> device through a pinned staging buffer (torch's caching
-    host allocator reuses it across calls)."""
+    """Host array -> device.  Pageable memory goes through a pinned staging
+    buffer (torch's caching host allocator reuses it across calls); an array
+    that already lives in page-locked memory (e.g. the NumPy view of a
+    ``pin_memory=True`` tensor) is copied from where it is -- the build
+    synchronises with its stream before it returns, so the caller may reuse
+    the array afterwards."""
     h = torch.from_numpy(np.ascontiguousarray(a))
+    if h.is_pinned():
+        return h.to(dev, non_blocking=True)
     pinned = torch.empty(h.shape, dtype=h.dtype, pin_memory=True)
     pinned.copy_(h)
     return pinned.to(dev, non_blocking=True)
@@ -311,6 +317,10 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
             src = tuple(a.to(dev) for a in (ps.x, ps.y, ps.z, ps.q))
         else:
             src = tuple(_to_device(a, dev) for a in ps.host_inputs())
+        # the tree's own copy of the caller's arrays (the reference's tree
+        # holds one): taken on a worker thread while the GPU builds (after
+        # the staging copies above, which want the memory bandwidth)
+        snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
         dcode = _lib.DTYPE_F64 if src[0].dtype == torch.float64 else _lib.DTYPE_F32
         x64 = torch.empty(n, dtype=f64, device=dev)
         y64, z64, q64 = torch.empty_like(x64), torch.empty_like(x64), torch.empty_like(x64)
@@ -334,7 +344,7 @@ def build_tree(ps: ParticleSet, ncrit: int = 30, shape: str = "cubic", center_mo
         del x64, y64, z64, q64, keys, iota
         tree = _carve_tree(dev, st, wsp, wsb, n, ncrit, shape, center_mode, allow_oversized_leaves, skeys, perm, root,
                            (xs, ys, zs, qs, b32, b32lo), inexact)
-    tree._input_snapshot = None if ps.on_device else _snap.submit(lambda a=ps.host_inputs(): [np.array(v) for v in a])
+    tree._input_snapshot = snapshot
     tree.build_time = time.perf_counter() - t0
     with torch.cuda.device(dev):  # the evaluation bills the host gap after the build to its first phase
         tree._ev_built = _build_event(dev)

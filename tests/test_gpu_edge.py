@@ -69,3 +69,33 @@ def test_anchored_fp32_for_float64_inputs():
     assert not t32.fp32_exact
     for k in ("phi", "fx", "fy", "fz"):
         assert rel_l2(getattr(t32.bodies, k), getattr(t64.bodies, k)) <= 1e-5, k
+
+
+def test_pinned_host_inputs_build_the_same_tree():
+    """Host arrays in page-locked memory are copied from where they are (no
+    staging pass); the tree and the results equal the pageable build's, and
+    the caller may overwrite the arrays once build_tree has returned."""
+    import torch
+    from paper_1209_3516_b200 import workloads
+    pos, q = workloads.config2(20000, 3)
+    cols = [np.ascontiguousarray(pos[:, k]) for k in range(3)] + [np.ascontiguousarray(q)]
+    pinned = []
+    for a in cols:
+        h = torch.empty(a.shape, dtype=torch.from_numpy(a).dtype, pin_memory=True).numpy()
+        h[...] = a
+        pinned.append(h)
+    assert all(torch.from_numpy(h).is_pinned() for h in pinned)
+    cfg = fb.EvalConfig(mac=fb.MacConfig("fmm", 0.4), p=4, precision="fp32")
+    t0 = fb.build_tree(fb.ParticleSet(*cols), ncrit=64)
+    fb.evaluate_on_tree(t0, cfg)
+    want = t0.results_in_input_order()
+    t1 = fb.build_tree(fb.ParticleSet(*pinned), ncrit=64)
+    t1._input_snapshot.result()  # (the tree's own copy of the inputs is taken on a worker thread)
+    for h in pinned:
+        h[...] = 0  # the device copy was complete when build_tree returned
+    fb.evaluate_on_tree(t1, cfg)
+    got = t1.results_in_input_order()
+    assert np.array_equal(t0.permutation, t1.permutation) and np.array_equal(t0.cell_bmax, t1.cell_bmax)
+    for k in ("phi", "fx", "fy", "fz"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert np.array_equal(np.asarray(got.x), np.asarray(want.x))  # the snapshot of the inputs, not the zeros
