@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--sharded", action="store_true",
                     help="N>1: each rank gets only its block of the input and keeps only its own bodies plus "
                          "the near-field halo (paper_1209_3516_b200.sharded) instead of the replicated cloud")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: the configuration's N per GPU (N x WORLD_SIZE bodies in all; BASELINE "
+                         "configs[4]: --config C5 --n 4194304 --weak), reported as \"scaling\": \"weak\"")
     ap.add_argument("--task-grain", type=int, default=5000, help="EvalConfig.task_grain (mutual partition)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -81,6 +84,8 @@ def parse():
 def workload(args):
     gen, n, solver = workloads.CONFIGS[args.config]
     n = args.n or n
+    if getattr(args, "weak", False):
+        n *= int(os.environ.get("WORLD_SIZE", "1"))
     pos, q = gen(n, 0)
     solver = dict(solver)
     if args.p:
@@ -445,7 +450,7 @@ def run_ours(args):
         "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": ms,
         "step_ms": {"min": 1e3 * float(np.min(times)), "median": 1e3 * float(np.median(times)),
                     "max": 1e3 * float(np.max(times)), "all": [round(1e3 * t, 3) for t in times]},
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
         "dtype": {"fp32": "f32 P2P / f64 tree+far field", "fp32acc": "f32 P2P terms, f64 sums / f64 tree+far field",
                   "fp64": "f64"}[args.precision],
         "data": "synthetic", "config": config_block(args, n, solver, {"precision": args.precision,
