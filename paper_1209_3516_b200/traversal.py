@@ -45,6 +45,7 @@ import ctypes as C
 import json
 import os
 import threading
+import weakref
 from dataclasses import dataclass, field
 
 import torch
@@ -173,6 +174,36 @@ def _setup_gap(tree: Tree, e0) -> float:
     if ev0 is not None:
         tree.build_time = ev0.elapsed_time(ev) * 1e-3
     return ev.elapsed_time(e0) * 1e-3
+
+
+_TIMED = frozenset(("stats", "build_time", "upward_time", "traversal_time", "downward_time", "spans"))
+
+
+class DeferredReport(EvalReport):
+    """An ``EvalReport`` whose times are read from the evaluation's CUDA
+    events on first use.  Each ``Event.elapsed_time`` costs ~7 us of host time
+    and the report needs 14 of them, all after the evaluation's final
+    synchronisation, when the GPU has nothing left to do: read eagerly they
+    are 0.7 % of a C2 step.  The counters are final when the report is
+    returned; ``stats.times``, the phase times and ``spans`` are filled by
+    ``resolve_times`` when any of them (or ``stats``) is first touched, or by
+    the thread's next evaluation while its kernels run (``_EventPool``: the
+    events are double-buffered, so they stay intact until then)."""
+
+    def __getattribute__(self, name):
+        if name in _TIMED:
+            d = object.__getattribute__(self, "__dict__")
+            thunk = d.get("_thunk")
+            if thunk is not None:
+                d["_thunk"] = None
+                thunk(self)
+        return object.__getattribute__(self, name)
+
+    def resolve_times(self) -> None:
+        thunk = self.__dict__.get("_thunk")
+        if thunk is not None:
+            self.__dict__["_thunk"] = None
+            thunk(self)
 
 
 # ---------------------------------------------------------------------------
@@ -1082,23 +1113,47 @@ class EndReadback:
 
 class _EventPool:
     """Timing events of one evaluation, reused across evaluations of the
-    calling thread (an evaluation synchronises before it returns, so its
-    events are free again): creating ~10-20 CUDA events per step costs host
-    time while the GPU waits for the first launch."""
+    calling thread: creating ~10-20 CUDA events per step costs host time
+    while the GPU waits for the first launch.  Two sets alternate, so the
+    events of the previous evaluation stay intact while this one runs: a
+    ``DeferredReport`` reads them late (``defer``), at the latest when its
+    set comes up for reuse."""
 
     _pools = threading.local()
 
-    def __init__(self, dev):
+    def __init__(self, dev, deferred: bool = False):
         key = torch.device(dev).index or 0
-        pools = self._pools.__dict__.setdefault("by_dev", {})
-        self.events = pools.setdefault(key, [])
+        st = self._pools.__dict__.setdefault("by_dev", {}).setdefault(
+            key, {"sets": ([], []), "gen": 0, "pending": [None, None]})
+        self._st, self._k = st, st["gen"] & 1
+        st["gen"] += 1
+        self._settle(self._k)  # this set's last report reads its events before they are re-recorded
+        if not deferred:  # an evaluator that reads its times eagerly: no report stays pending behind it
+            self._settle(1 - self._k)
+        self.events = st["sets"][self._k]
         self.i = 0
+
+    def _settle(self, k: int) -> None:
+        ref = self._st["pending"][k]
+        self._st["pending"][k] = None
+        rep = ref() if ref is not None else None
+        if rep is not None:
+            rep.resolve_times()
 
     def __call__(self) -> torch.cuda.Event:
         if self.i == len(self.events):
             self.events.append(torch.cuda.Event(enable_timing=True))
         self.i += 1
         return self.events[self.i - 1]
+
+    def defer(self, report: "DeferredReport") -> None:
+        """``report`` reads this evaluation's events later."""
+        self._st["pending"][self._k] = weakref.ref(report)
+
+    def settle_previous(self) -> None:
+        """Resolve the previous evaluation's report now (called once this
+        evaluation's kernels are queued: the host is about to wait anyway)."""
+        self._settle(1 - self._k)
 
 
 def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
@@ -1146,7 +1201,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         side = _side_stream(dev)
         pst = _side_stream(dev, 1)
         ust = _side_stream(dev, 3)  # the upward pass: launched after the first lists
-        E = _EventPool(dev)
+        E = _EventPool(dev, deferred=True)
         e0, e_alloc, e_up0, e_up1, e_down0, e_down1, e_l1, e_pend, e_end = (E() for _ in range(9))
         need_up = src._M is None or src.p != p
         nc = ncoef(p)
@@ -1244,6 +1299,7 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
         combine()
         rb = EndReadback([flag] + [t for x in parts for t in x.device_counters()] + coinc)
         e_end.record(main)
+        E.settle_previous()  # (the previous report's event reads, while this evaluation's kernels run)
         e_end.synchronize()
         host = rb.parts()
         redo = nf in ("fp32", "fp32acc") and int(host[0][0]) != 0
@@ -1285,30 +1341,41 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
     stats.p2p_skipped += int(skipped)
     stats.p2p_flops += 20 * int(pairs)
     stats.m2l_calls += lists.n_m2l
-    stats.add_time("list", e0.elapsed_time(e_l1) * 1e-3)
-    stats.add_time("m2l", sum(a.elapsed_time(b) for a, b in m2l_ev) * 1e-3)
-    stats.add_time("p2p", sum(a.elapsed_time(b) for a, b in p2p_ev) * 1e-3)  # kernel time, all chunks
     tree._results_changed()
     events = None
     if trace:
         events = []
-        mt, ms = lists.host_pairs("m2l")
-        events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms)]
+        mt, ms_ = lists.host_pairs("m2l")
+        events += [("m2l", int(a), int(b)) for a, b in zip(mt, ms_)]
         pt, ps = lists.host_pairs("p2p")
         events += [("p2p", int(a), int(b)) for a, b in zip(pt, ps)]
-    # phases overlap (far field on the side streams, near field on the P2P
-    # stream): the report splits the wall time along the critical path; the
-    # raw stream spans stay in ``spans``
-    ms = lambda a, b: a.elapsed_time(b) * 1e-3  # noqa: E731
-    wall = ms(e0, e_end)
-    up, trav, down = critical_path(ms(e0, e_pend), ms(e0, e_up1), max(ms(e0, b) for _, b in m2l_ev), wall)
-    up += _setup_gap(tree, e0)
-    spans = {"lists": ms(e0, e_l1), "upward": ms(e_up0, e_up1), "m2l": sum(ms(a, b) for a, b in m2l_ev),
-             "p2p": sum(ms(a, b) for a, b in p2p_ev), "downward": ms(e_down0, e_down1), "wall": wall}
-    return EvalReport(strategy="dualtree", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
-                      theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain, stats=stats,
-                      build_time=_build_time(tree, src), upward_time=up, traversal_time=trav, downward_time=down,
-                      trace=events, spans=spans, near_field=nf)
+
+    def times(rep):
+        # phases overlap (far field on the side streams, near field on the
+        # P2P stream): the report splits the wall time along the critical
+        # path; the raw stream spans stay in ``spans``
+        ms = lambda a, b: a.elapsed_time(b) * 1e-3  # noqa: E731
+        d = rep.__dict__
+        m2l_s, p2p_s = sum(ms(a, b) for a, b in m2l_ev), sum(ms(a, b) for a, b in p2p_ev)
+        t_lists = ms(e0, e_l1)
+        st_ = d["stats"]
+        st_.add_time("list", t_lists)
+        st_.add_time("m2l", m2l_s)
+        st_.add_time("p2p", p2p_s)  # kernel time, all chunks
+        wall = ms(e0, e_end)
+        up, trav, down = critical_path(ms(e0, e_pend), ms(e0, e_up1), max(ms(e0, b) for _, b in m2l_ev), wall)
+        up += _setup_gap(tree, e0)
+        d.update(build_time=_build_time(tree, src), upward_time=up, traversal_time=trav, downward_time=down,
+                 spans={"lists": t_lists, "upward": ms(e_up0, e_up1), "m2l": m2l_s, "p2p": p2p_s,
+                        "downward": ms(e_down0, e_down1), "wall": wall})
+
+    rep = DeferredReport(strategy="dualtree", n=tree.n, n_sources=src.n, p=p, mac_kind=cfg.mac.kind,
+                         theta=cfg.mac.theta, mutual=cfg.mutual, threads=threads, task_grain=cfg.task_grain,
+                         stats=stats, build_time=0.0, upward_time=0.0, traversal_time=0.0, downward_time=0.0,
+                         trace=events, near_field=nf)
+    rep.__dict__["_thunk"] = times
+    E.defer(rep)
+    return rep
 
 
 def evaluate_treecode(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None = None, threads: int = 1,
