@@ -428,6 +428,11 @@ def run_ours(args):
     peak, peaks = fp32_peak(torch, _lib.call, sh)
     p2p_s = float(np.median(p2p_times))
     achieved = 20.0 * rep.stats.p2p_pairs / p2p_s / 1e12
+    # target slots the near field computes per real target: a leaf of c
+    # bodies runs as blocks of 8 with a last block of 4 or 8, i.e. 4*ceil(c/4)
+    # slots (DESIGN.md (f) 1); `frac` counts real pairs only
+    leaf_cnt = (tree.d_end - tree.d_start)[tree.d_leaf.bool()].long()
+    slot_ratio = float((((leaf_cnt + 3) // 4) * 4).sum().item()) / max(float(leaf_cnt.sum().item()), 1.0)
     traffic = None
     if os.path.exists(TRAFFIC_PATH):
         try:
@@ -469,6 +474,7 @@ def run_ours(args):
         "kernel_ms": kernel_ms,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "target_slots_per_target": slot_ratio, "frac_with_padded_slots": achieved * slot_ratio / peak,
                      "peak_source": "FFMA/FFMA2 probe measured live in this run (%s); MEASURED_PEAKS.json has "
                                     "no FP32 figure" % ", ".join(f"{k} {v:.1f}" for k, v in peaks.items()),
                      "kernel": "p2p_f32_kernel", "flop_model": "20 flops/pair (src/_taylor.py:314)"},
