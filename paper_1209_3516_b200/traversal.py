@@ -271,6 +271,8 @@ class Lists:
 
     def host_pairs(self, which: str):
         """(targets, sources) int64 numpy arrays sorted by (target, source)."""
+        if self.__dict__.get("_deferred") is not None and not self.settle():
+            raise RuntimeError("interaction lists overflowed their capacity hint; build them again")
         rows = getattr(self, which + "_rows").cpu()
         src = getattr(self, which + "_src")[:int(rows[-1])].cpu().long()
         t = torch.repeat_interleave(torch.arange(rows.numel() - 1), rows[1:] - rows[:-1])
@@ -291,7 +293,7 @@ _hint = {}
 def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | None = None,
                       m2l_ready: torch.cuda.Event | None = None,
                       side: torch.cuda.Stream | None = None, m2l_owner_only: bool = False,
-                      src: Tree | None = None, defer: bool = True,
+                      src: Tree | None = None, defer: bool = False,
                       target_mask: torch.Tensor | None = None, sort_far: bool = True) -> Lists:
     """Dual traversal from (root, root) -> target-sorted CSR M2L/P2P lists
     (the sets of src/traversal.py:159-262).
@@ -301,7 +303,9 @@ def interaction_lists(tree: Tree, mac: MacConfig, body_range: tuple[int, int] | 
     ``src`` is a separate source tree (cross-tree lists: sources index its
     cells, the P2P plan points at its bodies appended after the targets).
     With ``defer`` and a capacity hint for this shape the host does not wait
-    for the traversal's counters (``Lists.settle``).  ``target_mask`` (uint8
+    for the traversal's counters: the caller must check ``Lists.settle`` and
+    redo the traversal when a list outgrew its hinted buffer (the evaluators
+    do, at their final read-back); the default waits and sizes exactly.  ``target_mask`` (uint8
     per target cell) keeps only the flagged targets' rows (sampled
     evaluations: ``tuner.ErrorProbe``)."""
     blo, bhi = body_range if body_range is not None else (0, tree.n)
@@ -404,7 +408,7 @@ def partition_owner(tree: Tree, grain: int) -> torch.Tensor:
 
 def mutual_lists(tree: Tree, mac: MacConfig, task_grain: int, body_range: tuple[int, int] | None = None,
                  m2l_ready: torch.cuda.Event | None = None, side: torch.cuda.Stream | None = None,
-                 defer: bool = True, sort_far: bool = True, symmetric: bool = False,
+                 defer: bool = False, sort_far: bool = True, symmetric: bool = False,
                  symmetric_m2l: bool = False) -> Lists:
     """Mutual dual traversal (src/traversal.py:159-262 with mutual units,
     :704-791 driver) -> DIRECTED target-sorted CSR M2L/P2P lists: each
@@ -1254,11 +1258,12 @@ def evaluate_dual_tree(tree: Tree, cfg: EvalConfig, *, source_tree: Tree | None 
                 sort_far = not m2l_grouped(tree, p, src)
                 if cfg.mutual:
                     lists = mutual_lists(tree, cfg.mac, cfg.task_grain, m2l_ready=ready, side=side, sort_far=sort_far,
-                                         symmetric=symmetric, symmetric_m2l=symmetric and m2l_symmetric(tree, p))
+                                         symmetric=symmetric, symmetric_m2l=symmetric and m2l_symmetric(tree, p),
+                                         defer=True)
                 else:
                     lists = interaction_lists(tree, cfg.mac, body_range=rng, m2l_ready=ready, side=side,
                                               m2l_owner_only=nch > 1, src=src, target_mask=target_mask,
-                                              sort_far=sort_far)
+                                              sort_far=sort_far, defer=True)
             parts.append(lists)
             if k == 0:
                 M, L, flag, far, bodies = allocate()

@@ -61,3 +61,27 @@ def test_listfmm_needs_cubic():
     t = build(c)
     with pytest.raises(ValueError, match="cubic"):
         fb.evaluate_on_tree(t, fb.EvalConfig(strategy="listfmm"))
+
+
+def test_lists_exact_after_a_capacity_hint_from_another_tree():
+    """A tree with the same cell and leaf counts but other centres (geometric
+    instead of centre-of-mass) leaves a capacity hint behind its evaluation;
+    the public list builder must not take it on trust (it sizes exactly), and
+    an evaluation that does take it must notice the overflow and redo."""
+    c = GeoCase("clustered3k_cubic_com")
+    pos = np.asarray(c.pos, np.float64)
+    mac = fb.MacConfig("fmm", c.theta)
+    other = fb.build_tree(fb.ParticleSet(pos[:, 0], pos[:, 1], pos[:, 2], c.q), ncrit=c.ncrit, shape=c.shape,
+                          center_mode="geometric")
+    for _ in range(2):  # the second evaluation runs from (and refreshes) the hint
+        fb.evaluate_on_tree(other, fb.EvalConfig(mac=mac, p=c.p))
+    t = build(c)
+    assert (t.ncells, t.nleaves) == (other.ncells, other.nleaves)
+    lists = fb.interaction_lists(t, mac)
+    assert sha(canon_pairs(*lists.host_pairs("m2l"))) == c.meta["m2l_sha"]
+    assert sha(canon_pairs(*lists.host_pairs("p2p"))) == c.meta["p2p_sha"]
+    rep = fb.evaluate_on_tree(t, fb.EvalConfig(mac=mac, p=c.p))
+    for k in ("p2p_pairs", "m2l_calls"):
+        assert getattr(rep.stats, k) == c.meta["stats_dualtree"][k], k
+    for k in ("phi", "fx", "fy", "fz"):
+        assert rel_l2(getattr(t.bodies, k), c[f"dualtree_{k}"]) <= 1e-11, k
