@@ -192,17 +192,14 @@ class DeferredReport(EvalReport):
 
     def __getattribute__(self, name):
         if name in _TIMED:
-            d = object.__getattribute__(self, "__dict__")
-            thunk = d.get("_thunk")
+            thunk = object.__getattribute__(self, "__dict__").pop("_thunk", None)  # (atomic: one caller runs it)
             if thunk is not None:
-                d["_thunk"] = None
                 thunk(self)
         return object.__getattribute__(self, name)
 
     def resolve_times(self) -> None:
-        thunk = self.__dict__.get("_thunk")
+        thunk = self.__dict__.pop("_thunk", None)
         if thunk is not None:
-            self.__dict__["_thunk"] = None
             thunk(self)
 
 

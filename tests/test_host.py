@@ -229,3 +229,26 @@ def test_fp32_promotion_rule(monkeypatch):
     monkeypatch.setenv("FMM_B200_NEAR_FIELD", "bf16")
     with pytest.raises(ValueError):
         near_field_precision(fb.EvalConfig(p=4))
+
+
+def test_deferred_report_fills_times_once_on_first_use():
+    """DeferredReport: counters are readable without resolving; the first
+    touch of a timed field (or total_time / to_dict) runs the thunk once."""
+    from paper_1209_3516_b200 import traversal as tv
+    rep = tv.DeferredReport(strategy="dualtree", n=8, n_sources=8, p=4, mac_kind="fmm", theta=0.4, mutual=False,
+                            threads=1, task_grain=5000, stats=tv.KernelStats(), build_time=0.0, upward_time=0.0,
+                            traversal_time=0.0, downward_time=0.0)
+    calls = []
+
+    def thunk(r):
+        calls.append(1)
+        r.__dict__["stats"].add_time("p2p", 0.25)
+        r.__dict__.update(build_time=1.0, upward_time=2.0, traversal_time=3.0, downward_time=4.0,
+                          spans={"wall": 9.0})
+
+    rep.__dict__["_thunk"] = thunk
+    assert rep.n == 8 and rep.strategy == "dualtree" and not calls
+    assert rep.total_time == 10.0 and calls == [1]
+    assert rep.stats.times["p2p"] == 0.25 and rep.spans == {"wall": 9.0}
+    rep.resolve_times()
+    assert calls == [1] and rep.to_dict()["times_ms"]["total"] == 10000
